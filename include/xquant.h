@@ -1,0 +1,220 @@
+/*
+ * xquant.h -- C ABI of the B200 (sm_100a) XQuant decode hot path.
+ *
+ * Drop-in boundary for the reference package `xcache` (arxiv 2508.10395,
+ * /root/reference/pkg/src/xcache). Every entry point takes plain device
+ * pointers, sizes and a cudaStream_t (as void*), performs no allocation and no
+ * host synchronisation, enqueues its work on `stream`, and returns a status
+ * code (XQ_OK or one of XQ_E*). The Python host layer maps the codes onto the
+ * reference's exception classes (errors.py:4-35): 1 -> ShapeError,
+ * 2 -> ConfigError, 3 -> UsageError, 4 -> DataError.
+ *
+ * Data layout in HBM (per layer, per payload stream):
+ *   codes  : uint8 [n_slots * L_max * row_bytes]; arena row (slot*L_max + t)
+ *            holds token t of sequence `slot` as the exact bytes of the
+ *            reference's pack_codes(row, bits) (fallback.py:58-79):
+ *            LSB-first little-endian bit stream, row_bytes =
+ *            ceil(cols*bits/64)*8.
+ *   params : fp16 scale + fp16 zero_point per group -- the 16+16 bits per
+ *            group the reference charges (quant.py:44-45, quant.py:58-62).
+ *            per-token  : __half2 (scale, zp) [n_slots * L_max][ceil(cols/G)]
+ *            per-channel: planar halves [n_slots * L_max / G][2][cols]
+ *                         (scales, then zero points; L_max % G == 0), the
+ *                         channels within each block stored in the order the
+ *                         fused kernel's dequant producer consumes them
+ *                         (paper_2508_10395_b200/csrc/xq_layout.cuh).
+ */
+#ifndef XQUANT_H_
+#define XQUANT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define XQ_OK 0
+#define XQ_ESHAPE 1     /* ShapeError  */
+#define XQ_ECONFIG 2    /* ConfigError */
+#define XQ_EUSAGE 3     /* UsageError  */
+#define XQ_ENONFINITE 4 /* DataError   */
+#define XQ_ECUDA 5      /* CUDA runtime error (launch / configuration) */
+
+/* element types of caller buffers */
+#define XQ_F32 0
+#define XQ_BF16 1
+#define XQ_F16 2
+#define XQ_F64 3
+
+/* A-operand sources of the fused decode kernel */
+#define XQ_A_CODES_TOKEN 0   /* per-token packed codes + half2 params            */
+#define XQ_A_CODES_CHANNEL 1 /* per-channel packed codes + residual fp32 rows    */
+#define XQ_A_F16_ROWS 2      /* plain fp16 rows (XQuant-CL accumulator, 16-bit)  */
+#define XQ_A_SAME 3          /* V side reuses the K-side A operand (MHA)         */
+
+const char* xq_version(void);
+/* Message describing the last non-zero status returned on this host thread. */
+const char* xq_last_error(void);
+
+/* ======================================================================
+ * Lane functions -- replace xcache._kernels (_kernels/__init__.py:20-26)
+ * ====================================================================== */
+
+/* quantize_groups: _native.pyx:111-153 / fallback.py:108-131.
+ * x: float64 [rows, cols] C-contiguous (device). Per row, contiguous groups
+ * of group_size: scale=(max-min)/(2^bits-1) (1 for a degenerate group),
+ * zp=min, code=clamp(floor((x-min)/scale+0.5),0,2^bits-1), all in float64,
+ * bit-identical to the reference. codes uint8 [rows, cols]; scales/zps
+ * float64 [rows, ceil(cols/group_size)]. bits in {2,3,4,8}. */
+int xq_quantize_groups(const double* x, int64_t rows, int64_t cols, int32_t group_size,
+                       int32_t bits, uint8_t* codes, double* scales, double* zero_points,
+                       void* stream);
+
+/* dequantize_groups: _native.pyx:156-177 / fallback.py:134-146.
+ * out = code*scale + zp in float64 with two roundings (no FMA). */
+int xq_dequantize_groups(const uint8_t* codes, const double* scales, const double* zero_points,
+                         int64_t rows, int64_t cols, int32_t group_size, double* out,
+                         void* stream);
+
+/* pack_codes / unpack_codes: _native.pyx:64-108 / fallback.py:58-94.
+ * words must hold ceil(n*bits/64) uint64. bits in {1..8}. */
+int xq_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint64_t* words, void* stream);
+int xq_unpack_codes(const uint64_t* words, int32_t bits, int64_t n, uint8_t* codes,
+                    void* stream);
+
+/* ======================================================================
+ * Packed cache arena -- replaces quant.append_rows / cache._Stream.push|bulk
+ * for the per-token payloads (cache.py:184-221, quant.py:198-228)
+ * ====================================================================== */
+
+/* Quantize n_rows rows (float32/bf16/f16/f64 per x_dtype, row stride in
+ * elements) per token in groups of group_size and write packed rows +
+ * half2 params into the arena.
+ *   destination arena row of input row i:
+ *     seq_lens != NULL : i*L_max + seq_lens[i] - 1  (decode: seq_lens counts
+ *                        the token being appended; one token per slot)
+ *     seq_lens == NULL : row0 + i                   (bulk / prefill)
+ *   sub_rows != NULL : quantize x - sub_rows[dst row] instead of x
+ *     (XQuant-CL delta against the fp32 accumulator, cache.py:478-479);
+ *   x_eff_out != NULL: float64 [n_rows, cols] copy of the exact quantizer
+ *     input (stage-wise parity hook).
+ *   nonfinite_flag != NULL: set to 1 if any input is NaN/Inf (quant.py:114-115).
+ */
+int xq_quantize_rows(const void* x, int32_t x_dtype, int64_t x_row_stride, int64_t n_rows,
+                     int64_t cols, int32_t bits, int32_t group_size, const int32_t* seq_lens,
+                     int64_t row0, int64_t L_max, const float* sub_rows, uint8_t* codes,
+                     int64_t row_bytes, void* params, double* x_eff_out, int32_t* nonfinite_flag,
+                     void* stream);
+
+/* Per-channel quantization of whole token groups (quant.py:124-134): block b
+ * is float32 [group_size, cols] at blocks + b*group_size*cols; its codes go to
+ * arena rows dst_row0[b] .. +group_size-1 and its params to param row
+ * dst_row0[b]/group_size. Used for the xq-gqa K latent flush (cache.py:218-221). */
+int xq_quantize_blocks_per_channel(const float* blocks, int64_t n_blocks, int64_t cols,
+                                   int32_t bits, int32_t group_size, const int64_t* dst_row0,
+                                   uint8_t* codes, int64_t row_bytes, void* params,
+                                   int32_t* nonfinite_flag, void* stream);
+
+/* Dequantize arena rows [row0, row0+n_rows) to float32 [n_rows, cols]
+ * (quant.dequantize, quant.py:137-153). axis 0 per-token, 1 per-channel. */
+int xq_dequant_rows(const uint8_t* codes, int64_t row_bytes, const void* params, int32_t axis,
+                    int32_t bits, int32_t group_size, int64_t cols, int64_t row0, int64_t n_rows,
+                    float* out, void* stream);
+
+/* ======================================================================
+ * Rematerialisation + decode attention (cache.py:271-281, model.py:150-182)
+ * ====================================================================== */
+
+/* cos/sin table [n_pos][head_dim/2] as float2, angle pos*theta^(-2j/hd)
+ * formed in float64 (linalg.py:84-88). */
+int xq_rope_table(void* cs_out, int64_t n_pos, int32_t head_dim, double theta, void* stream);
+
+/* Arrange K/V projection weights for the fused kernel: out is fp16
+ * [n_kv_heads][256][kdim]: rows 0..127 of head h are W_k[:, h*128 .. +128]^T,
+ * rows 128..255 are W_v[:, h*128 .. +128]^T, each K-major with the channel
+ * order permuted to match the dequant producer of the A stream that feeds it
+ * (a_mode_* in XQ_A_*, bits_* its code width). w_k / w_v: [kdim, n_kv_heads*128]
+ * row-major (x @ W convention, cache.py:385-387), dtype per w_dtype. */
+int xq_arrange_weights(const void* w_k, const void* w_v, int32_t w_dtype, int64_t kdim,
+                       int32_t n_kv_heads, int32_t a_mode_k, int32_t bits_k, int32_t a_mode_v,
+                       int32_t bits_v, void* w_out, void* stream);
+
+/* Workspace (bytes) the fused decode kernel needs for its split partials. */
+int64_t xq_decode_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_kv_heads,
+                                  int32_t group, int32_t tiles_per_chunk);
+
+/* Fused dequant -> rematerialise (tcgen05, TMEM accumulator) -> RoPE ->
+ * flash-decode. K and V are never written to HBM.
+ *   For every sequence b and KV head h: K = RoPE(A_K @ W_k[:, h]),
+ *   V = A_V @ W_v[:, h] over tokens [0, seq_lens[b]); every query head
+ *   h*group .. h*group+group-1 attends with q = RoPE(q_pre, seq_lens[b]-1).
+ *   out: float32 [n_seqs, n_kv_heads*group, 128].
+ *   A_K: ak_mode XQ_A_CODES_TOKEN / XQ_A_CODES_CHANNEL / XQ_A_F16_ROWS;
+ *        for CODES_CHANNEL, tokens t >= ak_nflushed[b] are read from the
+ *        float32 residual rows ak_resid + b*G*kdim (cache.py:223-230).
+ *   A_V: av_mode as above or XQ_A_SAME (MHA: one X cache feeds K and V).
+ *   rows of both A streams are arena rows b*L_max + t with row_bytes bytes
+ *   (codes) or kdim fp16 (F16_ROWS).
+ *   w_arranged: from xq_arrange_weights. rope_cs: from xq_rope_table with
+ *   n_pos >= max_len. sm_scale: 1/sqrt(128) for the reference (model.py:164). */
+int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                     const float* ak_resid, const int32_t* ak_nflushed, int32_t ak_bits,
+                     int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
+                     const void* av_params, int32_t av_bits, int64_t av_row_bytes,
+                     int32_t group_size, int64_t L_max, int64_t kdim, const int32_t* seq_lens,
+                     int32_t n_seqs, int32_t max_len, const void* w_arranged, int32_t n_kv_heads,
+                     int32_t group, const float* q_pre, const void* rope_cs, float sm_scale,
+                     int32_t tiles_per_chunk, void* workspace, int64_t workspace_bytes,
+                     float* out, void* stream);
+
+/* Debug / parity path: SIMT float32 rematerialisation that writes K and V
+ * to HBM (cache.rematerialize, cache.py:271-281). a_*: as xq_decode_attend
+ * for one sequence slot `slot` and tokens [0, n_tok). w_k/w_v float32
+ * [kdim, n_out]. k_out/v_out float32 [n_tok, n_out]; K gets RoPE at
+ * positions 0..n_tok-1 (head_dim 128). */
+int xq_remat_f32(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                 const float* ak_resid, int32_t ak_nflushed, int32_t ak_bits,
+                 int64_t ak_row_bytes, int32_t av_mode, const void* av_src, const void* av_params,
+                 int32_t av_bits, int64_t av_row_bytes, int32_t group_size, int64_t L_max,
+                 int64_t kdim, int32_t slot, int32_t n_tok, const float* w_k, const float* w_v,
+                 int64_t n_out, const void* rope_cs, float* k_out, float* v_out, void* stream);
+
+/* ======================================================================
+ * XQuant-CL accumulator (cache.py:124-146, 460-481)
+ * ====================================================================== */
+
+/* For every slot b and token t < seq_lens[b]:
+ *   seed != 0 : acc = deq(codes)          (base layer seeds, cache.py:473-477)
+ *   seed == 0 : acc = acc + deq(codes)    (delta layer, cache.py:481)
+ * and, if x16_out != NULL, x16_out = fp16(acc) for the remat A operand.
+ * acc/x16_out: [n_slots*L_max][cols]. */
+int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, const void* params,
+                     int32_t bits, int32_t group_size, int64_t cols, const int32_t* seq_lens,
+                     int32_t n_seqs, int32_t max_len, int64_t L_max, float* acc, void* x16_out,
+                     void* stream);
+
+/* ======================================================================
+ * fp16-KV decode baseline (FullPrecisionCache semantics, cache.py:302-323;
+ * the baseline stores post-RoPE K, which is mathematically identical)
+ * ====================================================================== */
+
+/* Append RoPE(k_new) and v_new (float32 [n_seqs, n_kv_heads*128]) at position
+ * seq_lens[b]-1 of bf16 caches [n_slots*L_max][n_kv_heads*128]. */
+int xq_kv_append(const float* k_new, const float* v_new, const int32_t* seq_lens, int32_t n_seqs,
+                 int32_t n_kv_heads, int64_t L_max, const void* rope_cs, void* k_cache,
+                 void* v_cache, void* stream);
+
+/* Split-K flash-decode over the bf16 caches for tokens [0, seq_lens[b]). */
+int64_t xq_kv_decode_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_kv_heads,
+                                     int32_t group, int32_t chunk_tokens);
+int xq_kv_decode_attend(const void* k_cache, const void* v_cache, int64_t L_max,
+                        const int32_t* seq_lens, int32_t n_seqs, int32_t max_len,
+                        int32_t n_kv_heads, int32_t group, const float* q_pre,
+                        const void* rope_cs, float sm_scale, int32_t chunk_tokens,
+                        void* workspace, int64_t workspace_bytes, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XQUANT_H_ */

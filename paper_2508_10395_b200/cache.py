@@ -1,0 +1,694 @@
+"""Per-layer cache backends on B200 -- batched, device-resident mirror of the
+reference's ``xcache.cache`` (/root/reference/pkg/src/xcache/cache.py).
+
+Same variant tags (``cache.py:41``), ``LayerPolicy`` (``cache.py:70-121``),
+``make_cache`` factory (``cache.py:620-630``) and backend interface
+``prefill / decode_append / rematerialize`` (``cache.py:255-281``). The
+differences are the ones the hot path needs:
+
+* a backend holds ``n_slots`` sequences (the reference holds one,
+  ``SPEC.md:311``); inputs carry a leading slot dimension;
+* payloads live in packed HBM arenas (codes byte-identical to the reference's
+  ``pack_codes`` per row, fp16 scale/zero-point per group) filled by the
+  sm_100a quantizer;
+* ``decode_attend(q, weights, acc)`` runs the fused dequant -> tcgen05
+  rematerialise -> RoPE -> flash-decode kernel and returns the attention
+  output without materialising K/V; ``rematerialize`` stays for parity and
+  returns float32 K/V (SIMT debug kernel).
+
+Variants on the hot path: ``fp16`` (baseline semantics), ``xq-mha``,
+``xq-gqa`` and ``xq-cl-mha``. ``kvq`` and ``xq-cl-gqa`` are "next" rows of the
+scope table and raise ``ConfigError`` here.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, DataError, ShapeError, UsageError
+
+VARIANTS = ("fp16", "kvq", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")  # cache.py:41
+CL_VARIANTS = ("xq-cl-mha", "xq-cl-gqa")
+SUPPORTED = ("fp16", "xq-mha", "xq-gqa", "xq-cl-mha")
+DEFAULT_GROUP_SIZE = 128
+HEAD_DIM = 128
+ROPE_THETA = 10000.0
+TOKEN, CHANNEL = 0, 1
+
+
+# ---------------------------------------------------------------------------
+# Policy (cache.py:70-121)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class LayerPolicy:
+    """Per-layer bit widths plus the cross-layer base/prefix structure."""
+
+    bits: list[int]
+    base_layers: int = 3
+    high_precision_prefix: int = 3
+
+    def __post_init__(self):
+        if self.base_layers > self.high_precision_prefix:
+            raise ConfigError("base_layers must not exceed high_precision_prefix")
+
+    @classmethod
+    def for_bits(cls, bits: int, n_layers: int, prefix: int = 3, prefix_bits: int = 4):
+        """Uniform ``bits`` with the leading layers kept at 4-bit (cache.py:89-112)."""
+        if bits == 16:
+            return cls([16] * n_layers, base_layers=min(prefix, n_layers))
+        per_layer = [max(bits, prefix_bits) if i < prefix else bits for i in range(n_layers)]
+        return cls(per_layer, base_layers=min(prefix, n_layers),
+                   high_precision_prefix=min(prefix, n_layers))
+
+    @classmethod
+    def uniform(cls, bits: int, n_layers: int):
+        n = min(3, n_layers)  # cache.py:114-118
+        return cls([bits] * n_layers, base_layers=n, high_precision_prefix=n)
+
+    def bits_for(self, layer: int) -> int:
+        return self.bits[layer]
+
+
+# ---------------------------------------------------------------------------
+# Weights and shared device tables
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class LayerWeights:
+    """K/V projections of one layer on the device (x @ W convention).
+
+    ``w_k``/``w_v``: [d, kv_width]. For ``xq-gqa`` the offline SVD factors
+    (linalg.py:103-126): ``u_k``/``u_v`` [d, r] and ``fused_k``/``fused_v``
+    [r, r] (= diag(sigma) B^T). Arranged fp16 copies for the fused kernel are
+    built lazily and cached.
+    """
+
+    w_k: torch.Tensor | None = None
+    w_v: torch.Tensor | None = None
+    u_k: torch.Tensor | None = None
+    u_v: torch.Tensor | None = None
+    fused_k: torch.Tensor | None = None
+    fused_v: torch.Tensor | None = None
+    _cache: dict = field(default_factory=dict, repr=False)
+
+    def arranged(self, key, a_mode_k, bits_k, a_mode_v, bits_v, wk, wv) -> torch.Tensor:
+        if key not in self._cache:
+            kdim, width = wk.shape
+            if width % HEAD_DIM:
+                raise ShapeError(f"kv width {width} not a multiple of {HEAD_DIM}")
+            n_kv = width // HEAD_DIM
+            out = torch.empty((n_kv, 256, kdim), dtype=torch.float16, device=wk.device)
+            wk_c, wv_c = wk.contiguous(), wv.contiguous()
+            N.call("xq_arrange_weights", N.ptr(wk_c), N.ptr(wv_c), _dtype_code(wk_c), kdim, n_kv,
+                   a_mode_k, bits_k, a_mode_v, bits_v, N.ptr(out), N.stream_of(wk.device))
+            self._cache[key] = out
+        return self._cache[key]
+
+    def f32(self, name: str) -> torch.Tensor:
+        key = ("f32", name)
+        if key not in self._cache:
+            self._cache[key] = getattr(self, name).float().contiguous()
+        return self._cache[key]
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    return {torch.float32: N.F32, torch.bfloat16: N.BF16, torch.float16: N.F16,
+            torch.float64: N.F64}[t.dtype]
+
+
+_ROPE: dict = {}
+
+
+def rope_table(n_pos: int, device) -> torch.Tensor:
+    """cos/sin table [n_pos, 64] float2 (angle formed in float64, linalg.py:84-88)."""
+    device = torch.device(device)
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    cur = _ROPE.get(key)
+    if cur is None or cur.shape[0] < n_pos:
+        n = max(1024, 1 << math.ceil(math.log2(max(n_pos, 1))))
+        t = torch.empty((n, HEAD_DIM), dtype=torch.float32, device=device)
+        N.call("xq_rope_table", N.ptr(t), n, HEAD_DIM, ROPE_THETA, N.stream_of(device))
+        _ROPE[key] = cur = t
+    return cur
+
+
+class Accumulator:
+    """XQuant-CL running reconstruction (cache.py:124-146) on the device.
+
+    ``x_hat`` float32 [n_slots, L_max, d] plus its fp16 copy ``x16`` (the
+    remat A operand of the delta layers). Transient per forward pass: the
+    base layer re-seeds it every step (model.py:228); the memory is reused.
+    """
+
+    def __init__(self, n_slots: int, max_len: int, width: int, device="cuda"):
+        self.x_hat = torch.zeros((n_slots, max_len, width), dtype=torch.float32, device=device)
+        self.x16 = torch.zeros((n_slots, max_len, width), dtype=torch.float16, device=device)
+        self.seeded = False
+
+
+# ---------------------------------------------------------------------------
+# Packed payload stream (cache.py:154-230 on the device)
+# ---------------------------------------------------------------------------
+
+
+class PackedStream:
+    """Quantized payload arena of one layer for ``n_slots`` sequences.
+
+    Per-token: codes [n_slots*L_max, row_bytes] + half2 params per group.
+    Per-channel (always buffered, cache.py:173): codes + planar params per
+    128-token group, plus an fp32 residual buffer [n_slots, G, width] holding
+    the rows of the current incomplete group (cache.py:203-208, 218-221).
+    """
+
+    def __init__(self, bits, axis, width, group_size, n_slots, max_len, device):
+        if bits not in (2, 3, 4, 8):
+            raise ConfigError(f"packed stream bits must be 2/3/4/8, got {bits}")
+        if axis == CHANNEL and max_len % group_size:
+            raise ConfigError("per-channel arena needs max_len % group_size == 0")
+        self.bits, self.axis, self.width, self.g = bits, axis, width, group_size
+        self.n_slots, self.L = n_slots, max_len
+        self.row_bytes = (width * bits + 63) // 64 * 8
+        self.codes = torch.zeros((n_slots * max_len, self.row_bytes), dtype=torch.uint8, device=device)
+        if axis == TOKEN:
+            ng = -(-width // group_size)
+            self.params = torch.zeros((n_slots * max_len, ng, 2), dtype=torch.float16, device=device)
+        else:
+            self.params = torch.zeros((n_slots * max_len // group_size, 2, width),
+                                      dtype=torch.float16, device=device)
+            self.resid = torch.zeros((n_slots, group_size, width), dtype=torch.float32, device=device)
+            self.n_flushed = np.zeros(n_slots, dtype=np.int64)
+            self.nflushed_dev = torch.zeros(n_slots, dtype=torch.int32, device=device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def nbytes(self) -> dict:
+        out = {"codes": self.codes.numel(), "params": self.params.numel() * 2}
+        if self.axis == CHANNEL:
+            out["residual"] = self.resid.numel() * 4
+        return out
+
+    # -- per-token ---------------------------------------------------------
+    def append_token_rows(self, x: torch.Tensor, lens_dev: torch.Tensor, sub=None, x_eff=None):
+        """Quantize one row per slot and store it at position lens[b]-1."""
+        N.call("xq_quantize_rows", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.width,
+               self.bits, self.g, N.ptr(lens_dev), 0, self.L, N.ptr(sub), N.ptr(self.codes),
+               self.row_bytes, N.ptr(self.params), N.ptr(x_eff), N.ptr(self.flag),
+               N.stream_of(x.device))
+
+    def fill_rows(self, x: torch.Tensor, slot: int, pos0: int, sub=None, x_eff=None):
+        """Bulk per-token quantization of x [n, width] into slot rows pos0.."""
+        if x.shape[0] == 0:
+            return
+        N.call("xq_quantize_rows", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.width,
+               self.bits, self.g, None, slot * self.L + pos0, self.L, N.ptr(sub),
+               N.ptr(self.codes), self.row_bytes, N.ptr(self.params), N.ptr(x_eff),
+               N.ptr(self.flag), N.stream_of(x.device))
+
+    # -- per-channel -------------------------------------------------------
+    def flush_blocks(self, blocks: torch.Tensor, dst_row0: list[int]):
+        dst = torch.tensor(dst_row0, dtype=torch.int64, device=blocks.device)
+        N.call("xq_quantize_blocks_per_channel", N.ptr(blocks), len(dst_row0), self.width,
+               self.bits, self.g, N.ptr(dst), N.ptr(self.codes), self.row_bytes,
+               N.ptr(self.params), N.ptr(self.flag), N.stream_of(blocks.device))
+
+    def check_finite(self):
+        """Raise DataError if any quantized input was NaN/Inf (quant.py:114-115).
+
+        Synchronises; the decode engine calls it once per step, not per layer."""
+        if int(self.flag.item()):
+            self.flag.zero_()
+            raise DataError("input contains NaN or Inf")
+
+
+# ---------------------------------------------------------------------------
+# Backends
+# ---------------------------------------------------------------------------
+
+
+class CacheBackend:
+    """Common interface (cache.py:238-299) with a slot dimension."""
+
+    variant = ""
+    needs_accumulator = False
+
+    def __init__(self, layer_index: int, policy: LayerPolicy, head_dim: int,
+                 group_size: int = DEFAULT_GROUP_SIZE, *, n_slots: int = 1, max_len: int = 4096,
+                 hidden_dim: int | None = None, n_heads: int | None = None, kv_group: int = 1,
+                 device="cuda"):
+        if head_dim != HEAD_DIM:
+            raise ConfigError(f"the B200 kernels are specialised for head_dim {HEAD_DIM}, got {head_dim}")
+        if hidden_dim is None or n_heads is None:
+            raise ConfigError("hidden_dim and n_heads are required (device arenas are preallocated)")
+        if hidden_dim != n_heads * head_dim or n_heads % kv_group:
+            raise ConfigError("hidden_dim must equal n_heads*head_dim and n_heads % kv_group == 0")
+        self.layer_index = layer_index
+        self.policy = policy
+        self.head_dim = head_dim
+        self.group_size = group_size
+        self.bits = policy.bits_for(layer_index)
+        self.n_slots, self.L = n_slots, max_len
+        self.d, self.n_heads, self.g = hidden_dim, n_heads, kv_group
+        self.kvw = hidden_dim // kv_group
+        self.n_kv = self.kvw // head_dim
+        self.device = torch.device(device)
+        self.n_tokens = np.zeros(n_slots, dtype=np.int64)
+        self.lens_dev = torch.zeros(n_slots, dtype=torch.int32, device=self.device)
+
+    # -- interface ---------------------------------------------------------
+    def prefill(self, x, weights: LayerWeights, acc: Accumulator | None = None, slot=None):
+        """Bulk-cache a prefix: x [n_slots, n, d] (all slots) or [n, d] for ``slot``."""
+        self._check_acc(acc)
+        slots, xs = self._split_slots(x, slot)
+        for s, xx in zip(slots, xs):
+            if self.n_tokens[s]:
+                raise UsageError("prefill on a non-empty cache")  # cache.py:258-259
+            if xx.shape[0] > self.L:
+                raise ShapeError(f"prefill of {xx.shape[0]} tokens exceeds max_len {self.L}")
+            self._prefill(s, xx, weights, acc)
+            self.n_tokens[s] = xx.shape[0]
+        self._sync_lens()
+
+    def decode_append(self, x_token, weights: LayerWeights, acc: Accumulator | None = None):
+        """Append one token per slot: x_token [n_slots, d] (cache.py:264-269)."""
+        self._check_acc(acc)
+        x_token = self._as_rows(x_token)
+        if x_token.shape[0] != self.n_slots:
+            raise ShapeError(f"expected {self.n_slots} rows, got {x_token.shape[0]}")
+        if np.any(self.n_tokens >= self.L):
+            raise ShapeError("cache full")
+        self.n_tokens += 1
+        self._sync_lens()
+        self._decode(x_token, weights, acc, self.lens_dev)
+
+    def rematerialize(self, weights: LayerWeights, positions, acc: Accumulator | None = None,
+                      slot: int = 0):
+        """(K, V) float32 of one slot (cache.py:271-281), SIMT parity path."""
+        n = int(self.n_tokens[slot])
+        if n == 0:
+            raise UsageError("rematerialize on an empty cache")
+        positions = np.asarray(positions).reshape(-1)
+        if positions.shape[0] != n:
+            raise ShapeError(f"got {positions.shape[0]} positions for {n} tokens")
+        if not np.array_equal(positions, np.arange(n)):
+            raise ShapeError("positions must be 0..n-1 (the cache's own timeline)")
+        self._check_acc(acc)
+        return self._rematerialize(weights, acc, slot, n)
+
+    def decode_attend(self, q_pre, weights: LayerWeights, acc: Accumulator | None = None,
+                      tiles_per_chunk: int | None = None):
+        """Fused remat + attention for the newest token of every slot.
+
+        q_pre: [n_slots, n_heads, 128] (or [n_slots, n_heads*128]) float32,
+        before RoPE; it is rotated to position n_tokens-1 in the kernel
+        (model.py:234). Returns float32 [n_slots, n_heads, 128].
+        """
+        self._check_acc(acc)
+        if np.any(self.n_tokens == 0):
+            raise UsageError("decode_attend on an empty cache")
+        q = q_pre.reshape(self.n_slots, self.n_heads, self.head_dim).float().contiguous()
+        out = torch.empty_like(q)
+        self._attend(q, weights, acc, self.lens_dev, int(self.n_tokens.max()), out, tiles_per_chunk)
+        return out
+
+    # -- helpers -------------------------------------------------------------
+    def _sync_lens(self):
+        self.lens_dev.copy_(torch.from_numpy(self.n_tokens.astype(np.int32)), non_blocking=False)
+
+    def _as_rows(self, x):
+        x = torch.as_tensor(x, device=self.device)
+        if x.dim() == 1:
+            x = x[None]
+        if x.dtype == torch.float64:
+            x = x.contiguous()
+        return x
+
+    def _split_slots(self, x, slot):
+        x = torch.as_tensor(x, device=self.device)
+        if slot is not None:
+            if x.dim() != 2:
+                raise ShapeError("prefill with slot= expects [n, d]")
+            return [slot], [x]
+        if x.dim() == 2 and self.n_slots == 1:
+            return [0], [x]
+        if x.dim() != 3 or x.shape[0] != self.n_slots:
+            raise ShapeError(f"prefill expects [{self.n_slots}, n, d]")
+        return list(range(self.n_slots)), [x[s] for s in range(self.n_slots)]
+
+    def _check_acc(self, acc):
+        if self.needs_accumulator and acc is None:
+            raise UsageError(f"{self.variant} requires an accumulator")  # cache.py:294-296
+
+    def _workspace(self, max_len, group, tpc):
+        nbytes = N.lib.xq_decode_workspace_bytes(self.n_slots, max_len, self.n_kv, group, tpc)
+        return torch.empty(nbytes // 4 + 1, dtype=torch.float32, device=self.device), nbytes
+
+    def _fused(self, ak_mode, ak_src, ak_params, ak_resid, ak_nfl, ak_bits, ak_rb, av_mode,
+               av_src, av_params, av_bits, av_rb, kdim, w_arr, group, q, lens, max_len, out, tpc):
+        tpc = tpc or default_tiles_per_chunk(self.n_slots, max_len, self.n_kv)
+        ws, nbytes = self._workspace(max_len, group, tpc)
+        rope = rope_table(max_len, self.device)
+        N.call("xq_decode_attend", ak_mode, N.ptr(ak_src), N.ptr(ak_params), N.ptr(ak_resid),
+               N.ptr(ak_nfl), ak_bits, ak_rb, av_mode, N.ptr(av_src), N.ptr(av_params), av_bits,
+               av_rb, self.group_size, self.L, kdim, N.ptr(lens), self.n_slots, max_len,
+               N.ptr(w_arr), self.n_kv, group, N.ptr(q), N.ptr(rope), 1.0 / math.sqrt(HEAD_DIM),
+               tpc, N.ptr(ws), nbytes, N.ptr(out), N.stream_of(self.device))
+
+    def _remat_f32(self, ak_mode, ak_src, ak_params, ak_resid, ak_nfl, ak_bits, ak_rb, av_mode,
+                   av_src, av_params, av_bits, av_rb, kdim, wk, wv, slot, n):
+        n_out = wk.shape[1]
+        k = torch.empty((n, n_out), dtype=torch.float32, device=self.device)
+        v = torch.empty((n, n_out), dtype=torch.float32, device=self.device)
+        rope = rope_table(n, self.device)
+        N.call("xq_remat_f32", ak_mode, N.ptr(ak_src), N.ptr(ak_params), N.ptr(ak_resid), ak_nfl,
+               ak_bits, ak_rb, av_mode, N.ptr(av_src), N.ptr(av_params), av_bits, av_rb,
+               self.group_size, self.L, kdim, slot, n, N.ptr(wk), N.ptr(wv), n_out, N.ptr(rope),
+               N.ptr(k), N.ptr(v), N.stream_of(self.device))
+        return k, v
+
+    def memory_bytes(self) -> dict:
+        return {}
+
+    # hooks
+    def _prefill(self, slot, x, weights, acc):  # pragma: no cover
+        raise NotImplementedError
+
+    def _decode(self, x, weights, acc, lens):  # pragma: no cover
+        raise NotImplementedError
+
+    def _rematerialize(self, weights, acc, slot, n):  # pragma: no cover
+        raise NotImplementedError
+
+    def _attend(self, q, weights, acc, lens, max_len, out, tpc):  # pragma: no cover
+        raise NotImplementedError
+
+
+def default_tiles_per_chunk(n_slots: int, max_len: int, n_kv: int, n_sm: int = 148) -> int:
+    """Split each sequence into enough chunks that units >= ~4 waves of SMs."""
+    n_tiles = max(1, -(-max_len // 128))
+    target_units = 4 * n_sm
+    per_seq_head = max(1, n_slots * n_kv)
+    chunks = max(1, min(n_tiles, -(-target_units // per_seq_head)))
+    return max(1, -(-n_tiles // chunks))
+
+
+class FullPrecisionCache(CacheBackend):
+    """``fp16`` baseline (cache.py:302-323): bf16 post-RoPE K/V in HBM."""
+
+    variant = "fp16"
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        shape = (self.n_slots * self.L, self.kvw)
+        self.k = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
+        self.v = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
+
+    def _project(self, x, weights):
+        xf = x.float()
+        return xf @ weights.f32("w_k"), xf @ weights.f32("w_v")
+
+    def _prefill(self, slot, x, weights, acc):
+        k, v = self._project(x, weights)
+        self._append_rows(k, v, slot, 0)
+
+    def _append_rows(self, k, v, slot, pos0):
+        """Bulk append with RoPE at positions pos0.. (torch ops; prefill only)."""
+        n = k.shape[0]
+        rope = rope_table(pos0 + n, self.device)
+        cos = rope[pos0:pos0 + n, 0::2]
+        sin = rope[pos0:pos0 + n, 1::2]
+        kk = k.view(n, self.n_kv, 64, 2)
+        e, o = kk[..., 0], kk[..., 1]
+        c, s = cos[:, None, :], sin[:, None, :]
+        rot = torch.stack([e * c - o * s, e * s + o * c], dim=-1).view(n, self.kvw)
+        base = slot * self.L + pos0
+        self.k[base:base + n] = rot.to(torch.bfloat16)
+        self.v[base:base + n] = v.to(torch.bfloat16)
+
+    def _decode(self, x, weights, acc, lens):
+        k, v = self._project(x, weights)
+        rope = rope_table(int(self.n_tokens.max()), self.device)
+        N.call("xq_kv_append", N.ptr(k.contiguous()), N.ptr(v.contiguous()), N.ptr(lens),
+               self.n_slots, self.n_kv, self.L, N.ptr(rope), N.ptr(self.k), N.ptr(self.v),
+               N.stream_of(self.device))
+
+    def _rematerialize(self, weights, acc, slot, n):
+        base = slot * self.L
+        return self.k[base:base + n].float(), self.v[base:base + n].float()
+
+    def _attend(self, q, weights, acc, lens, max_len, out, tpc):
+        chunk = tpc * 128 if tpc else kv_chunk_tokens(self.n_slots, max_len, self.n_kv)
+        nbytes = N.lib.xq_kv_decode_workspace_bytes(self.n_slots, max_len, self.n_kv, self.g, chunk)
+        ws = torch.empty(nbytes // 4 + 1, dtype=torch.float32, device=self.device)
+        rope = rope_table(max_len, self.device)
+        N.call("xq_kv_decode_attend", N.ptr(self.k), N.ptr(self.v), self.L, N.ptr(lens),
+               self.n_slots, max_len, self.n_kv, self.g, N.ptr(q), N.ptr(rope),
+               1.0 / math.sqrt(HEAD_DIM), chunk, N.ptr(ws), nbytes, N.ptr(out),
+               N.stream_of(self.device))
+
+    def memory_bytes(self):
+        return {"kv_cache": 2 * self.k.numel() * 2}
+
+
+def kv_chunk_tokens(n_slots, max_len, n_kv, n_sm=148):
+    units_per_chunk = max(1, n_slots * n_kv)
+    chunks = max(1, -(-8 * n_sm // units_per_chunk))
+    return max(256, -(-max_len // chunks))
+
+
+class InputCacheMHA(CacheBackend):
+    """``xq-mha`` (cache.py:363-387): per-token X codes; K/V rebuilt from X."""
+
+    variant = "xq-mha"
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        self.passthrough = self.bits == 16
+        if self.passthrough:  # bits=16 -> fp16 rows (quant.py:117-118 keeps raw data)
+            self.x16 = torch.zeros((self.n_slots * self.L, self.d), dtype=torch.float16,
+                                   device=self.device)
+        else:
+            self.stream = PackedStream(self.bits, TOKEN, self.d, self.group_size, self.n_slots,
+                                       self.L, self.device)
+
+    def _prefill(self, slot, x, weights, acc):
+        if self.passthrough:
+            self.x16[slot * self.L:slot * self.L + x.shape[0]] = x.to(torch.float16)
+        else:
+            self.stream.fill_rows(x.contiguous(), slot, 0)
+
+    def _decode(self, x, weights, acc, lens):
+        if self.passthrough:
+            idx = torch.arange(self.n_slots, device=self.device) * self.L + lens.long() - 1
+            self.x16[idx] = x.to(torch.float16)
+        else:
+            self.stream.append_token_rows(x.contiguous(), lens)
+
+    def _a_operand(self):
+        if self.passthrough:
+            return N.A_F16_ROWS, self.x16, None, 16, 0
+        s = self.stream
+        return N.A_CODES_TOKEN, s.codes, s.params, s.bits, s.row_bytes
+
+    def _rematerialize(self, weights, acc, slot, n):
+        mode, src, params, bits, rb = self._a_operand()
+        return self._remat_f32(mode, src, params, None, 0, bits, rb, N.A_SAME, None, None, 0, 0,
+                               self.d, weights.f32("w_k"), weights.f32("w_v"), slot, n)
+
+    def _attend(self, q, weights, acc, lens, max_len, out, tpc):
+        mode, src, params, bits, rb = self._a_operand()
+        w_arr = weights.arranged(("mha", mode, bits), mode, bits, N.A_SAME, bits,
+                                 weights.w_k, weights.w_v)
+        self._fused(mode, src, params, None, None, bits, rb, N.A_SAME, None, None, 0, 0, self.d,
+                    w_arr, 1, q, lens, max_len, out, tpc)
+
+    def memory_bytes(self):
+        if self.passthrough:
+            return {"x16": self.x16.numel() * 2}
+        return self.stream.nbytes()
+
+
+class LatentInputCacheGQA(CacheBackend):
+    """``xq-gqa`` (cache.py:390-437): K latent per-channel (buffered) + V latent
+    per-token; K/V rebuilt through fused = diag(sigma) B^T."""
+
+    variant = "xq-gqa"
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        if self.bits == 16:
+            raise ConfigError("xq-gqa on the B200 path needs a quantized width (2/3/4/8)")
+        r = self.kvw
+        self.k_stream = PackedStream(self.bits, CHANNEL, r, self.group_size, self.n_slots, self.L,
+                                     self.device)
+        self.v_stream = PackedStream(self.bits, TOKEN, r, self.group_size, self.n_slots, self.L,
+                                     self.device)
+
+    def _latents(self, x, weights):
+        xf = x.float()
+        return xf @ weights.f32("u_k"), xf @ weights.f32("u_v")
+
+    def _prefill(self, slot, x, weights, acc):
+        lat_k, lat_v = self._latents(x, weights)
+        self.v_stream.fill_rows(lat_v.contiguous(), slot, 0)
+        ks, g = self.k_stream, self.group_size
+        n = x.shape[0]
+        n_full = n // g * g  # cache.py:203-208
+        if n_full:
+            blocks = lat_k[:n_full].contiguous()
+            ks.flush_blocks(blocks, [slot * self.L + i for i in range(0, n_full, g)])
+        ks.resid[slot, :n - n_full] = lat_k[n_full:]
+        ks.n_flushed[slot] = n_full
+        ks.nflushed_dev[slot] = n_full
+
+    def _decode(self, x, weights, acc, lens):
+        lat_k, lat_v = self._latents(x, weights)
+        self.v_stream.append_token_rows(lat_v.contiguous(), lens)
+        ks, g = self.k_stream, self.group_size
+        buf_pos = torch.as_tensor(self.n_tokens - 1 - ks.n_flushed, device=self.device)
+        ks.resid[torch.arange(self.n_slots, device=self.device), buf_pos] = lat_k
+        full = np.nonzero(self.n_tokens - ks.n_flushed >= g)[0]  # cache.py:218-221
+        if len(full):
+            blocks = ks.resid[torch.as_tensor(full, device=self.device)].contiguous()
+            ks.flush_blocks(blocks, [int(s) * self.L + int(ks.n_flushed[s]) for s in full])
+            ks.n_flushed[full] += g
+            ks.nflushed_dev.copy_(torch.from_numpy(ks.n_flushed.astype(np.int32)))
+
+    def _rematerialize(self, weights, acc, slot, n):
+        ks, vs = self.k_stream, self.v_stream
+        return self._remat_f32(N.A_CODES_CHANNEL, ks.codes, ks.params, ks.resid,
+                               int(ks.n_flushed[slot]), ks.bits, ks.row_bytes, N.A_CODES_TOKEN,
+                               vs.codes, vs.params, vs.bits, vs.row_bytes, self.kvw,
+                               weights.f32("fused_k"), weights.f32("fused_v"), slot, n)
+
+    def _attend(self, q, weights, acc, lens, max_len, out, tpc):
+        ks, vs = self.k_stream, self.v_stream
+        w_arr = weights.arranged(("gqa", self.bits), N.A_CODES_CHANNEL, ks.bits, N.A_CODES_TOKEN,
+                                 vs.bits, weights.fused_k, weights.fused_v)
+        self._fused(N.A_CODES_CHANNEL, ks.codes, ks.params, ks.resid, ks.nflushed_dev, ks.bits,
+                    ks.row_bytes, N.A_CODES_TOKEN, vs.codes, vs.params, vs.bits, vs.row_bytes,
+                    self.kvw, w_arr, self.g, q, lens, max_len, out, tpc)
+
+    def memory_bytes(self):
+        out = {f"k_{k}": v for k, v in self.k_stream.nbytes().items()}
+        out.update({f"v_{k}": v for k, v in self.v_stream.nbytes().items()})
+        return out
+
+
+class DeltaInputCacheMHA(CacheBackend):
+    """``xq-cl-mha`` (cache.py:440-535): base layers cache X; the last base
+    layer seeds the accumulator; delta layers cache x - acc[pos] and add the
+    reconstruction of all their deltas to the accumulator; delta-layer K/V are
+    rebuilt from the accumulator."""
+
+    variant = "xq-cl-mha"
+    needs_accumulator = True
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        if self.policy.base_layers < 1:
+            raise ConfigError("cross-layer variants need at least one base layer")
+        if self.bits == 16:
+            raise ConfigError("xq-cl-mha on the B200 path needs a quantized width (2/3/4/8)")
+        self.stream = PackedStream(self.bits, TOKEN, self.d, self.group_size, self.n_slots,
+                                   self.L, self.device)
+
+    @property
+    def is_base(self):
+        return self.layer_index < self.policy.base_layers
+
+    @property
+    def seeds_accumulator(self):
+        return self.layer_index == self.policy.base_layers - 1
+
+    def _accumulate(self, acc, seed, max_len, lens):
+        s = self.stream
+        N.call("xq_cl_accumulate", 1 if seed else 0, N.ptr(s.codes), s.row_bytes, N.ptr(s.params),
+               s.bits, self.group_size, self.d, N.ptr(lens), self.n_slots, max_len, self.L,
+               N.ptr(acc.x_hat), None if seed else N.ptr(acc.x16), N.stream_of(self.device))
+        acc.seeded = True
+
+    def _prefill(self, slot, x, weights, acc):
+        n = x.shape[0]
+        lens = torch.zeros(self.n_slots, dtype=torch.int32, device=self.device)
+        lens[slot] = n
+        if self.is_base:
+            self.stream.fill_rows(x.contiguous(), slot, 0)
+            if self.seeds_accumulator:
+                self._accumulate(acc, True, n, lens)
+            return
+        if not acc.seeded:
+            raise UsageError("accumulator used before the base layer seeded it")
+        sub = acc.x_hat.view(-1, self.d)
+        self.stream.fill_rows(x.contiguous(), slot, 0, sub=sub)
+        self._accumulate(acc, False, n, lens)
+
+    def _decode(self, x, weights, acc, lens):
+        max_len = int(self.n_tokens.max())
+        if self.is_base:
+            self.stream.append_token_rows(x.contiguous(), lens)
+            if self.seeds_accumulator:
+                self._accumulate(acc, True, max_len, lens)
+            return
+        if not acc.seeded:
+            raise UsageError("accumulator used before the base layer seeded it")
+        self.stream.append_token_rows(x.contiguous(), lens, sub=acc.x_hat.view(-1, self.d))
+        self._accumulate(acc, False, max_len, lens)
+
+    def _rematerialize(self, weights, acc, slot, n):
+        wk, wv = weights.f32("w_k"), weights.f32("w_v")
+        if self.is_base:
+            s = self.stream
+            return self._remat_f32(N.A_CODES_TOKEN, s.codes, s.params, None, 0, s.bits,
+                                   s.row_bytes, N.A_SAME, None, None, 0, 0, self.d, wk, wv, slot, n)
+        return self._remat_acc(acc, wk, wv, slot, n)
+
+    def _remat_acc(self, acc, wk, wv, slot, n):
+        # parity path from the float32 accumulator itself (cache.py:531-535)
+        xh = acc.x_hat[slot, :n]
+        k = xh @ wk
+        v = xh @ wv
+        rope = rope_table(n, self.device)
+        cos, sin = rope[:n, 0::2], rope[:n, 1::2]
+        kk = k.view(n, -1, 64, 2)
+        e, o = kk[..., 0], kk[..., 1]
+        c, s = cos[:, None, :], sin[:, None, :]
+        return torch.stack([e * c - o * s, e * s + o * c], dim=-1).view(n, -1), v
+
+    def _attend(self, q, weights, acc, lens, max_len, out, tpc):
+        if self.is_base:
+            s = self.stream
+            w_arr = weights.arranged(("mha", N.A_CODES_TOKEN, s.bits), N.A_CODES_TOKEN, s.bits,
+                                     N.A_SAME, s.bits, weights.w_k, weights.w_v)
+            self._fused(N.A_CODES_TOKEN, s.codes, s.params, None, None, s.bits, s.row_bytes,
+                        N.A_SAME, None, None, 0, 0, self.d, w_arr, 1, q, lens, max_len, out, tpc)
+        else:
+            w_arr = weights.arranged(("mha", N.A_F16_ROWS, 16), N.A_F16_ROWS, 16, N.A_SAME, 16,
+                                     weights.w_k, weights.w_v)
+            self._fused(N.A_F16_ROWS, acc.x16, None, None, None, 16, 0, N.A_SAME, None, None, 0,
+                        0, self.d, w_arr, 1, q, lens, max_len, out, tpc)
+
+    def memory_bytes(self):
+        return self.stream.nbytes()
+
+
+_BACKENDS = {
+    cls.variant: cls
+    for cls in (FullPrecisionCache, InputCacheMHA, LatentInputCacheGQA, DeltaInputCacheMHA)
+}
+
+
+def make_cache(variant: str, layer_index: int, policy: LayerPolicy, head_dim: int,
+               group_size: int = DEFAULT_GROUP_SIZE, **kw) -> CacheBackend:
+    """Instantiate the backend for one layer (cache.py:620-630)."""
+    if variant not in VARIANTS:
+        raise ConfigError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    if variant not in _BACKENDS:
+        raise ConfigError(f"variant {variant!r} is not on the B200 hot path (next row)")
+    return _BACKENDS[variant](layer_index, policy, head_dim, group_size, **kw)

@@ -1,0 +1,725 @@
+// Fused XQuant decode: dequant -> rematerialise on tcgen05 -> RoPE ->
+// flash-decode, for sm_100a. K and V never touch HBM.
+//
+// Reference semantics (the thing this replaces, per sequence and layer):
+//   x_hat = stream.reconstruct()                          cache.py:223-230
+//   K = apply_rope(x_hat @ W_k, 0..l-1), V = x_hat @ W_v    cache.py:385-387 (xq-mha)
+//   K = RoPE(lat_k_hat @ fused_k), V = lat_v_hat @ fused_v  cache.py:434-437 (xq-gqa)
+//   out_h = softmax(q_h K_{h//g}^T / sqrt(hd)) V_{h//g}     model.py:150-182
+//
+// One persistent CTA per SM (512 threads, warp-specialised):
+//   warp 0       TMA producer of the weight tiles (W_k|W_v rows of one KV head)
+//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 4-11   two groups of 4 dequant producers (even / odd K-chunks):
+//                packed codes -> fp16 pairs (magic-number convert + HFMA2)
+//                -> SWIZZLE_128B K-major A tile in shared memory
+//   warps 12-15  epilogue: tcgen05.ld the [128 x 256] fp32 accumulator
+//                (cols 0-127 = K_pre, 128-255 = V), RoPE, q.k, per-warp online
+//                softmax, p.V via warp reduce-scatter -> split partials
+// Work unit = (sequence, chunk of 128-token tiles, KV head); a combine
+// kernel merges the per-(chunk, warp) partials.
+#include <cudaTypedefs.h>
+#include <math.h>
+
+#include "xq_common.cuh"
+#include "xq_host.h"
+#include "xq_layout.cuh"
+
+namespace xq {
+
+constexpr int kTileM = 128;
+constexpr int kChunk = 64;  // K elements per stage (128 B of fp16 = one swizzle row)
+constexpr int kThreads = 512;
+constexpr int kProdWarp0 = 4;
+constexpr int kEpiWarp0 = 12;
+constexpr int kPartStride = 2 + kHeadDim;  // m, l, o[128]
+constexpr uint32_t kABytes = kTileM * 128;  // 16 KB
+constexpr uint32_t kBBytes = 256 * 128;     // 32 KB
+
+struct DecodeParams {
+  const uint8_t* ak_src;
+  const void* ak_params;
+  const float* ak_resid;
+  const int32_t* ak_nflushed;
+  int64_t ak_row_bytes;
+  const uint8_t* av_src;
+  const void* av_params;
+  int64_t av_row_bytes;
+  int32_t group_size;
+  int64_t L_max;
+  int32_t kdim;
+  const int32_t* seq_lens;
+  int32_t n_chunks;
+  int32_t tiles_per_chunk;
+  int32_t n_kv;
+  int32_t n_units;
+  const float* q_pre;
+  const float2* rope;
+  float q_scale;  // sm_scale * log2(e)
+  float* partials;
+};
+
+struct Unit {
+  int b, chunk, h, t0, t1, len;
+};
+
+XQ_DEVINL Unit get_unit(const DecodeParams& p, int u) {
+  Unit w;
+  w.h = u % p.n_kv;
+  const int rest = u / p.n_kv;
+  w.chunk = rest % p.n_chunks;
+  w.b = rest / p.n_chunks;
+  w.len = p.seq_lens[w.b];
+  const int nt = (w.len + kTileM - 1) / kTileM;
+  w.t0 = w.chunk * p.tiles_per_chunk;
+  w.t1 = min(w.t0 + p.tiles_per_chunk, nt);
+  if (w.t1 < w.t0) w.t1 = w.t0;
+  return w;
+}
+
+template <typename T>
+XQ_DEVINL uint32_t as_u32(T v) {
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+template <typename T>
+XQ_DEVINL T from_u32(uint32_t v) {
+  return *reinterpret_cast<T*>(&v);
+}
+
+// codes (at bits 0.. and 16..) -> fp16 pair c*s + z, one rounding
+XQ_DEVINL uint32_t deq_pair(uint32_t masked, __half2 s2, __half2 z2) {
+  const __half2 c = __hsub2(from_u32<__half2>(masked | 0x64006400u), __float2half2_rn(1024.f));
+  return as_u32(__hfma2(c, s2, z2));
+}
+
+// 64 codes of one row -> 32 fp16 pairs in producer order (xq_layout.cuh).
+// src: the 8*BITS bytes of the chunk. s2/z2: per pair (per-channel) or uniform.
+template <int BITS, bool PER_PAIR>
+XQ_DEVINL void dequant_chunk(const uint8_t* src, const __half2* s2, const __half2* z2,
+                             uint32_t (&out)[32]) {
+  auto S = [&](int j) { return PER_PAIR ? s2[j] : s2[0]; };
+  auto Z = [&](int j) { return PER_PAIR ? z2[j] : z2[0]; };
+  if constexpr (BITS == 4) {
+    const uint4 a = reinterpret_cast<const uint4*>(src)[0];
+    const uint4 b = reinterpret_cast<const uint4*>(src)[1];
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int wi = 0; wi < 8; ++wi)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        out[4 * wi + j] = deq_pair((w[wi] >> (4 * j)) & 0x000F000Fu, S(4 * wi + j), Z(4 * wi + j));
+  } else if constexpr (BITS == 2) {
+    const uint4 a = reinterpret_cast<const uint4*>(src)[0];
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        out[8 * wi + j] = deq_pair((w[wi] >> (2 * j)) & 0x00030003u, S(8 * wi + j), Z(8 * wi + j));
+  } else if constexpr (BITS == 8) {
+    uint32_t w[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 a = reinterpret_cast<const uint4*>(src)[q];
+      w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+    }
+#pragma unroll
+    for (int wi = 0; wi < 16; ++wi)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        out[2 * wi + j] = deq_pair((w[wi] >> (8 * j)) & 0x00FF00FFu, S(2 * wi + j), Z(2 * wi + j));
+  } else {  // 3-bit: two 32-code blocks of 3 words each
+    uint32_t w[6];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const uint2 a = reinterpret_cast<const uint2*>(src)[q];
+      w[2 * q] = a.x;
+      w[2 * q + 1] = a.y;
+    }
+#pragma unroll
+    for (int bi = 0; bi < 2; ++bi) {
+      const uint32_t w0 = w[3 * bi], w1 = w[3 * bi + 1], w2 = w[3 * bi + 2];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        // code j at bit 3j, code j+16 at bit 3j+48 of the 96-bit block
+        const int o_lo = 3 * j, o_hi = 3 * j + 32;
+        const uint32_t lo = (o_lo < 32) ? __funnelshift_r(w0, w1, o_lo) : (w1 >> (o_lo - 32));
+        const uint32_t hi = (o_hi < 64) ? __funnelshift_r(w1, w2, o_hi - 32) : (w2 >> (o_hi - 64));
+        const uint32_t m = __byte_perm(lo, hi, 0x7610) & 0x00070007u;
+        out[16 * bi + j] = deq_pair(m, S(16 * bi + j), Z(16 * bi + j));
+      }
+    }
+  }
+}
+
+XQ_DEVINL void store_row_sw128(uint8_t* tile, int row, const uint32_t (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 q = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    *reinterpret_cast<uint4*>(tile + sw128_offset(row, c)) = q;
+  }
+}
+
+// Produce one 64-channel chunk of one row of an A stream into `tile`.
+template <int MODE, int BITS>
+XQ_DEVINL void produce_row(uint8_t* tile, int row, bool valid, int64_t arow, int tok, int b,
+                           int kc, const uint8_t* src, const void* params, int64_t row_bytes,
+                           const float* resid, int nflushed, const DecodeParams& p) {
+  uint32_t v[32];
+  if (!valid) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0u;
+  } else if constexpr (MODE == XQ_A_F16_ROWS) {
+    const uint4* s = reinterpret_cast<const uint4*>(
+        reinterpret_cast<const __half*>(src) + arow * p.kdim + kc * kChunk);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 q = s[c];
+      v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+    }
+  } else if constexpr (MODE == XQ_A_CODES_TOKEN) {
+    const int64_t ng = p.kdim / p.group_size;
+    const __half2 sz = static_cast<const __half2*>(params)[arow * ng + (kc * kChunk) / p.group_size];
+    const __half2 s2 = __low2half2(sz), z2 = __high2half2(sz);
+    dequant_chunk<BITS, false>(src + arow * row_bytes + kc * 8 * BITS, &s2, &z2, v);
+  } else {  // XQ_A_CODES_CHANNEL
+    constexpr int BS = BITS == 2 ? 16 : BITS == 3 ? 32 : BITS == 4 ? 8 : 4;
+    if (tok < nflushed) {
+      const __half* prow =
+          static_cast<const __half*>(params) + (arow / p.group_size) * 2 * p.kdim + kc * kChunk;
+      __half2 s2[32], z2[32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 a = reinterpret_cast<const uint4*>(prow)[c];
+        const uint4 z = reinterpret_cast<const uint4*>(prow + p.kdim)[c];
+        s2[4 * c] = from_u32<__half2>(a.x); s2[4 * c + 1] = from_u32<__half2>(a.y);
+        s2[4 * c + 2] = from_u32<__half2>(a.z); s2[4 * c + 3] = from_u32<__half2>(a.w);
+        z2[4 * c] = from_u32<__half2>(z.x); z2[4 * c + 1] = from_u32<__half2>(z.y);
+        z2[4 * c + 2] = from_u32<__half2>(z.z); z2[4 * c + 3] = from_u32<__half2>(z.w);
+      }
+      dequant_chunk<BITS, true>(src + arow * row_bytes + kc * 8 * BITS, s2, z2, v);
+    } else {  // residual full-precision row (cache.py:228-229)
+      const float* r = resid + ((int64_t)b * p.group_size + (tok - nflushed)) * p.kdim + kc * kChunk;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int blk = (2 * j) / BS, jj = j % (BS / 2);
+        const int c0 = blk * BS + jj, c1 = c0 + BS / 2;
+        v[j] = as_u32(__floats2half2_rn(r[c0], r[c1]));
+      }
+    }
+  }
+  store_row_sw128(tile, row, v);
+}
+
+template <int AK, int AV, int BITS, int GROUP>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_decode_attend(const __grid_constant__ CUtensorMap tmap_w, const DecodeParams p) {
+  constexpr int A_TILES = (AV == XQ_A_SAME) ? 1 : 2;
+  constexpr int STAGES = A_TILES == 1 ? 4 : 3;
+  constexpr int AVM = (AV == XQ_A_SAME) ? AK : AV;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * A_TILES * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kBBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* q_s = reinterpret_cast<float*>(tmem_slot + 4);  // [GROUP][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 4 + 1);  // 4 producer warps + the TMA expect_tx arrive
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap_w);
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nkc = p.kdim / kChunk;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (W tiles)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Unit w = get_unit(p, u);
+        for (int t = w.t0; t < w.t1; ++t)
+          for (int kc = 0; kc < nkc; ++kc, ++it) {
+            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&full[s], kBBytes);
+            tma_load_2d(sB + s * kBBytes, &tmap_w, &full[s], kc * kChunk, w.h * 256, kEvictLast);
+          }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t kIdesc256 = idesc_f16_f32(128, 256);
+      constexpr uint32_t kIdesc128 = idesc_f16_f32(128, 128);
+      uint32_t it = 0, tc = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Unit w = get_unit(p, u);
+        for (int t = w.t0; t < w.t1; ++t, ++tc) {
+          const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+          mbar_wait(&tempty[a], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + a * 256;
+          for (int kc = 0; kc < nkc; ++kc, ++it) {
+            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + s * A_TILES * kABytes);
+            const uint32_t b0 = smem_u32(sB + s * kBBytes);
+#pragma unroll
+            for (int k = 0; k < kChunk / 16; ++k) {
+              const uint32_t acc = (kc | k) != 0;
+              if constexpr (A_TILES == 1) {
+                mma_f16_ss(d, sdesc_sw128(a0 + 32 * k), sdesc_sw128(b0 + 32 * k), kIdesc256, acc);
+              } else {
+                mma_f16_ss(d, sdesc_sw128(a0 + 32 * k), sdesc_sw128(b0 + 32 * k), kIdesc128, acc);
+                mma_f16_ss(d + 128, sdesc_sw128(a0 + kABytes + 32 * k),
+                           sdesc_sw128(b0 + 128 * 128 + 32 * k), kIdesc128, acc);
+              }
+            }
+            mma_commit(&empty[s]);
+          }
+          mma_commit(&tfull[a]);
+        }
+      }
+    }
+  } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
+    // ------------------------------------------------ dequant producers
+    const int gp = (warp - kProdWarp0) >> 2;              // even / odd K-chunks
+    const int row = ((warp - kProdWarp0) & 3) * 32 + lane;  // tile row = token
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const Unit w = get_unit(p, u);
+      const int nfl = (AK == XQ_A_CODES_CHANNEL) ? p.ak_nflushed[w.b] : 0;
+      for (int t = w.t0; t < w.t1; ++t) {
+        const int tok = t * kTileM + row;
+        const bool valid = tok < w.len;
+        const int64_t arow = (int64_t)w.b * p.L_max + tok;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          if ((it & 1) != static_cast<uint32_t>(gp)) continue;
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* tile = sA + s * A_TILES * kABytes;
+          produce_row<AK, BITS>(tile, row, valid, arow, tok, w.b, kc, p.ak_src, p.ak_params,
+                                p.ak_row_bytes, p.ak_resid, nfl, p);
+          if constexpr (A_TILES == 2)
+            produce_row<AVM, BITS>(tile + kABytes, row, valid, arow, tok, w.b, kc, p.av_src,
+                                   p.av_params, p.av_row_bytes, nullptr, 0, p);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[s]);
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------ epilogue
+    const int ew = warp - kEpiWarp0;  // == warp % 4: TMEM lanes 32*ew ..
+    const int et = threadIdx.x - kEpiWarp0 * 32;
+    const int row = ew * 32 + lane;
+    const uint32_t tlane = static_cast<uint32_t>(ew * 32) << 16;
+    const int n_q = p.n_kv * GROUP;
+    uint32_t tc = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const Unit w = get_unit(p, u);
+      const int pos = w.len - 1;
+      named_bar_sync(1, 128);
+      if (pos >= 0) {
+        const float2 cs = p.rope[(int64_t)pos * 64 + (et >> 1)];
+#pragma unroll
+        for (int gi = 0; gi < GROUP; ++gi) {
+          const float* qp = p.q_pre + ((int64_t)w.b * n_q + w.h * GROUP + gi) * kHeadDim;
+          const float e0 = qp[et & ~1], e1 = qp[et | 1];
+          const float r = (et & 1) ? (e0 * cs.y + e1 * cs.x) : (e0 * cs.x - e1 * cs.y);
+          q_s[gi * kHeadDim + et] = r * p.q_scale;
+        }
+      }
+      named_bar_sync(1, 128);
+      float m_run[GROUP], l_run[GROUP], o_run[GROUP][4];
+#pragma unroll
+      for (int gi = 0; gi < GROUP; ++gi) {
+        m_run[gi] = -INFINITY;
+        l_run[gi] = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o_run[gi][c] = 0.f;
+      }
+      for (int t = w.t0; t < w.t1; ++t, ++tc) {
+        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+        mbar_wait(&tfull[a], aph);
+        tc_fence_after();
+        const int tok = t * kTileM + row;
+        const bool valid = tok < w.len;
+        const float2* rp = p.rope + (int64_t)(valid ? tok : 0) * 64;
+        float sc[GROUP];
+#pragma unroll
+        for (int gi = 0; gi < GROUP; ++gi) sc[gi] = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float kb[32];
+          tmem_ld32(tmem + tlane + a * 256 + c * 32, kb);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 cs = rp[c * 16 + i];
+            const float k0 = kb[2 * i], k1 = kb[2 * i + 1];
+            const float r0 = k0 * cs.x - k1 * cs.y;  // linalg.py:92-93
+            const float r1 = k0 * cs.y + k1 * cs.x;
+#pragma unroll
+            for (int gi = 0; gi < GROUP; ++gi) {
+              const float* qq = q_s + gi * kHeadDim + c * 32 + 2 * i;
+              sc[gi] = fmaf(qq[0], r0, fmaf(qq[1], r1, sc[gi]));
+            }
+          }
+        }
+        float pr[GROUP];
+#pragma unroll
+        for (int gi = 0; gi < GROUP; ++gi) {
+          const float s = valid ? sc[gi] : -INFINITY;
+          const float mn = fmaxf(m_run[gi], warp_max(s));
+          const float alpha = (m_run[gi] == -INFINITY) ? 0.f : exp2f(m_run[gi] - mn);
+          pr[gi] = valid ? exp2f(s - mn) : 0.f;
+          l_run[gi] = l_run[gi] * alpha + warp_sum(pr[gi]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) o_run[gi][c] *= alpha;
+          m_run[gi] = mn;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float vb[32];
+          tmem_ld32(tmem + tlane + a * 256 + 128 + c * 32, vb);
+          tmem_wait_ld();
+#pragma unroll
+          for (int gi = 0; gi < GROUP; ++gi) {
+            float tmp[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tmp[j] = pr[gi] * vb[j];
+            o_run[gi][c] += warp_reduce_scatter32(tmp, lane);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
+      }
+#pragma unroll
+      for (int gi = 0; gi < GROUP; ++gi) {
+        const int hq = w.h * GROUP + gi;
+        float* dst =
+            p.partials + ((((int64_t)w.b * n_q + hq) * p.n_chunks + w.chunk) * 4 + ew) * kPartStride;
+        if (lane == 0) {
+          dst[0] = m_run[gi];
+          dst[1] = l_run[gi];
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dst[2 + c * 32 + lane] = o_run[gi][c];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Merge split partials (m in log2 domain): out = sum_i 2^(m_i-M) o_i / sum_i 2^(m_i-M) l_i
+__global__ void k_combine(const float* __restrict__ partials, int n_parts, float* __restrict__ out) {
+  const int64_t bh = blockIdx.x;
+  const int d = threadIdx.x;
+  const float* base = partials + bh * n_parts * kPartStride;
+  float M = -INFINITY;
+  for (int i = 0; i < n_parts; ++i) M = fmaxf(M, base[(int64_t)i * kPartStride]);
+  float L = 0.f, O = 0.f;
+  if (M != -INFINITY) {
+    for (int i = 0; i < n_parts; ++i) {
+      const float m = base[(int64_t)i * kPartStride];
+      if (m == -INFINITY) continue;
+      const float wgt = exp2f(m - M);
+      L = fmaf(wgt, base[(int64_t)i * kPartStride + 1], L);
+      O = fmaf(wgt, base[(int64_t)i * kPartStride + 2 + d], O);
+    }
+  }
+  out[bh * kHeadDim + d] = L > 0.f ? O / L : 0.f;
+}
+
+// ------------------------------------------------------------ debug remat
+struct RematParams {
+  int ak_mode, av_mode, ak_bits, av_bits, group_size, nflushed, slot;
+  const void* ak_src;
+  const void* ak_params;
+  const float* ak_resid;
+  int64_t ak_row_bytes;
+  const void* av_src;
+  const void* av_params;
+  int64_t av_row_bytes;
+  int64_t L_max, kdim, n_out;
+  const float* w_k;
+  const float* w_v;
+  const float2* rope;
+  float* k_out;
+  float* v_out;
+};
+
+XQ_DEVINL uint32_t read_code_dbg(const uint8_t* row, int64_t c, int bits) {
+  const int64_t off = c * bits;
+  const int64_t byte = off >> 3;
+  const int sh = off & 7;
+  uint32_t v = row[byte];
+  if (sh + bits > 8) v |= static_cast<uint32_t>(row[byte + 1]) << 8;
+  return (v >> sh) & ((1u << bits) - 1);
+}
+
+XQ_DEVINL float deq_natural(int mode, int bits, const void* src, const void* params,
+                            const float* resid, int64_t row_bytes, int G, int64_t kdim,
+                            int64_t L_max, int slot, int t, int nflushed, int64_t c) {
+  const int64_t arow = (int64_t)slot * L_max + t;
+  if (mode == XQ_A_F16_ROWS)
+    return __half2float(static_cast<const __half*>(src)[arow * kdim + c]);
+  if (mode == XQ_A_CODES_TOKEN) {
+    const uint32_t code = read_code_dbg(static_cast<const uint8_t*>(src) + arow * row_bytes, c, bits);
+    const __half2 sz = static_cast<const __half2*>(params)[arow * (kdim / G) + c / G];
+    return fmaf(static_cast<float>(code), __low2float(sz), __high2float(sz));
+  }
+  if (t >= nflushed) return resid[((int64_t)slot * G + (t - nflushed)) * kdim + c];
+  const uint32_t code = read_code_dbg(static_cast<const uint8_t*>(src) + arow * row_bytes, c, bits);
+  const int bs = perm_block(XQ_A_CODES_CHANNEL, bits);
+  const int64_t pos = (c / bs) * bs + perm_position(static_cast<int>(c % bs), bs);
+  const __half* prow = static_cast<const __half*>(params) + (arow / G) * 2 * kdim;
+  return fmaf(static_cast<float>(code), __half2float(prow[pos]), __half2float(prow[kdim + pos]));
+}
+
+__global__ void k_remat_f32(const RematParams p) {
+  extern __shared__ float sh[];
+  float* xk = sh;
+  float* xv = sh + p.kdim;
+  float* kp = sh + 2 * p.kdim;
+  const int t = blockIdx.x;
+  const bool same = p.av_mode == XQ_A_SAME;
+  for (int64_t c = threadIdx.x; c < p.kdim; c += blockDim.x) {
+    xk[c] = deq_natural(p.ak_mode, p.ak_bits, p.ak_src, p.ak_params, p.ak_resid, p.ak_row_bytes,
+                        p.group_size, p.kdim, p.L_max, p.slot, t, p.nflushed, c);
+    xv[c] = same ? xk[c]
+                 : deq_natural(p.av_mode, p.av_bits, p.av_src, p.av_params, nullptr,
+                               p.av_row_bytes, p.group_size, p.kdim, p.L_max, p.slot, t, 1 << 30, c);
+  }
+  __syncthreads();
+  for (int64_t n = threadIdx.x; n < p.n_out; n += blockDim.x) {
+    float ak = 0.f, av = 0.f;
+    for (int64_t c = 0; c < p.kdim; ++c) {
+      ak = fmaf(xk[c], p.w_k[c * p.n_out + n], ak);
+      av = fmaf(xv[c], p.w_v[c * p.n_out + n], av);
+    }
+    kp[n] = ak;
+    p.v_out[(int64_t)t * p.n_out + n] = av;
+  }
+  __syncthreads();
+  for (int64_t n = threadIdx.x; n < p.n_out; n += blockDim.x) {
+    const float2 cs = p.rope[(int64_t)t * 64 + (n % kHeadDim) / 2];
+    const float e0 = kp[n & ~1ll], e1 = kp[n | 1];
+    p.k_out[(int64_t)t * p.n_out + n] = (n & 1) ? (e0 * cs.y + e1 * cs.x) : (e0 * cs.x - e1 * cs.y);
+  }
+}
+
+// ------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+static int64_t n_chunks_for(int32_t max_len, int32_t tpc) {
+  const int64_t nt = (max_len + kTileM - 1) / kTileM;
+  return nt == 0 ? 1 : (nt + tpc - 1) / tpc;
+}
+
+template <int AK, int AV, int BITS, int GROUP>
+static int launch_decode(const CUtensorMap& tmap, const DecodeParams& p, cudaStream_t st) {
+  constexpr int A_TILES = (AV == XQ_A_SAME) ? 1 : 2;
+  constexpr int STAGES = A_TILES == 1 ? 4 : 3;
+  constexpr size_t smem = 1024 + STAGES * (A_TILES * kABytes + kBBytes) + 2 * STAGES * 8 + 4 * 8 +
+                          16 + GROUP * kHeadDim * 4;
+  auto kern = k_decode_attend<AK, AV, BITS, GROUP>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return check_launch("cudaFuncSetAttribute(decode)");
+    configured = true;
+  }
+  const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
+  kern<<<grid, kThreads, smem, st>>>(tmap, p);
+  return check_launch("k_decode_attend");
+}
+
+template <int AK, int AV, int GROUP>
+static int dispatch_bits(int bits, const CUtensorMap& tmap, const DecodeParams& p,
+                         cudaStream_t st) {
+  switch (bits) {
+    case 2: return launch_decode<AK, AV, 2, GROUP>(tmap, p, st);
+    case 3: return launch_decode<AK, AV, 3, GROUP>(tmap, p, st);
+    case 4: return launch_decode<AK, AV, 4, GROUP>(tmap, p, st);
+    case 8: return launch_decode<AK, AV, 8, GROUP>(tmap, p, st);
+    default: return fail(XQ_ECONFIG, "unsupported bits %d", bits);
+  }
+}
+
+}  // namespace xq
+
+using namespace xq;
+
+extern "C" {
+
+int64_t xq_decode_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_kv_heads,
+                                  int32_t group, int32_t tiles_per_chunk) {
+  if (tiles_per_chunk < 1) tiles_per_chunk = 1;
+  return (int64_t)n_seqs * n_kv_heads * group * n_chunks_for(max_len, tiles_per_chunk) * 4 *
+         kPartStride * sizeof(float);
+}
+
+int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                     const float* ak_resid, const int32_t* ak_nflushed, int32_t ak_bits,
+                     int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
+                     const void* av_params, int32_t av_bits, int64_t av_row_bytes,
+                     int32_t group_size, int64_t L_max, int64_t kdim, const int32_t* seq_lens,
+                     int32_t n_seqs, int32_t max_len, const void* w_arranged, int32_t n_kv_heads,
+                     int32_t group, const float* q_pre, const void* rope_cs, float sm_scale,
+                     int32_t tiles_per_chunk, void* workspace, int64_t workspace_bytes,
+                     float* out, void* stream) {
+  XQ_REQUIRE(kdim % kChunk == 0 && kdim >= kChunk, XQ_ESHAPE,
+             "kdim must be a positive multiple of 64, got %lld", (long long)kdim);
+  XQ_REQUIRE(group_size % kChunk == 0, XQ_ECONFIG,
+             "fused kernel needs group_size a multiple of 64, got %d", group_size);
+  XQ_REQUIRE(tiles_per_chunk >= 1, XQ_ECONFIG, "tiles_per_chunk must be >= 1");
+  XQ_REQUIRE(n_seqs >= 1 && n_kv_heads >= 1, XQ_ESHAPE, "empty batch");
+  XQ_REQUIRE(max_len <= L_max, XQ_ESHAPE, "max_len > L_max");
+  XQ_REQUIRE(workspace_bytes >= xq_decode_workspace_bytes(n_seqs, max_len, n_kv_heads, group,
+                                                          tiles_per_chunk),
+             XQ_ESHAPE, "workspace too small");
+  const bool mha = av_mode == XQ_A_SAME;
+  if (!mha) {
+    XQ_REQUIRE(ak_mode == XQ_A_CODES_CHANNEL && av_mode == XQ_A_CODES_TOKEN, XQ_ECONFIG,
+               "split K/V A operands support (CODES_CHANNEL, CODES_TOKEN) only");
+    XQ_REQUIRE(ak_bits == av_bits, XQ_ECONFIG, "K and V latent bits must match");
+    XQ_REQUIRE(L_max % group_size == 0 && group_size == kTileM, XQ_ECONFIG,
+               "per-channel K latent needs group_size 128 and L_max % 128 == 0");
+  } else {
+    XQ_REQUIRE(ak_mode == XQ_A_CODES_TOKEN || ak_mode == XQ_A_F16_ROWS, XQ_ECONFIG,
+               "shared A operand must be CODES_TOKEN or F16_ROWS");
+  }
+  XQ_REQUIRE(ak_mode == XQ_A_F16_ROWS || valid_bits(ak_bits), XQ_ECONFIG, "bad bits %d", ak_bits);
+  auto enc = encode_fn();
+  XQ_REQUIRE(enc != nullptr, XQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+
+  CUtensorMap tmap;
+  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(kdim), static_cast<cuuint64_t>(n_kv_heads) * 256};
+  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(kdim) * 2};
+  const cuuint32_t box[2] = {kChunk, 256};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(w_arranged), gdim,
+                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  XQ_REQUIRE(r == CUDA_SUCCESS, XQ_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+
+  DecodeParams p;
+  p.ak_src = static_cast<const uint8_t*>(ak_src);
+  p.ak_params = ak_params;
+  p.ak_resid = ak_resid;
+  p.ak_nflushed = ak_nflushed;
+  p.ak_row_bytes = ak_row_bytes;
+  p.av_src = static_cast<const uint8_t*>(mha ? ak_src : av_src);
+  p.av_params = mha ? ak_params : av_params;
+  p.av_row_bytes = mha ? ak_row_bytes : av_row_bytes;
+  p.group_size = group_size;
+  p.L_max = L_max;
+  p.kdim = static_cast<int32_t>(kdim);
+  p.seq_lens = seq_lens;
+  p.tiles_per_chunk = tiles_per_chunk;
+  p.n_chunks = static_cast<int32_t>(n_chunks_for(max_len, tiles_per_chunk));
+  p.n_kv = n_kv_heads;
+  p.n_units = n_seqs * p.n_chunks * n_kv_heads;
+  p.q_pre = q_pre;
+  p.rope = static_cast<const float2*>(rope_cs);
+  p.q_scale = sm_scale * 1.4426950408889634f;
+  p.partials = static_cast<float*>(workspace);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  int status;
+  if (mha) {
+    XQ_REQUIRE(group == 1, XQ_ECONFIG, "MHA (shared A) needs group 1, got %d", group);
+    if (ak_mode == XQ_A_F16_ROWS)
+      status = launch_decode<XQ_A_F16_ROWS, XQ_A_SAME, 4, 1>(tmap, p, st);
+    else
+      status = dispatch_bits<XQ_A_CODES_TOKEN, XQ_A_SAME, 1>(ak_bits, tmap, p, st);
+  } else {
+    switch (group) {
+      case 1: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 1>(ak_bits, tmap, p, st); break;
+      case 2: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 2>(ak_bits, tmap, p, st); break;
+      case 4: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 4>(ak_bits, tmap, p, st); break;
+      default: return fail(XQ_ECONFIG, "unsupported GQA group %d (1, 2, 4)", group);
+    }
+  }
+  if (status != XQ_OK) return status;
+  const int n_parts = p.n_chunks * 4;
+  k_combine<<<static_cast<unsigned>(n_seqs) * n_kv_heads * group, kHeadDim, 0, st>>>(
+      p.partials, n_parts, out);
+  return check_launch("k_combine");
+}
+
+int xq_remat_f32(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                 const float* ak_resid, int32_t ak_nflushed, int32_t ak_bits,
+                 int64_t ak_row_bytes, int32_t av_mode, const void* av_src, const void* av_params,
+                 int32_t av_bits, int64_t av_row_bytes, int32_t group_size, int64_t L_max,
+                 int64_t kdim, int32_t slot, int32_t n_tok, const float* w_k, const float* w_v,
+                 int64_t n_out, const void* rope_cs, float* k_out, float* v_out, void* stream) {
+  XQ_REQUIRE(n_out % kHeadDim == 0, XQ_ESHAPE, "n_out must be a multiple of 128");
+  XQ_REQUIRE(2 * kdim + n_out <= 48 * 1024, XQ_ESHAPE, "debug remat: shapes too large");
+  if (n_tok == 0) return XQ_OK;
+  RematParams p;
+  p.ak_mode = ak_mode; p.av_mode = av_mode; p.ak_bits = ak_bits; p.av_bits = av_bits;
+  p.group_size = group_size; p.nflushed = ak_nflushed; p.slot = slot;
+  p.ak_src = ak_src; p.ak_params = ak_params; p.ak_resid = ak_resid; p.ak_row_bytes = ak_row_bytes;
+  p.av_src = av_src; p.av_params = av_params; p.av_row_bytes = av_row_bytes;
+  p.L_max = L_max; p.kdim = kdim; p.n_out = n_out; p.w_k = w_k; p.w_v = w_v;
+  p.rope = static_cast<const float2*>(rope_cs); p.k_out = k_out; p.v_out = v_out;
+  const size_t smem = (2 * kdim + n_out) * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_remat_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_remat_f32<<<n_tok, 256, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return check_launch("k_remat_f32");
+}
+
+}  // extern "C"

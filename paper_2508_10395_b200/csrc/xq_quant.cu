@@ -1,0 +1,501 @@
+// Quantizer, bit packing, arena append/dequant, RoPE table, weight
+// arrangement and the XQuant-CL accumulator -- sm_100a.
+//
+// Arithmetic contract (bit-exact with the reference quantizer,
+// _native.pyx:111-153 / fallback.py:108-131): group min/max on the exactly
+// upcast float64 inputs, scale = (max-min)/(2^e-1) (1.0 for a degenerate
+// group), code = clamp(floor((x-min)/scale + 0.5), 0, 2^e-1), every step an
+// IEEE float64 op with explicit rounding intrinsics so nvcc cannot contract.
+#include <math.h>
+
+#include "xq_common.cuh"
+#include "xq_host.h"
+#include "xq_layout.cuh"
+
+namespace xq {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+// ------------------------------------------------------------------ device
+
+XQ_DEVINL double load_as_f64(const void* base, int dt, int64_t i) {
+  switch (dt) {
+    case XQ_F32: return static_cast<double>(static_cast<const float*>(base)[i]);
+    case XQ_BF16:
+      return static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]));
+    case XQ_F16: return static_cast<double>(__half2float(static_cast<const __half*>(base)[i]));
+    default: return static_cast<const double*>(base)[i];
+  }
+}
+
+XQ_DEVINL double shfl_xor_d(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+
+// Quantize one row (block-cooperative: warps over groups, lanes over
+// elements). Codes land in `codes_out` (shared or global bytes); the group
+// parameters are handed to `sink(g, scale, zp)` by lane 0 of the owning warp.
+template <class Sink>
+__device__ void quantize_row(const void* x, int dt, int64_t x_off, int64_t cols, int G, int bits,
+                             const float* sub, uint8_t* codes_out, double* x_eff, int* bad,
+                             Sink sink) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int64_t ngroups = (cols + G - 1) / G;
+  const double qmax = static_cast<double>((1 << bits) - 1);
+  for (int64_t g = warp; g < ngroups; g += nw) {
+    const int64_t lo = g * G;
+    const int64_t hi = min(lo + G, cols);
+    double mn = INFINITY, mx = -INFINITY;
+    bool finite = true;
+    for (int64_t j = lo + lane; j < hi; j += 32) {
+      double v = load_as_f64(x, dt, x_off + j);
+      if (sub) v = __dsub_rn(v, static_cast<double>(sub[j]));
+      finite &= isfinite(v);
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, shfl_xor_d(mn, o));
+      mx = fmax(mx, shfl_xor_d(mx, o));
+    }
+    if (!__all_sync(0xffffffffu, finite) && lane == 0) *bad = 1;
+    const double span = __dsub_rn(mx, mn);
+    const double scale = (span == 0.0) ? 1.0 : __ddiv_rn(span, qmax);
+    if (lane == 0) sink(g, scale, mn);
+    for (int64_t j = lo + lane; j < hi; j += 32) {
+      double v = load_as_f64(x, dt, x_off + j);
+      if (sub) v = __dsub_rn(v, static_cast<double>(sub[j]));
+      double q = floor(__dadd_rn(__ddiv_rn(__dsub_rn(v, mn), scale), 0.5));
+      q = q < 0.0 ? 0.0 : (q > qmax ? qmax : q);
+      codes_out[j] = static_cast<uint8_t>(q);
+      if (x_eff) x_eff[j] = v;
+    }
+  }
+}
+
+// 32-bit word w of the LSB-first stream of `n` codes of `bits` bits.
+XQ_DEVINL uint32_t stream_word32(const uint8_t* codes, int64_t n, int bits, int64_t w) {
+  const int64_t b0 = w * 32;
+  int64_t i0 = b0 / bits;
+  int64_t i1 = (b0 + 31) / bits;
+  if (i1 > n - 1) i1 = n - 1;
+  uint32_t word = 0;
+  for (int64_t i = i0; i <= i1; ++i) {
+    const int64_t off = i * bits - b0;
+    const uint32_t c = codes[i];
+    word |= off >= 0 ? (c << off) : (c >> (-off));
+  }
+  return word;
+}
+
+__global__ void k_quantize_groups(const double* __restrict__ x, int64_t cols, int G, int bits,
+                                  uint8_t* __restrict__ codes, double* __restrict__ scales,
+                                  double* __restrict__ zps) {
+  const int64_t r = blockIdx.x;
+  const int64_t ng = (cols + G - 1) / G;
+  int bad = 0;
+  quantize_row(x, XQ_F64, r * cols, cols, G, bits, nullptr, codes + r * cols, nullptr, &bad,
+               [&](int64_t g, double s, double z) {
+                 scales[r * ng + g] = s;
+                 zps[r * ng + g] = z;
+               });
+}
+
+__global__ void k_dequantize_groups(const uint8_t* __restrict__ codes,
+                                    const double* __restrict__ scales,
+                                    const double* __restrict__ zps, int64_t rows, int64_t cols,
+                                    int G, double* __restrict__ out) {
+  const int64_t ng = (cols + G - 1) / G;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * cols;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const int64_t p = r * ng + c / G;
+    out[i] = __dadd_rn(__dmul_rn(static_cast<double>(codes[i]), scales[p]), zps[p]);
+  }
+}
+
+__global__ void k_pack(const uint8_t* __restrict__ codes, int64_t n, int bits,
+                       uint64_t* __restrict__ words, int64_t n_words) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t lo = stream_word32(codes, n, bits, 2 * w);
+    const uint64_t hi = stream_word32(codes, n, bits, 2 * w + 1);
+    words[w] = lo | (hi << 32);
+  }
+}
+
+__global__ void k_unpack(const uint64_t* __restrict__ words, int bits, int64_t n,
+                         uint8_t* __restrict__ codes) {
+  const uint64_t mask = (1ull << bits) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t off = static_cast<uint64_t>(i) * bits;
+    const int64_t w = off >> 6;
+    const int s = off & 63;
+    uint64_t v = words[w] >> s;
+    if (s + bits > 64) v |= words[w + 1] << (64 - s);
+    codes[i] = static_cast<uint8_t>(v & mask);
+  }
+}
+
+__global__ void k_quantize_rows(const void* __restrict__ x, int dt, int64_t x_stride,
+                                int64_t cols, int G, int bits, const int32_t* __restrict__ lens,
+                                int64_t row0, int64_t L_max, const float* __restrict__ sub_rows,
+                                uint8_t* __restrict__ codes, int64_t row_bytes,
+                                __half2* __restrict__ params, double* __restrict__ x_eff,
+                                int32_t* __restrict__ flag) {
+  extern __shared__ uint8_t s_codes[];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  const int64_t i = blockIdx.x;
+  const int64_t dst = lens ? i * L_max + (lens[i] - 1) : row0 + i;
+  const int64_t ng = (cols + G - 1) / G;
+  int bad = 0;
+  quantize_row(x, dt, i * x_stride, cols, G, bits, sub_rows ? sub_rows + dst * cols : nullptr,
+               s_codes, x_eff ? x_eff + i * cols : nullptr, &bad,
+               [&](int64_t g, double s, double z) {
+                 params[dst * ng + g] = __halves2half2(__double2half(s), __double2half(z));
+               });
+  if (bad) s_bad = 1;
+  __syncthreads();
+  uint32_t* out = reinterpret_cast<uint32_t*>(codes + dst * row_bytes);
+  for (int64_t w = threadIdx.x; w < row_bytes / 4; w += blockDim.x)
+    out[w] = stream_word32(s_codes, cols, bits, w);
+  if (threadIdx.x == 0 && s_bad && flag) atomicExch(flag, 1);
+}
+
+// One CTA per (block, 32-channel slice): per-channel min/max over the G rows.
+__global__ void k_quantize_blocks_per_channel(const float* __restrict__ blocks, int64_t cols,
+                                              int bits, int G, const int64_t* __restrict__ dst0,
+                                              uint8_t* __restrict__ codes, int64_t row_bytes,
+                                              __half* __restrict__ params,
+                                              int32_t* __restrict__ flag) {
+  extern __shared__ uint8_t s_codes[];  // [G][32]
+  __shared__ double s_mn[4][32], s_mx[4][32];
+  __shared__ double s_scale[32], s_zp[32];
+  __shared__ int s_bad;
+  const int b = blockIdx.x, slice = blockIdx.y;
+  const int c = threadIdx.x & 31, part = threadIdx.x >> 5;
+  const int64_t ch = (int64_t)slice * 32 + c;
+  const float* blk = blocks + (int64_t)b * G * cols;
+  if (threadIdx.x == 0) s_bad = 0;
+  double mn = INFINITY, mx = -INFINITY;
+  bool finite = true;
+  for (int r = part; r < G; r += 4) {
+    const double v = static_cast<double>(blk[(int64_t)r * cols + ch]);
+    finite &= isfinite(v);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  s_mn[part][c] = mn;
+  s_mx[part][c] = mx;
+  __syncthreads();
+  if (!finite) s_bad = 1;
+  const double qmax = static_cast<double>((1 << bits) - 1);
+  if (part == 0) {
+    for (int p = 1; p < 4; ++p) {
+      mn = fmin(mn, s_mn[p][c]);
+      mx = fmax(mx, s_mx[p][c]);
+    }
+    const double span = __dsub_rn(mx, mn);
+    const double scale = (span == 0.0) ? 1.0 : __ddiv_rn(span, qmax);
+    s_scale[c] = scale;
+    s_zp[c] = mn;
+    // planar [token group][2][cols] halves in producer channel order (xq_layout.cuh)
+    const int bs = perm_block(XQ_A_CODES_CHANNEL, bits);
+    const int64_t pos = (int64_t)slice * 32 + (c / bs) * bs + perm_position(c % bs, bs);
+    __half* prow = params + (dst0[b] / G) * 2 * cols;
+    prow[pos] = __double2half(scale);
+    prow[cols + pos] = __double2half(mn);
+  }
+  __syncthreads();
+  const double scale = s_scale[c], zp = s_zp[c];
+  for (int r = part; r < G; r += 4) {
+    const double v = static_cast<double>(blk[(int64_t)r * cols + ch]);
+    double q = floor(__dadd_rn(__ddiv_rn(__dsub_rn(v, zp), scale), 0.5));
+    q = q < 0.0 ? 0.0 : (q > qmax ? qmax : q);
+    s_codes[r * 32 + c] = static_cast<uint8_t>(q);
+  }
+  __syncthreads();
+  // row r of this slice: 32 codes -> `bits` 32-bit words at byte 4*bits*slice
+  for (int idx = threadIdx.x; idx < G * bits; idx += blockDim.x) {
+    const int r = idx / bits, w = idx % bits;
+    uint32_t* out = reinterpret_cast<uint32_t*>(codes + (dst0[b] + r) * row_bytes +
+                                                (int64_t)slice * 4 * bits);
+    out[w] = stream_word32(s_codes + r * 32, 32, bits, w);
+  }
+  if (threadIdx.x == 0 && s_bad && flag) atomicExch(flag, 1);
+}
+
+XQ_DEVINL uint32_t read_code(const uint8_t* row, int64_t c, int bits) {
+  const int64_t off = c * bits;
+  const int64_t byte = off >> 3;
+  const int sh = off & 7;
+  uint32_t v = row[byte];
+  if (sh + bits > 8) v |= static_cast<uint32_t>(row[byte + 1]) << 8;
+  return (v >> sh) & ((1u << bits) - 1);
+}
+
+// (scale, zp) of element (arena row r, channel c): per-token half2 grid, or the
+// planar permuted per-channel layout written by k_quantize_blocks_per_channel.
+XQ_DEVINL float2 load_params(const void* params, int axis, int bits, int G, int64_t cols,
+                             int64_t r, int64_t c) {
+  if (axis == 0) {
+    const int64_t ng = (cols + G - 1) / G;
+    const __half2 p = static_cast<const __half2*>(params)[r * ng + c / G];
+    return make_float2(__low2float(p), __high2float(p));
+  }
+  const int bs = perm_block(XQ_A_CODES_CHANNEL, bits);
+  const int64_t pos = (c / bs) * bs + perm_position(static_cast<int>(c % bs), bs);
+  const __half* prow = static_cast<const __half*>(params) + (r / G) * 2 * cols;
+  return make_float2(__half2float(prow[pos]), __half2float(prow[cols + pos]));
+}
+
+__global__ void k_dequant_rows(const uint8_t* __restrict__ codes, int64_t row_bytes,
+                               const void* __restrict__ params, int axis, int bits, int G,
+                               int64_t cols, int64_t row0, int64_t n_rows,
+                               float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows * cols;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = row0 + i / cols, c = i % cols;
+    const uint32_t code = read_code(codes + r * row_bytes, c, bits);
+    const float2 p = load_params(params, axis, bits, G, cols, r, c);
+    out[i] = fmaf(static_cast<float>(code), p.x, p.y);
+  }
+}
+
+__global__ void k_rope_table(float2* __restrict__ cs, int64_t n_pos, int hd, double theta) {
+  const int half = hd / 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pos * half;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = i / half;
+    const int j = i % half;
+    const double freq = pow(theta, (-2.0 * j) / hd);  // linalg.py:85
+    const double ang = static_cast<double>(pos) * freq;  // linalg.py:86
+    cs[i] = make_float2(static_cast<float>(cos(ang)), static_cast<float>(sin(ang)));
+  }
+}
+
+XQ_DEVINL float load_as_f32(const void* base, int dt, int64_t i) {
+  switch (dt) {
+    case XQ_F32: return static_cast<const float*>(base)[i];
+    case XQ_BF16: return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]);
+    case XQ_F16: return __half2float(static_cast<const __half*>(base)[i]);
+    default: return static_cast<float>(static_cast<const double*>(base)[i]);
+  }
+}
+
+__global__ void k_arrange_weights(const void* __restrict__ w_k, const void* __restrict__ w_v,
+                                  int dt, int64_t kdim, int n_kv, int bs_k, int bs_v,
+                                  __half* __restrict__ out) {
+  const int64_t ld = (int64_t)n_kv * 128;
+  const int64_t total = (int64_t)n_kv * 256 * kdim;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i % kdim;
+    const int64_t rowi = i / kdim;
+    const int h = static_cast<int>(rowi / 256), n = static_cast<int>(rowi % 256);
+    const bool is_k = n < 128;
+    const int bs = is_k ? bs_k : bs_v;
+    const int64_t k = (p / bs) * bs + perm_channel(static_cast<int>(p % bs), bs);
+    const int64_t col = (int64_t)h * 128 + (is_k ? n : n - 128);
+    out[i] = __float2half_rn(load_as_f32(is_k ? w_k : w_v, dt, k * ld + col));
+  }
+}
+
+// XQuant-CL accumulator: one CTA per (slot, token); each thread 8 channels.
+__global__ void k_cl_accumulate(int seed, const uint8_t* __restrict__ codes, int64_t row_bytes,
+                                const __half2* __restrict__ params, int bits, int G, int64_t cols,
+                                const int32_t* __restrict__ lens, int32_t max_len, int64_t L_max,
+                                float* __restrict__ acc, __half* __restrict__ x16) {
+  const int b = blockIdx.x / max_len, t = blockIdx.x % max_len;
+  if (t >= lens[b]) return;
+  const int64_t r = (int64_t)b * L_max + t;
+  const int64_t ng = (cols + G - 1) / G;
+  const uint8_t* crow = codes + r * row_bytes;
+  for (int64_t c0 = (int64_t)threadIdx.x * 8; c0 < cols; c0 += (int64_t)blockDim.x * 8) {
+    uint64_t packed = 0;  // 8 codes = `bits` bytes, starting at byte bits*c0/8
+    const uint8_t* src = crow + (c0 / 8) * bits;
+    for (int k = 0; k < bits; ++k) packed |= static_cast<uint64_t>(src[k]) << (8 * k);
+    float4* a4 = reinterpret_cast<float4*>(acc + r * cols + c0);
+    float v[8];
+    if (seed) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = 0.f;
+    } else {
+      const float4 p0 = a4[0], p1 = a4[1];
+      v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
+      v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
+    }
+    const uint32_t mask = (1u << bits) - 1;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const __half2 p = params[r * ng + (c0 + k) / G];
+      const float code = static_cast<float>((packed >> (k * bits)) & mask);
+      v[k] += fmaf(code, __low2float(p), __high2float(p));
+    }
+    a4[0] = make_float4(v[0], v[1], v[2], v[3]);
+    a4[1] = make_float4(v[4], v[5], v[6], v[7]);
+    if (x16) {
+      __half2 h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = __floats2half2_rn(v[2 * k], v[2 * k + 1]);
+      *reinterpret_cast<uint4*>(x16 + r * cols + c0) = *reinterpret_cast<uint4*>(h);
+    }
+  }
+}
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace xq
+
+using namespace xq;
+
+extern "C" {
+
+const char* xq_version(void) { return "xquant-b200 0.1 (sm_100a)"; }
+const char* xq_last_error(void) { return g_err; }
+
+int xq_quantize_groups(const double* x, int64_t rows, int64_t cols, int32_t group_size,
+                       int32_t bits, uint8_t* codes, double* scales, double* zero_points,
+                       void* stream) {
+  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bits must be one of (2, 3, 4, 8), got %d", bits);
+  XQ_REQUIRE(group_size >= 1, XQ_ECONFIG, "group_size must be >= 1, got %d", group_size);
+  XQ_REQUIRE(rows >= 0 && cols >= 0, XQ_ESHAPE, "negative shape");
+  if (rows == 0 || cols == 0) return XQ_OK;
+  XQ_REQUIRE(rows < (1ll << 31), XQ_ESHAPE, "too many rows");
+  k_quantize_groups<<<static_cast<unsigned>(rows), 128, 0, (cudaStream_t)stream>>>(
+      x, cols, group_size, bits, codes, scales, zero_points);
+  return check_launch("xq_quantize_groups");
+}
+
+int xq_dequantize_groups(const uint8_t* codes, const double* scales, const double* zero_points,
+                         int64_t rows, int64_t cols, int32_t group_size, double* out,
+                         void* stream) {
+  XQ_REQUIRE(group_size >= 1, XQ_ECONFIG, "group_size must be >= 1");
+  if (rows * cols == 0) return XQ_OK;
+  k_dequantize_groups<<<grid_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
+      codes, scales, zero_points, rows, cols, group_size, out);
+  return check_launch("xq_dequantize_groups");
+}
+
+int xq_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint64_t* words, void* stream) {
+  XQ_REQUIRE(bits >= 1 && bits <= 8, XQ_ECONFIG, "bits must be in 1..8, got %d", bits);
+  const int64_t n_words = (n * bits + 63) / 64;
+  if (n_words == 0) return XQ_OK;
+  k_pack<<<grid_for(n_words, 256), 256, 0, (cudaStream_t)stream>>>(codes, n, bits, words,
+                                                                    n_words);
+  return check_launch("xq_pack_codes");
+}
+
+int xq_unpack_codes(const uint64_t* words, int32_t bits, int64_t n, uint8_t* codes,
+                    void* stream) {
+  XQ_REQUIRE(bits >= 1 && bits <= 8, XQ_ECONFIG, "bits must be in 1..8, got %d", bits);
+  if (n == 0) return XQ_OK;
+  k_unpack<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(words, bits, n, codes);
+  return check_launch("xq_unpack_codes");
+}
+
+int xq_quantize_rows(const void* x, int32_t x_dtype, int64_t x_row_stride, int64_t n_rows,
+                     int64_t cols, int32_t bits, int32_t group_size, const int32_t* seq_lens,
+                     int64_t row0, int64_t L_max, const float* sub_rows, uint8_t* codes,
+                     int64_t row_bytes, void* params, double* x_eff_out, int32_t* nonfinite_flag,
+                     void* stream) {
+  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bits must be one of (2, 3, 4, 8), got %d", bits);
+  XQ_REQUIRE(group_size >= 1, XQ_ECONFIG, "group_size must be >= 1");
+  XQ_REQUIRE(dtype_size(x_dtype) > 0, XQ_ECONFIG, "unknown dtype %d", x_dtype);
+  XQ_REQUIRE(row_bytes == row_bytes_for(cols, bits), XQ_ESHAPE,
+             "row_bytes %lld != ceil(cols*bits/64)*8 = %lld", (long long)row_bytes,
+             (long long)row_bytes_for(cols, bits));
+  XQ_REQUIRE(cols <= 48 * 1024, XQ_ESHAPE, "cols %lld too wide for one CTA", (long long)cols);
+  if (n_rows == 0 || cols == 0) return XQ_OK;
+  k_quantize_rows<<<static_cast<unsigned>(n_rows), 128, static_cast<size_t>(cols),
+                    (cudaStream_t)stream>>>(x, x_dtype, x_row_stride, cols, group_size, bits,
+                                            seq_lens, row0, L_max, sub_rows, codes, row_bytes,
+                                            static_cast<__half2*>(params), x_eff_out,
+                                            nonfinite_flag);
+  return check_launch("xq_quantize_rows");
+}
+
+int xq_quantize_blocks_per_channel(const float* blocks, int64_t n_blocks, int64_t cols,
+                                   int32_t bits, int32_t group_size, const int64_t* dst_row0,
+                                   uint8_t* codes, int64_t row_bytes, void* params,
+                                   int32_t* nonfinite_flag, void* stream) {
+  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bits must be one of (2, 3, 4, 8), got %d", bits);
+  XQ_REQUIRE(cols % 32 == 0, XQ_ESHAPE, "per-channel width must be a multiple of 32");
+  XQ_REQUIRE(group_size >= 1 && group_size <= 1024, XQ_ECONFIG, "bad group_size");
+  XQ_REQUIRE(row_bytes == row_bytes_for(cols, bits), XQ_ESHAPE, "bad row_bytes");
+  if (n_blocks == 0) return XQ_OK;
+  dim3 grid(static_cast<unsigned>(n_blocks), static_cast<unsigned>(cols / 32));
+  k_quantize_blocks_per_channel<<<grid, 128, static_cast<size_t>(group_size) * 32,
+                                  (cudaStream_t)stream>>>(blocks, cols, bits, group_size,
+                                                          dst_row0, codes, row_bytes,
+                                                          static_cast<__half*>(params),
+                                                          nonfinite_flag);
+  return check_launch("xq_quantize_blocks_per_channel");
+}
+
+int xq_dequant_rows(const uint8_t* codes, int64_t row_bytes, const void* params, int32_t axis,
+                    int32_t bits, int32_t group_size, int64_t cols, int64_t row0, int64_t n_rows,
+                    float* out, void* stream) {
+  XQ_REQUIRE(bits >= 1 && bits <= 8, XQ_ECONFIG, "bad bits");
+  XQ_REQUIRE(axis == 0 || axis == 1, XQ_ECONFIG, "axis must be 0 or 1");
+  if (n_rows * cols == 0) return XQ_OK;
+  k_dequant_rows<<<grid_for(n_rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
+      codes, row_bytes, params, axis, bits, group_size, cols, row0, n_rows, out);
+  return check_launch("xq_dequant_rows");
+}
+
+int xq_rope_table(void* cs_out, int64_t n_pos, int32_t head_dim, double theta, void* stream) {
+  XQ_REQUIRE(head_dim % 2 == 0, XQ_ECONFIG, "head_dim must be even, got %d", head_dim);
+  if (n_pos == 0) return XQ_OK;
+  k_rope_table<<<grid_for(n_pos * head_dim / 2, 256), 256, 0, (cudaStream_t)stream>>>(
+      static_cast<float2*>(cs_out), n_pos, head_dim, theta);
+  return check_launch("xq_rope_table");
+}
+
+int xq_arrange_weights(const void* w_k, const void* w_v, int32_t w_dtype, int64_t kdim,
+                       int32_t n_kv_heads, int32_t a_mode_k, int32_t bits_k, int32_t a_mode_v,
+                       int32_t bits_v, void* w_out, void* stream) {
+  XQ_REQUIRE(kdim % 64 == 0, XQ_ESHAPE, "kdim must be a multiple of 64, got %lld",
+             (long long)kdim);
+  XQ_REQUIRE(dtype_size(w_dtype) > 0, XQ_ECONFIG, "unknown dtype");
+  if (a_mode_v == XQ_A_SAME) {
+    a_mode_v = a_mode_k;
+    bits_v = bits_k;
+  }
+  const int bs_k = perm_block(a_mode_k, bits_k), bs_v = perm_block(a_mode_v, bits_v);
+  const int64_t total = (int64_t)n_kv_heads * 256 * kdim;
+  k_arrange_weights<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+      w_k, w_v, w_dtype, kdim, n_kv_heads, bs_k, bs_v, static_cast<__half*>(w_out));
+  return check_launch("xq_arrange_weights");
+}
+
+int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, const void* params,
+                     int32_t bits, int32_t group_size, int64_t cols, const int32_t* seq_lens,
+                     int32_t n_seqs, int32_t max_len, int64_t L_max, float* acc, void* x16_out,
+                     void* stream) {
+  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bad bits %d", bits);
+  XQ_REQUIRE(cols % 8 == 0, XQ_ESHAPE, "cols must be a multiple of 8");
+  XQ_REQUIRE(max_len <= L_max, XQ_ESHAPE, "max_len > L_max");
+  if (n_seqs == 0 || max_len == 0) return XQ_OK;
+  const int threads = static_cast<int>(cols / 8 < 512 ? cols / 8 : 512);
+  k_cl_accumulate<<<static_cast<unsigned>(n_seqs) * max_len, threads, 0, (cudaStream_t)stream>>>(
+      seed, codes, row_bytes, static_cast<const __half2*>(params), bits, group_size, cols,
+      seq_lens, max_len, L_max, acc, static_cast<__half*>(x16_out));
+  return check_launch("xq_cl_accumulate");
+}
+
+}  // extern "C"
