@@ -168,6 +168,11 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
                      int32_t tiles_per_chunk, void* workspace, int64_t workspace_bytes,
                      float* out, void* stream);
 
+/* Debug hook: when buf != NULL, xq_decode_attend also dumps the raw fp32
+ * accumulator of every tile t < n_tiles to buf[b][kv_head][t][128][256]
+ * (columns 0-127 = pre-RoPE K, 128-255 = V). NULL disables (default). */
+int xq_debug_set_acc_dump(float* buf, int32_t n_tiles);
+
 /* Debug / parity path: SIMT float32 rematerialisation that writes K and V
  * to HBM (cache.rematerialize, cache.py:271-281). a_*: as xq_decode_attend
  * for one sequence slot `slot` and tokens [0, n_tok). w_k/w_v float32

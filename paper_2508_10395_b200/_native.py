@@ -42,6 +42,7 @@ _SIGS = {
                      _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P],
     "xq_cl_accumulate": [_I32, _P, _I64, _P, _I32, _I32, _I64, _P, _I32, _I32, _I64, _P, _P,
                          _P],
+    "xq_debug_set_acc_dump": [_P, _I32],
     "xq_kv_append": [_P, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P],
     "xq_kv_decode_attend": [_P, _P, _I64, _P, _I32, _I32, _I32, _I32, _P, _P, _F, _I32, _P,
                             _I64, _P, _P],

@@ -57,7 +57,12 @@ struct DecodeParams {
   const float2* rope;
   float q_scale;  // sm_scale * log2(e)
   float* partials;
+  float* dbg_acc;  // optional: raw [b][h][tile][128][256] accumulator dump
+  int32_t dbg_tiles;
 };
+
+static float* g_dbg_acc = nullptr;
+static int32_t g_dbg_tiles = 0;
 
 struct Unit {
   int b, chunk, h, t0, t1, len;
@@ -187,9 +192,9 @@ XQ_DEVINL void produce_row(uint8_t* tile, int row, bool valid, int64_t arow, int
     if (tok < nflushed) {
       const __half* prow =
           static_cast<const __half*>(params) + (arow / p.group_size) * 2 * p.kdim + kc * kChunk;
-      __half2 s2[32], z2[32];
+      __half2 s2[32], z2[32];  // 64 channels = 8 x uint4 of halves each
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 8; ++c) {
         const uint4 a = reinterpret_cast<const uint4*>(prow)[c];
         const uint4 z = reinterpret_cast<const uint4*>(prow + p.kdim)[c];
         s2[4 * c] = from_u32<__half2>(a.x); s2[4 * c + 1] = from_u32<__half2>(a.y);
@@ -389,6 +394,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float* qq = q_s + gi * kHeadDim + c * 32 + 2 * i;
               sc[gi] = fmaf(qq[0], r0, fmaf(qq[1], r1, sc[gi]));
             }
+          }
+        }
+        if (p.dbg_acc != nullptr && t < p.dbg_tiles) {
+          float* drow = p.dbg_acc + ((((int64_t)w.b * p.n_kv + w.h) * p.dbg_tiles + t) * kTileM + row) * 256;
+          for (int c = 0; c < 8; ++c) {
+            float tmpv[32];
+            tmem_ld32(tmem + tlane + a * 256 + c * 32, tmpv);
+            tmem_wait_ld();
+            for (int j = 0; j < 32; ++j) drow[c * 32 + j] = tmpv[j];
           }
         }
         float pr[GROUP];
@@ -603,6 +617,12 @@ using namespace xq;
 
 extern "C" {
 
+int xq_debug_set_acc_dump(float* buf, int32_t n_tiles) {
+  g_dbg_acc = buf;
+  g_dbg_tiles = n_tiles;
+  return XQ_OK;
+}
+
 int64_t xq_decode_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_kv_heads,
                                   int32_t group, int32_t tiles_per_chunk) {
   if (tiles_per_chunk < 1) tiles_per_chunk = 1;
@@ -675,6 +695,8 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
   p.rope = static_cast<const float2*>(rope_cs);
   p.q_scale = sm_scale * 1.4426950408889634f;
   p.partials = static_cast<float*>(workspace);
+  p.dbg_acc = g_dbg_acc;
+  p.dbg_tiles = g_dbg_tiles;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   int status;

@@ -144,7 +144,9 @@ def main():
         for t in range(n_dec):
             st.decode_append(x[n_pre + t], lw)
             k, v = st.rematerialize(lw, np.arange(n_pre + t + 1))
-            outs.append(_attention(q[t:t + 1], k, v, H, 1)[0])
+            # q = RoPE(x W_q) at the new token's position (model.py:234)
+            qr = apply_rope(q[t:t + 1], np.array([n_pre + t]), hd)
+            outs.append(_attention(qr, k, v, H, 1)[0])
         key = f"mha_b{bits}"
         be[key + "_x"], be[key + "_wk"], be[key + "_wv"], be[key + "_q"] = xb, wkb, wvb, qb
         if bits in (3, 16):  # final-step K/V kept for two widths (fixture size)
@@ -162,7 +164,8 @@ def main():
     st.prefill(xx, lw)
     k, v = st.rematerialize(lw, np.arange(xx.shape[0]))
     be["fp16_k"], be["fp16_v"] = k.astype(np.float32), v.astype(np.float32)
-    be["fp16_attn"] = _attention(from_bf16_bits(be["mha_b4_q"])[-1:], k, v, H, 1)[0]
+    qr = apply_rope(from_bf16_bits(be["mha_b4_q"])[-1:], np.array([xx.shape[0] - 1]), hd)
+    be["fp16_attn"] = _attention(qr, k, v, H, 1)[0]
 
     # xq-gqa: d=1024, H=8, KV heads 2 (kv_group 4), r = 256; injected SVD factors
     d, H, g = 1024, 8, 4
@@ -183,7 +186,8 @@ def main():
     for t in range(n_dec):
         st.decode_append(x[n_pre + t], lw)
         k, v = st.rematerialize(lw, np.arange(n_pre + t + 1))
-        outs.append(_attention(q[t:t + 1], k, v, H, g)[0])
+        qr = apply_rope(q[t:t + 1], np.array([n_pre + t]), 128)
+        outs.append(_attention(qr, k, v, H, g)[0])
         bufs.append(len(st.k_stream.buf))
     be.update({
         "gqa_x": xb, "gqa_uk": ukb, "gqa_uv": uvb, "gqa_fk": fkb, "gqa_fv": fvb,
@@ -227,7 +231,8 @@ def main():
             accs.append(acc.x_hat.copy() if acc.x_hat is not None else np.zeros((0, d)))
             ks.append(k)
             vs.append(v)
-            attn.append(_attention(q[i:i + 1], k, v, H, 1)[0])
+            qr = apply_rope(q[i:i + 1], np.array([n_pre + t]), 128)
+            attn.append(_attention(qr, k, v, H, 1)[0])
     be.update({
         "cl_x": np.stack(xbits), "cl_wk": np.stack(wks), "cl_wv": np.stack(wvs),
         "cl_q": qb, "cl_bits": np.array(pol.bits), "cl_base": np.array(pol.base_layers),

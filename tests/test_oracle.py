@@ -106,7 +106,8 @@ class TestBackendsGolden:
         for t in range(n_dec):
             st.append(x[n_pre + t])
             kk, vv = st.remat(wk, wv)
-            outs.append(O.attention(q[t:t + 1], kk, vv, 2, 1)[0])
+            qr = O.apply_rope(q[t:t + 1], [n_pre + t], 128)  # model.py:234
+            outs.append(O.attention(qr, kk, vv, 2, 1)[0])
         if bits != 16:
             assert np.array_equal(st.stream.codes, z[k + "_codes"])
             assert np.array_equal(st.stream.scales, z[k + "_scales"])
@@ -122,7 +123,8 @@ class TestBackendsGolden:
         st.append(x, wk, wv)
         kk, vv = st.remat()
         assert rel(kk, z["fp16_k"]) <= 1e-6
-        assert rel(O.attention(q[-1:], kk, vv, 2, 1)[0], z["fp16_attn"]) <= 1e-12
+        qr = O.apply_rope(q[-1:], [x.shape[0] - 1], 128)
+        assert rel(O.attention(qr, kk, vv, 2, 1)[0], z["fp16_attn"]) <= 1e-12
 
     def test_xq_gqa(self):
         z = load("backends")
@@ -134,7 +136,8 @@ class TestBackendsGolden:
         for t in range(n_dec):
             st.push(x[n_pre + t] @ uk, x[n_pre + t] @ uv)
             kk, vv = st.remat(fk, fv)
-            outs.append(O.attention(q[t:t + 1], kk, vv, 8, 4)[0])
+            qr = O.apply_rope(q[t:t + 1], [n_pre + t], 128)
+            outs.append(O.attention(qr, kk, vv, 8, 4)[0])
             bufs.append(len(st.k_stream.buf))
         assert bufs == list(z["gqa_buf_len"])
         assert np.array_equal(st.k_stream.codes, z["gqa_kcodes"])
@@ -162,7 +165,9 @@ class TestBackendsGolden:
         assert rel(kvs[2][0], z["cl_k"][0]) <= 1e-6
         assert rel(kvs[-1][0], z["cl_k"][1]) <= 1e-6
         assert rel(kvs[-1][1], z["cl_v"][1]) <= 1e-6
-        attn = np.stack([O.attention(q[i:i + 1], kv[0], kv[1], 2, 1)[0] for i, kv in enumerate(kvs)])
+        pos = [n_pre + n_dec - 1]
+        attn = np.stack([O.attention(O.apply_rope(q[i:i + 1], pos, 128), kv[0], kv[1], 2, 1)[0]
+                         for i, kv in enumerate(kvs)])
         assert rel(attn, z["cl_attn"]) <= 1e-12
 
 
