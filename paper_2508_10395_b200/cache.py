@@ -410,8 +410,9 @@ class FullPrecisionCache(CacheBackend):
         self.v = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
 
     def _project(self, x, weights):
-        xf = x.float()
-        return xf @ weights.f32("w_k"), xf @ weights.f32("w_v")
+        # bf16 GEMM with fp32 accumulation (cuBLAS); K/V are stored in bf16 anyway
+        xb = x.to(weights.w_k.dtype)
+        return (xb @ weights.w_k).float(), (xb @ weights.w_v).float()
 
     def _prefill(self, slot, x, weights, acc):
         k, v = self._project(x, weights)

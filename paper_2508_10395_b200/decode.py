@@ -1,0 +1,202 @@
+"""Multi-layer decode-step driver on B200 (the attention block of
+``model._Session.decode``, model.py:223-240).
+
+Per layer, in strict order (model.py:230-235):
+  q = x @ W_q                       (cuBLAS GEMV; RoPE at pos is applied in-kernel)
+  cache.decode_append(x)            (quantize-and-pack kernel; CL: delta vs acc,
+                                     then acc += deq(all deltas); GQA: latents)
+  ctx = fused remat + attention     (tcgen05 kernel + split combine)
+The per-layer input ``x`` is a synthetic post-norm activation supplied by the
+caller (layer >= 1 inputs depend on upstream math the hot path does not own),
+so W_o / MLP are outside the step, identically for XQuant and the fp16-KV
+baseline.
+
+Shapes: ``SHAPES`` mirrors BASELINE.json configs (Llama-2-7B, Llama-3.1-8B,
+Llama-2-13B). Batch slots share one length vector; a step appends one token
+to every slot.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import cache as C
+from .errors import ConfigError
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    name: str
+    hidden_dim: int
+    n_layers: int
+    n_heads: int
+    kv_group: int = 1
+    head_dim: int = 128
+
+    @property
+    def kv_width(self) -> int:
+        return self.hidden_dim // self.kv_group
+
+
+SHAPES = {
+    "llama2-7b": ModelShape("llama2-7b", 4096, 32, 32, 1),
+    "llama3.1-8b": ModelShape("llama3.1-8b", 4096, 32, 32, 4),
+    "llama2-13b": ModelShape("llama2-13b", 5120, 40, 40, 1),
+}
+
+
+def synthetic_weights(shape: ModelShape, variant: str, device, seed: int = 0,
+                      layers: int | None = None):
+    """Random-init bf16 weights, N(0, 1/d) like gen_weights (linalg.py:231-236).
+
+    For xq-gqa the offline SVD factors (linalg.py:103-126) are computed in
+    float32 on the device with the reference sign rule (linalg.py:171-176)."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    d, kvw = shape.hidden_dim, shape.kv_width
+    n = shape.n_layers if layers is None else layers
+    out, wq = [], []
+    std = 1.0 / math.sqrt(d)
+    for _ in range(n):
+        w_k = (torch.randn(d, kvw, generator=g, device=device) * std).to(torch.bfloat16)
+        w_v = (torch.randn(d, kvw, generator=g, device=device) * std).to(torch.bfloat16)
+        wq.append((torch.randn(d, d, generator=g, device=device) * std).to(torch.bfloat16))
+        lw = C.LayerWeights(w_k=w_k, w_v=w_v)
+        if variant == "xq-gqa":
+            lw.u_k, lw.fused_k = _svd_factors(w_k)
+            lw.u_v, lw.fused_v = _svd_factors(w_v)
+        out.append(lw)
+    return out, wq
+
+
+def _svd_factors(w: torch.Tensor):
+    u, s, vt = torch.linalg.svd(w.float(), full_matrices=False)
+    idx = torch.argmax(u.abs(), dim=0)
+    sign = torch.sign(u[idx, torch.arange(u.shape[1], device=u.device)])
+    sign[sign == 0] = 1
+    u = u * sign[None, :]
+    vt = vt * sign[:, None]
+    fused = s[:, None] * vt
+    return u.to(torch.bfloat16), fused.to(torch.bfloat16)
+
+
+class Decoder:
+    """Per-layer caches of one model shape for ``n_slots`` sequences."""
+
+    def __init__(self, shape: ModelShape, variant: str, bits: int, n_slots: int, max_len: int,
+                 weights, w_q, device="cuda", policy: C.LayerPolicy | None = None,
+                 tiles_per_chunk: int | None = None):
+        if variant not in C.SUPPORTED:
+            raise ConfigError(f"variant {variant!r} not supported by the decoder")
+        self.shape, self.variant = shape, variant
+        self.device = torch.device(device)
+        self.n_slots, self.L = n_slots, max_len
+        self.policy = policy or (C.LayerPolicy.uniform(16, shape.n_layers) if variant == "fp16"
+                                 else C.LayerPolicy.for_bits(bits, shape.n_layers))
+        self.weights, self.w_q = weights, w_q
+        kw = dict(n_slots=n_slots, max_len=max_len, hidden_dim=shape.hidden_dim,
+                  n_heads=shape.n_heads, kv_group=shape.kv_group, device=self.device)
+        self.caches = [C.make_cache(variant, i, self.policy, shape.head_dim, **kw)
+                       for i in range(len(weights))]
+        self.acc = (C.Accumulator(n_slots, max_len, shape.hidden_dim, self.device)
+                    if variant in C.CL_VARIANTS else None)
+        # one shared length vector (host + device) for all layers
+        self.n_tokens = np.zeros(n_slots, dtype=np.int64)
+        self.lens_dev = torch.zeros(n_slots, dtype=torch.int32, device=self.device)
+        for c in self.caches:
+            c.n_tokens = self.n_tokens
+            c.lens_dev = self.lens_dev
+        self.tpc = tiles_per_chunk
+        self.launches = 0  # kernels of this library launched by step()
+
+    # ------------------------------------------------------------------ fill
+    def fill_synthetic(self, n_tokens: int, seed: int = 1, rows_per_chunk: int = 8192,
+                       mlp_scale: float = 0.03):
+        """Cache a synthetic prefix of ``n_tokens`` per slot with the GPU quantizer.
+
+        X rows ~ N(0,1) (unit-RMS post-norm activations); for XQuant-CL the
+        per-layer inputs drift like the residual stream, X_i = X_{i-1} +
+        mlp_scale * N(0,1) (tests/test_acceptance.py:31-33 uses 0.03)."""
+        if n_tokens > self.L:
+            raise ConfigError("prefix longer than max_len")
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        d = self.shape.hidden_dim
+        for s in range(self.n_slots):
+            x_prev = None
+            for i, (cache, lw) in enumerate(zip(self.caches, self.weights)):
+                if self.variant in C.CL_VARIANTS:
+                    noise = torch.randn(n_tokens, d, generator=g, device=self.device)
+                    x_prev = noise if x_prev is None else x_prev + mlp_scale * noise
+                    x = x_prev.to(torch.bfloat16)
+                else:
+                    x = torch.randn(n_tokens, d, generator=g, device=self.device).to(torch.bfloat16)
+                cache._prefill(s, x, lw, self.acc)
+            if self.acc is not None:
+                pass
+        self.n_tokens[:] = n_tokens
+        self.lens_dev.fill_(n_tokens)
+        torch.cuda.synchronize(self.device)
+
+    # ------------------------------------------------------------------ step
+    def step(self, x_layers: torch.Tensor, attn_out: torch.Tensor | None = None,
+             timers: list | None = None) -> torch.Tensor:
+        """One decode step: x_layers [n_layers, n_slots, d] (bf16/fp32, device).
+
+        Returns the last layer's attention output [n_slots, n_heads, 128]
+        (all layers' outputs when ``attn_out`` [n_layers, n_slots, H, 128]
+        is given). ``timers``: optional list that receives (start, end) CUDA
+        event pairs around every fused attention launch."""
+        if np.any(self.n_tokens >= self.L):
+            raise ConfigError("cache full")
+        self.n_tokens += 1
+        self.lens_dev.add_(1)
+        max_len = int(self.n_tokens.max())
+        H = self.shape.n_heads
+        out = None
+        for i, (cache, lw) in enumerate(zip(self.caches, self.weights)):
+            x = x_layers[i]
+            q = torch.matmul(x, self.w_q[i]).float().view(self.n_slots, H, 128)
+            cache._decode(x, lw, self.acc, self.lens_dev)
+            out = attn_out[i] if attn_out is not None else torch.empty_like(q)
+            if timers is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            cache._attend(q, lw, self.acc, self.lens_dev, max_len, out, self.tpc)
+            if timers is not None:
+                e1.record()
+                timers.append((e0, e1))
+            self.launches += self._launches_per_layer(cache)
+        return out
+
+    def _launches_per_layer(self, cache) -> int:
+        if self.variant == "fp16":
+            return 3  # kv_append, kv_decode, combine
+        if self.variant == "xq-gqa":
+            return 3  # v-latent quantize, decode, combine (+ a flush every 128 steps)
+        if self.variant == "xq-cl-mha":
+            base = cache.layer_index < self.policy.base_layers
+            seed = cache.layer_index == self.policy.base_layers - 1
+            return 3 + (0 if base and not seed else 1)
+        return 3  # quantize, decode, combine
+
+    # ------------------------------------------------------------- accounting
+    def memory_bytes(self) -> dict:
+        tot: dict = {}
+        for c in self.caches:
+            for k, v in c.memory_bytes().items():
+                tot[k] = tot.get(k, 0) + v
+        if self.acc is not None:
+            tot["cl_accumulator_f32"] = self.acc.x_hat.numel() * 4
+            tot["cl_accumulator_f16"] = self.acc.x16.numel() * 2
+        return tot
+
+    def check_finite(self):
+        for c in self.caches:
+            for s in ("stream", "k_stream", "v_stream"):
+                st = getattr(c, s, None)
+                if st is not None:
+                    st.check_finite()
