@@ -17,7 +17,9 @@
  *            ceil(cols*bits/64)*8.
  *   params : fp16 scale + fp16 zero_point per group -- the 16+16 bits per
  *            group the reference charges (quant.py:44-45, quant.py:58-62).
- *            per-token  : __half2 (scale, zp) [n_slots * L_max][ceil(cols/G)]
+ *            per-token  : __half2 (scale, zp) [n_slots * L_max][P], row stride
+ *                         P = ceil(ceil(cols/G)/4)*4 (padded to whole 16-byte
+ *                         quads so the fused kernel can stage it by TMA)
  *            per-channel: planar halves [n_slots * L_max / G][2][cols]
  *                         (scales, then zero points; L_max % G == 0), the
  *                         channels within each block stored in the order the
@@ -126,9 +128,12 @@ int xq_dequant_rows(const uint8_t* codes, int64_t row_bytes, const void* params,
  * Rematerialisation + decode attention (cache.py:271-281, model.py:150-182)
  * ====================================================================== */
 
-/* cos/sin table [n_pos][head_dim/2] as float2, angle pos*theta^(-2j/hd)
- * formed in float64 (linalg.py:84-88). */
-int xq_rope_table(void* cs_out, int64_t n_pos, int32_t head_dim, double theta, void* stream);
+/* cos/sin table as float2, angle pos*theta^(-2j/hd) formed in float64
+ * (linalg.py:84-88). j_major == 0: [n_pos][head_dim/2] (position-major, used
+ * by the fp16-KV baseline and the debug remat); j_major != 0:
+ * [head_dim/2][n_pos] (frequency-major, coalesced reads in the fused kernel). */
+int xq_rope_table(void* cs_out, int64_t n_pos, int32_t head_dim, double theta, int32_t j_major,
+                  void* stream);
 
 /* Arrange K/V projection weights for the fused kernel: out is fp16
  * [n_kv_heads][256][kdim]: rows 0..127 of head h are W_k[:, h*128 .. +128]^T,
@@ -156,17 +161,18 @@ int64_t xq_decode_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_kv_
  *   A_V: av_mode as above or XQ_A_SAME (MHA: one X cache feeds K and V).
  *   rows of both A streams are arena rows b*L_max + t with row_bytes bytes
  *   (codes) or kdim fp16 (F16_ROWS).
- *   w_arranged: from xq_arrange_weights. rope_cs: from xq_rope_table with
- *   n_pos >= max_len. sm_scale: 1/sqrt(128) for the reference (model.py:164). */
+ *   w_arranged: from xq_arrange_weights. rope_cs: frequency-major table from
+ *   xq_rope_table(j_major=1) with rope_n >= max_len positions. sm_scale:
+ *   1/sqrt(128) for the reference (model.py:164). */
 int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
                      const float* ak_resid, const int32_t* ak_nflushed, int32_t ak_bits,
                      int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
                      const void* av_params, int32_t av_bits, int64_t av_row_bytes,
                      int32_t group_size, int64_t L_max, int64_t kdim, const int32_t* seq_lens,
                      int32_t n_seqs, int32_t max_len, const void* w_arranged, int32_t n_kv_heads,
-                     int32_t group, const float* q_pre, const void* rope_cs, float sm_scale,
-                     int32_t tiles_per_chunk, void* workspace, int64_t workspace_bytes,
-                     float* out, void* stream);
+                     int32_t group, const float* q_pre, const void* rope_cs, int64_t rope_n,
+                     float sm_scale, int32_t tiles_per_chunk, void* workspace,
+                     int64_t workspace_bytes, float* out, void* stream);
 
 /* Debug hook: when buf != NULL, xq_decode_attend also dumps the raw fp32
  * accumulator of every tile t < n_tiles to buf[b][kv_head][t][128][256]

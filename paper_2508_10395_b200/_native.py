@@ -33,11 +33,11 @@ _SIGS = {
                          _P, _P, _P, _P],
     "xq_quantize_blocks_per_channel": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P],
     "xq_dequant_rows": [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _I64, _P, _P],
-    "xq_rope_table": [_P, _I64, _I32, _D, _P],
+    "xq_rope_table": [_P, _I64, _I32, _D, _I32, _P],
     "xq_arrange_weights": [_P, _P, _I32, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P],
     "xq_decode_attend": [_I32, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32, _I64,
-                         _I64, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _F, _I32, _P, _I64, _P,
-                         _P],
+                         _I64, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _I64, _F, _I32, _P, _I64,
+                         _P, _P],
     "xq_remat_f32": [_I32, _P, _P, _P, _I32, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32, _I64,
                      _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P],
     "xq_cl_accumulate": [_I32, _P, _I64, _P, _I32, _I32, _I64, _P, _I32, _I32, _I64, _P, _P,

@@ -127,17 +127,28 @@ def _dtype_code(t: torch.Tensor) -> int:
 _ROPE: dict = {}
 
 
-def rope_table(n_pos: int, device) -> torch.Tensor:
-    """cos/sin table [n_pos, 64] float2 (angle formed in float64, linalg.py:84-88)."""
+def _rope(n_pos: int, device, j_major: int) -> torch.Tensor:
     device = torch.device(device)
-    key = device.index if device.index is not None else torch.cuda.current_device()
+    key = (device.index if device.index is not None else torch.cuda.current_device(), j_major)
     cur = _ROPE.get(key)
-    if cur is None or cur.shape[0] < n_pos:
+    have = (cur.shape[1] // 2 if j_major else cur.shape[0]) if cur is not None else 0
+    if have < n_pos:
         n = max(1024, 1 << math.ceil(math.log2(max(n_pos, 1))))
-        t = torch.empty((n, HEAD_DIM), dtype=torch.float32, device=device)
-        N.call("xq_rope_table", N.ptr(t), n, HEAD_DIM, ROPE_THETA, N.stream_of(device))
+        shape = (HEAD_DIM // 2, 2 * n) if j_major else (n, HEAD_DIM)
+        t = torch.empty(shape, dtype=torch.float32, device=device)
+        N.call("xq_rope_table", N.ptr(t), n, HEAD_DIM, ROPE_THETA, j_major, N.stream_of(device))
         _ROPE[key] = cur = t
     return cur
+
+
+def rope_table(n_pos: int, device) -> torch.Tensor:
+    """cos/sin table [n_pos, 64] float2 (angle formed in float64, linalg.py:84-88)."""
+    return _rope(n_pos, device, 0)
+
+
+def rope_table_t(n_pos: int, device) -> torch.Tensor:
+    """Frequency-major cos/sin table [64, n] float2 (n >= n_pos) for the fused kernel."""
+    return _rope(n_pos, device, 1)
 
 
 class Accumulator:
@@ -179,7 +190,8 @@ class PackedStream:
         self.codes = torch.zeros((n_slots * max_len, self.row_bytes), dtype=torch.uint8, device=device)
         if axis == TOKEN:
             ng = -(-width // group_size)
-            self.params = torch.zeros((n_slots * max_len, ng, 2), dtype=torch.float16, device=device)
+            ngp = -(-ng // 4) * 4  # row stride padded to 16-byte quads (include/xquant.h)
+            self.params = torch.zeros((n_slots * max_len, ngp, 2), dtype=torch.float16, device=device)
         else:
             self.params = torch.zeros((n_slots * max_len // group_size, 2, width),
                                       dtype=torch.float16, device=device)
@@ -353,12 +365,13 @@ class CacheBackend:
                av_src, av_params, av_bits, av_rb, kdim, w_arr, group, q, lens, max_len, out, tpc):
         tpc = tpc or default_tiles_per_chunk(self.n_slots, max_len, self.n_kv)
         ws, nbytes = self._workspace(max_len, group, tpc)
-        rope = rope_table(max_len, self.device)
+        rope = rope_table_t(max_len, self.device)
         N.call("xq_decode_attend", ak_mode, N.ptr(ak_src), N.ptr(ak_params), N.ptr(ak_resid),
                N.ptr(ak_nfl), ak_bits, ak_rb, av_mode, N.ptr(av_src), N.ptr(av_params), av_bits,
                av_rb, self.group_size, self.L, kdim, N.ptr(lens), self.n_slots, max_len,
-               N.ptr(w_arr), self.n_kv, group, N.ptr(q), N.ptr(rope), 1.0 / math.sqrt(HEAD_DIM),
-               tpc, N.ptr(ws), nbytes, N.ptr(out), N.stream_of(self.device))
+               N.ptr(w_arr), self.n_kv, group, N.ptr(q), N.ptr(rope), rope.shape[1] // 2,
+               1.0 / math.sqrt(HEAD_DIM), tpc, N.ptr(ws), nbytes, N.ptr(out),
+               N.stream_of(self.device))
 
     def _remat_f32(self, ak_mode, ak_src, ak_params, ak_resid, ak_nfl, ak_bits, ak_rb, av_mode,
                    av_src, av_params, av_bits, av_rb, kdim, wk, wv, slot, n):
@@ -389,13 +402,18 @@ class CacheBackend:
         raise NotImplementedError
 
 
-def default_tiles_per_chunk(n_slots: int, max_len: int, n_kv: int, n_sm: int = 148) -> int:
-    """Split each sequence into enough chunks that units >= ~4 waves of SMs."""
+def default_tiles_per_chunk(n_slots: int, max_len: int, n_kv: int, n_sm: int = 148,
+                            max_tiles: int = 4) -> int:
+    """Tiles (of 128 tokens) per work unit.
+
+    Enough units for >= ~4 waves of SMs, and at most ``max_tiles`` tiles per
+    unit: units are ordered KV-head-fastest, so the CTAs in flight cover only
+    a few token ranges and every head re-reads those codes from L2, not HBM."""
     n_tiles = max(1, -(-max_len // 128))
     target_units = 4 * n_sm
     per_seq_head = max(1, n_slots * n_kv)
     chunks = max(1, min(n_tiles, -(-target_units // per_seq_head)))
-    return max(1, -(-n_tiles // chunks))
+    return max(1, min(max_tiles, -(-n_tiles // chunks)))
 
 
 class FullPrecisionCache(CacheBackend):

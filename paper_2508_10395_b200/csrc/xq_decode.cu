@@ -54,7 +54,8 @@ struct DecodeParams {
   int32_t n_kv;
   int32_t n_units;
   const float* q_pre;
-  const float2* rope;
+  const float2* rope;  // frequency-major [64][rope_n]
+  int64_t rope_n;
   float q_scale;  // sm_scale * log2(e)
   float* partials;
   float* dbg_acc;  // optional: raw [b][h][tile][128][256] accumulator dump
@@ -97,50 +98,51 @@ XQ_DEVINL uint32_t deq_pair(uint32_t masked, __half2 s2, __half2 z2) {
   return as_u32(__hfma2(c, s2, z2));
 }
 
-// 64 codes of one row -> 32 fp16 pairs in producer order (xq_layout.cuh).
-// src: the 8*BITS bytes of the chunk. s2/z2: per pair (per-channel) or uniform.
+// 64 codes of one row = 8*BITS bytes = 2*BITS words, loaded ahead of use.
+template <int BITS>
+XQ_DEVINL void load_raw(const uint8_t* src, uint32_t (&w)[2 * BITS]) {
+  if constexpr (BITS == 3) {  // 24 bytes at an 8-byte aligned offset
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(src) + q);
+      w[2 * q] = a.x;
+      w[2 * q + 1] = a.y;
+    }
+  } else {  // 16 / 32 / 64 bytes at 16-byte aligned offsets
+#pragma unroll
+    for (int q = 0; q < BITS / 2; ++q) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(src) + q);
+      w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+    }
+  }
+}
+
+// 64 codes -> 32 fp16 pairs in producer order (xq_layout.cuh).
+// s2/z2: per pair (per-channel) or uniform.
 template <int BITS, bool PER_PAIR>
-XQ_DEVINL void dequant_chunk(const uint8_t* src, const __half2* s2, const __half2* z2,
-                             uint32_t (&out)[32]) {
+XQ_DEVINL void convert_raw(const uint32_t (&w)[2 * BITS], const __half2* s2, const __half2* z2,
+                           uint32_t (&out)[32]) {
   auto S = [&](int j) { return PER_PAIR ? s2[j] : s2[0]; };
   auto Z = [&](int j) { return PER_PAIR ? z2[j] : z2[0]; };
   if constexpr (BITS == 4) {
-    const uint4 a = reinterpret_cast<const uint4*>(src)[0];
-    const uint4 b = reinterpret_cast<const uint4*>(src)[1];
-    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
     for (int wi = 0; wi < 8; ++wi)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         out[4 * wi + j] = deq_pair((w[wi] >> (4 * j)) & 0x000F000Fu, S(4 * wi + j), Z(4 * wi + j));
   } else if constexpr (BITS == 2) {
-    const uint4 a = reinterpret_cast<const uint4*>(src)[0];
-    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
     for (int wi = 0; wi < 4; ++wi)
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         out[8 * wi + j] = deq_pair((w[wi] >> (2 * j)) & 0x00030003u, S(8 * wi + j), Z(8 * wi + j));
   } else if constexpr (BITS == 8) {
-    uint32_t w[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 a = reinterpret_cast<const uint4*>(src)[q];
-      w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
-    }
 #pragma unroll
     for (int wi = 0; wi < 16; ++wi)
 #pragma unroll
       for (int j = 0; j < 2; ++j)
         out[2 * wi + j] = deq_pair((w[wi] >> (8 * j)) & 0x00FF00FFu, S(2 * wi + j), Z(2 * wi + j));
   } else {  // 3-bit: two 32-code blocks of 3 words each
-    uint32_t w[6];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const uint2 a = reinterpret_cast<const uint2*>(src)[q];
-      w[2 * q] = a.x;
-      w[2 * q + 1] = a.y;
-    }
 #pragma unroll
     for (int bi = 0; bi < 2; ++bi) {
       const uint32_t w0 = w[3 * bi], w1 = w[3 * bi + 1], w2 = w[3 * bi + 2];
@@ -165,44 +167,94 @@ XQ_DEVINL void store_row_sw128(uint8_t* tile, int row, const uint32_t (&v)[32]) 
   }
 }
 
-// Produce one 64-channel chunk of one row of an A stream into `tile`.
+// ---------------------------------------------------------------------------
+// Codes ring: a dedicated TMA thread stages, per 128-channel group of a
+// 128-token tile, the packed codes of every A stream (box [16*BITS B, 128
+// rows]) and, for per-token streams, the half2 (scale, zp) quads (box
+// [4 x u32, 128 rows]) into shared memory. Producers then read shared memory
+// only, so the LSU pipe carries no uncoalesced global traffic.
+// ---------------------------------------------------------------------------
+template <int AK, int AV, int BITS>
+struct Ring {
+  static constexpr bool kProducers = AK != XQ_A_F16_ROWS;
+  static constexpr int kStreams = (AV == XQ_A_SAME) ? 1 : 2;
+  static constexpr int kGB = 16 * BITS;                           // code bytes per row per group
+  static constexpr int kTokenStreams = (AK == XQ_A_CODES_TOKEN) + (AV == XQ_A_CODES_TOKEN);
+  static constexpr uint32_t kCodeBytes = kTileM * kGB;
+  static constexpr uint32_t kParamBytes = kTileM * 16;
+  static constexpr uint32_t kStageBytes =
+      kProducers ? ((kStreams * kCodeBytes + kTokenStreams * kParamBytes + 127) / 128 * 128) : 0;
+  static constexpr int kABStages = kStreams == 1 ? (BITS == 8 ? 3 : 4) : (BITS == 8 ? 2 : 3);
+  static constexpr uint32_t kABBytes = kABStages * (kStreams * kABytes + kBBytes);
+  static constexpr uint32_t kBudget = 225 * 1024 - kABBytes - 8 * 1024;
+  static constexpr int kCodeStages =
+      !kProducers ? 0 : (kBudget / kStageBytes >= 4 ? 4 : (kBudget / kStageBytes < 1 ? 1 : kBudget / kStageBytes));
+  // stage layout: [s0 codes][s1 codes][s0 params if TOKEN][s1 params if TOKEN]
+  __host__ __device__ static constexpr uint32_t code_off(int stream) { return stream * kCodeBytes; }
+  __host__ __device__ static constexpr uint32_t param_off(int stream) {
+    return kStreams * kCodeBytes + ((stream == 1 && AK == XQ_A_CODES_TOKEN) ? kParamBytes : 0);
+  }
+};
+
+// 2*BITS words of one row's 64-code chunk from shared memory
+template <int BITS>
+XQ_DEVINL void lds_raw(const uint8_t* src, uint32_t (&w)[2 * BITS]) {
+  if constexpr (BITS == 3) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const uint2 a = *reinterpret_cast<const uint2*>(src + 8 * q);
+      w[2 * q] = a.x;
+      w[2 * q + 1] = a.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < BITS / 2; ++q) {
+      const uint4 a = *reinterpret_cast<const uint4*>(src + 16 * q);
+      w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+    }
+  }
+}
+
+// One producer thread: convert its row's 64-channel chunk of one A stream.
 template <int MODE, int BITS>
-XQ_DEVINL void produce_row(uint8_t* tile, int row, bool valid, int64_t arow, int tok, int b,
-                           int kc, const uint8_t* src, const void* params, int64_t row_bytes,
-                           const float* resid, int nflushed, const DecodeParams& p) {
+XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t* pstage, int row,
+                             bool valid, int tok, int b, int nflushed, int64_t arow, int kc,
+                             const void* gparams, const float* resid, const DecodeParams& p) {
   uint32_t v[32];
   if (!valid) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = 0u;
-  } else if constexpr (MODE == XQ_A_F16_ROWS) {
-    const uint4* s = reinterpret_cast<const uint4*>(
-        reinterpret_cast<const __half*>(src) + arow * p.kdim + kc * kChunk);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint4 q = s[c];
-      v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
-    }
-  } else if constexpr (MODE == XQ_A_CODES_TOKEN) {
-    const int64_t ng = p.kdim / p.group_size;
-    const __half2 sz = static_cast<const __half2*>(params)[arow * ng + (kc * kChunk) / p.group_size];
+    store_row_sw128(tile, row, v);
+    return;
+  }
+  const uint8_t* crow = cstage + row * (16 * BITS) + (kc & 1) * 8 * BITS;
+  if constexpr (MODE == XQ_A_CODES_TOKEN) {
+    uint32_t raw[2 * BITS];
+    lds_raw<BITS>(crow, raw);
+    // params quad starts at group ((128*(kc/2))/G) & ~3; this chunk's group is (64*kc)/G
+    const int gq = (kChunk * kc) / p.group_size - (((2 * kChunk * (kc >> 1)) / p.group_size) & ~3);
+    const __half2 sz = *reinterpret_cast<const __half2*>(pstage + row * 16 + 4 * gq);
     const __half2 s2 = __low2half2(sz), z2 = __high2half2(sz);
-    dequant_chunk<BITS, false>(src + arow * row_bytes + kc * 8 * BITS, &s2, &z2, v);
+    convert_raw<BITS, false>(raw, &s2, &z2, v);
   } else {  // XQ_A_CODES_CHANNEL
     constexpr int BS = BITS == 2 ? 16 : BITS == 3 ? 32 : BITS == 4 ? 8 : 4;
     if (tok < nflushed) {
+      uint32_t raw[2 * BITS];
+      lds_raw<BITS>(crow, raw);
+      // per-channel params: shared by the whole tile -> L1 broadcast
       const __half* prow =
-          static_cast<const __half*>(params) + (arow / p.group_size) * 2 * p.kdim + kc * kChunk;
-      __half2 s2[32], z2[32];  // 64 channels = 8 x uint4 of halves each
+          static_cast<const __half*>(gparams) + (arow / p.group_size) * 2 * p.kdim + kc * kChunk;
+      __half2 s2[32], z2[32];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const uint4 a = reinterpret_cast<const uint4*>(prow)[c];
-        const uint4 z = reinterpret_cast<const uint4*>(prow + p.kdim)[c];
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(prow) + c);
+        const uint4 z = __ldg(reinterpret_cast<const uint4*>(prow + p.kdim) + c);
         s2[4 * c] = from_u32<__half2>(a.x); s2[4 * c + 1] = from_u32<__half2>(a.y);
         s2[4 * c + 2] = from_u32<__half2>(a.z); s2[4 * c + 3] = from_u32<__half2>(a.w);
         z2[4 * c] = from_u32<__half2>(z.x); z2[4 * c + 1] = from_u32<__half2>(z.y);
         z2[4 * c + 2] = from_u32<__half2>(z.z); z2[4 * c + 3] = from_u32<__half2>(z.w);
       }
-      dequant_chunk<BITS, true>(src + arow * row_bytes + kc * 8 * BITS, s2, z2, v);
+      convert_raw<BITS, true>(raw, s2, z2, v);
     } else {  // residual full-precision row (cache.py:228-229)
       const float* r = resid + ((int64_t)b * p.group_size + (tok - nflushed)) * p.kdim + kc * kChunk;
 #pragma unroll
@@ -218,9 +270,16 @@ XQ_DEVINL void produce_row(uint8_t* tile, int row, bool valid, int64_t arow, int
 
 template <int AK, int AV, int BITS, int GROUP>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_decode_attend(const __grid_constant__ CUtensorMap tmap_w, const DecodeParams p) {
-  constexpr int A_TILES = (AV == XQ_A_SAME) ? 1 : 2;
-  constexpr int STAGES = A_TILES == 1 ? 4 : 3;
+    k_decode_attend(const __grid_constant__ CUtensorMap tmap_w,
+                    const __grid_constant__ CUtensorMap tmap_ca,
+                    const __grid_constant__ CUtensorMap tmap_pa,
+                    const __grid_constant__ CUtensorMap tmap_cb,
+                    const __grid_constant__ CUtensorMap tmap_pb, const DecodeParams p) {
+  using R = Ring<AK, AV, BITS>;
+  constexpr int A_TILES = R::kStreams;
+  constexpr int STAGES = R::kABStages;
+  constexpr int CSTAGES = R::kCodeStages;
+  constexpr bool PROD = R::kProducers;
   constexpr int AVM = (AV == XQ_A_SAME) ? AK : AV;
 
   extern __shared__ uint8_t smem_raw[];
@@ -228,9 +287,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_TILES * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * kBBytes);
+  uint8_t* sC = sB + STAGES * kBBytes;  // codes ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + CSTAGES * R::kStageBytes);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* cfull = empty + STAGES;
+  uint64_t* cempty = cfull + 4;
+  uint64_t* tfull = cempty + 4;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* q_s = reinterpret_cast<float*>(tmem_slot + 4);  // [GROUP][128]
@@ -238,8 +300,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 4 + 1);  // 4 producer warps + the TMA expect_tx arrive
+      mbar_init(&full[s], PROD ? 4 + 1 : 1);  // producer warps of one group + TMA expect_tx
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < CSTAGES; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 8);  // every producer warp reads every codes stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -247,7 +313,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) tma_prefetch_desc(&tmap_w);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    if constexpr (!PROD) tma_prefetch_desc(&tmap_ca);
+  }
+  if (warp == 2 && lane == 0 && PROD) {
+    tma_prefetch_desc(&tmap_ca);
+    if constexpr (AK == XQ_A_CODES_TOKEN) tma_prefetch_desc(&tmap_pa);
+    if constexpr (A_TILES == 2) {
+      tma_prefetch_desc(&tmap_cb);
+      tma_prefetch_desc(&tmap_pb);
+    }
+  }
   if (warp == 1) {
     tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
@@ -259,18 +336,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkc = p.kdim / kChunk;
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer (W tiles)
+    // ------------------------------------------------ TMA: W tiles (+ fp16 A rows)
     if (lane == 0) {
       uint32_t it = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Unit w = get_unit(p, u);
-        for (int t = w.t0; t < w.t1; ++t)
+        for (int t = w.t0; t < w.t1; ++t) {
+          const int32_t arow0 = static_cast<int32_t>((int64_t)w.b * p.L_max + t * kTileM);
           for (int kc = 0; kc < nkc; ++kc, ++it) {
             const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
             mbar_wait(&empty[s], ph ^ 1);
-            mbar_arrive_expect_tx(&full[s], kBBytes);
+            mbar_arrive_expect_tx(&full[s], kBBytes + (PROD ? 0u : kABytes));
             tma_load_2d(sB + s * kBBytes, &tmap_w, &full[s], kc * kChunk, w.h * 256, kEvictLast);
+            if constexpr (!PROD)
+              tma_load_2d(sA + s * kABytes, &tmap_ca, &full[s], kc * kChunk, arow0, kEvictNormal);
           }
+        }
       }
     }
   } else if (warp == 1) {
@@ -309,31 +390,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if (warp == 2) {
+    // ------------------------------------------------ TMA: codes ring
+    if (PROD && lane == 0) {
+      uint32_t ci = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Unit w = get_unit(p, u);
+        for (int t = w.t0; t < w.t1; ++t) {
+          const int32_t arow0 = static_cast<int32_t>((int64_t)w.b * p.L_max + t * kTileM);
+          for (int g = 0; g < nkc / 2; ++g, ++ci) {
+            const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
+            mbar_wait(&cempty[cs], cph ^ 1);
+            uint8_t* st = sC + cs * R::kStageBytes;
+            mbar_arrive_expect_tx(&cfull[cs], A_TILES * R::kCodeBytes + R::kTokenStreams * R::kParamBytes);
+            // params quad holding this 128-channel block's group(s); a TMA box must
+            // start on a 16-byte boundary of the inner dimension
+            const int32_t pq = ((2 * kChunk * g) / p.group_size) & ~3;
+            tma_load_2d(st + R::code_off(0), &tmap_ca, &cfull[cs], g * R::kGB, arow0, kEvictFirst);
+            if constexpr (AK == XQ_A_CODES_TOKEN)
+              tma_load_2d(st + R::param_off(0), &tmap_pa, &cfull[cs], 4 * pq, arow0, kEvictFirst);
+            if constexpr (A_TILES == 2) {
+              tma_load_2d(st + R::code_off(1), &tmap_cb, &cfull[cs], g * R::kGB, arow0, kEvictFirst);
+              tma_load_2d(st + R::param_off(1), &tmap_pb, &cfull[cs], 4 * pq, arow0, kEvictFirst);
+            }
+          }
+        }
+      }
+    }
   } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
     // ------------------------------------------------ dequant producers
-    const int gp = (warp - kProdWarp0) >> 2;              // even / odd K-chunks
-    const int row = ((warp - kProdWarp0) & 3) * 32 + lane;  // tile row = token
-    uint32_t it = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-      const Unit w = get_unit(p, u);
-      const int nfl = (AK == XQ_A_CODES_CHANNEL) ? p.ak_nflushed[w.b] : 0;
-      for (int t = w.t0; t < w.t1; ++t) {
-        const int tok = t * kTileM + row;
-        const bool valid = tok < w.len;
-        const int64_t arow = (int64_t)w.b * p.L_max + tok;
-        for (int kc = 0; kc < nkc; ++kc, ++it) {
-          if ((it & 1) != static_cast<uint32_t>(gp)) continue;
-          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* tile = sA + s * A_TILES * kABytes;
-          produce_row<AK, BITS>(tile, row, valid, arow, tok, w.b, kc, p.ak_src, p.ak_params,
-                                p.ak_row_bytes, p.ak_resid, nfl, p);
-          if constexpr (A_TILES == 2)
-            produce_row<AVM, BITS>(tile + kABytes, row, valid, arow, tok, w.b, kc, p.av_src,
-                                   p.av_params, p.av_row_bytes, nullptr, 0, p);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[s]);
+    // Group gp owns the K-chunks kc == gp (mod 2) of every tile (nkc is even).
+    if constexpr (PROD) {
+      const int gp = (warp - kProdWarp0) >> 2;
+      const int row = ((warp - kProdWarp0) & 3) * 32 + lane;  // tile row = token
+      uint32_t tcount = 0;
+      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Unit w = get_unit(p, u);
+        const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.ak_nflushed + w.b) : 0;
+        for (int t = w.t0; t < w.t1; ++t, ++tcount) {
+          const int tok = t * kTileM + row;
+          const bool valid = tok < w.len;
+          const int64_t arow = (int64_t)w.b * p.L_max + tok;
+          for (int kc = gp; kc < nkc; kc += 2) {
+            const uint32_t ci = tcount * (nkc / 2) + (kc >> 1);
+            const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
+            const uint32_t it = tcount * nkc + kc;
+            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+            const uint8_t* st = sC + cs * R::kStageBytes;
+            mbar_wait(&cfull[cs], cph);
+            mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* tile = sA + s * A_TILES * kABytes;
+            produce_chunk<AK, BITS>(tile, st + R::code_off(0), st + R::param_off(0), row, valid,
+                                    tok, w.b, nfl, arow, kc, p.ak_params, p.ak_resid, p);
+            if constexpr (A_TILES == 2)
+              produce_chunk<AVM, BITS>(tile + kABytes, st + R::code_off(1), st + R::param_off(1),
+                                       row, valid, tok, w.b, 1 << 30, arow, kc, p.av_params,
+                                       nullptr, p);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive(&full[s]);
+              mbar_arrive(&cempty[cs]);
+            }
+          }
         }
       }
     }
@@ -350,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int pos = w.len - 1;
       named_bar_sync(1, 128);
       if (pos >= 0) {
-        const float2 cs = p.rope[(int64_t)pos * 64 + (et >> 1)];
+        const float2 cs = p.rope[(int64_t)(et >> 1) * p.rope_n + pos];
 #pragma unroll
         for (int gi = 0; gi < GROUP; ++gi) {
           const float* qp = p.q_pre + ((int64_t)w.b * n_q + w.h * GROUP + gi) * kHeadDim;
@@ -370,11 +489,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int t = w.t0; t < w.t1; ++t, ++tc) {
         const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-        mbar_wait(&tfull[a], aph);
-        tc_fence_after();
         const int tok = t * kTileM + row;
         const bool valid = tok < w.len;
-        const float2* rp = p.rope + (int64_t)(valid ? tok : 0) * 64;
+        // frequency-major table: lanes read consecutive positions (coalesced)
+        const float2* rp = p.rope + (valid ? tok : 0);
+        mbar_wait(&tfull[a], aph);
+        tc_fence_after();
         float sc[GROUP];
 #pragma unroll
         for (int gi = 0; gi < GROUP; ++gi) sc[gi] = 0.f;
@@ -382,10 +502,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 4; ++c) {
           float kb[32];
           tmem_ld32(tmem + tlane + a * 256 + c * 32, kb);
+          float2 csv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) csv[i] = __ldg(rp + (int64_t)(c * 16 + i) * p.rope_n);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float2 cs = rp[c * 16 + i];
+            const float2 cs = csv[i];
             const float k0 = kb[2 * i], k1 = kb[2 * i + 1];
             const float r0 = k0 * cs.x - k1 * cs.y;  // linalg.py:92-93
             const float r1 = k0 * cs.y + k1 * cs.x;
@@ -511,7 +634,7 @@ XQ_DEVINL float deq_natural(int mode, int bits, const void* src, const void* par
     return __half2float(static_cast<const __half*>(src)[arow * kdim + c]);
   if (mode == XQ_A_CODES_TOKEN) {
     const uint32_t code = read_code_dbg(static_cast<const uint8_t*>(src) + arow * row_bytes, c, bits);
-    const __half2 sz = static_cast<const __half2*>(params)[arow * (kdim / G) + c / G];
+    const __half2 sz = static_cast<const __half2*>(params)[arow * param_stride(kdim, G) + c / G];
     return fmaf(static_cast<float>(code), __low2float(sz), __high2float(sz));
   }
   if (t >= nflushed) return resid[((int64_t)slot * G + (t - nflushed)) * kdim + c];
@@ -580,12 +703,16 @@ static int64_t n_chunks_for(int32_t max_len, int32_t tpc) {
   return nt == 0 ? 1 : (nt + tpc - 1) / tpc;
 }
 
+struct Maps {
+  CUtensorMap w, ca, pa, cb, pb;
+};
+
 template <int AK, int AV, int BITS, int GROUP>
-static int launch_decode(const CUtensorMap& tmap, const DecodeParams& p, cudaStream_t st) {
-  constexpr int A_TILES = (AV == XQ_A_SAME) ? 1 : 2;
-  constexpr int STAGES = A_TILES == 1 ? 4 : 3;
-  constexpr size_t smem = 1024 + STAGES * (A_TILES * kABytes + kBBytes) + 2 * STAGES * 8 + 4 * 8 +
-                          16 + GROUP * kHeadDim * 4;
+static int launch_decode(const Maps& m, const DecodeParams& p, cudaStream_t st) {
+  using R = Ring<AK, AV, BITS>;
+  constexpr size_t smem = 1024 + R::kABBytes + R::kCodeStages * R::kStageBytes +
+                          (2 * R::kABStages + 8 + 4) * 8 + 16 + GROUP * kHeadDim * 4;
+  static_assert(smem <= 227 * 1024, "shared memory budget");
   auto kern = k_decode_attend<AK, AV, BITS, GROUP>;
   static bool configured = false;
   if (!configured) {
@@ -595,20 +722,56 @@ static int launch_decode(const CUtensorMap& tmap, const DecodeParams& p, cudaStr
     configured = true;
   }
   const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
-  kern<<<grid, kThreads, smem, st>>>(tmap, p);
+  kern<<<grid, kThreads, smem, st>>>(m.w, m.ca, m.pa, m.cb, m.pb, p);
   return check_launch("k_decode_attend");
 }
 
 template <int AK, int AV, int GROUP>
-static int dispatch_bits(int bits, const CUtensorMap& tmap, const DecodeParams& p,
-                         cudaStream_t st) {
+static int dispatch_bits(int bits, const Maps& m, const DecodeParams& p, cudaStream_t st) {
   switch (bits) {
-    case 2: return launch_decode<AK, AV, 2, GROUP>(tmap, p, st);
-    case 3: return launch_decode<AK, AV, 3, GROUP>(tmap, p, st);
-    case 4: return launch_decode<AK, AV, 4, GROUP>(tmap, p, st);
-    case 8: return launch_decode<AK, AV, 8, GROUP>(tmap, p, st);
+    case 2: return launch_decode<AK, AV, 2, GROUP>(m, p, st);
+    case 3: return launch_decode<AK, AV, 3, GROUP>(m, p, st);
+    case 4: return launch_decode<AK, AV, 4, GROUP>(m, p, st);
+    case 8: return launch_decode<AK, AV, 8, GROUP>(m, p, st);
     default: return fail(XQ_ECONFIG, "unsupported bits %d", bits);
   }
+}
+
+static int make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
+                    uint64_t inner, uint64_t rows, uint32_t box_inner, uint32_t box_rows,
+                    CUtensorMapSwizzle sw, const char* what) {
+  auto enc = encode_fn();
+  XQ_REQUIRE(enc != nullptr, XQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  XQ_REQUIRE(reinterpret_cast<uintptr_t>(base) % 16 == 0, XQ_ESHAPE, "%s: base not 16-byte aligned", what);
+  XQ_REQUIRE((inner * esize) % 16 == 0, XQ_ESHAPE, "%s: row pitch %llu B not a multiple of 16", what,
+             (unsigned long long)(inner * esize));
+  const cuuint64_t gdim[2] = {inner, rows};
+  const cuuint64_t gstride[1] = {inner * esize};
+  const cuuint32_t box[2] = {box_inner, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  XQ_REQUIRE(r == CUDA_SUCCESS, XQ_ECUDA, "%s: cuTensorMapEncodeTiled failed (%d)", what, (int)r);
+  return XQ_OK;
+}
+
+// codes (uint8 [rows][row_bytes], box = one 128-channel group) + per-token params
+static int stream_maps(int mode, int bits, const void* src, const void* params, int64_t row_bytes,
+                       int64_t kdim, int G, int64_t rows, CUtensorMap* codes, CUtensorMap* pmap) {
+  int st;
+  if (mode == XQ_A_F16_ROWS)
+    return make_map(codes, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, src, kdim, rows, kChunk, kTileM,
+                    CU_TENSOR_MAP_SWIZZLE_128B, "fp16 A rows");
+  XQ_REQUIRE(row_bytes == row_bytes_for(kdim, bits), XQ_ESHAPE, "row_bytes mismatch");
+  if ((st = make_map(codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, src, row_bytes, rows, 16 * bits,
+                     kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "codes")) != XQ_OK)
+    return st;
+  if (mode == XQ_A_CODES_TOKEN)  // byte view of the half2 grid: one 16-byte quad per row
+    return make_map(pmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, params, param_stride(kdim, G) * 4, rows,
+                    16, kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "params");
+  *pmap = *codes;
+  return XQ_OK;
 }
 
 }  // namespace xq
@@ -636,11 +799,12 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
                      const void* av_params, int32_t av_bits, int64_t av_row_bytes,
                      int32_t group_size, int64_t L_max, int64_t kdim, const int32_t* seq_lens,
                      int32_t n_seqs, int32_t max_len, const void* w_arranged, int32_t n_kv_heads,
-                     int32_t group, const float* q_pre, const void* rope_cs, float sm_scale,
-                     int32_t tiles_per_chunk, void* workspace, int64_t workspace_bytes,
-                     float* out, void* stream) {
-  XQ_REQUIRE(kdim % kChunk == 0 && kdim >= kChunk, XQ_ESHAPE,
-             "kdim must be a positive multiple of 64, got %lld", (long long)kdim);
+                     int32_t group, const float* q_pre, const void* rope_cs, int64_t rope_n,
+                     float sm_scale, int32_t tiles_per_chunk, void* workspace,
+                     int64_t workspace_bytes, float* out, void* stream) {
+  XQ_REQUIRE(rope_n >= max_len, XQ_ESHAPE, "rope table shorter than max_len");
+  XQ_REQUIRE(kdim % (2 * kChunk) == 0 && kdim >= 2 * kChunk, XQ_ESHAPE,
+             "kdim must be a positive multiple of 128, got %lld", (long long)kdim);
   XQ_REQUIRE(group_size % kChunk == 0, XQ_ECONFIG,
              "fused kernel needs group_size a multiple of 64, got %d", group_size);
   XQ_REQUIRE(tiles_per_chunk >= 1, XQ_ECONFIG, "tiles_per_chunk must be >= 1");
@@ -661,18 +825,24 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
                "shared A operand must be CODES_TOKEN or F16_ROWS");
   }
   XQ_REQUIRE(ak_mode == XQ_A_F16_ROWS || valid_bits(ak_bits), XQ_ECONFIG, "bad bits %d", ak_bits);
-  auto enc = encode_fn();
-  XQ_REQUIRE(enc != nullptr, XQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
-
-  CUtensorMap tmap;
-  const cuuint64_t gdim[2] = {static_cast<cuuint64_t>(kdim), static_cast<cuuint64_t>(n_kv_heads) * 256};
-  const cuuint64_t gstride[1] = {static_cast<cuuint64_t>(kdim) * 2};
-  const cuuint32_t box[2] = {kChunk, 256};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(w_arranged), gdim,
-                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  XQ_REQUIRE(r == CUDA_SUCCESS, XQ_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  Maps maps;
+  int st_;
+  if ((st_ = make_map(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_arranged, kdim,
+                      (uint64_t)n_kv_heads * 256, kChunk, 256, CU_TENSOR_MAP_SWIZZLE_128B,
+                      "weights")) != XQ_OK)
+    return st_;
+  const int64_t arena_rows = (int64_t)n_seqs * L_max;
+  if ((st_ = stream_maps(ak_mode, ak_bits, ak_src, ak_params, ak_row_bytes, kdim, group_size,
+                         arena_rows, &maps.ca, &maps.pa)) != XQ_OK)
+    return st_;
+  if (!mha) {
+    if ((st_ = stream_maps(av_mode, av_bits, av_src, av_params, av_row_bytes, kdim, group_size,
+                           arena_rows, &maps.cb, &maps.pb)) != XQ_OK)
+      return st_;
+  } else {
+    maps.cb = maps.ca;
+    maps.pb = maps.pa;
+  }
 
   DecodeParams p;
   p.ak_src = static_cast<const uint8_t*>(ak_src);
@@ -693,6 +863,7 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
   p.n_units = n_seqs * p.n_chunks * n_kv_heads;
   p.q_pre = q_pre;
   p.rope = static_cast<const float2*>(rope_cs);
+  p.rope_n = rope_n;
   p.q_scale = sm_scale * 1.4426950408889634f;
   p.partials = static_cast<float*>(workspace);
   p.dbg_acc = g_dbg_acc;
@@ -703,14 +874,14 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
   if (mha) {
     XQ_REQUIRE(group == 1, XQ_ECONFIG, "MHA (shared A) needs group 1, got %d", group);
     if (ak_mode == XQ_A_F16_ROWS)
-      status = launch_decode<XQ_A_F16_ROWS, XQ_A_SAME, 4, 1>(tmap, p, st);
+      status = launch_decode<XQ_A_F16_ROWS, XQ_A_SAME, 4, 1>(maps, p, st);
     else
-      status = dispatch_bits<XQ_A_CODES_TOKEN, XQ_A_SAME, 1>(ak_bits, tmap, p, st);
+      status = dispatch_bits<XQ_A_CODES_TOKEN, XQ_A_SAME, 1>(ak_bits, maps, p, st);
   } else {
     switch (group) {
-      case 1: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 1>(ak_bits, tmap, p, st); break;
-      case 2: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 2>(ak_bits, tmap, p, st); break;
-      case 4: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 4>(ak_bits, tmap, p, st); break;
+      case 1: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 1>(ak_bits, maps, p, st); break;
+      case 2: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 2>(ak_bits, maps, p, st); break;
+      case 4: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 4>(ak_bits, maps, p, st); break;
       default: return fail(XQ_ECONFIG, "unsupported GQA group %d (1, 2, 4)", group);
     }
   }

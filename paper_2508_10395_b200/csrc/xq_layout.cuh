@@ -40,4 +40,11 @@ __host__ __device__ inline int perm_position(int j, int bs) {
   return j < h ? 2 * j : 2 * (j - h) + 1;
 }
 
+// Row stride (in half2 entries) of the per-token (scale, zp) grid: padded to a
+// multiple of 4 groups so a 128-row TMA box of 16-byte rows can stage it.
+__host__ __device__ inline int64_t param_stride(int64_t cols, int G) {
+  const int64_t ng = (cols + G - 1) / G;
+  return (ng + 3) / 4 * 4;
+}
+
 }  // namespace xq

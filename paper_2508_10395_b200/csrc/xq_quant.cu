@@ -156,7 +156,7 @@ __global__ void k_quantize_rows(const void* __restrict__ x, int dt, int64_t x_st
   __syncthreads();
   const int64_t i = blockIdx.x;
   const int64_t dst = lens ? i * L_max + (lens[i] - 1) : row0 + i;
-  const int64_t ng = (cols + G - 1) / G;
+  const int64_t ng = param_stride(cols, G);
   int bad = 0;
   quantize_row(x, dt, i * x_stride, cols, G, bits, sub_rows ? sub_rows + dst * cols : nullptr,
                s_codes, x_eff ? x_eff + i * cols : nullptr, &bad,
@@ -248,7 +248,7 @@ XQ_DEVINL uint32_t read_code(const uint8_t* row, int64_t c, int bits) {
 XQ_DEVINL float2 load_params(const void* params, int axis, int bits, int G, int64_t cols,
                              int64_t r, int64_t c) {
   if (axis == 0) {
-    const int64_t ng = (cols + G - 1) / G;
+    const int64_t ng = param_stride(cols, G);
     const __half2 p = static_cast<const __half2*>(params)[r * ng + c / G];
     return make_float2(__low2float(p), __high2float(p));
   }
@@ -271,7 +271,8 @@ __global__ void k_dequant_rows(const uint8_t* __restrict__ codes, int64_t row_by
   }
 }
 
-__global__ void k_rope_table(float2* __restrict__ cs, int64_t n_pos, int hd, double theta) {
+__global__ void k_rope_table(float2* __restrict__ cs, int64_t n_pos, int hd, double theta,
+                             int j_major) {
   const int half = hd / 2;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pos * half;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -279,7 +280,8 @@ __global__ void k_rope_table(float2* __restrict__ cs, int64_t n_pos, int hd, dou
     const int j = i % half;
     const double freq = pow(theta, (-2.0 * j) / hd);  // linalg.py:85
     const double ang = static_cast<double>(pos) * freq;  // linalg.py:86
-    cs[i] = make_float2(static_cast<float>(cos(ang)), static_cast<float>(sin(ang)));
+    const float2 v = make_float2(static_cast<float>(cos(ang)), static_cast<float>(sin(ang)));
+    cs[j_major ? (int64_t)j * n_pos + pos : i] = v;
   }
 }
 
@@ -318,7 +320,7 @@ __global__ void k_cl_accumulate(int seed, const uint8_t* __restrict__ codes, int
   const int b = blockIdx.x / max_len, t = blockIdx.x % max_len;
   if (t >= lens[b]) return;
   const int64_t r = (int64_t)b * L_max + t;
-  const int64_t ng = (cols + G - 1) / G;
+  const int64_t ng = param_stride(cols, G);
   const uint8_t* crow = codes + r * row_bytes;
   for (int64_t c0 = (int64_t)threadIdx.x * 8; c0 < cols; c0 += (int64_t)blockDim.x * 8) {
     uint64_t packed = 0;  // 8 codes = `bits` bytes, starting at byte bits*c0/8
@@ -458,11 +460,12 @@ int xq_dequant_rows(const uint8_t* codes, int64_t row_bytes, const void* params,
   return check_launch("xq_dequant_rows");
 }
 
-int xq_rope_table(void* cs_out, int64_t n_pos, int32_t head_dim, double theta, void* stream) {
+int xq_rope_table(void* cs_out, int64_t n_pos, int32_t head_dim, double theta, int32_t j_major,
+                  void* stream) {
   XQ_REQUIRE(head_dim % 2 == 0, XQ_ECONFIG, "head_dim must be even, got %d", head_dim);
   if (n_pos == 0) return XQ_OK;
   k_rope_table<<<grid_for(n_pos * head_dim / 2, 256), 256, 0, (cudaStream_t)stream>>>(
-      static_cast<float2*>(cs_out), n_pos, head_dim, theta);
+      static_cast<float2*>(cs_out), n_pos, head_dim, theta, j_major);
   return check_launch("xq_rope_table");
 }
 

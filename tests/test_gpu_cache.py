@@ -29,7 +29,8 @@ def M():
 
 
 def _params_np(stream, n_rows):
-    p = stream.params[:n_rows].float().cpu().numpy()
+    ng = -(-stream.width // stream.g)
+    p = stream.params[:n_rows, :ng].float().cpu().numpy()
     return p[..., 0].astype(np.float64), p[..., 1].astype(np.float64)
 
 
