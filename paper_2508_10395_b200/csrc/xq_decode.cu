@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmap_w);
     if constexpr (!PROD) tma_prefetch_desc(&tmap_ca);
   }
-  if (warp == 2 && lane == 0 && PROD) {
+  if (warp == 2 && lane == 0 && PROD) {  // descriptor prefetch
     tma_prefetch_desc(&tmap_ca);
     if constexpr (AK == XQ_A_CODES_TOKEN) tma_prefetch_desc(&tmap_pa);
     if constexpr (A_TILES == 2) {
@@ -337,62 +337,69 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------ TMA: W tiles (+ fp16 A rows)
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const Unit w = get_unit(p, u);
-        for (int t = w.t0; t < w.t1; ++t) {
-          const int32_t arow0 = static_cast<int32_t>((int64_t)w.b * p.L_max + t * kTileM);
-          for (int kc = 0; kc < nkc; ++kc, ++it) {
-            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-            mbar_wait(&empty[s], ph ^ 1);
+    // Converged warp; one elected lane issues (uniform operands, no waterfall).
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const Unit w = get_unit(p, u);
+      for (int t = w.t0; t < w.t1; ++t) {
+        const int32_t arow0 = static_cast<int32_t>((int64_t)w.b * p.L_max + t * kTileM);
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
             mbar_arrive_expect_tx(&full[s], kBBytes + (PROD ? 0u : kABytes));
             tma_load_2d(sB + s * kBBytes, &tmap_w, &full[s], kc * kChunk, w.h * 256, kEvictLast);
             if constexpr (!PROD)
               tma_load_2d(sA + s * kABytes, &tmap_ca, &full[s], kc * kChunk, arow0, kEvictNormal);
           }
+          __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t kIdesc256 = idesc_f16_f32(128, 256);
-      constexpr uint32_t kIdesc128 = idesc_f16_f32(128, 128);
-      uint32_t it = 0, tc = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const Unit w = get_unit(p, u);
-        for (int t = w.t0; t < w.t1; ++t, ++tc) {
-          const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-          mbar_wait(&tempty[a], aph ^ 1);
+    constexpr uint32_t kIdesc256 = idesc_f16_f32(128, 256);
+    constexpr uint32_t kIdesc128 = idesc_f16_f32(128, 128);
+    const uint64_t a_desc0 = sdesc_sw128(smem_u32(sA));
+    const uint64_t b_desc0 = sdesc_sw128(smem_u32(sB));
+    uint32_t it = 0, tc = 0;
+    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const Unit w = get_unit(p, u);
+      for (int t = w.t0; t < w.t1; ++t, ++tc) {
+        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+        mbar_wait(&tempty[a], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + a * 256;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t d = tmem + a * 256;
-          for (int kc = 0; kc < nkc; ++kc, ++it) {
-            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-            mbar_wait(&full[s], ph);
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + s * A_TILES * kABytes);
-            const uint32_t b0 = smem_u32(sB + s * kBBytes);
+          // descriptor start-address field is addr>>4: +2 per 32-byte K step
+          const uint64_t ad = a_desc0 + ((s * A_TILES * kABytes) >> 4);
+          const uint64_t bd = b_desc0 + ((s * kBBytes) >> 4);
+          if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < kChunk / 16; ++k) {
               const uint32_t acc = (kc | k) != 0;
               if constexpr (A_TILES == 1) {
-                mma_f16_ss(d, sdesc_sw128(a0 + 32 * k), sdesc_sw128(b0 + 32 * k), kIdesc256, acc);
+                mma_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc256, acc);
               } else {
-                mma_f16_ss(d, sdesc_sw128(a0 + 32 * k), sdesc_sw128(b0 + 32 * k), kIdesc128, acc);
-                mma_f16_ss(d + 128, sdesc_sw128(a0 + kABytes + 32 * k),
-                           sdesc_sw128(b0 + 128 * 128 + 32 * k), kIdesc128, acc);
+                mma_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc128, acc);
+                mma_f16_ss(d + 128, ad + (kABytes >> 4) + 2 * k, bd + ((128 * 128) >> 4) + 2 * k,
+                           kIdesc128, acc);
               }
             }
             mma_commit(&empty[s]);
           }
-          mma_commit(&tfull[a]);
+          __syncwarp();
         }
+        if (elect_one()) mma_commit(&tfull[a]);
+        __syncwarp();
       }
     }
   } else if (warp == 2) {
     // ------------------------------------------------ TMA: codes ring
-    if (PROD && lane == 0) {
+    if constexpr (PROD) {
       uint32_t ci = 0;
       for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Unit w = get_unit(p, u);
@@ -401,18 +408,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int g = 0; g < nkc / 2; ++g, ++ci) {
             const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
             mbar_wait(&cempty[cs], cph ^ 1);
-            uint8_t* st = sC + cs * R::kStageBytes;
-            mbar_arrive_expect_tx(&cfull[cs], A_TILES * R::kCodeBytes + R::kTokenStreams * R::kParamBytes);
-            // params quad holding this 128-channel block's group(s); a TMA box must
-            // start on a 16-byte boundary of the inner dimension
-            const int32_t pq = ((2 * kChunk * g) / p.group_size) & ~3;
-            tma_load_2d(st + R::code_off(0), &tmap_ca, &cfull[cs], g * R::kGB, arow0, kEvictFirst);
-            if constexpr (AK == XQ_A_CODES_TOKEN)
-              tma_load_2d(st + R::param_off(0), &tmap_pa, &cfull[cs], 4 * pq, arow0, kEvictFirst);
-            if constexpr (A_TILES == 2) {
-              tma_load_2d(st + R::code_off(1), &tmap_cb, &cfull[cs], g * R::kGB, arow0, kEvictFirst);
-              tma_load_2d(st + R::param_off(1), &tmap_pb, &cfull[cs], 4 * pq, arow0, kEvictFirst);
+            if (elect_one()) {
+              uint8_t* st = sC + cs * R::kStageBytes;
+              mbar_arrive_expect_tx(&cfull[cs],
+                                    A_TILES * R::kCodeBytes + R::kTokenStreams * R::kParamBytes);
+              // params quad holding this 128-channel block's group(s); a TMA box must
+              // start on a 16-byte boundary of the inner dimension
+              const int32_t pq = ((2 * kChunk * g) / p.group_size) & ~3;
+              tma_load_2d(st + R::code_off(0), &tmap_ca, &cfull[cs], g * R::kGB, arow0, kEvictNormal);
+              if constexpr (AK == XQ_A_CODES_TOKEN)
+                tma_load_2d(st + R::param_off(0), &tmap_pa, &cfull[cs], 4 * pq, arow0, kEvictNormal);
+              if constexpr (A_TILES == 2) {
+                tma_load_2d(st + R::code_off(1), &tmap_cb, &cfull[cs], g * R::kGB, arow0, kEvictNormal);
+                tma_load_2d(st + R::param_off(1), &tmap_pb, &cfull[cs], 4 * pq, arow0, kEvictNormal);
+              }
             }
+            __syncwarp();
           }
         }
       }
@@ -739,7 +750,8 @@ static int dispatch_bits(int bits, const Maps& m, const DecodeParams& p, cudaStr
 
 static int make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base,
                     uint64_t inner, uint64_t rows, uint32_t box_inner, uint32_t box_rows,
-                    CUtensorMapSwizzle sw, const char* what) {
+                    CUtensorMapSwizzle sw, const char* what,
+                    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   auto enc = encode_fn();
   XQ_REQUIRE(enc != nullptr, XQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
   XQ_REQUIRE(reinterpret_cast<uintptr_t>(base) % 16 == 0, XQ_ESHAPE, "%s: base not 16-byte aligned", what);
@@ -750,8 +762,7 @@ static int make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const voi
   const cuuint32_t box[2] = {box_inner, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   XQ_REQUIRE(r == CUDA_SUCCESS, XQ_ECUDA, "%s: cuTensorMapEncodeTiled failed (%d)", what, (int)r);
   return XQ_OK;
 }
@@ -765,11 +776,11 @@ static int stream_maps(int mode, int bits, const void* src, const void* params, 
                     CU_TENSOR_MAP_SWIZZLE_128B, "fp16 A rows");
   XQ_REQUIRE(row_bytes == row_bytes_for(kdim, bits), XQ_ESHAPE, "row_bytes mismatch");
   if ((st = make_map(codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, src, row_bytes, rows, 16 * bits,
-                     kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "codes")) != XQ_OK)
+                     kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "codes", CU_TENSOR_MAP_L2_PROMOTION_L2_128B)) != XQ_OK)
     return st;
   if (mode == XQ_A_CODES_TOKEN)  // byte view of the half2 grid: one 16-byte quad per row
     return make_map(pmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, params, param_stride(kdim, G) * 4, rows,
-                    16, kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "params");
+                    16, kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "params", CU_TENSOR_MAP_L2_PROMOTION_NONE);
   *pmap = *codes;
   return XQ_OK;
 }
