@@ -403,14 +403,14 @@ class CacheBackend:
 
 
 def default_tiles_per_chunk(n_slots: int, max_len: int, n_kv: int, n_sm: int = 148,
-                            max_tiles: int = 4) -> int:
-    """Tiles (of 128 tokens) per work unit.
+                            max_tiles: int = 2) -> int:
+    """Tiles (of 256 tokens, one per CTA pair) per work unit.
 
-    Enough units for >= ~4 waves of SMs, and at most ``max_tiles`` tiles per
-    unit: units are ordered KV-head-fastest, so the CTAs in flight cover only
-    a few token ranges and every head re-reads those codes from L2, not HBM."""
-    n_tiles = max(1, -(-max_len // 128))
-    target_units = 4 * n_sm
+    Enough units for >= ~4 waves of CTA pairs, and at most ``max_tiles`` tiles
+    per unit: units are ordered KV-head-fastest, so the pairs in flight cover
+    only a few token ranges and every head re-reads those codes from L2."""
+    n_tiles = max(1, -(-max_len // 256))
+    target_units = 2 * n_sm
     per_seq_head = max(1, n_slots * n_kv)
     chunks = max(1, min(n_tiles, -(-target_units // per_seq_head)))
     return max(1, min(max_tiles, -(-n_tiles // chunks)))

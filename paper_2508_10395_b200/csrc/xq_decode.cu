@@ -20,6 +20,7 @@
 // kernel merges the per-(chunk, warp) partials.
 #include <cudaTypedefs.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "xq_common.cuh"
 #include "xq_host.h"
@@ -27,14 +28,16 @@
 
 namespace xq {
 
-constexpr int kTileM = 128;
+constexpr int kTileM = 128;  // token rows per CTA (TMEM lanes)
+constexpr int kPairM = 256;  // token rows per CTA pair (cta_group::2 MMA, M = 256)
 constexpr int kChunk = 64;  // K elements per stage (128 B of fp16 = one swizzle row)
 constexpr int kThreads = 512;
 constexpr int kProdWarp0 = 4;
 constexpr int kEpiWarp0 = 12;
 constexpr int kPartStride = 2 + kHeadDim;  // m, l, o[128]
+constexpr int kPartsPerChunk = 8;          // 2 CTAs x 4 epilogue warps
 constexpr uint32_t kABytes = kTileM * 128;  // 16 KB
-constexpr uint32_t kBBytes = 256 * 128;     // 32 KB
+constexpr uint32_t kBBytes = 128 * 128;     // 16 KB: this CTA's half (N/2 = 128 rows) of W
 
 struct DecodeParams {
   const uint8_t* ak_src;
@@ -60,6 +63,7 @@ struct DecodeParams {
   float* partials;
   float* dbg_acc;  // optional: raw [b][h][tile][128][256] accumulator dump
   int32_t dbg_tiles;
+  uint64_t w_hint;  // L2 cache policy of the weight TMA loads
 };
 
 static float* g_dbg_acc = nullptr;
@@ -76,7 +80,7 @@ XQ_DEVINL Unit get_unit(const DecodeParams& p, int u) {
   w.chunk = rest % p.n_chunks;
   w.b = rest / p.n_chunks;
   w.len = p.seq_lens[w.b];
-  const int nt = (w.len + kTileM - 1) / kTileM;
+  const int nt = (w.len + kPairM - 1) / kPairM;  // tiles of 256 tokens (one per CTA pair)
   w.t0 = w.chunk * p.tiles_per_chunk;
   w.t1 = min(w.t0 + p.tiles_per_chunk, nt);
   if (w.t1 < w.t0) w.t1 = w.t0;
@@ -184,9 +188,10 @@ struct Ring {
   static constexpr uint32_t kParamBytes = kTileM * 16;
   static constexpr uint32_t kStageBytes =
       kProducers ? ((kStreams * kCodeBytes + kTokenStreams * kParamBytes + 127) / 128 * 128) : 0;
-  static constexpr int kABStages = kStreams == 1 ? (BITS == 8 ? 3 : 4) : (BITS == 8 ? 2 : 3);
-  static constexpr uint32_t kABBytes = kABStages * (kStreams * kABytes + kBBytes);
-  static constexpr uint32_t kBudget = 225 * 1024 - kABBytes - 8 * 1024;
+  static constexpr uint32_t kABStage = kStreams * kABytes + kBBytes;
+  static constexpr int kABStages = kStreams == 1 ? (BITS == 8 ? 4 : 5) : (BITS == 8 ? 2 : 3);
+  static constexpr uint32_t kABBytes = kABStages * kABStage;
+  static constexpr uint32_t kBudget = 222 * 1024 - kABBytes - 6 * 1024;
   static constexpr int kCodeStages =
       !kProducers ? 0 : (kBudget / kStageBytes >= 4 ? 4 : (kBudget / kStageBytes < 1 ? 1 : kBudget / kStageBytes));
   // stage layout: [s0 codes][s1 codes][s0 params if TOKEN][s1 params if TOKEN]
@@ -269,7 +274,7 @@ XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t
 }
 
 template <int AK, int AV, int BITS, int GROUP>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_decode_attend(const __grid_constant__ CUtensorMap tmap_w,
                     const __grid_constant__ CUtensorMap tmap_ca,
                     const __grid_constant__ CUtensorMap tmap_pa,
@@ -285,9 +290,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + STAGES * A_TILES * kABytes;
-  uint8_t* sC = sB + STAGES * kBBytes;  // codes ring
+  // per stage: [A stream 0][A stream 1][B half]
+  uint8_t* sAB = smem;
+  uint8_t* sC = sAB + STAGES * R::kABStage;  // codes ring
   uint64_t* full = reinterpret_cast<uint64_t*>(sC + CSTAGES * R::kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* cfull = empty + STAGES;
@@ -298,18 +303,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* q_s = reinterpret_cast<float*>(tmem_slot + 4);  // [GROUP][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMA), 1 = peer
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], PROD ? 4 + 1 : 1);  // producer warps of one group + TMA expect_tx
-      mbar_init(&empty[s], 1);
+      // leader's full: 2 TMA arrivals (one per CTA) + 8 producer warps (4 per CTA)
+      mbar_init(&full[s], PROD ? 2 + 8 : 2);
+      mbar_init(&empty[s], 1);  // multicast MMA commit
     }
     for (int s = 0; s < CSTAGES; ++s) {
       mbar_init(&cfull[s], 1);
-      mbar_init(&cempty[s], 8);  // every producer warp reads every codes stage
+      mbar_init(&cempty[s], 8);  // every producer warp of this CTA reads every codes stage
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tfull[a], 1);   // multicast MMA commit
+      mbar_init(&tempty[a], 8);  // leader's: 4 epilogue warps per CTA
     }
     fence_mbar_init();
   }
@@ -326,85 +335,99 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, 512);
-    tmem_relinquish();
+    tmem_alloc2(tmem_slot, 512);
+    tmem_relinquish2();
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nkc = p.kdim / kChunk;
+  const uint32_t full_leader0 = mapa_shared(smem_u32(&full[0]), 0);
+  const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA: W tiles (+ fp16 A rows)
-    // Converged warp; one elected lane issues (uniform operands, no waterfall).
+    // ------------------------------------------------ TMA: this CTA's W half (+ fp16 A rows)
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    for (int u = cluster; u < p.n_units; u += n_clusters) {
       const Unit w = get_unit(p, u);
       for (int t = w.t0; t < w.t1; ++t) {
-        const int32_t arow0 = static_cast<int32_t>((int64_t)w.b * p.L_max + t * kTileM);
+        const int32_t arow0 = static_cast<int32_t>((int64_t)w.b * p.L_max + t * kPairM + rank * kTileM);
         for (int kc = 0; kc < nkc; ++kc, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           if (elect_one()) {
-            mbar_arrive_expect_tx(&full[s], kBBytes + (PROD ? 0u : kABytes));
-            tma_load_2d(sB + s * kBBytes, &tmap_w, &full[s], kc * kChunk, w.h * 256, kEvictLast);
+            uint8_t* st = sAB + s * R::kABStage;
+            constexpr uint32_t kTx = 2 * (kBBytes + (PROD ? 0u : kABytes));  // both CTAs
+            if (leader) mbar_arrive_expect_tx(&full[s], kTx);
+            else mbar_arrive_remote(full_leader0 + 8 * s);
+            if constexpr (A_TILES == 1) {  // rows [K_h | V_h] of head h: this CTA's 128
+              tma_load_2d_pair(st + kABytes, &tmap_w, &full[s], kc * kChunk,
+                               w.h * 256 + rank * 128, p.w_hint);
+            } else {  // K half (64 rows of W_k) + V half (64 rows of W_v)
+              tma_load_2d_pair(st + 2 * kABytes, &tmap_w, &full[s], kc * kChunk,
+                               w.h * 256 + rank * 64, p.w_hint);
+              tma_load_2d_pair(st + 2 * kABytes + 64 * 128, &tmap_w, &full[s], kc * kChunk,
+                               w.h * 256 + 128 + rank * 64, p.w_hint);
+            }
             if constexpr (!PROD)
-              tma_load_2d(sA + s * kABytes, &tmap_ca, &full[s], kc * kChunk, arow0, kEvictNormal);
+              tma_load_2d_pair(st, &tmap_ca, &full[s], kc * kChunk, arow0, kEvictNormal);
           }
           __syncwarp();
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    constexpr uint32_t kIdesc256 = idesc_f16_f32(128, 256);
-    constexpr uint32_t kIdesc128 = idesc_f16_f32(128, 128);
-    const uint64_t a_desc0 = sdesc_sw128(smem_u32(sA));
-    const uint64_t b_desc0 = sdesc_sw128(smem_u32(sB));
-    uint32_t it = 0, tc = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-      const Unit w = get_unit(p, u);
-      for (int t = w.t0; t < w.t1; ++t, ++tc) {
-        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-        mbar_wait(&tempty[a], aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + a * 256;
-        for (int kc = 0; kc < nkc; ++kc, ++it) {
-          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-          mbar_wait(&full[s], ph);
+    // ------------------------------------------------ MMA issuer (leader CTA only)
+    if (leader) {
+      constexpr uint32_t kIdesc256 = idesc_f16_f32(256, 256);
+      constexpr uint32_t kIdesc128 = idesc_f16_f32(256, 128);
+      const uint64_t desc0 = sdesc_sw128(smem_u32(sAB));
+      uint32_t it = 0, tc = 0;
+      for (int u = cluster; u < p.n_units; u += n_clusters) {
+        const Unit w = get_unit(p, u);
+        for (int t = w.t0; t < w.t1; ++t, ++tc) {
+          const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+          mbar_wait_cluster(&tempty[a], aph ^ 1);
           tc_fence_after();
-          // descriptor start-address field is addr>>4: +2 per 32-byte K step
-          const uint64_t ad = a_desc0 + ((s * A_TILES * kABytes) >> 4);
-          const uint64_t bd = b_desc0 + ((s * kBBytes) >> 4);
-          if (elect_one()) {
+          const uint32_t d = tmem + a * 256;
+          for (int kc = 0; kc < nkc; ++kc, ++it) {
+            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+            mbar_wait_cluster(&full[s], ph);
+            tc_fence_after();
+            // descriptor start-address field is addr>>4: +2 per 32-byte K step
+            const uint64_t ad = desc0 + ((s * R::kABStage) >> 4);
+            const uint64_t bd = ad + ((A_TILES * kABytes) >> 4);
+            if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < kChunk / 16; ++k) {
-              const uint32_t acc = (kc | k) != 0;
-              if constexpr (A_TILES == 1) {
-                mma_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc256, acc);
-              } else {
-                mma_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc128, acc);
-                mma_f16_ss(d + 128, ad + (kABytes >> 4) + 2 * k, bd + ((128 * 128) >> 4) + 2 * k,
-                           kIdesc128, acc);
+              for (int k = 0; k < kChunk / 16; ++k) {
+                const uint32_t acc = (kc | k) != 0;
+                if constexpr (A_TILES == 1) {
+                  mma2_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc256, acc);
+                } else {
+                  mma2_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc128, acc);
+                  mma2_f16_ss(d + 128, ad + (kABytes >> 4) + 2 * k, bd + ((64 * 128) >> 4) + 2 * k,
+                              kIdesc128, acc);
+                }
               }
+              mma2_commit_both(&empty[s]);
             }
-            mma_commit(&empty[s]);
+            __syncwarp();
           }
+          if (elect_one()) mma2_commit_both(&tfull[a]);
           __syncwarp();
         }
-        if (elect_one()) mma_commit(&tfull[a]);
-        __syncwarp();
       }
     }
   } else if (warp == 2) {
-    // ------------------------------------------------ TMA: codes ring
+    // ------------------------------------------------ TMA: codes ring (this CTA's rows)
     if constexpr (PROD) {
       uint32_t ci = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int u = cluster; u < p.n_units; u += n_clusters) {
         const Unit w = get_unit(p, u);
         for (int t = w.t0; t < w.t1; ++t) {
-          const int32_t arow0 = static_cast<int32_t>((int64_t)w.b * p.L_max + t * kTileM);
+          const int32_t arow0 =
+              static_cast<int32_t>((int64_t)w.b * p.L_max + t * kPairM + rank * kTileM);
           for (int g = 0; g < nkc / 2; ++g, ++ci) {
             const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
             mbar_wait(&cempty[cs], cph ^ 1);
@@ -435,11 +458,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int gp = (warp - kProdWarp0) >> 2;
       const int row = ((warp - kProdWarp0) & 3) * 32 + lane;  // tile row = token
       uint32_t tcount = 0;
-      for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      for (int u = cluster; u < p.n_units; u += n_clusters) {
         const Unit w = get_unit(p, u);
         const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.ak_nflushed + w.b) : 0;
         for (int t = w.t0; t < w.t1; ++t, ++tcount) {
-          const int tok = t * kTileM + row;
+          const int tok = t * kPairM + rank * kTileM + row;
           const bool valid = tok < w.len;
           const int64_t arow = (int64_t)w.b * p.L_max + tok;
           for (int kc = gp; kc < nkc; kc += 2) {
@@ -450,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint8_t* st = sC + cs * R::kStageBytes;
             mbar_wait(&cfull[cs], cph);
             mbar_wait(&empty[s], ph ^ 1);
-            uint8_t* tile = sA + s * A_TILES * kABytes;
+            uint8_t* tile = sAB + s * R::kABStage;
             produce_chunk<AK, BITS>(tile, st + R::code_off(0), st + R::param_off(0), row, valid,
                                     tok, w.b, nfl, arow, kc, p.ak_params, p.ak_resid, p);
             if constexpr (A_TILES == 2)
@@ -460,7 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              mbar_arrive(&full[s]);
+              if (leader) mbar_arrive(&full[s]);
+              else mbar_arrive_remote(full_leader0 + 8 * s);
               mbar_arrive(&cempty[cs]);
             }
           }
@@ -468,14 +492,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= kEpiWarp0) {
-    // ------------------------------------------------ epilogue
+    // ------------------------------------------------ epilogue (this CTA's 128 rows)
     const int ew = warp - kEpiWarp0;  // == warp % 4: TMEM lanes 32*ew ..
     const int et = threadIdx.x - kEpiWarp0 * 32;
     const int row = ew * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(ew * 32) << 16;
     const int n_q = p.n_kv * GROUP;
     uint32_t tc = 0;
-    for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    for (int u = cluster; u < p.n_units; u += n_clusters) {
       const Unit w = get_unit(p, u);
       const int pos = w.len - 1;
       named_bar_sync(1, 128);
@@ -500,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int t = w.t0; t < w.t1; ++t, ++tc) {
         const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-        const int tok = t * kTileM + row;
+        const int tok = t * kPairM + rank * kTileM + row;
         const bool valid = tok < w.len;
         // frequency-major table: lanes read consecutive positions (coalesced)
         const float2* rp = p.rope + (valid ? tok : 0);
@@ -530,8 +554,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (p.dbg_acc != nullptr && t < p.dbg_tiles) {
-          float* drow = p.dbg_acc + ((((int64_t)w.b * p.n_kv + w.h) * p.dbg_tiles + t) * kTileM + row) * 256;
+        if (p.dbg_acc != nullptr && 2 * t + (int)rank < p.dbg_tiles) {
+          float* drow = p.dbg_acc +
+              ((((int64_t)w.b * p.n_kv + w.h) * p.dbg_tiles + 2 * t + rank) * kTileM + row) * 256;
           for (int c = 0; c < 8; ++c) {
             float tmpv[32];
             tmem_ld32(tmem + tlane + a * 256 + c * 32, tmpv);
@@ -566,13 +591,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[a]);
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[a]);
+          else mbar_arrive_remote(tempty_leader0 + 8 * a);
+        }
       }
 #pragma unroll
       for (int gi = 0; gi < GROUP; ++gi) {
         const int hq = w.h * GROUP + gi;
-        float* dst =
-            p.partials + ((((int64_t)w.b * n_q + hq) * p.n_chunks + w.chunk) * 4 + ew) * kPartStride;
+        float* dst = p.partials + ((((int64_t)w.b * n_q + hq) * p.n_chunks + w.chunk) * kPartsPerChunk +
+                                   rank * 4 + ew) * kPartStride;
         if (lane == 0) {
           dst[0] = m_run[gi];
           dst[1] = l_run[gi];
@@ -583,10 +611,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // the leader's MMAs have finished writing both CTAs' TMEM
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc2(tmem, 512);
   }
 }
 
@@ -710,7 +738,7 @@ static int num_sms() {
 }
 
 static int64_t n_chunks_for(int32_t max_len, int32_t tpc) {
-  const int64_t nt = (max_len + kTileM - 1) / kTileM;
+  const int64_t nt = (max_len + kPairM - 1) / kPairM;
   return nt == 0 ? 1 : (nt + tpc - 1) / tpc;
 }
 
@@ -723,6 +751,7 @@ static int launch_decode(const Maps& m, const DecodeParams& p, cudaStream_t st) 
   using R = Ring<AK, AV, BITS>;
   constexpr size_t smem = 1024 + R::kABBytes + R::kCodeStages * R::kStageBytes +
                           (2 * R::kABStages + 8 + 4) * 8 + 16 + GROUP * kHeadDim * 4;
+  static_assert(R::kABStage % 1024 == 0, "stages must keep 1024-byte swizzle alignment");
   static_assert(smem <= 227 * 1024, "shared memory budget");
   auto kern = k_decode_attend<AK, AV, BITS, GROUP>;
   static bool configured = false;
@@ -732,8 +761,9 @@ static int launch_decode(const Maps& m, const DecodeParams& p, cudaStream_t st) 
       return check_launch("cudaFuncSetAttribute(decode)");
     configured = true;
   }
-  const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
-  kern<<<grid, kThreads, smem, st>>>(m.w, m.ca, m.pa, m.cb, m.pb, p);
+  // one CTA pair per unit in flight; an even grid of at most one CTA per SM
+  const int pairs = p.n_units < num_sms() / 2 ? p.n_units : num_sms() / 2;
+  kern<<<2 * pairs, kThreads, smem, st>>>(m.w, m.ca, m.pa, m.cb, m.pb, p);
   return check_launch("k_decode_attend");
 }
 
@@ -800,8 +830,8 @@ int xq_debug_set_acc_dump(float* buf, int32_t n_tiles) {
 int64_t xq_decode_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_kv_heads,
                                   int32_t group, int32_t tiles_per_chunk) {
   if (tiles_per_chunk < 1) tiles_per_chunk = 1;
-  return (int64_t)n_seqs * n_kv_heads * group * n_chunks_for(max_len, tiles_per_chunk) * 4 *
-         kPartStride * sizeof(float);
+  return (int64_t)n_seqs * n_kv_heads * group * n_chunks_for(max_len, tiles_per_chunk) *
+         kPartsPerChunk * kPartStride * sizeof(float);
 }
 
 int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
@@ -839,8 +869,8 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
   Maps maps;
   int st_;
   if ((st_ = make_map(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_arranged, kdim,
-                      (uint64_t)n_kv_heads * 256, kChunk, 256, CU_TENSOR_MAP_SWIZZLE_128B,
-                      "weights")) != XQ_OK)
+                      (uint64_t)n_kv_heads * 256, kChunk, mha ? 128 : 64,
+                      CU_TENSOR_MAP_SWIZZLE_128B, "weights")) != XQ_OK)
     return st_;
   const int64_t arena_rows = (int64_t)n_seqs * L_max;
   if ((st_ = stream_maps(ak_mode, ak_bits, ak_src, ak_params, ak_row_bytes, kdim, group_size,
@@ -879,6 +909,11 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
   p.partials = static_cast<float*>(workspace);
   p.dbg_acc = g_dbg_acc;
   p.dbg_tiles = g_dbg_tiles;
+  {
+    const char* e = getenv("XQ_W_HINT");  // experiment knob: 0 normal, 1 evict_last, 2 evict_first
+    const int h = e ? atoi(e) : 1;
+    p.w_hint = h == 0 ? kEvictNormal : (h == 2 ? kEvictFirst : kEvictLast);
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   int status;
@@ -897,7 +932,7 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
     }
   }
   if (status != XQ_OK) return status;
-  const int n_parts = p.n_chunks * 4;
+  const int n_parts = p.n_chunks * kPartsPerChunk;
   k_combine<<<static_cast<unsigned>(n_seqs) * n_kv_heads * group, kHeadDim, 0, st>>>(
       p.partials, n_parts, out);
   return check_launch("k_combine");

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--layers", type=int, default=None)
 ap.add_argument("--variant", default=None)
+ap.add_argument("--tpc", type=int, default=None)
 args = ap.parse_args()
 cfg = dict(bench.CONFIGS[args.config])
 if args.variant:
@@ -27,7 +28,7 @@ n_layers = args.layers or cfg.get("layers", shape.n_layers)
 B, ctx = cfg["batch"], cfg["ctx"]
 L_max = -(-(ctx + 8) // 128) * 128
 w, wq = D.synthetic_weights(shape, cfg["variant"], dev, layers=n_layers)
-dec = D.Decoder(shape, cfg["variant"], cfg["bits"], B, L_max, w, wq, device=dev)
+dec = D.Decoder(shape, cfg["variant"], cfg["bits"], B, L_max, w, wq, device=dev, tiles_per_chunk=args.tpc)
 dec.fill_synthetic(ctx)
 xs = [torch.randn(n_layers, B, shape.hidden_dim, device=dev).to(torch.bfloat16) for _ in range(2)]
 dec.step(xs[0])
