@@ -36,6 +36,7 @@ constexpr int kProdWarp0 = 4;
 constexpr int kEpiWarp0 = 12;
 constexpr int kPartStride = 2 + kHeadDim;  // m, l, o[128]
 constexpr int kPartsPerChunk = 8;          // 2 CTAs x 4 epilogue warps
+constexpr int kG = 128;                    // quantization group (the reference default, cache.py:44)
 constexpr uint32_t kABytes = kTileM * 128;  // 16 KB
 constexpr uint32_t kBBytes = 128 * 128;     // 16 KB: this CTA's half (N/2 = 128 rows) of W
 
@@ -96,9 +97,19 @@ XQ_DEVINL T from_u32(uint32_t v) {
   return *reinterpret_cast<T*>(&v);
 }
 
-// codes (at bits 0.. and 16..) -> fp16 pair c*s + z, one rounding
-XQ_DEVINL uint32_t deq_pair(uint32_t masked, __half2 s2, __half2 z2) {
-  const __half2 c = __hsub2(from_u32<__half2>(masked | 0x64006400u), __float2half2_rn(1024.f));
+// (a & mask) | magic in one LOP3: both constants live in registers (a LOP3
+// takes a single immediate, so nvcc would otherwise emit two instructions).
+XQ_DEVINL uint32_t and_or(uint32_t a, uint32_t mask, uint32_t magic) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(mask), "r"(magic));
+  return d;
+}
+
+// codes at bits 0.. and 16.. of `bits` (unmasked) -> fp16 pair c*s + z, one rounding:
+// 0x6400|c is the fp16 value 1024+c, exactly; subtracting 1024 is exact.
+XQ_DEVINL uint32_t deq_pair(uint32_t bits, uint32_t mask, __half2 s2, __half2 z2) {
+  const uint32_t magic = 0x64006400u;
+  const __half2 c = __hsub2(from_u32<__half2>(and_or(bits, mask, magic)), __float2half2_rn(1024.f));
   return as_u32(__hfma2(c, s2, z2));
 }
 
@@ -133,19 +144,19 @@ XQ_DEVINL void convert_raw(const uint32_t (&w)[2 * BITS], const __half2* s2, con
     for (int wi = 0; wi < 8; ++wi)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        out[4 * wi + j] = deq_pair((w[wi] >> (4 * j)) & 0x000F000Fu, S(4 * wi + j), Z(4 * wi + j));
+        out[4 * wi + j] = deq_pair(w[wi] >> (4 * j), 0x000F000Fu, S(4 * wi + j), Z(4 * wi + j));
   } else if constexpr (BITS == 2) {
 #pragma unroll
     for (int wi = 0; wi < 4; ++wi)
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        out[8 * wi + j] = deq_pair((w[wi] >> (2 * j)) & 0x00030003u, S(8 * wi + j), Z(8 * wi + j));
+        out[8 * wi + j] = deq_pair(w[wi] >> (2 * j), 0x00030003u, S(8 * wi + j), Z(8 * wi + j));
   } else if constexpr (BITS == 8) {
 #pragma unroll
     for (int wi = 0; wi < 16; ++wi)
 #pragma unroll
       for (int j = 0; j < 2; ++j)
-        out[2 * wi + j] = deq_pair((w[wi] >> (8 * j)) & 0x00FF00FFu, S(2 * wi + j), Z(2 * wi + j));
+        out[2 * wi + j] = deq_pair(w[wi] >> (8 * j), 0x00FF00FFu, S(2 * wi + j), Z(2 * wi + j));
   } else {  // 3-bit: two 32-code blocks of 3 words each
 #pragma unroll
     for (int bi = 0; bi < 2; ++bi) {
@@ -156,8 +167,8 @@ XQ_DEVINL void convert_raw(const uint32_t (&w)[2 * BITS], const __half2* s2, con
         const int o_lo = 3 * j, o_hi = 3 * j + 32;
         const uint32_t lo = (o_lo < 32) ? __funnelshift_r(w0, w1, o_lo) : (w1 >> (o_lo - 32));
         const uint32_t hi = (o_hi < 64) ? __funnelshift_r(w1, w2, o_hi - 32) : (w2 >> (o_hi - 64));
-        const uint32_t m = __byte_perm(lo, hi, 0x7610) & 0x00070007u;
-        out[16 * bi + j] = deq_pair(m, S(16 * bi + j), Z(16 * bi + j));
+        out[16 * bi + j] = deq_pair(__byte_perm(lo, hi, 0x7610), 0x00070007u, S(16 * bi + j),
+                                    Z(16 * bi + j));
       }
     }
   }
@@ -236,8 +247,8 @@ XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t
   if constexpr (MODE == XQ_A_CODES_TOKEN) {
     uint32_t raw[2 * BITS];
     lds_raw<BITS>(crow, raw);
-    // params quad starts at group ((128*(kc/2))/G) & ~3; this chunk's group is (64*kc)/G
-    const int gq = (kChunk * kc) / p.group_size - (((2 * kChunk * (kc >> 1)) / p.group_size) & ~3);
+    // G = 128: this chunk's group is kc/2; the staged quad starts at group (kc/2) & ~3
+    const int gq = (kc >> 1) & 3;
     const __half2 sz = *reinterpret_cast<const __half2*>(pstage + row * 16 + 4 * gq);
     const __half2 s2 = __low2half2(sz), z2 = __high2half2(sz);
     convert_raw<BITS, false>(raw, &s2, &z2, v);
@@ -248,7 +259,7 @@ XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t
       lds_raw<BITS>(crow, raw);
       // per-channel params: shared by the whole tile -> L1 broadcast
       const __half* prow =
-          static_cast<const __half*>(gparams) + (arow / p.group_size) * 2 * p.kdim + kc * kChunk;
+          static_cast<const __half*>(gparams) + (arow / kG) * 2 * p.kdim + kc * kChunk;
       __half2 s2[32], z2[32];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -261,7 +272,7 @@ XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t
       }
       convert_raw<BITS, true>(raw, s2, z2, v);
     } else {  // residual full-precision row (cache.py:228-229)
-      const float* r = resid + ((int64_t)b * p.group_size + (tok - nflushed)) * p.kdim + kc * kChunk;
+      const float* r = resid + ((int64_t)b * kG + (tok - nflushed)) * p.kdim + kc * kChunk;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int blk = (2 * j) / BS, jj = j % (BS / 2);
@@ -314,7 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < CSTAGES; ++s) {
       mbar_init(&cfull[s], 1);
-      mbar_init(&cempty[s], 8);  // every producer warp of this CTA reads every codes stage
+      mbar_init(&cempty[s], 4);  // the 4 warps of the producer group that owns the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);   // multicast MMA commit
@@ -437,7 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                     A_TILES * R::kCodeBytes + R::kTokenStreams * R::kParamBytes);
               // params quad holding this 128-channel block's group(s); a TMA box must
               // start on a 16-byte boundary of the inner dimension
-              const int32_t pq = ((2 * kChunk * g) / p.group_size) & ~3;
+              const int32_t pq = g & ~3;  // G = 128: group g of the row
               tma_load_2d(st + R::code_off(0), &tmap_ca, &cfull[cs], g * R::kGB, arow0, kEvictNormal);
               if constexpr (AK == XQ_A_CODES_TOKEN)
                 tma_load_2d(st + R::param_off(0), &tmap_pa, &cfull[cs], 4 * pq, arow0, kEvictNormal);
@@ -453,10 +464,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
     // ------------------------------------------------ dequant producers
-    // Group gp owns the K-chunks kc == gp (mod 2) of every tile (nkc is even).
+    // Group gp owns the codes groups (128 channels = two K-chunks) whose running
+    // index is == gp (mod 2); per owned group: one codes-stage wait, two A stages.
     if constexpr (PROD) {
       const int gp = (warp - kProdWarp0) >> 2;
       const int row = ((warp - kProdWarp0) & 3) * 32 + lane;  // tile row = token
+      const int ngrp = nkc / 2;
       uint32_t tcount = 0;
       for (int u = cluster; u < p.n_units; u += n_clusters) {
         const Unit w = get_unit(p, u);
@@ -465,28 +478,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int tok = t * kPairM + rank * kTileM + row;
           const bool valid = tok < w.len;
           const int64_t arow = (int64_t)w.b * p.L_max + tok;
-          for (int kc = gp; kc < nkc; kc += 2) {
-            const uint32_t ci = tcount * (nkc / 2) + (kc >> 1);
+          const uint32_t ci0 = tcount * ngrp;
+          for (int g = (ci0 & 1) == static_cast<uint32_t>(gp) ? 0 : 1; g < ngrp; g += 2) {
+            const uint32_t ci = ci0 + g;
             const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
-            const uint32_t it = tcount * nkc + kc;
-            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
             const uint8_t* st = sC + cs * R::kStageBytes;
             mbar_wait(&cfull[cs], cph);
-            mbar_wait(&empty[s], ph ^ 1);
-            uint8_t* tile = sAB + s * R::kABStage;
-            produce_chunk<AK, BITS>(tile, st + R::code_off(0), st + R::param_off(0), row, valid,
-                                    tok, w.b, nfl, arow, kc, p.ak_params, p.ak_resid, p);
-            if constexpr (A_TILES == 2)
-              produce_chunk<AVM, BITS>(tile + kABytes, st + R::code_off(1), st + R::param_off(1),
-                                       row, valid, tok, w.b, 1 << 30, arow, kc, p.av_params,
-                                       nullptr, p);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              if (leader) mbar_arrive(&full[s]);
-              else mbar_arrive_remote(full_leader0 + 8 * s);
-              mbar_arrive(&cempty[cs]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int kc = 2 * g + h;
+              const uint32_t it = tcount * nkc + kc;
+              const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+              mbar_wait(&empty[s], ph ^ 1);
+              uint8_t* tile = sAB + s * R::kABStage;
+              produce_chunk<AK, BITS>(tile, st + R::code_off(0), st + R::param_off(0), row, valid,
+                                      tok, w.b, nfl, arow, kc, p.ak_params, p.ak_resid, p);
+              if constexpr (A_TILES == 2)
+                produce_chunk<AVM, BITS>(tile + kABytes, st + R::code_off(1), st + R::param_off(1),
+                                         row, valid, tok, w.b, 1 << 30, arow, kc, p.av_params,
+                                         nullptr, p);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                if (leader) mbar_arrive(&full[s]);
+                else mbar_arrive_remote(full_leader0 + 8 * s);
+              }
             }
+            if (lane == 0) mbar_arrive(&cempty[cs]);
           }
         }
       }
@@ -846,8 +864,9 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
   XQ_REQUIRE(rope_n >= max_len, XQ_ESHAPE, "rope table shorter than max_len");
   XQ_REQUIRE(kdim % (2 * kChunk) == 0 && kdim >= 2 * kChunk, XQ_ESHAPE,
              "kdim must be a positive multiple of 128, got %lld", (long long)kdim);
-  XQ_REQUIRE(group_size % kChunk == 0, XQ_ECONFIG,
-             "fused kernel needs group_size a multiple of 64, got %d", group_size);
+  XQ_REQUIRE(group_size == kG, XQ_ECONFIG,
+             "the fused kernel is specialised for group_size 128 (the reference default), got %d",
+             group_size);
   XQ_REQUIRE(tiles_per_chunk >= 1, XQ_ECONFIG, "tiles_per_chunk must be >= 1");
   XQ_REQUIRE(n_seqs >= 1 && n_kv_heads >= 1, XQ_ESHAPE, "empty batch");
   XQ_REQUIRE(max_len <= L_max, XQ_ESHAPE, "max_len > L_max");
