@@ -43,7 +43,8 @@ CONFIGS = {
     "c3": dict(workload="XQuant-CL 2-bit, Llama-2-7B shape, batch 16, 32K context",
                shape="llama2-7b", variant="xq-cl-mha", bits=2, batch=16, ctx=32768),
     "c4": dict(workload="xq-gqa 3-bit latent, Llama-3.1-8B shape, batch 32, 16K context",
-               shape="llama3.1-8b", variant="xq-gqa", bits=3, batch=32, ctx=16384),
+               shape="llama3.1-8b", variant="xq-gqa", bits=3, batch=32, ctx=16384,
+               parallel="heads"),
     "c1": dict(workload="XQuant 4-bit, one Llama-2-7B layer, batch 1, 2K context",
                shape="llama2-7b", variant="xq-mha", bits=4, batch=1, ctx=2048, layers=1),
 }
@@ -324,15 +325,22 @@ def run_xquant(args, cfg):
     B, ctx = cfg["batch"], cfg["ctx"]
     total_steps = args.warmup + 2 * args.steps + 2
     L_max = -(-(ctx + total_steps) // 128) * 128
-    weights, w_q = D.synthetic_weights(shape, cfg["variant"], dev, seed=rank, layers=n_layers)
+    # "heads": KV-head-group sharding of one global batch (strong scaling, one
+    # all-gather of attention outputs per layer); otherwise every rank decodes
+    # its own batch (weak scaling, no collective)
+    heads = cfg.get("parallel") == "heads" and world > 1
+    wseed = 0 if heads else rank
+    weights, w_q = D.synthetic_weights(shape, cfg["variant"], dev, seed=wseed, layers=n_layers)
+    shard = (world, rank) if heads else None
 
     def make(variant):
-        dec = D.Decoder(shape, variant, cfg["bits"], B, L_max, weights, w_q, device=dev)
+        dec = D.Decoder(shape, variant, cfg["bits"], B, L_max, weights, w_q, device=dev,
+                        head_shard=shard)
         t0 = time.perf_counter()
-        dec.fill_synthetic(ctx, seed=1 + rank)
+        dec.fill_synthetic(ctx, seed=1 + wseed)
         return dec, time.perf_counter() - t0
 
-    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    g = torch.Generator(device=dev).manual_seed(100 + wseed)
     d = shape.hidden_dim
     n_in = args.warmup + args.steps
     xs = [torch.randn(n_layers, B, d, generator=g, device=dev).to(torch.bfloat16) for _ in range(n_in)]
@@ -351,13 +359,14 @@ def run_xquant(args, cfg):
     t = _max_over_ranks(world, t)
     kern_s = sum(a.elapsed_time(b) for a, b in timers) / 1e3
     kern_s = _max_over_ranks(world, kern_s)
-    value = world * B * args.steps / t
+    tokens_per_step = B if heads else world * B
+    value = tokens_per_step * args.steps / t
     ms_per_step = t / args.steps * 1e3
     l_avg = ctx_before + (args.steps + 1) / 2.0
 
     # ---------------- end to end through the public API ----------------
     x_host = [x.cpu().pin_memory() for x in xs[:args.steps]]
-    out_host = torch.empty((B, shape.n_heads, 128), dtype=torch.float32).pin_memory()
+    out_host = torch.empty((B, shape.n_heads, 128), dtype=torch.float32).pin_memory()  # gathered
     x_dev = torch.empty_like(xs[0])
     _barrier(world)
     torch.cuda.synchronize()
@@ -371,7 +380,7 @@ def run_xquant(args, cfg):
     e1.record()
     torch.cuda.synchronize()
     t_e2e = _max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
-    e2e_value = world * B * args.steps / t_e2e
+    e2e_value = tokens_per_step * args.steps / t_e2e
     mem = dec.memory_bytes()
     bits_per_layer = dec.policy.bits
     del dec
@@ -390,7 +399,7 @@ def run_xquant(args, cfg):
             t16 = _time_steps(fdec, xs[args.warmup:], args.steps, world)
             t16 = _max_over_ranks(world, t16)
             kv_bytes = S.cache_bytes("fp16", l_avg, d, 16, shape.kv_group) * n_layers * B
-            fp16 = {"value": world * B * args.steps / t16, "unit": "tokens/s",
+            fp16 = {"value": tokens_per_step * args.steps / t16, "unit": "tokens/s",
                     "ms_per_step": t16 / args.steps * 1e3,
                     "kv_cache_bytes": fdec.memory_bytes().get("kv_cache"),
                     "hbm_gbs_achieved": kv_bytes / (t16 / args.steps) / 1e9,
@@ -406,7 +415,7 @@ def run_xquant(args, cfg):
     # ---------------- roofline of the dominant kernel ----------------
     peaks, peak_src = _peaks()
     flops_launch = B * (S.remat_flops(cfg["variant"], l_avg, d, shape.kv_group)
-                        + S.attention_flops(l_avg, shape.n_heads))
+                        + S.attention_flops(l_avg, shape.n_heads)) / (world if heads else 1)
     per_launch = kern_s / (args.steps * n_layers)
     achieved = flops_launch / per_launch / 1e12
     peak = peaks["bf16_tflops_sustained"]
@@ -435,12 +444,14 @@ def run_xquant(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "higher_is_better": True, "scaling": "strong" if heads else "weak", "vs_baseline": None,
+        "dtype": "f16",
         "data": "synthetic (random-init weights, N(0,1) activations)",
         "config": {"workload": cfg["workload"], "shape": cfg["shape"], "variant": cfg["variant"],
                    "bits": cfg["bits"], "policy_bits": bits_per_layer[:4] + ["..."],
                    "batch_per_gpu": B, "context": ctx + 1, "layers": n_layers,
-                   "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                   "parallelism": (f"kv-head-group x{world} (NCCL all-gather of attention outputs)"
+                                   if heads else f"batch-sharded x{world} (no data-path collective)"),
                    "l2": "no flush: per-step inputs (packed caches, GBs) exceed the 126 MB L2"},
         "fp16_kv": fp16,
         "speedup_vs_fp16_kv": (value / fp16["value"]) if fp16 and fp16.get("value") else None,

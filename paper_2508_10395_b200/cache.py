@@ -253,12 +253,16 @@ class CacheBackend:
     def __init__(self, layer_index: int, policy: LayerPolicy, head_dim: int,
                  group_size: int = DEFAULT_GROUP_SIZE, *, n_slots: int = 1, max_len: int = 4096,
                  hidden_dim: int | None = None, n_heads: int | None = None, kv_group: int = 1,
-                 device="cuda"):
+                 n_heads_total: int | None = None, device="cuda"):
+        """``n_heads`` is the number of query heads this backend serves; with
+        KV-head-group sharding (parallel.py) it is a slice of
+        ``n_heads_total`` and the weights passed in are column-sliced."""
         if head_dim != HEAD_DIM:
             raise ConfigError(f"the B200 kernels are specialised for head_dim {HEAD_DIM}, got {head_dim}")
         if hidden_dim is None or n_heads is None:
             raise ConfigError("hidden_dim and n_heads are required (device arenas are preallocated)")
-        if hidden_dim != n_heads * head_dim or n_heads % kv_group:
+        total = n_heads_total or n_heads
+        if hidden_dim != total * head_dim or n_heads % kv_group or total % kv_group:
             raise ConfigError("hidden_dim must equal n_heads*head_dim and n_heads % kv_group == 0")
         self.layer_index = layer_index
         self.policy = policy
@@ -267,8 +271,9 @@ class CacheBackend:
         self.bits = policy.bits_for(layer_index)
         self.n_slots, self.L = n_slots, max_len
         self.d, self.n_heads, self.g = hidden_dim, n_heads, kv_group
-        self.kvw = hidden_dim // kv_group
-        self.n_kv = self.kvw // head_dim
+        self.latent = hidden_dim // kv_group  # full K/V width = SVD latent rank r (xq-gqa)
+        self.n_kv = n_heads // kv_group       # KV heads served here
+        self.kvw = self.n_kv * head_dim       # K/V width served here
         self.device = torch.device(device)
         self.n_tokens = np.zeros(n_slots, dtype=np.int64)
         self.lens_dev = torch.zeros(n_slots, dtype=torch.int32, device=self.device)
@@ -543,7 +548,7 @@ class LatentInputCacheGQA(CacheBackend):
         super().__init__(*a, **kw)
         if self.bits == 16:
             raise ConfigError("xq-gqa on the B200 path needs a quantized width (2/3/4/8)")
-        r = self.kvw
+        r = self.latent  # the latent cache is whole even when heads are sharded
         self.k_stream = PackedStream(self.bits, CHANNEL, r, self.group_size, self.n_slots, self.L,
                                      self.device)
         self.v_stream = PackedStream(self.bits, TOKEN, r, self.group_size, self.n_slots, self.L,
@@ -583,7 +588,7 @@ class LatentInputCacheGQA(CacheBackend):
         ks, vs = self.k_stream, self.v_stream
         return self._remat_f32(N.A_CODES_CHANNEL, ks.codes, ks.params, ks.resid,
                                int(ks.n_flushed[slot]), ks.bits, ks.row_bytes, N.A_CODES_TOKEN,
-                               vs.codes, vs.params, vs.bits, vs.row_bytes, self.kvw,
+                               vs.codes, vs.params, vs.bits, vs.row_bytes, self.latent,
                                weights.f32("fused_k"), weights.f32("fused_v"), slot, n)
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
@@ -592,7 +597,7 @@ class LatentInputCacheGQA(CacheBackend):
                                  vs.bits, weights.fused_k, weights.fused_v)
         self._fused(N.A_CODES_CHANNEL, ks.codes, ks.params, ks.resid, ks.nflushed_dev, ks.bits,
                     ks.row_bytes, N.A_CODES_TOKEN, vs.codes, vs.params, vs.bits, vs.row_bytes,
-                    self.kvw, w_arr, self.g, q, lens, max_len, out, tpc)
+                    self.latent, w_arr, self.g, q, lens, max_len, out, tpc)
 
     def memory_bytes(self):
         out = {f"k_{k}": v for k, v in self.k_stream.nbytes().items()}

@@ -88,7 +88,13 @@ class Decoder:
 
     def __init__(self, shape: ModelShape, variant: str, bits: int, n_slots: int, max_len: int,
                  weights, w_q, device="cuda", policy: C.LayerPolicy | None = None,
-                 tiles_per_chunk: int | None = None):
+                 tiles_per_chunk: int | None = None, head_shard: tuple[int, int] | None = None,
+                 group=None):
+        """``head_shard=(world, rank)``: KV-head-group sharding (parallel.py).
+        This rank serves KV heads parallel.head_shard(...) with column-sliced
+        weights; step() all-gathers the attention outputs of all ranks."""
+        from . import parallel as P
+
         if variant not in C.SUPPORTED:
             raise ConfigError(f"variant {variant!r} not supported by the decoder")
         self.shape, self.variant = shape, variant
@@ -96,9 +102,20 @@ class Decoder:
         self.n_slots, self.L = n_slots, max_len
         self.policy = policy or (C.LayerPolicy.uniform(16, shape.n_layers) if variant == "fp16"
                                  else C.LayerPolicy.for_bits(bits, shape.n_layers))
+        n_heads = shape.n_heads
+        self.gather = None
+        if head_shard is not None and head_shard[0] > 1:
+            world, rank = head_shard
+            kv = P.head_shard(shape.n_heads // shape.kv_group, world, rank)
+            weights = [P.shard_layer_weights(lw, variant, kv) for lw in weights]
+            w_q = [P.shard_wq(w, kv, shape.kv_group) for w in w_q]
+            n_heads = len(kv) * shape.kv_group
+            self.gather = P.HeadGather(n_slots, n_heads, world, self.device, group)
+        self.n_heads_local = n_heads
         self.weights, self.w_q = weights, w_q
         kw = dict(n_slots=n_slots, max_len=max_len, hidden_dim=shape.hidden_dim,
-                  n_heads=shape.n_heads, kv_group=shape.kv_group, device=self.device)
+                  n_heads=n_heads, n_heads_total=shape.n_heads, kv_group=shape.kv_group,
+                  device=self.device)
         self.caches = [C.make_cache(variant, i, self.policy, shape.head_dim, **kw)
                        for i in range(len(weights))]
         self.acc = (C.Accumulator(n_slots, max_len, shape.hidden_dim, self.device)
@@ -134,8 +151,6 @@ class Decoder:
                 else:
                     x = torch.randn(n_tokens, d, generator=g, device=self.device).to(torch.bfloat16)
                 cache._prefill(s, x, lw, self.acc)
-            if self.acc is not None:
-                pass
         self.n_tokens[:] = n_tokens
         self.lens_dev.fill_(n_tokens)
         torch.cuda.synchronize(self.device)
@@ -154,7 +169,7 @@ class Decoder:
         self.n_tokens += 1
         self.lens_dev.add_(1)
         max_len = int(self.n_tokens.max())
-        H = self.shape.n_heads
+        H = self.n_heads_local
         out = None
         for i, (cache, lw) in enumerate(zip(self.caches, self.weights)):
             x = x_layers[i]
@@ -170,6 +185,8 @@ class Decoder:
                 e1.record()
                 timers.append((e0, e1))
             self.launches += self._launches_per_layer(cache)
+            if self.gather is not None:  # KV-head-group sharding: [B, H_local, 128] -> [B, H, 128]
+                out = self.gather(out)
         return out
 
     def _launches_per_layer(self, cache) -> int:

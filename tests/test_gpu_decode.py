@@ -1,0 +1,104 @@
+"""Decode engine (decode.Decoder) on the GPU: a multi-layer step against the
+CPU oracle, and KV-head-group shards reassembling the unsharded output."""
+
+import numpy as np
+import pytest
+
+from _util import rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+def _setup(variant, bits, n_layers=4, d=512, H=4, g=1, B=2, n=300, seed=0):
+    import torch
+
+    from paper_2508_10395_b200 import decode as D
+
+    shape = D.ModelShape("tiny", d, n_layers, H, g)
+    dev = torch.device("cuda", 0)
+    w, wq = D.synthetic_weights(shape, variant, dev, seed=seed)
+    gen = torch.Generator(device="cpu").manual_seed(seed + 1)
+    xs = torch.randn(n_layers, B, n + 1, d, generator=gen).to(torch.bfloat16)
+    return shape, w, wq, xs, dev
+
+
+def _run(shape, variant, bits, w, wq, xs, dev, head_shard=None):
+    import torch
+
+    from paper_2508_10395_b200 import decode as D
+
+    L, B, n1, d = xs.shape
+    dec = D.Decoder(shape, variant, bits, B, 512, w, wq, device=dev, head_shard=head_shard)
+    dec.gather = None  # single process: shards are concatenated by the test
+    for s in range(B):
+        for i, c in enumerate(dec.caches):
+            c._prefill(s, xs[i, s, :-1].to(dev), dec.weights[i], dec.acc)
+    dec.n_tokens[:] = n1 - 1
+    dec.lens_dev.fill_(n1 - 1)
+    out = torch.empty((L, B, dec.n_heads_local, 128), dtype=torch.float32, device=dev)
+    dec.step(xs[:, :, -1].to(dev).contiguous(), attn_out=out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), dec
+
+
+@pytest.mark.parametrize("variant,bits", [("xq-mha", 3), ("xq-mha", 4), ("fp16", 16)])
+def test_decoder_step_matches_oracle(variant, bits):
+    import xq_oracle as O
+
+    shape, w, wq, xs, dev = _setup(variant, bits)
+    out, dec = _run(shape, variant, bits, w, wq, xs, dev)
+    L, B, n1, d = xs.shape
+    x = xs.double().numpy()
+    for i in range(L):
+        wk, wv = w[i].w_k.double().cpu().numpy(), w[i].w_v.double().cpu().numpy()
+        wqi = wq[i].double().cpu().numpy()
+        for b in range(B):
+            if variant == "fp16":
+                st = O.Fp16Cache(128)
+                st.append(x[i, b], wk, wv)
+                k, v = st.remat()
+            else:
+                st = O.XqMhaCache(dec.policy.bits[i], 128, 128)
+                st.append(x[i, b])
+                k, v = st.remat(wk, wv)
+            q = x[i, b, -1:] @ wqi
+            ref = O.attention(O.apply_rope(q, [n1 - 1], 128), k, v, shape.n_heads, 1)[0]
+            assert rel_err(out[i, b].reshape(-1), ref) <= TOL, (i, b)
+
+
+@pytest.mark.parametrize("variant,g", [("xq-mha", 1), ("xq-gqa", 2)])
+def test_head_shards_reassemble(variant, g):
+    shape, w, wq, xs, dev = _setup(variant, 3, n_layers=2, d=1024, H=8, g=g)
+    full, _ = _run(shape, variant, 3, w, wq, xs, dev)
+    parts = [_run(shape, variant, 3, w, wq, xs, dev, head_shard=(2, r))[0] for r in range(2)]
+    got = np.concatenate(parts, axis=2)
+    assert got.shape == full.shape
+    assert np.max(np.abs(got - full)) <= 1e-5 * np.max(np.abs(full))
+
+
+def test_decoder_cl_step_matches_oracle():
+    import xq_oracle as O
+
+    shape, w, wq, xs, dev = _setup("xq-cl-mha", 2, n_layers=5, d=256, H=2)
+    # residual-stream-like inputs (the regime CL is for): x_i = x_{i-1} + 0.03 noise
+    import torch
+
+    base = xs[0].float()
+    drift = [base]
+    for i in range(1, xs.shape[0]):
+        drift.append(drift[-1] + 0.03 * xs[i].float())
+    xs = torch.stack(drift).to(torch.bfloat16)
+    out, dec = _run(shape, "xq-cl-mha", 2, w, wq, xs, dev)
+    L, B, n1, d = xs.shape
+    x = xs.double().numpy()
+    for b in range(B):
+        stack = O.XqClMhaStack(dec.policy.bits, dec.policy.base_layers, 128, 128)
+        stack.step([x[i, b, :-1] for i in range(L)])
+        weights = [(w[i].w_k.double().cpu().numpy(), w[i].w_v.double().cpu().numpy()) for i in range(L)]
+        _, kvs = stack.step([x[i, b, -1] for i in range(L)], weights)
+        for i in range(L):
+            q = x[i, b, -1:] @ wq[i].double().cpu().numpy()
+            ref = O.attention(O.apply_rope(q, [n1 - 1], 128), kvs[i][0], kvs[i][1], shape.n_heads, 1)[0]
+            assert rel_err(out[i, b].reshape(-1), ref) <= TOL, (i, b)
