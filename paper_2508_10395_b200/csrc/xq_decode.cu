@@ -196,60 +196,80 @@ struct Ring {
   static constexpr int kGB = 16 * BITS;                           // code bytes per row per group
   static constexpr int kTokenStreams = (AK == XQ_A_CODES_TOKEN) + (AV == XQ_A_CODES_TOKEN);
   static constexpr uint32_t kCodeBytes = kTileM * kGB;
-  static constexpr uint32_t kParamBytes = kTileM * 16;
-  static constexpr uint32_t kStageBytes =
-      kProducers ? ((kStreams * kCodeBytes + kTokenStreams * kParamBytes + 127) / 128 * 128) : 0;
+  static constexpr uint32_t kParamBytes = kTileM * 16;        // per-token (scale, zp) quads
+  static constexpr uint32_t kChanParamBytes = 2 * 128 * 2;     // per-channel scales + zps
+  static constexpr uint32_t kParam0Bytes =
+      AK == XQ_A_CODES_TOKEN ? kParamBytes : (AK == XQ_A_CODES_CHANNEL ? kChanParamBytes : 0);
+  static constexpr uint32_t kParam1Bytes = AV == XQ_A_CODES_TOKEN ? kParamBytes : 0;
+  static constexpr uint32_t kTxBytes = kStreams * kCodeBytes + kParam0Bytes + kParam1Bytes;
+  static constexpr uint32_t kStageBytes = kProducers ? ((kTxBytes + 127) / 128 * 128) : 0;
   static constexpr uint32_t kABStage = kStreams * kABytes + kBBytes;
   static constexpr int kABStages = kStreams == 1 ? (BITS == 8 ? 4 : 5) : (BITS == 8 ? 2 : 3);
   static constexpr uint32_t kABBytes = kABStages * kABStage;
-  static constexpr uint32_t kBudget = 222 * 1024 - kABBytes - 6 * 1024;
+  static constexpr uint32_t kEpiScratch = 4 * 32 * 33 * 4 + 4 * 32 * 8 * 4;  // V transpose + p
+  static constexpr uint32_t kBudget = 222 * 1024 - kABBytes - 6 * 1024 - kEpiScratch;
   static constexpr int kCodeStages =
       !kProducers ? 0 : (kBudget / kStageBytes >= 4 ? 4 : (kBudget / kStageBytes < 1 ? 1 : kBudget / kStageBytes));
   // stage layout: [s0 codes][s1 codes][s0 params if TOKEN][s1 params if TOKEN]
   __host__ __device__ static constexpr uint32_t code_off(int stream) { return stream * kCodeBytes; }
   __host__ __device__ static constexpr uint32_t param_off(int stream) {
-    return kStreams * kCodeBytes + ((stream == 1 && AK == XQ_A_CODES_TOKEN) ? kParamBytes : 0);
+    return kStreams * kCodeBytes + (stream == 1 ? kParam0Bytes : 0);
   }
 };
 
-// 2*BITS words of one row's 64-code chunk from shared memory
+// 2*BITS words of one row's 64-code chunk from shared memory (32-bit address)
 template <int BITS>
-XQ_DEVINL void lds_raw(const uint8_t* src, uint32_t (&w)[2 * BITS]) {
+XQ_DEVINL void lds_raw(uint32_t src, uint32_t (&w)[2 * BITS]) {
   if constexpr (BITS == 3) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const uint2 a = *reinterpret_cast<const uint2*>(src + 8 * q);
+      const uint2 a = lds64(src + 8 * q);
       w[2 * q] = a.x;
       w[2 * q + 1] = a.y;
     }
   } else {
 #pragma unroll
     for (int q = 0; q < BITS / 2; ++q) {
-      const uint4 a = *reinterpret_cast<const uint4*>(src + 16 * q);
+      const uint4 a = lds128(src + 16 * q);
       w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
     }
   }
 }
 
+// Per-thread constants of the SWIZZLE_128B row store: byte offsets of the 8
+// 16-byte chunks of this row (chunk c goes to slot c ^ (row % 8)).
+struct RowSwizzle {
+  uint32_t off[8];
+  XQ_DEVINL explicit RowSwizzle(int row) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) off[c] = sw128_offset(row, c);
+  }
+  XQ_DEVINL void store(uint32_t tile, const uint32_t (&v)[32]) const {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sts128(tile + off[c], v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+};
+
 // One producer thread: convert its row's 64-channel chunk of one A stream.
+// tile / cstage / pstage are 32-bit shared addresses.
 template <int MODE, int BITS>
-XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t* pstage, int row,
-                             bool valid, int tok, int b, int nflushed, int64_t arow, int kc,
-                             const void* gparams, const float* resid, const DecodeParams& p) {
+XQ_DEVINL void produce_chunk(uint32_t tile, uint32_t cstage, uint32_t pstage, const RowSwizzle& sw,
+                             int row, bool valid, int tok, int b, int nflushed, int64_t arow,
+                             int kc, const void* gparams, const float* resid,
+                             const DecodeParams& p) {
   uint32_t v[32];
   if (!valid) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = 0u;
-    store_row_sw128(tile, row, v);
+    sw.store(tile, v);
     return;
   }
-  const uint8_t* crow = cstage + row * (16 * BITS) + (kc & 1) * 8 * BITS;
+  const uint32_t crow = cstage + row * (16 * BITS) + (kc & 1) * 8 * BITS;
   if constexpr (MODE == XQ_A_CODES_TOKEN) {
     uint32_t raw[2 * BITS];
     lds_raw<BITS>(crow, raw);
     // G = 128: this chunk's group is kc/2; the staged quad starts at group (kc/2) & ~3
-    const int gq = (kc >> 1) & 3;
-    const __half2 sz = *reinterpret_cast<const __half2*>(pstage + row * 16 + 4 * gq);
+    const __half2 sz = from_u32<__half2>(lds32(pstage + row * 16 + 4 * ((kc >> 1) & 3)));
     const __half2 s2 = __low2half2(sz), z2 = __high2half2(sz);
     convert_raw<BITS, false>(raw, &s2, &z2, v);
   } else {  // XQ_A_CODES_CHANNEL
@@ -257,14 +277,14 @@ XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t
     if (tok < nflushed) {
       uint32_t raw[2 * BITS];
       lds_raw<BITS>(crow, raw);
-      // per-channel params: shared by the whole tile -> L1 broadcast
-      const __half* prow =
-          static_cast<const __half*>(gparams) + (arow / kG) * 2 * p.kdim + kc * kChunk;
+      // per-channel params of this token group, staged by TMA as [scales(128) | zps(128)]
+      // halves in producer order: broadcast shared loads (every row reads the same)
+      const uint32_t ps = pstage + (kc & 1) * 128;
       __half2 s2[32], z2[32];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4*>(prow) + c);
-        const uint4 z = __ldg(reinterpret_cast<const uint4*>(prow + p.kdim) + c);
+        const uint4 a = lds128(ps + 16 * c);
+        const uint4 z = lds128(ps + 256 + 16 * c);
         s2[4 * c] = from_u32<__half2>(a.x); s2[4 * c + 1] = from_u32<__half2>(a.y);
         s2[4 * c + 2] = from_u32<__half2>(a.z); s2[4 * c + 3] = from_u32<__half2>(a.w);
         z2[4 * c] = from_u32<__half2>(z.x); z2[4 * c + 1] = from_u32<__half2>(z.y);
@@ -281,7 +301,7 @@ XQ_DEVINL void produce_chunk(uint8_t* tile, const uint8_t* cstage, const uint8_t
       }
     }
   }
-  store_row_sw128(tile, row, v);
+  sw.store(tile, v);
 }
 
 template <int AK, int AV, int BITS, int GROUP>
@@ -312,6 +332,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* q_s = reinterpret_cast<float*>(tmem_slot + 4);  // [GROUP][128]
+  float* epi_v = q_s + GROUP * kHeadDim;                  // [4 warps][32 rows][33]
+  float* epi_p = epi_v + 4 * 32 * 33;                     // [4 warps][32 rows][GROUP]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMA), 1 = peer
@@ -339,7 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   if (warp == 2 && lane == 0 && PROD) {  // descriptor prefetch
     tma_prefetch_desc(&tmap_ca);
-    if constexpr (AK == XQ_A_CODES_TOKEN) tma_prefetch_desc(&tmap_pa);
+    tma_prefetch_desc(&tmap_pa);
     if constexpr (A_TILES == 2) {
       tma_prefetch_desc(&tmap_cb);
       tma_prefetch_desc(&tmap_pb);
@@ -444,14 +466,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&cempty[cs], cph ^ 1);
             if (elect_one()) {
               uint8_t* st = sC + cs * R::kStageBytes;
-              mbar_arrive_expect_tx(&cfull[cs],
-                                    A_TILES * R::kCodeBytes + R::kTokenStreams * R::kParamBytes);
+              mbar_arrive_expect_tx(&cfull[cs], R::kTxBytes);
               // params quad holding this 128-channel block's group(s); a TMA box must
               // start on a 16-byte boundary of the inner dimension
               const int32_t pq = g & ~3;  // G = 128: group g of the row
               tma_load_2d(st + R::code_off(0), &tmap_ca, &cfull[cs], g * R::kGB, arow0, kEvictNormal);
               if constexpr (AK == XQ_A_CODES_TOKEN)
                 tma_load_2d(st + R::param_off(0), &tmap_pa, &cfull[cs], 4 * pq, arow0, kEvictNormal);
+              if constexpr (AK == XQ_A_CODES_CHANNEL)  // [scales | zps] of this token group
+                tma_load_2d(st + R::param_off(0), &tmap_pa, &cfull[cs], g * 128,
+                            2 * (arow0 / kG), kEvictNormal);
               if constexpr (A_TILES == 2) {
                 tma_load_2d(st + R::code_off(1), &tmap_cb, &cfull[cs], g * R::kGB, arow0, kEvictNormal);
                 tma_load_2d(st + R::param_off(1), &tmap_pb, &cfull[cs], 4 * pq, arow0, kEvictNormal);
@@ -469,6 +493,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if constexpr (PROD) {
       const int gp = (warp - kProdWarp0) >> 2;
       const int row = ((warp - kProdWarp0) & 3) * 32 + lane;  // tile row = token
+      const RowSwizzle sw(row);
+      const uint32_t sAB_a = smem_u32(sAB), sC_a = smem_u32(sC);
       const int ngrp = nkc / 2;
       uint32_t tcount = 0;
       for (int u = cluster; u < p.n_units; u += n_clusters) {
@@ -482,7 +508,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int g = (ci0 & 1) == static_cast<uint32_t>(gp) ? 0 : 1; g < ngrp; g += 2) {
             const uint32_t ci = ci0 + g;
             const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
-            const uint8_t* st = sC + cs * R::kStageBytes;
+            const uint32_t st = sC_a + cs * R::kStageBytes;
             mbar_wait(&cfull[cs], cph);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -490,21 +516,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const uint32_t it = tcount * nkc + kc;
               const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
               mbar_wait(&empty[s], ph ^ 1);
-              uint8_t* tile = sAB + s * R::kABStage;
-              produce_chunk<AK, BITS>(tile, st + R::code_off(0), st + R::param_off(0), row, valid,
-                                      tok, w.b, nfl, arow, kc, p.ak_params, p.ak_resid, p);
+              const uint32_t tile = sAB_a + s * R::kABStage;
+              produce_chunk<AK, BITS>(tile, st + R::code_off(0), st + R::param_off(0), sw, row,
+                                      valid, tok, w.b, nfl, arow, kc, p.ak_params, p.ak_resid, p);
               if constexpr (A_TILES == 2)
                 produce_chunk<AVM, BITS>(tile + kABytes, st + R::code_off(1), st + R::param_off(1),
-                                         row, valid, tok, w.b, 1 << 30, arow, kc, p.av_params,
+                                         sw, row, valid, tok, w.b, 1 << 30, arow, kc, p.av_params,
                                          nullptr, p);
               fence_proxy_async_smem();
               __syncwarp();
-              if (lane == 0) {
-                if (leader) mbar_arrive(&full[s]);
-                else mbar_arrive_remote(full_leader0 + 8 * s);
-              }
+              if (leader) mbar_arrive_if(&full[s], lane == 0);
+              else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
             }
-            if (lane == 0) mbar_arrive(&cempty[cs]);
+            mbar_arrive_if(&cempty[cs], lane == 0);
           }
         }
       }
@@ -594,18 +618,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 4; ++c) o_run[gi][c] *= alpha;
           m_run[gi] = mn;
         }
+        // p.V over this warp's 32 rows: transpose each 32x32 block of V through
+        // shared memory (row stride 33: conflict-free both ways), then lane L sums
+        // column 32c+L over the rows with the rows' p broadcast from shared memory.
+        float* vw = epi_v + ew * (32 * 33);
+        float* pw = epi_p + ew * (32 * GROUP);
+#pragma unroll
+        for (int gi = 0; gi < GROUP; ++gi) pw[lane * GROUP + gi] = pr[gi];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float vb[32];
           tmem_ld32(tmem + tlane + a * 256 + 128 + c * 32, vb);
           tmem_wait_ld();
 #pragma unroll
-          for (int gi = 0; gi < GROUP; ++gi) {
-            float tmp[32];
+          for (int j = 0; j < 32; ++j) vw[lane * 33 + j] = vb[j];
+          __syncwarp();
+          float acc[GROUP];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) tmp[j] = pr[gi] * vb[j];
-            o_run[gi][c] += warp_reduce_scatter32(tmp, lane);
+          for (int gi = 0; gi < GROUP; ++gi) acc[gi] = 0.f;
+#pragma unroll 8
+          for (int r = 0; r < 32; ++r) {
+            const float v = vw[r * 33 + lane];
+#pragma unroll
+            for (int gi = 0; gi < GROUP; ++gi) acc[gi] = fmaf(pw[r * GROUP + gi], v, acc[gi]);
           }
+#pragma unroll
+          for (int gi = 0; gi < GROUP; ++gi) o_run[gi][c] += acc[gi];
+          __syncwarp();
         }
         tc_fence_before();
         __syncwarp();
@@ -768,7 +807,8 @@ template <int AK, int AV, int BITS, int GROUP>
 static int launch_decode(const Maps& m, const DecodeParams& p, cudaStream_t st) {
   using R = Ring<AK, AV, BITS>;
   constexpr size_t smem = 1024 + R::kABBytes + R::kCodeStages * R::kStageBytes +
-                          (2 * R::kABStages + 8 + 4) * 8 + 16 + GROUP * kHeadDim * 4;
+                          (2 * R::kABStages + 8 + 4) * 8 + 16 + GROUP * kHeadDim * 4 +
+                          R::kEpiScratch;
   static_assert(R::kABStage % 1024 == 0, "stages must keep 1024-byte swizzle alignment");
   static_assert(smem <= 227 * 1024, "shared memory budget");
   auto kern = k_decode_attend<AK, AV, BITS, GROUP>;
@@ -829,8 +869,10 @@ static int stream_maps(int mode, int bits, const void* src, const void* params, 
   if (mode == XQ_A_CODES_TOKEN)  // byte view of the half2 grid: one 16-byte quad per row
     return make_map(pmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, params, param_stride(kdim, G) * 4, rows,
                     16, kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "params", CU_TENSOR_MAP_L2_PROMOTION_NONE);
-  *pmap = *codes;
-  return XQ_OK;
+  // per-channel: planar halves [rows/G][2][kdim] viewed as [2*rows/G][kdim]; box = one
+  // 128-channel group of scales and zps (2 x 256 B)
+  return make_map(pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, params, kdim, 2 * (rows / G), 128, 2,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, "channel params", CU_TENSOR_MAP_L2_PROMOTION_NONE);
 }
 
 }  // namespace xq
