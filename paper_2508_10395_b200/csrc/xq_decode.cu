@@ -206,7 +206,7 @@ struct Ring {
   static constexpr uint32_t kABStage = kStreams * kABytes + kBBytes;
   static constexpr int kABStages = kStreams == 1 ? (BITS == 8 ? 4 : 5) : (BITS == 8 ? 2 : 3);
   static constexpr uint32_t kABBytes = kABStages * kABStage;
-  static constexpr uint32_t kEpiScratch = 4 * 32 * 33 * 4 + 4 * 32 * 8 * 4;  // V transpose + p
+  static constexpr uint32_t kEpiScratch = 4 * 32 * 36 * 4 + 4 * 32 * 8 * 4;  // V transpose + p
   static constexpr uint32_t kBudget = 222 * 1024 - kABBytes - 6 * 1024 - kEpiScratch;
   static constexpr int kCodeStages =
       !kProducers ? 0 : (kBudget / kStageBytes >= 4 ? 4 : (kBudget / kStageBytes < 1 ? 1 : kBudget / kStageBytes));
@@ -249,6 +249,25 @@ struct RowSwizzle {
     for (int c = 0; c < 8; ++c) sts128(tile + off[c], v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
   }
 };
+
+// p rows of the epilogue's shared scratch: padded to a 16-byte vector
+template <int GROUP>
+constexpr int kPStride = GROUP == 1 ? 1 : (GROUP == 2 ? 2 : 4 * ((GROUP + 3) / 4));
+template <int GROUP>
+XQ_DEVINL void load_p(const float* src, float (&pv)[kPStride<GROUP>]) {
+  if constexpr (GROUP == 1) {
+    pv[0] = src[0];
+  } else if constexpr (GROUP == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(src);
+    pv[0] = t.x; pv[1] = t.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < kPStride<GROUP> / 4; ++q) {
+      const float4 t = reinterpret_cast<const float4*>(src)[q];
+      pv[4 * q] = t.x; pv[4 * q + 1] = t.y; pv[4 * q + 2] = t.z; pv[4 * q + 3] = t.w;
+    }
+  }
+}
 
 // One producer thread: convert its row's 64-channel chunk of one A stream.
 // tile / cstage / pstage are 32-bit shared addresses.
@@ -332,8 +351,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* q_s = reinterpret_cast<float*>(tmem_slot + 4);  // [GROUP][128]
-  float* epi_v = q_s + GROUP * kHeadDim;                  // [4 warps][32 rows][33]
-  float* epi_p = epi_v + 4 * 32 * 33;                     // [4 warps][32 rows][GROUP]
+  float* epi_v = q_s + GROUP * kHeadDim;                  // [4 warps][32 rows][36]
+  float* epi_p = epi_v + 4 * 32 * 36;                     // [4 warps][32 rows][GROUP pad]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMA), 1 = peer
@@ -584,15 +603,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 16; ++i) csv[i] = __ldg(rp + (int64_t)(c * 16 + i) * p.rope_n);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < 16; ++i) {  // RoPE in place (linalg.py:92-93)
             const float2 cs = csv[i];
             const float k0 = kb[2 * i], k1 = kb[2 * i + 1];
-            const float r0 = k0 * cs.x - k1 * cs.y;  // linalg.py:92-93
-            const float r1 = k0 * cs.y + k1 * cs.x;
+            kb[2 * i] = k0 * cs.x - k1 * cs.y;
+            kb[2 * i + 1] = k0 * cs.y + k1 * cs.x;
+          }
 #pragma unroll
-            for (int gi = 0; gi < GROUP; ++gi) {
-              const float* qq = q_s + gi * kHeadDim + c * 32 + 2 * i;
-              sc[gi] = fmaf(qq[0], r0, fmaf(qq[1], r1, sc[gi]));
+          for (int gi = 0; gi < GROUP; ++gi) {  // q (broadcast) as 128-bit shared loads
+            const float4* qq = reinterpret_cast<const float4*>(q_s + gi * kHeadDim + c * 32);
+#pragma unroll
+            for (int v4 = 0; v4 < 8; ++v4) {
+              const float4 q4 = qq[v4];
+              sc[gi] = fmaf(q4.x, kb[4 * v4], sc[gi]);
+              sc[gi] = fmaf(q4.y, kb[4 * v4 + 1], sc[gi]);
+              sc[gi] = fmaf(q4.z, kb[4 * v4 + 2], sc[gi]);
+              sc[gi] = fmaf(q4.w, kb[4 * v4 + 3], sc[gi]);
             }
           }
         }
@@ -619,28 +645,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           m_run[gi] = mn;
         }
         // p.V over this warp's 32 rows: transpose each 32x32 block of V through
-        // shared memory (row stride 33: conflict-free both ways), then lane L sums
-        // column 32c+L over the rows with the rows' p broadcast from shared memory.
-        float* vw = epi_v + ew * (32 * 33);
-        float* pw = epi_p + ew * (32 * GROUP);
+        // shared memory (row stride 36 floats: 128-bit stores and column reads are
+        // both bank-conflict-free), then lane L sums column 32c+L over the rows
+        // with the rows' p broadcast from shared memory.
+        constexpr int kVS = 36;
+        float* vw = epi_v + ew * (32 * kVS);
+        float* pw = epi_p + ew * (32 * kPStride<GROUP>);
 #pragma unroll
-        for (int gi = 0; gi < GROUP; ++gi) pw[lane * GROUP + gi] = pr[gi];
+        for (int gi = 0; gi < GROUP; ++gi) pw[lane * kPStride<GROUP> + gi] = pr[gi];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float vb[32];
           tmem_ld32(tmem + tlane + a * 256 + 128 + c * 32, vb);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) vw[lane * 33 + j] = vb[j];
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(vw + lane * kVS + 4 * j) =
+                make_float4(vb[4 * j], vb[4 * j + 1], vb[4 * j + 2], vb[4 * j + 3]);
           __syncwarp();
           float acc[GROUP];
 #pragma unroll
           for (int gi = 0; gi < GROUP; ++gi) acc[gi] = 0.f;
 #pragma unroll 8
           for (int r = 0; r < 32; ++r) {
-            const float v = vw[r * 33 + lane];
+            const float v = vw[r * kVS + lane];
+            float pv[kPStride<GROUP>];
+            load_p<GROUP>(pw + r * kPStride<GROUP>, pv);
 #pragma unroll
-            for (int gi = 0; gi < GROUP; ++gi) acc[gi] = fmaf(pw[r * GROUP + gi], v, acc[gi]);
+            for (int gi = 0; gi < GROUP; ++gi) acc[gi] = fmaf(pv[gi], v, acc[gi]);
           }
 #pragma unroll
           for (int gi = 0; gi < GROUP; ++gi) o_run[gi][c] += acc[gi];
