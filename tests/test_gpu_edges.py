@@ -1,0 +1,194 @@
+"""Edge cases and full-size properties of the fused path on the GPU.
+
+* ragged batches (different lengths per slot), l = 1, lengths that are not
+  multiples of the 256-token pair tile;
+* every code width (2/3/4/8) and the 16-bit pass-through of xq-mha;
+* NaN/Inf input -> DataError (quant.py:114-115), group_size != 128 ->
+  ConfigError, empty cache -> UsageError;
+* xq-gqa before its first per-channel flush (all rows in the residual buffer);
+* full C2 shape (d=4096, 32 heads, l=32769, 3-bit): the fused output against
+  an independent float32 computation on the GPU (torch) from the same codes.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from _util import rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _mha(bits, n_slots, max_len, d=256, H=2, device="cuda"):
+    from paper_2508_10395_b200 import cache as M
+
+    pol = M.LayerPolicy.uniform(bits, 1)
+    return M.make_cache("xq-mha", 0, pol, 128, 128, n_slots=n_slots, max_len=max_len,
+                        hidden_dim=d, n_heads=H, device=device)
+
+
+def _weights(d, kvw, seed=0):
+    import torch
+
+    from paper_2508_10395_b200 import cache as M
+
+    g = torch.Generator().manual_seed(seed)
+    wk = (torch.randn(d, kvw, generator=g) / math.sqrt(d)).to(torch.bfloat16).cuda()
+    wv = (torch.randn(d, kvw, generator=g) / math.sqrt(d)).to(torch.bfloat16).cuda()
+    return M.LayerWeights(w_k=wk, w_v=wv)
+
+
+def _oracle_mha(x, wk, wv, q, bits, H):
+    import xq_oracle as O
+
+    st = O.XqMhaCache(bits, 128, 128)
+    st.append(x)
+    k, v = st.remat(wk, wv) if bits != 16 else (None, None)
+    if bits == 16:
+        xf = x.astype(np.float16).astype(np.float64)  # the GPU stores fp16 rows
+        k = O.apply_rope(xf @ wk, np.arange(len(x)), 128)
+        v = xf @ wv
+    n = x.shape[0]
+    return O.attention(O.apply_rope(q[None], [n - 1], 128), k, v, H, 1)[0]
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 8, 16])
+def test_ragged_batch_every_width(bits):
+    import torch
+
+    d, H = 256, 2
+    lens = [1, 130, 257, 600]  # l=1, within one tile, just past a pair tile, several
+    st = _mha(bits, len(lens), 1024, d, H)
+    w = _weights(d, d, seed=bits)
+    g = torch.Generator().manual_seed(7)
+    xs = [torch.randn(n, d, generator=g).to(torch.bfloat16) for n in lens]
+    for s, x in enumerate(xs):
+        if len(x) > 1:
+            st.prefill(x[:-1].cuda(), w, slot=s)
+    st.decode_append(torch.stack([x[-1] for x in xs]).cuda(), w)
+    q = torch.randn(len(lens), H, 128, generator=g)
+    out = st.decode_attend(q.cuda(), w).cpu().numpy()
+    wk, wv = w.w_k.double().cpu().numpy(), w.w_v.double().cpu().numpy()
+    for s, x in enumerate(xs):
+        ref = _oracle_mha(x.double().numpy(), wk, wv, q[s].double().numpy().reshape(-1), bits, H)
+        assert rel_err(out[s].reshape(-1), ref) <= TOL, (bits, lens[s])
+
+
+def test_nonfinite_input_raises_data_error():
+    import torch
+
+    from paper_2508_10395_b200.errors import DataError
+
+    st = _mha(3, 1, 256)
+    w = _weights(256, 256)
+    x = torch.randn(10, 256).to(torch.bfloat16)
+    x[3, 17] = float("nan")
+    st.prefill(x.cuda(), w)
+    with pytest.raises(DataError):
+        st.stream.check_finite()
+
+
+def test_group_size_other_than_128_rejected_by_fused_kernel():
+    import torch
+
+    from paper_2508_10395_b200 import cache as M
+    from paper_2508_10395_b200.errors import ConfigError
+
+    st = M.make_cache("xq-mha", 0, M.LayerPolicy.uniform(4, 1), 128, 64, n_slots=1,
+                      max_len=256, hidden_dim=256, n_heads=2)
+    w = _weights(256, 256)
+    st.prefill(torch.randn(5, 256).to(torch.bfloat16).cuda(), w)
+    with pytest.raises(ConfigError):
+        st.decode_attend(torch.randn(1, 2, 128).cuda(), w)
+
+
+def test_empty_cache_usage_errors():
+    import torch
+
+    from paper_2508_10395_b200.errors import UsageError
+
+    st = _mha(3, 1, 256)
+    w = _weights(256, 256)
+    with pytest.raises(UsageError):
+        st.decode_attend(torch.randn(1, 2, 128).cuda(), w)
+    with pytest.raises(UsageError):
+        st.rematerialize(w, np.arange(0))
+    st.prefill(torch.randn(4, 256).to(torch.bfloat16).cuda(), w)
+    with pytest.raises(UsageError):
+        st.prefill(torch.randn(4, 256).to(torch.bfloat16).cuda(), w)  # cache.py:258-259
+
+
+def test_gqa_residual_only_before_first_flush():
+    import torch
+
+    import xq_oracle as O
+    from paper_2508_10395_b200 import cache as M
+    from paper_2508_10395_b200 import decode as D
+
+    d, H, g = 512, 4, 2
+    shape = D.ModelShape("t", d, 1, H, g)
+    w, _ = D.synthetic_weights(shape, "xq-gqa", "cuda", seed=3)
+    w = w[0]
+    st = M.make_cache("xq-gqa", 0, M.LayerPolicy.uniform(3, 1), 128, 128, n_slots=1,
+                      max_len=256, hidden_dim=d, n_heads=H, kv_group=g)
+    gen = torch.Generator().manual_seed(5)
+    x = torch.randn(60, d, generator=gen).to(torch.bfloat16)
+    st.prefill(x[:-1].cuda(), w)
+    st.decode_append(x[-1:].cuda(), w)
+    assert st.k_stream.n_flushed[0] == 0
+    q = torch.randn(1, H, 128, generator=gen)
+    out = st.decode_attend(q.cuda(), w).cpu().numpy().reshape(-1)
+    xf = x.double().numpy()
+    uk, uv = w.u_k.double().cpu().numpy(), w.u_v.double().cpu().numpy()
+    fk, fv = w.fused_k.double().cpu().numpy(), w.fused_v.double().cpu().numpy()
+    ref_st = O.XqGqaCache(3, 128, 128)
+    ref_st.prefill(xf @ uk, xf @ uv)
+    k, v = ref_st.remat(fk, fv)
+    ref = O.attention(O.apply_rope(q.double().numpy().reshape(1, -1), [59], 128), k, v, H, g)[0]
+    assert rel_err(out, ref) <= TOL
+
+
+def test_full_c2_shape_against_independent_fp32():
+    """d=4096, 32 heads, l=32769, 3-bit: fused tcgen05 output vs torch fp32 from the same codes."""
+    import torch
+
+    from paper_2508_10395_b200 import _native as N
+    from paper_2508_10395_b200 import cache as M
+
+    d, H, n = 4096, 32, 32769
+    st = _mha(3, 1, 32896, d, H)
+    w = _weights(d, d, seed=11)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(n, d, generator=gen, device="cuda").to(torch.bfloat16)
+    st.prefill(x[:-1], w)
+    st.decode_append(x[-1:], w)
+    q = torch.randn(1, H, 128, generator=gen, device="cuda")
+    out = st.decode_attend(q, w)[0]
+    # independent path: dequantized rows (xq_dequant_rows) -> fp32 GEMM -> RoPE -> softmax
+    xh = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    s = st.stream
+    N.call("xq_dequant_rows", N.ptr(s.codes), s.row_bytes, N.ptr(s.params), 0, 3, 128, d, 0, n,
+           N.ptr(xh), N.stream_of())
+    torch.backends.cuda.matmul.allow_tf32 = False
+    k = xh @ w.w_k.float()
+    v = xh @ w.w_v.float()
+    pos = torch.arange(n, device="cuda", dtype=torch.float64)
+    freqs = 10000.0 ** (-2.0 * torch.arange(64, device="cuda", dtype=torch.float64) / 128)
+    ang = pos[:, None] * freqs[None, :]
+    c, sn = torch.cos(ang).float(), torch.sin(ang).float()
+
+    def rope(m, cc, ss):
+        mm = m.view(m.shape[0], -1, 64, 2)
+        e, o = mm[..., 0], mm[..., 1]
+        return torch.stack([e * cc[:, None] - o * ss[:, None], e * ss[:, None] + o * cc[:, None]],
+                           -1).view(m.shape[0], -1)
+
+    kr = rope(k, c, sn).view(n, H, 128)
+    qr = rope(q.view(1, -1), c[-1:], sn[-1:]).view(H, 128)
+    sc = torch.einsum("hd,nhd->hn", qr, kr) / math.sqrt(128)
+    p = torch.softmax(sc, dim=-1)
+    ref = torch.einsum("hn,nhd->hd", p, v.view(n, H, 128))
+    err = (out - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= TOL, err
