@@ -481,9 +481,10 @@ class FullPrecisionCache(CacheBackend):
 
 
 def kv_chunk_tokens(n_slots, max_len, n_kv, n_sm=148):
+    """Tokens per CTA of the fp16-KV flash-decode: >= ~4 CTAs per SM in total."""
     units_per_chunk = max(1, n_slots * n_kv)
-    chunks = max(1, -(-8 * n_sm // units_per_chunk))
-    return max(256, -(-max_len // chunks))
+    chunks = max(1, -(-4 * n_sm // units_per_chunk))
+    return max(512, -(-max_len // chunks))
 
 
 class InputCacheMHA(CacheBackend):

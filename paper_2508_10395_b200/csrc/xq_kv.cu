@@ -11,7 +11,7 @@ namespace xq {
 
 __global__ void k_combine(const float* __restrict__ partials, int n_parts, float* __restrict__ out);
 
-constexpr int kKvThreads = 128;
+constexpr int kKvThreads = 256;
 constexpr int kKvUnroll = 8;  // tokens in flight per warp
 constexpr int kKvPart = 2 + kHeadDim;
 
@@ -33,14 +33,19 @@ __global__ void k_kv_append(const float* __restrict__ k_new, const float* __rest
   }
 }
 
-XQ_DEVINL void bf16x4(uint2 u, float (&f)[4]) {
-  const __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&u.x);
-  const __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&u.y);
-  f[0] = __low2float(a); f[1] = __high2float(a);
-  f[2] = __low2float(b); f[3] = __high2float(b);
+XQ_DEVINL void bf16x8(uint4 u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+    f[2 * i] = __low2float(h);
+    f[2 * i + 1] = __high2float(h);
+  }
 }
 
-// One CTA per (sequence, KV head, chunk of tokens). Lane l owns dims 4l..4l+3.
+// One CTA per (sequence, KV head, chunk of tokens). Each half-warp streams its
+// own tokens: lane l of a half owns dims 8l..8l+7 (16-byte loads, one 256-byte
+// K row per half-warp load), kKvUnroll rows in flight per half-warp.
 template <int GROUP>
 __global__ void __launch_bounds__(kKvThreads)
     k_kv_decode(const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
@@ -52,43 +57,53 @@ __global__ void __launch_bounds__(kKvThreads)
   const int h = (unit / n_chunks) % n_kv;
   const int b = unit / (n_chunks * n_kv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const int stream = warp * 2 + half;  // 0 .. 2*nw-1
+  constexpr int kNw = kKvThreads / 32;
+  constexpr int kStreams = 2 * kNw;
   const int len = lens[b];
   const int t0 = chunk * chunk_tokens;
   const int t1 = min(t0 + chunk_tokens, len);
   const int64_t width = (int64_t)n_kv * kHeadDim;
   const int n_q = n_kv * GROUP;
 
-  float q[GROUP][4];
+  float q[GROUP][8];
   {
     const int pos = len - 1;
-    const float2 c0 = rope[(int64_t)pos * 64 + 2 * lane], c1 = rope[(int64_t)pos * 64 + 2 * lane + 1];
 #pragma unroll
     for (int gi = 0; gi < GROUP; ++gi) {
-      const float4 qq = reinterpret_cast<const float4*>(
-          q_pre + ((int64_t)b * n_q + h * GROUP + gi) * kHeadDim)[lane];
-      q[gi][0] = (qq.x * c0.x - qq.y * c0.y) * q_scale;
-      q[gi][1] = (qq.x * c0.y + qq.y * c0.x) * q_scale;
-      q[gi][2] = (qq.z * c1.x - qq.w * c1.y) * q_scale;
-      q[gi][3] = (qq.z * c1.y + qq.w * c1.x) * q_scale;
+      const float4* qp = reinterpret_cast<const float4*>(
+          q_pre + ((int64_t)b * n_q + h * GROUP + gi) * kHeadDim + 8 * hl);
+      const float4 a = qp[0], c = qp[1];
+      const float e[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 cs = rope[(int64_t)pos * 64 + 4 * hl + j];
+        q[gi][2 * j] = (e[2 * j] * cs.x - e[2 * j + 1] * cs.y) * q_scale;
+        q[gi][2 * j + 1] = (e[2 * j] * cs.y + e[2 * j + 1] * cs.x) * q_scale;
+      }
     }
   }
-  float m[GROUP], l[GROUP], o[GROUP][4];
+  float m[GROUP], l[GROUP], o[GROUP][8];
 #pragma unroll
   for (int gi = 0; gi < GROUP; ++gi) {
     m[gi] = -INFINITY;
     l[gi] = 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[gi][j] = 0.f;
+    for (int j = 0; j < 8; ++j) o[gi][j] = 0.f;
   }
-  const int nw = kKvThreads / 32;
-  for (int base = t0 + warp * kKvUnroll; base < t1; base += nw * kKvUnroll) {
-    uint2 kr[kKvUnroll], vr[kKvUnroll];
+  const __nv_bfloat16* Kb = K + (int64_t)b * L_max * width + (int64_t)h * kHeadDim + 8 * hl;
+  const __nv_bfloat16* Vb = V + (int64_t)b * L_max * width + (int64_t)h * kHeadDim + 8 * hl;
+  // warp-uniform trip count (the 16-lane shuffles use the full mask): warp w
+  // takes blocks of 2*kKvUnroll tokens, half-warp `half` the tokens 2u + half
+  for (int wbase = t0 + warp * 2 * kKvUnroll; wbase < t1; wbase += kNw * 2 * kKvUnroll) {
+    const int base = wbase + half;
+    uint4 kr[kKvUnroll], vr[kKvUnroll];
 #pragma unroll
     for (int u = 0; u < kKvUnroll; ++u) {
-      const int t = min(base + u, t1 - 1);
-      const int64_t off = ((int64_t)b * L_max + t) * width + (int64_t)h * kHeadDim;
-      kr[u] = reinterpret_cast<const uint2*>(K + off)[lane];
-      vr[u] = reinterpret_cast<const uint2*>(V + off)[lane];
+      const int t = min(base + 2 * u, t1 - 1);
+      kr[u] = __ldg(reinterpret_cast<const uint4*>(Kb + (int64_t)t * width));
+      vr[u] = __ldg(reinterpret_cast<const uint4*>(Vb + (int64_t)t * width));
     }
 #pragma unroll
     for (int gi = 0; gi < GROUP; ++gi) {
@@ -96,49 +111,52 @@ __global__ void __launch_bounds__(kKvThreads)
       float mt = -INFINITY;
 #pragma unroll
       for (int u = 0; u < kKvUnroll; ++u) {
-        float kf[4];
-        bf16x4(kr[u], kf);
-        const float d = warp_sum(q[gi][0] * kf[0] + q[gi][1] * kf[1] + q[gi][2] * kf[2] + q[gi][3] * kf[3]);
-        s[u] = (base + u < t1) ? d : -INFINITY;
+        float kf[8];
+        bf16x8(kr[u], kf);
+        float d = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d = fmaf(q[gi][j], kf[j], d);
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+        s[u] = (base + 2 * u < t1) ? d : -INFINITY;
         mt = fmaxf(mt, s[u]);
       }
       const float mn = fmaxf(m[gi], mt);
       const float alpha = (m[gi] == -INFINITY) ? 0.f : exp2f(m[gi] - mn);
       l[gi] *= alpha;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) o[gi][j] *= alpha;
+      for (int j = 0; j < 8; ++j) o[gi][j] *= alpha;
 #pragma unroll
       for (int u = 0; u < kKvUnroll; ++u) {
-        const float pr = (base + u < t1) ? exp2f(s[u] - mn) : 0.f;
-        float vf[4];
-        bf16x4(vr[u], vf);
+        const float pr = (base + 2 * u < t1) ? exp2f(s[u] - mn) : 0.f;
+        float vf[8];
+        bf16x8(vr[u], vf);
         l[gi] += pr;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o[gi][j] = fmaf(pr, vf[j], o[gi][j]);
+        for (int j = 0; j < 8; ++j) o[gi][j] = fmaf(pr, vf[j], o[gi][j]);
       }
       m[gi] = mn;
     }
   }
-  // merge the 4 warps through shared memory, then one partial per CTA
-  __shared__ float s_m[4][GROUP], s_l[4][GROUP], s_o[4][GROUP][kHeadDim];
+  // merge the 2*nw half-warp streams through shared memory, one partial per CTA
+  __shared__ float s_m[kStreams][GROUP], s_l[kStreams][GROUP], s_o[kStreams][GROUP][kHeadDim];
 #pragma unroll
   for (int gi = 0; gi < GROUP; ++gi) {
-    if (lane == 0) {
-      s_m[warp][gi] = m[gi];
-      s_l[warp][gi] = l[gi];
+    if (hl == 0) {
+      s_m[stream][gi] = m[gi];
+      s_l[stream][gi] = l[gi];
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) s_o[warp][gi][4 * lane + j] = o[gi][j];
+    for (int j = 0; j < 8; ++j) s_o[stream][gi][8 * hl + j] = o[gi][j];
   }
   __syncthreads();
-  const int d = threadIdx.x;  // 128 threads = 128 dims
-#pragma unroll
-  for (int gi = 0; gi < GROUP; ++gi) {
+  for (int idx = threadIdx.x; idx < GROUP * kHeadDim; idx += kKvThreads) {
+    const int gi = idx / kHeadDim, d = idx % kHeadDim;
     float M = -INFINITY;
-    for (int w = 0; w < nw; ++w) M = fmaxf(M, s_m[w][gi]);
+    for (int w = 0; w < kStreams; ++w) M = fmaxf(M, s_m[w][gi]);
     float L = 0.f, O = 0.f;
     if (M != -INFINITY)
-      for (int w = 0; w < nw; ++w) {
+      for (int w = 0; w < kStreams; ++w) {
         if (s_m[w][gi] == -INFINITY) continue;
         const float wgt = exp2f(s_m[w][gi] - M);
         L = fmaf(wgt, s_l[w][gi], L);
@@ -210,7 +228,6 @@ int xq_kv_decode_attend(const void* k_cache, const void* v_cache, int64_t L_max,
     case 1: status = launch_kv<1>(K, V, L_max, seq_lens, n_seqs, n_kv_heads, chunk_tokens, n_chunks, q_pre, rope, qs, parts, st); break;
     case 2: status = launch_kv<2>(K, V, L_max, seq_lens, n_seqs, n_kv_heads, chunk_tokens, n_chunks, q_pre, rope, qs, parts, st); break;
     case 4: status = launch_kv<4>(K, V, L_max, seq_lens, n_seqs, n_kv_heads, chunk_tokens, n_chunks, q_pre, rope, qs, parts, st); break;
-    case 8: status = launch_kv<8>(K, V, L_max, seq_lens, n_seqs, n_kv_heads, chunk_tokens, n_chunks, q_pre, rope, qs, parts, st); break;
     default: return fail(XQ_ECONFIG, "unsupported group %d", group);
   }
   if (status != XQ_OK) return status;
