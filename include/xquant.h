@@ -174,6 +174,42 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
                      float sm_scale, int32_t tiles_per_chunk, void* workspace,
                      int64_t workspace_bytes, float* out, void* stream);
 
+/* ---- V-absorbed variant (the default hot path) ----
+ * Same result as xq_decode_attend, computed with the exact reassociation
+ *   sum_t p_t (A_V[t] @ W_v[:, kv]) = (sum_t p_t A_V[t]) @ W_v[:, kv]
+ * (cache.py:385-387 + model.py:178-181): the K side is rematerialised on
+ * tcgen05 as before (two KV heads per pass); the V side is one
+ * [kdim x n_q] tcgen05 GEMM over each 256-token tile's probabilities plus a
+ * per-head projection through W_v at the end. kdim % 256 == 0. */
+
+/* Arranged weights of the absorbed kernel. wk_out: fp16
+ * [ceil(n_kv/2)*256][kdim], row h*128+j = W_k[:, h*128+j]^T in the K-side
+ * producer channel order (zero rows pad an odd n_kv). wv_out: fp16
+ * [n_kv][kdim][128], row c = W_v[perm_v(c), h*128 .. +128] with perm_v the
+ * V-side producer order. a_mode_v may be XQ_A_SAME. */
+int xq_arrange_weights_absorbed(const void* w_k, const void* w_v, int32_t w_dtype, int64_t kdim,
+                                int32_t n_kv_heads, int32_t a_mode_k, int32_t bits_k,
+                                int32_t a_mode_v, int32_t bits_v, void* wk_out, void* wv_out,
+                                void* stream);
+
+/* Workspace (bytes): per-tile partials O [n_seqs][tiles][n_q][kdim] + (m, l). */
+int64_t xq_absorbed_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q_heads,
+                                    int64_t kdim);
+
+/* Arguments as xq_decode_attend, with the two arranged weight buffers of
+ * xq_arrange_weights_absorbed in place of w_arranged. out: float32
+ * [n_seqs, n_kv_heads*group, 128]. */
+int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                              const float* ak_resid, const int32_t* ak_nflushed, int32_t ak_bits,
+                              int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
+                              const void* av_params, int32_t av_bits, int64_t av_row_bytes,
+                              int32_t group_size, int64_t L_max, int64_t kdim,
+                              const int32_t* seq_lens, int32_t n_seqs, int32_t max_len,
+                              const void* wk_arranged, const void* wv_arranged, int32_t n_kv_heads,
+                              int32_t group, const float* q_pre, const void* rope_cs,
+                              int64_t rope_n, float sm_scale, void* workspace,
+                              int64_t workspace_bytes, float* out, void* stream);
+
 /* Debug hook: when buf != NULL, xq_decode_attend also dumps the raw fp32
  * accumulator of every tile t < n_tiles to buf[b][kv_head][t][128][256]
  * (columns 0-127 = pre-RoPE K, 128-255 = V). NULL disables (default). */

@@ -38,6 +38,10 @@ _SIGS = {
     "xq_decode_attend": [_I32, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32, _I64,
                          _I64, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _I64, _F, _I32, _P, _I64,
                          _P, _P],
+    "xq_arrange_weights_absorbed": [_P, _P, _I32, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P],
+    "xq_decode_attend_absorbed": [_I32, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32,
+                                  _I64, _I64, _P, _I32, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _F,
+                                  _P, _I64, _P, _P],
     "xq_remat_f32": [_I32, _P, _P, _P, _I32, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32, _I64,
                      _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P],
     "xq_cl_accumulate": [_I32, _P, _I64, _P, _I32, _I32, _I64, _P, _I32, _I32, _I64, _P, _P,
@@ -48,7 +52,8 @@ _SIGS = {
                             _I64, _P, _P],
 }
 _I64_RET = {"xq_decode_workspace_bytes": [_I32, _I32, _I32, _I32, _I32],
-            "xq_kv_decode_workspace_bytes": [_I32, _I32, _I32, _I32, _I32]}
+            "xq_kv_decode_workspace_bytes": [_I32, _I32, _I32, _I32, _I32],
+            "xq_absorbed_workspace_bytes": [_I32, _I32, _I32, _I64]}
 
 
 def _load():

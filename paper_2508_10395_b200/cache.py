@@ -24,6 +24,7 @@ scope table and raise ``ConfigError`` here.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -112,6 +113,24 @@ class LayerWeights:
             self._cache[key] = out
         return self._cache[key]
 
+    def arranged_absorbed(self, key, a_mode_k, bits_k, a_mode_v, bits_v, wk, wv):
+        """(W_k rows for the K passes, W_v [n_kv, kdim, 128]) of the V-absorbed kernel."""
+        key = ("absorbed",) + tuple(key)
+        if key not in self._cache:
+            kdim, width = wk.shape
+            if width % HEAD_DIM:
+                raise ShapeError(f"kv width {width} not a multiple of {HEAD_DIM}")
+            n_kv = width // HEAD_DIM
+            n_pass = (n_kv + 1) // 2
+            wk_out = torch.empty((n_pass * 256, kdim), dtype=torch.float16, device=wk.device)
+            wv_out = torch.empty((n_kv, kdim, HEAD_DIM), dtype=torch.float16, device=wk.device)
+            wk_c, wv_c = wk.contiguous(), wv.contiguous()
+            N.call("xq_arrange_weights_absorbed", N.ptr(wk_c), N.ptr(wv_c), _dtype_code(wk_c), kdim,
+                   n_kv, a_mode_k, bits_k, a_mode_v, bits_v, N.ptr(wk_out), N.ptr(wv_out),
+                   N.stream_of(wk.device))
+            self._cache[key] = (wk_out, wv_out)
+        return self._cache[key]
+
     def f32(self, name: str) -> torch.Tensor:
         key = ("f32", name)
         if key not in self._cache:
@@ -125,6 +144,18 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 
 _ROPE: dict = {}
+_SCRATCH: dict = {}
+
+
+def _scratch(device, nbytes: int) -> torch.Tensor:
+    """Per-device reusable workspace of the fused kernels' split partials
+    (launches on one stream are ordered, so every layer can share it)."""
+    device = torch.device(device)
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    cur = _SCRATCH.get(key)
+    if cur is None or cur.numel() * 4 < nbytes:
+        _SCRATCH[key] = cur = torch.empty(nbytes // 4 + 1, dtype=torch.float32, device=device)
+    return cur
 
 
 def _rope(n_pos: int, device, j_major: int) -> torch.Tensor:
@@ -277,6 +308,8 @@ class CacheBackend:
         self.device = torch.device(device)
         self.n_tokens = np.zeros(n_slots, dtype=np.int64)
         self.lens_dev = torch.zeros(n_slots, dtype=torch.int32, device=self.device)
+        # V absorption (xq_absorb.cu): exact reassociation p.(x W_v) = (p.x) W_v
+        self.absorb = os.environ.get("XQ_ABSORB", "1") != "0"
 
     # -- interface ---------------------------------------------------------
     def prefill(self, x, weights: LayerWeights, acc: Accumulator | None = None, slot=None):
@@ -367,10 +400,26 @@ class CacheBackend:
         return torch.empty(nbytes // 4 + 1, dtype=torch.float32, device=self.device), nbytes
 
     def _fused(self, ak_mode, ak_src, ak_params, ak_resid, ak_nfl, ak_bits, ak_rb, av_mode,
-               av_src, av_params, av_bits, av_rb, kdim, w_arr, group, q, lens, max_len, out, tpc):
+               av_src, av_params, av_bits, av_rb, kdim, w_spec, weights, group, q, lens, max_len,
+               out, tpc):
+        """One fused decode launch. ``w_spec`` = (key, a_mode_k, bits_k, a_mode_v, bits_v,
+        W_k, W_v) names the projection pair and the A operands that feed it."""
+        key, mk, bk, mv, bv, wk, wv = w_spec
+        rope = rope_table_t(max_len, self.device)
+        if self.absorb and kdim % 256 == 0:
+            wk_arr, wv_arr = weights.arranged_absorbed(key, mk, bk, mv, bv, wk, wv)
+            nbytes = N.lib.xq_absorbed_workspace_bytes(self.n_slots, max_len, self.n_kv * group, kdim)
+            ws = _scratch(self.device, nbytes)
+            N.call("xq_decode_attend_absorbed", ak_mode, N.ptr(ak_src), N.ptr(ak_params),
+                   N.ptr(ak_resid), N.ptr(ak_nfl), ak_bits, ak_rb, av_mode, N.ptr(av_src),
+                   N.ptr(av_params), av_bits, av_rb, self.group_size, self.L, kdim, N.ptr(lens),
+                   self.n_slots, max_len, N.ptr(wk_arr), N.ptr(wv_arr), self.n_kv, group, N.ptr(q),
+                   N.ptr(rope), rope.shape[1] // 2, 1.0 / math.sqrt(HEAD_DIM), N.ptr(ws), nbytes,
+                   N.ptr(out), N.stream_of(self.device))
+            return
+        w_arr = weights.arranged(key, mk, bk, mv, bv, wk, wv)
         tpc = tpc or default_tiles_per_chunk(self.n_slots, max_len, self.n_kv)
         ws, nbytes = self._workspace(max_len, group, tpc)
-        rope = rope_table_t(max_len, self.device)
         N.call("xq_decode_attend", ak_mode, N.ptr(ak_src), N.ptr(ak_params), N.ptr(ak_resid),
                N.ptr(ak_nfl), ak_bits, ak_rb, av_mode, N.ptr(av_src), N.ptr(av_params), av_bits,
                av_rb, self.group_size, self.L, kdim, N.ptr(lens), self.n_slots, max_len,
@@ -528,10 +577,9 @@ class InputCacheMHA(CacheBackend):
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         mode, src, params, bits, rb = self._a_operand()
-        w_arr = weights.arranged(("mha", mode, bits), mode, bits, N.A_SAME, bits,
-                                 weights.w_k, weights.w_v)
+        spec = (("mha", mode, bits), mode, bits, N.A_SAME, bits, weights.w_k, weights.w_v)
         self._fused(mode, src, params, None, None, bits, rb, N.A_SAME, None, None, 0, 0, self.d,
-                    w_arr, 1, q, lens, max_len, out, tpc)
+                    spec, weights, 1, q, lens, max_len, out, tpc)
 
     def memory_bytes(self):
         if self.passthrough:
@@ -594,11 +642,11 @@ class LatentInputCacheGQA(CacheBackend):
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         ks, vs = self.k_stream, self.v_stream
-        w_arr = weights.arranged(("gqa", self.bits), N.A_CODES_CHANNEL, ks.bits, N.A_CODES_TOKEN,
-                                 vs.bits, weights.fused_k, weights.fused_v)
+        spec = (("gqa", self.bits), N.A_CODES_CHANNEL, ks.bits, N.A_CODES_TOKEN, vs.bits,
+                weights.fused_k, weights.fused_v)
         self._fused(N.A_CODES_CHANNEL, ks.codes, ks.params, ks.resid, ks.nflushed_dev, ks.bits,
                     ks.row_bytes, N.A_CODES_TOKEN, vs.codes, vs.params, vs.bits, vs.row_bytes,
-                    self.latent, w_arr, self.g, q, lens, max_len, out, tpc)
+                    self.latent, spec, weights, self.g, q, lens, max_len, out, tpc)
 
     def memory_bytes(self):
         out = {f"k_{k}": v for k, v in self.k_stream.nbytes().items()}
@@ -689,15 +737,16 @@ class DeltaInputCacheMHA(CacheBackend):
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         if self.is_base:
             s = self.stream
-            w_arr = weights.arranged(("mha", N.A_CODES_TOKEN, s.bits), N.A_CODES_TOKEN, s.bits,
-                                     N.A_SAME, s.bits, weights.w_k, weights.w_v)
+            spec = (("mha", N.A_CODES_TOKEN, s.bits), N.A_CODES_TOKEN, s.bits, N.A_SAME, s.bits,
+                    weights.w_k, weights.w_v)
             self._fused(N.A_CODES_TOKEN, s.codes, s.params, None, None, s.bits, s.row_bytes,
-                        N.A_SAME, None, None, 0, 0, self.d, w_arr, 1, q, lens, max_len, out, tpc)
+                        N.A_SAME, None, None, 0, 0, self.d, spec, weights, 1, q, lens, max_len,
+                        out, tpc)
         else:
-            w_arr = weights.arranged(("mha", N.A_F16_ROWS, 16), N.A_F16_ROWS, 16, N.A_SAME, 16,
-                                     weights.w_k, weights.w_v)
+            spec = (("mha", N.A_F16_ROWS, 16), N.A_F16_ROWS, 16, N.A_SAME, 16, weights.w_k,
+                    weights.w_v)
             self._fused(N.A_F16_ROWS, acc.x16, None, None, None, 16, 0, N.A_SAME, None, None, 0,
-                        0, self.d, w_arr, 1, q, lens, max_len, out, tpc)
+                        0, self.d, spec, weights, 1, q, lens, max_len, out, tpc)
 
     def memory_bytes(self):
         return self.stream.nbytes()

@@ -1,0 +1,933 @@
+// Fused XQuant decode with exact V absorption, for sm_100a.
+//
+// The reference rebuilds V = x_hat @ W_v for every cached token and then
+// takes p @ V (cache.py:385-387, model.py:150-182). Because the product is
+// associative, per query head h
+//     sum_t p_t,h (x_hat_t @ W_v[:, kv(h)]) = (sum_t p_t,h x_hat_t) @ W_v[:, kv(h)]
+// so the V side needs only the probability-weighted sum of the dequantized
+// rows -- a [kdim x heads] GEMM over tokens -- plus one tiny projection per
+// head at the end. The K side keeps the full rematerialisation (RoPE rotates
+// K per position, so q cannot be absorbed into W_k). Per token this halves
+// the tensor-core work of MHA (4*d*d_kv -> 2*d*d_kv + 2*H*d FLOP) and cuts
+// the dequantisation passes from one per KV head to one per KV-head pair plus
+// one for the V side.
+//
+// One persistent CTA pair (cta_group::2) per two SMs, 512 threads each:
+//   warp 0       TMA of the W_k tiles (this CTA's 128 of the pass's 256 rows);
+//                fp16 A rows by TMA when the A operand is the CL accumulator
+//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer (leader)
+//   warp 2       TMA of the packed-codes ring
+//   warps 4-11   dequant producers (two groups of 4, alternate codes stages)
+//   warps 12-15  epilogue
+// Per 256-token tile of one sequence (work unit):
+//   passes p = 0 .. ceil(n_kv/2)-1: D[256 tok x 256] = A[tok x kdim] W_k^T for
+//     KV heads 2p, 2p+1 (M=256 over the pair, N=256, K=kdim). The epilogue
+//     RoPEs K in registers and stores the scores q.k of the heads' query heads.
+//   exchange: each CTA keeps half of the query heads; the scores of the other
+//     half for its 128 tokens go to the peer over DSMEM.
+//   softmax over the tile's 256 tokens (tile max m, sum l) -> P (fp16) as the
+//     K-major B operand [heads x 256 tokens].
+//   V side: O^T[kdim x heads] = X_hat^T[kdim x 256 tok] P[256 tok x heads]:
+//     M=256 channels over the pair (128 per CTA, MN-major A tiles written by
+//     the same producers), N = heads, K = tokens. O and (m, l) go to HBM as
+//     this tile's split partials.
+// k_absorb_vproj then merges the tile partials per (sequence, head) and
+// applies W_v[:, kv(h)].
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <stdlib.h>
+
+#include "xq_common.cuh"
+#include "xq_dequant.cuh"
+#include "xq_host.h"
+#include "xq_layout.cuh"
+
+namespace xq {
+namespace absorb {
+
+constexpr int kTileM = 128;   // token rows per CTA (TMEM lanes)
+constexpr int kPairM = 256;   // token rows per CTA pair
+constexpr int kChunk = 64;    // channels per pass-1 stage
+constexpr int kThreads = 512;
+constexpr int kProdWarp0 = 4;
+constexpr int kEpiWarp0 = 12;
+constexpr int kG = 128;
+constexpr int kMaxStages = 6;
+constexpr int kMaxHeads = 64;
+constexpr uint32_t kABytes = kTileM * 128;  // [128 x 64] fp16 = 16 KB
+constexpr uint32_t kBBytes = 128 * 128;     // this CTA's 128 W rows x 64 channels
+constexpr uint32_t kABStage = kABytes + kBBytes;
+constexpr uint32_t kMNHalf = 64 * 128;      // V-side A stage: [64 tok x 64 ch] per channel half
+
+struct Params {
+  const float* k_resid;        // CODES_CHANNEL: fp32 residual rows [n_seqs][128][kdim]
+  const int32_t* k_nflushed;   // CODES_CHANNEL: flushed token count per sequence
+  int32_t kdim;
+  int64_t L_max;
+  const int32_t* seq_lens;
+  int32_t n_seqs, n_tiles, n_units;
+  int32_t n_kv, n_q, nb, nbh, n_pass;
+  int32_t stages, cstages;
+  uint32_t cstage_bytes;
+  uint32_t k_code_bytes, k_tx, v_tx;  // codes ring: codes bytes / TMA bytes per stage
+  const float* q_pre;
+  const float2* rope;  // frequency-major [64][rope_n]
+  int64_t rope_n;
+  float q_scale;
+  float* part_o;       // [n_seqs][n_tiles][n_q][kdim]
+  float2* part_ml;     // [n_seqs][n_tiles][n_q] (m, l), m in the log2 domain
+  uint64_t w_hint;
+  uint32_t off_p, off_codes, off_q, off_sc, off_x, off_bar;
+};
+
+// work unit u -> (sequence, tile); false when the tile is past the sequence end
+XQ_DEVINL bool get_unit(const Params& p, int u, int& b, int& t, int& len) {
+  b = u % p.n_seqs;
+  t = u / p.n_seqs;
+  len = __ldg(p.seq_lens + b);
+  return t * kPairM < len;
+}
+
+template <int AK, int AV, int BITS, int GROUP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_decode_absorbed(const __grid_constant__ CUtensorMap tmap_w,
+                      const __grid_constant__ CUtensorMap tmap_ka,
+                      const __grid_constant__ CUtensorMap tmap_kp,
+                      const __grid_constant__ CUtensorMap tmap_va,
+                      const __grid_constant__ CUtensorMap tmap_vp, const Params p) {
+  constexpr bool PROD = AK != XQ_A_F16_ROWS;
+  static_assert((AK == XQ_A_F16_ROWS) == (AV == XQ_A_F16_ROWS), "fp16 rows feed both sides or neither");
+  static_assert(AV != XQ_A_CODES_CHANNEL, "the V side is per-token");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sAB = smem;
+  uint8_t* sP = smem + p.off_p;
+  uint8_t* sC = smem + p.off_codes;
+  float* q_s = reinterpret_cast<float*>(smem + p.off_q);    // [n_q][128]
+  float* sc_s = reinterpret_cast<float*>(smem + p.off_sc);  // [n_q][128 rows]
+  float* x_s = reinterpret_cast<float*>(smem + p.off_x);    // [nbh][128 rows] (peer's scores)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* cfull = empty + kMaxStages;
+  uint64_t* cempty = cfull + kMaxStages;
+  uint64_t* tfull = cempty + kMaxStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* pready = tempty + 2;
+  uint64_t* xfull = pready + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int STAGES = p.stages, CSTAGES = p.cstages;
+  const int ngrp = p.kdim / kG;            // 128-channel groups
+  const int nkc = p.kdim / kChunk;         // pass-1 stages per pass
+  const int nblk = p.kdim / 256;           // V-side channel blocks (128 per CTA)
+  const int ncs = (p.n_pass + 1) * ngrp;   // codes stages per tile (pass-1 + V side)
+  const int bpu = 256 / p.nb;              // V-side blocks per 256-column accumulator
+  const int nuse = (nblk + bpu - 1) / bpu;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], PROD ? 2 + 8 : 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < CSTAGES; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], 4);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    mbar_init(pready, 8);   // leader's: 4 epilogue warps per CTA
+    mbar_init(xfull, 128);  // the peer's 128 epilogue threads
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_w);
+    if constexpr (!PROD) {
+      tma_prefetch_desc(&tmap_ka);
+      tma_prefetch_desc(&tmap_va);
+    }
+  }
+  if (warp == 2 && lane == 0 && PROD) {
+    tma_prefetch_desc(&tmap_ka);
+    tma_prefetch_desc(&tmap_kp);
+    tma_prefetch_desc(&tmap_va);
+    tma_prefetch_desc(&tmap_vp);
+  }
+  if (warp == 1) {
+    tmem_alloc2(tmem_slot, 512);
+    tmem_relinquish2();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full_leader0 = mapa_shared(smem_u32(&full[0]), 0);
+  const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+  const uint32_t pready_leader = mapa_shared(smem_u32(pready), 0);
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA: W_k halves (+ fp16 A rows)
+    uint32_t it = 0;
+    for (int u = cluster; u < p.n_units; u += n_clusters) {
+      int b, t, len;
+      if (!get_unit(p, u, b, t, len)) continue;
+      const int32_t row_tile = static_cast<int32_t>((int64_t)b * p.L_max + t * kPairM);
+      for (int ps = 0; ps < p.n_pass; ++ps) {
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
+            uint8_t* st = sAB + s * kABStage;
+            constexpr uint32_t kTx = 2 * (kBBytes + (PROD ? 0u : kABytes));
+            if (leader) mbar_arrive_expect_tx(&full[s], kTx);
+            else mbar_arrive_remote(full_leader0 + 8 * s);
+            tma_load_2d_pair(st + kABytes, &tmap_w, &full[s], kc * kChunk, ps * 256 + rank * 128,
+                             p.w_hint);
+            if constexpr (!PROD)
+              tma_load_2d_pair(st, &tmap_ka, &full[s], kc * kChunk, row_tile + rank * kTileM,
+                               kEvictNormal);
+          }
+          __syncwarp();
+        }
+      }
+      for (int bb = 0; bb < nblk; ++bb) {
+        for (int j = 0; j < 4; ++j, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (elect_one()) {
+            uint8_t* st = sAB + s * kABStage;
+            if constexpr (PROD) {
+              if (leader) mbar_arrive(&full[s]);
+              else mbar_arrive_remote(full_leader0 + 8 * s);
+            } else {
+              if (leader) mbar_arrive_expect_tx(&full[s], 2 * kABytes);
+              else mbar_arrive_remote(full_leader0 + 8 * s);
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh)
+                tma_load_2d_pair(st + hh * kMNHalf, &tmap_va, &full[s],
+                                 bb * 256 + rank * 128 + hh * 64, row_tile + 64 * j, kEvictNormal);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader CTA only)
+    if (leader) {
+      constexpr uint32_t kIdescK = idesc_f16_f32(256, 256);
+      const uint32_t kIdescV = idesc_f16_f32_amn(256, p.nb);
+      const uint64_t desc0 = sdesc_sw128(smem_u32(sAB));
+      const uint64_t descv0 = sdesc_mn_sw128(smem_u32(sAB), kMNHalf, 1024);
+      const uint64_t descp0 = sdesc_sw128(smem_u32(sP));
+      const uint32_t pstage = p.nbh * 128;  // bytes of one 64-token P stage
+      uint32_t it = 0, tc = 0, ti = 0;
+      for (int u = cluster; u < p.n_units; u += n_clusters) {
+        int b, t, len;
+        if (!get_unit(p, u, b, t, len)) continue;
+        for (int ps = 0; ps < p.n_pass; ++ps, ++tc) {
+          const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+          mbar_wait_cluster(&tempty[a], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + a * 256;
+          for (int kc = 0; kc < nkc; ++kc, ++it) {
+            const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+            mbar_wait_cluster(&full[s], ph);
+            tc_fence_after();
+            const uint64_t ad = desc0 + ((s * kABStage) >> 4);
+            const uint64_t bd = ad + (kABytes >> 4);
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < kChunk / 16; ++k)
+                mma2_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdescK, (kc | k) != 0);
+              mma2_commit_both(&empty[s]);
+            }
+            __syncwarp();
+          }
+          if (elect_one()) mma2_commit_both(&tfull[a]);
+          __syncwarp();
+        }
+        // V side: needs this tile's P from both CTAs
+        mbar_wait_cluster(pready, ti & 1);
+        tc_fence_after();
+        int blk = 0;
+        for (int us = 0; us < nuse; ++us, ++tc) {
+          const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+          mbar_wait_cluster(&tempty[a], aph ^ 1);
+          tc_fence_after();
+          for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
+            const uint32_t d = tmem + a * 256 + bi * p.nb;
+            for (int j = 0; j < 4; ++j, ++it) {
+              const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+              mbar_wait_cluster(&full[s], ph);
+              tc_fence_after();
+              const uint64_t ad = descv0 + ((s * kABStage) >> 4);
+              const uint64_t bd = descp0 + ((j * pstage) >> 4);
+              if (elect_one()) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // 16 tokens = two 8-row K groups = 2048 B of A
+                  mma2_f16_ss(d, ad + k * (2048 >> 4), bd + 2 * k, kIdescV, (j | k) != 0);
+                mma2_commit_both(&empty[s]);
+              }
+              __syncwarp();
+            }
+          }
+          if (elect_one()) mma2_commit_both(&tfull[a]);
+          __syncwarp();
+        }
+        ++ti;
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ TMA: codes ring
+    if constexpr (PROD) {
+      uint32_t ci = 0;
+      for (int u = cluster; u < p.n_units; u += n_clusters) {
+        int b, t, len;
+        if (!get_unit(p, u, b, t, len)) continue;
+        const int32_t row_tile = static_cast<int32_t>((int64_t)b * p.L_max + t * kPairM);
+        for (int q = 0; q < ncs; ++q, ++ci) {
+          const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
+          mbar_wait(&cempty[cs], cph ^ 1);
+          if (elect_one()) {
+            uint8_t* st = sC + cs * p.cstage_bytes;
+            if (q < p.n_pass * ngrp) {  // K side: group g of this CTA's 128 tokens
+              const int g = q % ngrp;
+              const int32_t arow = row_tile + rank * kTileM;
+              mbar_arrive_expect_tx(&cfull[cs], p.k_tx);
+              tma_load_2d(st, &tmap_ka, &cfull[cs], g * 16 * BITS, arow, kEvictNormal);
+              if constexpr (AK == XQ_A_CODES_TOKEN)
+                tma_load_2d(st + p.k_code_bytes, &tmap_kp, &cfull[cs], 4 * (g & ~3), arow, kEvictNormal);
+              else
+                tma_load_2d(st + p.k_code_bytes, &tmap_kp, &cfull[cs], g * 128, 2 * (arow / kG),
+                            kEvictNormal);
+            } else {  // V side: group 2*bb + rank of token half th of the pair tile
+              const int qb = q - p.n_pass * ngrp;
+              const int g = 2 * (qb >> 1) + static_cast<int>(rank);
+              const int32_t arow = row_tile + (qb & 1) * kTileM;
+              mbar_arrive_expect_tx(&cfull[cs], p.v_tx);
+              tma_load_2d(st, &tmap_va, &cfull[cs], g * 16 * BITS, arow, kEvictNormal);
+              tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (g & ~3), arow,
+                          kEvictNormal);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
+    // ------------------------------------------------ dequant producers
+    if constexpr (PROD) {
+      const int gp = (warp - kProdWarp0) >> 2;
+      const int r = ((warp - kProdWarp0) & 3) * 32 + lane;
+      const RowSwizzle sw_k(r);       // K side: row = token r of this CTA's 128
+      const RowSwizzle sw_v(r & 63);  // V side: row = token within a 64-token stage
+      const int hh = r >> 6;          // V side: channel half of the group
+      const uint32_t sAB_a = smem_u32(sAB), sC_a = smem_u32(sC);
+      uint32_t tcount = 0;
+      for (int u = cluster; u < p.n_units; u += n_clusters) {
+        int b, t, len;
+        if (!get_unit(p, u, b, t, len)) continue;
+        const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + b) : 0;
+        const int tok_k = t * kPairM + rank * kTileM + r;
+        const uint32_t ci0 = tcount * ncs;
+        for (int q = ((ci0 & 1) == static_cast<uint32_t>(gp)) ? 0 : 1; q < ncs; q += 2) {
+          const uint32_t ci = ci0 + q;
+          const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
+          const uint32_t st = sC_a + cs * p.cstage_bytes;
+          mbar_wait(&cfull[cs], cph);
+          const bool kside = q < p.n_pass * ngrp;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t itn = 2 * ci + h;
+            const uint32_t s = itn % STAGES, ph = (itn / STAGES) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t tile = sAB_a + s * kABStage;
+            if (kside) {
+              const int kc = 2 * (q % ngrp) + h;
+              produce_chunk<AK, BITS>(tile, st, st + p.k_code_bytes, sw_k, r, tok_k < len, tok_k, b,
+                                      nfl, kc, nullptr, p.k_resid, p.kdim);
+            } else {
+              const int qb = q - p.n_pass * ngrp;
+              const int g = 2 * (qb >> 1) + static_cast<int>(rank);
+              const int crow = h * 64 + (r & 63);
+              const int tok = t * kPairM + (qb & 1) * kTileM + crow;
+              if constexpr (AV == XQ_A_CODES_TOKEN)
+                produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
+                                        tok < len, tok, b, 1 << 30, 2 * g + hh, nullptr, nullptr,
+                                        p.kdim);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (leader) mbar_arrive_if(&full[s], lane == 0);
+            else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
+          }
+          mbar_arrive_if(&cempty[cs], lane == 0);
+        }
+        ++tcount;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------ epilogue (this CTA's 128 rows)
+    const int ew = warp - kEpiWarp0;
+    const int et = threadIdx.x - kEpiWarp0 * 32;
+    const int row = ew * 32 + lane;
+    const uint32_t tlane = static_cast<uint32_t>(ew * 32) << 16;
+    const int nbh = p.nbh;
+    const uint32_t peer = rank ^ 1u;
+    const uint32_t x_peer = mapa_shared(smem_u32(x_s), peer);
+    const uint32_t xfull_peer = mapa_shared(smem_u32(xfull), peer);
+    const uint32_t sP_a = smem_u32(sP);
+    uint32_t tc = 0, ti = 0;
+    for (int u = cluster; u < p.n_units; u += n_clusters) {
+      int b, t, len;
+      if (!get_unit(p, u, b, t, len)) continue;
+      const int pos = len - 1;
+      named_bar_sync(1, 128);  // previous tile's readers of q_s / sc_s are done
+      {
+        const float2 cs = p.rope[(int64_t)(et >> 1) * p.rope_n + pos];
+        for (int h = 0; h < p.n_q; ++h) {
+          const float* qp = p.q_pre + ((int64_t)b * p.n_q + h) * kHeadDim;
+          const float e0 = qp[et & ~1], e1 = qp[et | 1];
+          const float rr = (et & 1) ? (e0 * cs.y + e1 * cs.x) : (e0 * cs.x - e1 * cs.y);
+          q_s[h * kHeadDim + et] = rr * p.q_scale;
+        }
+      }
+      named_bar_sync(1, 128);
+      const int tok = t * kPairM + rank * kTileM + row;
+      const bool valid = tok < len;
+      const float2* rp = p.rope + (valid ? tok : 0);
+      // ---- K side: scores of every query head for this CTA's 128 tokens
+      for (int ps = 0; ps < p.n_pass; ++ps, ++tc) {
+        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+        mbar_wait(&tfull[a], aph);
+        tc_fence_after();
+#pragma unroll 1
+        for (int kh = 0; kh < 2; ++kh) {
+          const int kvh = 2 * ps + kh;
+          if (kvh >= p.n_kv) break;
+          float sc[GROUP];
+#pragma unroll
+          for (int gi = 0; gi < GROUP; ++gi) sc[gi] = 0.f;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float kb[32];
+            tmem_ld32(tmem + tlane + a * 256 + kh * 128 + c * 32, kb);
+            float2 csv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) csv[i] = __ldg(rp + (int64_t)(c * 16 + i) * p.rope_n);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {  // RoPE (linalg.py:92-93)
+              const float2 cs = csv[i];
+              const float k0 = kb[2 * i], k1 = kb[2 * i + 1];
+              kb[2 * i] = k0 * cs.x - k1 * cs.y;
+              kb[2 * i + 1] = k0 * cs.y + k1 * cs.x;
+            }
+#pragma unroll
+            for (int gi = 0; gi < GROUP; ++gi) {
+              const float4* qq =
+                  reinterpret_cast<const float4*>(q_s + (kvh * GROUP + gi) * kHeadDim + c * 32);
+#pragma unroll
+              for (int v4 = 0; v4 < 8; ++v4) {
+                const float4 q4 = qq[v4];
+                sc[gi] = fmaf(q4.x, kb[4 * v4], sc[gi]);
+                sc[gi] = fmaf(q4.y, kb[4 * v4 + 1], sc[gi]);
+                sc[gi] = fmaf(q4.z, kb[4 * v4 + 2], sc[gi]);
+                sc[gi] = fmaf(q4.w, kb[4 * v4 + 3], sc[gi]);
+              }
+            }
+          }
+#pragma unroll
+          for (int gi = 0; gi < GROUP; ++gi)
+            sc_s[(kvh * GROUP + gi) * kTileM + row] = valid ? sc[gi] : -INFINITY;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[a]);
+          else mbar_arrive_remote(tempty_leader0 + 8 * a);
+        }
+      }
+      // ---- exchange: the peer owns query heads [peer*nbh, peer*nbh + nbh)
+      for (int hl = 0; hl < nbh; ++hl) {
+        const int h = static_cast<int>(peer) * nbh + hl;
+        st_cluster_f32(x_peer + 4u * (hl * kTileM + row), h < p.n_q ? sc_s[h * kTileM + row] : -INFINITY);
+      }
+      mbar_arrive_remote_release(xfull_peer);
+      mbar_wait_cluster(xfull, ti & 1);
+      // ---- softmax over the 256 tokens of the tile for this CTA's heads -> P
+      {
+        const int seg = et & 7;  // tokens seg*32 .. +31 of the pair tile
+        const int half = seg >> 2;
+        for (int hl = et >> 3; hl < nbh; hl += 16) {
+          const int h = static_cast<int>(rank) * nbh + hl;
+          const float* src = (half == static_cast<int>(rank)) ? (sc_s + h * kTileM) : (x_s + hl * kTileM);
+          float s[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 v = (h < p.n_q) ? reinterpret_cast<const float4*>(src + (seg & 3) * 32)[i]
+                                         : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            s[4 * i] = v.x; s[4 * i + 1] = v.y; s[4 * i + 2] = v.z; s[4 * i + 3] = v.w;
+          }
+          float m = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) m = fmaxf(m, s[i]);
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+          float l = 0.f;
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = (m == -INFINITY) ? 0.f : exp2f(s[2 * i] - m);
+            const float p1 = (m == -INFINITY) ? 0.f : exp2f(s[2 * i + 1] - m);
+            const __half2 hp = __floats2half2_rn(p0, p1);
+            // sum what the MMA will see (the fp16-rounded p)
+            const float2 pr = __half22float2(hp);
+            l += pr.x + pr.y;
+            pk[i] = as_u32(hp);
+          }
+          l += __shfl_xor_sync(0xffffffffu, l, 1);
+          l += __shfl_xor_sync(0xffffffffu, l, 2);
+          l += __shfl_xor_sync(0xffffffffu, l, 4);
+          // P stage j = seg/2 holds tokens 64j..64j+63 as one 128-byte row per head
+          const uint32_t pst = sP_a + (seg >> 1) * (nbh * 128);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            sts128(pst + sw128_offset(hl, (seg & 1) * 4 + c), pk[4 * c], pk[4 * c + 1],
+                   pk[4 * c + 2], pk[4 * c + 3]);
+          if (seg == 0 && h < p.n_q)
+            p.part_ml[((int64_t)b * p.n_tiles + t) * p.n_q + h] = make_float2(m, l);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(pready);
+          else mbar_arrive_remote(pready_leader);
+        }
+      }
+      ++ti;
+      // ---- V side: drain O^T[channels x heads] of this tile
+      int blk = 0;
+      for (int us = 0; us < nuse; ++us, ++tc) {
+        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+        mbar_wait(&tfull[a], aph);
+        tc_fence_after();
+        for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
+          const int ch = blk * 256 + static_cast<int>(rank) * 128 + row;  // storage channel
+          float* dst = p.part_o + ((int64_t)b * p.n_tiles + t) * p.n_q * (int64_t)p.kdim + ch;
+          for (int c16 = 0; c16 < p.nb / 16; ++c16) {
+            float v[16];
+            tmem_ld16(tmem + tlane + a * 256 + bi * p.nb + c16 * 16, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int h = c16 * 16 + jj;
+              if (h < p.n_q) dst[(int64_t)h * p.kdim] = v[jj];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[a]);
+          else mbar_arrive_remote(tempty_leader0 + 8 * a);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, 512);
+  }
+}
+
+// Merge the tile partials of one (sequence, query head) and project through
+// W_v: out = ((sum_i 2^(m_i-M) O_i) / (sum_i 2^(m_i-M) l_i)) @ W_v[:, kv(h)].
+// wv: fp16 [n_kv][kdim][128], rows in the storage channel order of O.
+__global__ void __launch_bounds__(256) k_absorb_vproj(const float* __restrict__ part_o,
+                                                      const float2* __restrict__ part_ml,
+                                                      const int32_t* __restrict__ seq_lens,
+                                                      int n_tiles, int n_q, int group, int kdim,
+                                                      const __half* __restrict__ wv,
+                                                      float* __restrict__ out) {
+  extern __shared__ float sm[];
+  float* x = sm;              // [kdim]
+  float* wts = sm + kdim;     // [n_tiles]
+  __shared__ float red[8];
+  __shared__ float acc4[4][128];
+  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int len = seq_lens[b];
+  const int nt = (len + kPairM - 1) / kPairM;
+  const float2* ml = part_ml + (int64_t)b * n_tiles * n_q + h;
+  float M = -INFINITY;
+  for (int i = tid; i < nt; i += 256) M = fmaxf(M, ml[(int64_t)i * n_q].x);
+  M = warp_max(M);
+  if ((tid & 31) == 0) red[tid >> 5] = M;
+  __syncthreads();
+  M = red[0];
+  for (int w = 1; w < 8; ++w) M = fmaxf(M, red[w]);
+  __syncthreads();
+  float L = 0.f;
+  for (int i = tid; i < nt; i += 256) {
+    const float2 v = ml[(int64_t)i * n_q];
+    const float wgt = (v.x == -INFINITY) ? 0.f : exp2f(v.x - M);
+    wts[i] = wgt;
+    L = fmaf(wgt, v.y, L);
+  }
+  L = warp_sum(L);
+  if ((tid & 31) == 0) red[tid >> 5] = L;
+  __syncthreads();
+  L = 0.f;
+  for (int w = 0; w < 8; ++w) L += red[w];
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  const float* po = part_o + (int64_t)b * n_tiles * n_q * kdim + (int64_t)h * kdim;
+  for (int c = tid; c < kdim; c += 256) {
+    float acc = 0.f;
+#pragma unroll 4
+    for (int i = 0; i < nt; ++i) acc = fmaf(wts[i], po[(int64_t)i * n_q * kdim + c], acc);
+    x[c] = acc * inv;
+  }
+  __syncthreads();
+  const int j2 = tid & 63, qtr = tid >> 6;
+  const __half2* w2 = reinterpret_cast<const __half2*>(wv + (int64_t)(h / group) * kdim * 128) + j2;
+  const int c0 = qtr * (kdim / 4), c1 = c0 + kdim / 4;
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+  for (int c = c0; c < c1; ++c) {
+    const float2 wf = __half22float2(w2[(int64_t)c * 64]);
+    a0 = fmaf(x[c], wf.x, a0);
+    a1 = fmaf(x[c], wf.y, a1);
+  }
+  acc4[qtr][2 * j2] = a0;
+  acc4[qtr][2 * j2 + 1] = a1;
+  __syncthreads();
+  if (tid < 128)
+    out[((int64_t)b * n_q + h) * kHeadDim + tid] = acc4[0][tid] + acc4[1][tid] + acc4[2][tid] + acc4[3][tid];
+}
+
+// Arranged weights. wk_out: fp16 [n_pass*256][kdim], row kvh*128 + j =
+// W_k[:, kvh*128 + j]^T with the channels in the K-side producer order (zero
+// rows pad an odd n_kv). wv_out: fp16 [n_kv][kdim][128], row c = W_v[perm(c),
+// kvh*128 .. +128] with perm the V-side producer order.
+__global__ void k_arrange_absorbed(const void* __restrict__ w_k, const void* __restrict__ w_v, int dt,
+                                   int64_t kdim, int n_kv, int n_pass, int bs_k, int bs_v,
+                                   __half* __restrict__ wk_out, __half* __restrict__ wv_out) {
+  const int64_t ld = (int64_t)n_kv * 128;
+  const int64_t nk = (int64_t)n_pass * 256 * kdim;
+  const int64_t nv = (int64_t)n_kv * kdim * 128;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nk + nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nk) {
+      const int64_t pch = i % kdim, rowi = i / kdim;
+      const int64_t k = (pch / bs_k) * bs_k + perm_channel(static_cast<int>(pch % bs_k), bs_k);
+      wk_out[i] = rowi < ld ? __float2half_rn(load_as_f32(w_k, dt, k * ld + rowi)) : __float2half_rn(0.f);
+    } else {
+      const int64_t e = i - nk;
+      const int64_t j = e % 128, pch = (e / 128) % kdim, kvh = e / (128 * kdim);
+      const int64_t k = (pch / bs_v) * bs_v + perm_channel(static_cast<int>(pch % bs_v), bs_v);
+      wv_out[e] = __float2half_rn(load_as_f32(w_v, dt, k * ld + kvh * 128 + j));
+    }
+  }
+}
+
+}  // namespace absorb
+
+// ------------------------------------------------------------ host side
+namespace {
+
+using namespace absorb;
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int make_map(CUtensorMap* m, CUtensorMapDataType dt, int esize, const void* base, uint64_t inner,
+             uint64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw,
+             const char* what, CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
+  auto enc = encode_fn();
+  XQ_REQUIRE(enc != nullptr, XQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  XQ_REQUIRE(reinterpret_cast<uintptr_t>(base) % 16 == 0, XQ_ESHAPE, "%s: base not 16-byte aligned", what);
+  XQ_REQUIRE((inner * esize) % 16 == 0, XQ_ESHAPE, "%s: row pitch %llu B not a multiple of 16", what,
+             (unsigned long long)(inner * esize));
+  const cuuint64_t gdim[2] = {inner, rows};
+  const cuuint64_t gstride[1] = {inner * esize};
+  const cuuint32_t box[2] = {box_inner, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  XQ_REQUIRE(r == CUDA_SUCCESS, XQ_ECUDA, "%s: cuTensorMapEncodeTiled failed (%d)", what, (int)r);
+  return XQ_OK;
+}
+
+// codes map (box = one 128-channel group of 128 rows) + params map
+int stream_maps(int mode, int bits, const void* src, const void* params, int64_t row_bytes,
+                int64_t kdim, int G, int64_t rows, uint32_t f16_box_rows, CUtensorMap* codes,
+                CUtensorMap* pmap) {
+  int st;
+  if (mode == XQ_A_F16_ROWS) {
+    *pmap = CUtensorMap{};
+    return make_map(codes, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, src, kdim, rows, kChunk, f16_box_rows,
+                    CU_TENSOR_MAP_SWIZZLE_128B, "fp16 A rows");
+  }
+  XQ_REQUIRE(row_bytes == row_bytes_for(kdim, bits), XQ_ESHAPE, "row_bytes mismatch");
+  if ((st = make_map(codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, src, row_bytes, rows, 16 * bits,
+                     kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "codes", CU_TENSOR_MAP_L2_PROMOTION_L2_128B)) != XQ_OK)
+    return st;
+  if (mode == XQ_A_CODES_TOKEN)
+    return make_map(pmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, params, param_stride(kdim, G) * 4, rows,
+                    16, kTileM, CU_TENSOR_MAP_SWIZZLE_NONE, "params", CU_TENSOR_MAP_L2_PROMOTION_NONE);
+  return make_map(pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, params, kdim, 2 * (rows / G), 128, 2,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, "channel params", CU_TENSOR_MAP_L2_PROMOTION_NONE);
+}
+
+struct Maps {
+  CUtensorMap w, ka, kp, va, vp;
+};
+
+int nb_for(int n_q) {
+  const int nb = (n_q + 15) / 16 * 16;
+  return nb < 16 ? 16 : nb;
+}
+
+int64_t n_tiles_for(int32_t max_len) {
+  const int64_t nt = (max_len + kPairM - 1) / kPairM;
+  return nt < 1 ? 1 : nt;
+}
+
+// Shared-memory plan: [AB ring][P][codes ring][q][scores][peer scores][barriers]
+template <int AK, int AV, int BITS>
+int plan_smem(Params& p, size_t& total) {
+  constexpr bool PROD = AK != XQ_A_F16_ROWS;
+  const uint32_t k_code = PROD ? 128u * 16u * BITS : 0u;
+  const uint32_t k_par = AK == XQ_A_CODES_TOKEN ? 128u * 16u : (AK == XQ_A_CODES_CHANNEL ? 512u : 0u);
+  const uint32_t v_par = PROD ? 128u * 16u : 0u;
+  p.k_code_bytes = k_code;
+  p.k_tx = k_code + k_par;
+  p.v_tx = k_code + v_par;
+  const uint32_t cst = PROD ? ((k_code + (k_par > v_par ? k_par : v_par) + 127) / 128 * 128) : 0u;
+  p.cstage_bytes = cst;
+  const uint32_t fixed = 512u * p.nbh                      // P
+                         + 2u * 512u * p.n_q                // q, scores
+                         + 512u * p.nbh                     // peer scores
+                         + (4 * kMaxStages + 6) * 8 + 16;   // barriers + tmem slot
+  const uint32_t budget = 227u * 1024u - 1024u;
+  int stages = 4, cstages = PROD ? 4 : 0;
+  auto need = [&]() { return stages * kABStage + cstages * cst + fixed; };
+  while (need() > budget && cstages > 2) --cstages;
+  while (need() > budget && stages > 2) --stages;
+  XQ_REQUIRE(need() <= budget, XQ_ESHAPE, "shared memory plan does not fit (%u heads)", p.n_q);
+  p.stages = stages;
+  p.cstages = cstages;
+  p.off_p = stages * kABStage;
+  p.off_codes = p.off_p + 512u * p.nbh;
+  p.off_q = p.off_codes + cstages * cst;
+  p.off_sc = p.off_q + 512u * p.n_q;
+  p.off_x = p.off_sc + 512u * p.n_q;
+  p.off_bar = (p.off_x + 512u * p.nbh + 7) / 8 * 8;
+  total = 1024 + need();
+  return XQ_OK;
+}
+
+template <int AK, int AV, int BITS, int GROUP>
+int launch(const Maps& m, Params p, cudaStream_t st) {
+  size_t smem = 0;
+  int status = plan_smem<AK, AV, BITS>(p, smem);
+  if (status != XQ_OK) return status;
+  auto kern = k_decode_absorbed<AK, AV, BITS, GROUP>;
+  static size_t configured = 0;
+  if (configured < smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+        cudaSuccess)
+      return check_launch("cudaFuncSetAttribute(decode_absorbed)");
+    configured = 227 * 1024;
+  }
+  const int pairs = p.n_units < num_sms() / 2 ? p.n_units : num_sms() / 2;
+  kern<<<2 * pairs, kThreads, smem, st>>>(m.w, m.ka, m.kp, m.va, m.vp, p);
+  return check_launch("k_decode_absorbed");
+}
+
+template <int AK, int AV, int GROUP>
+int dispatch_bits(int bits, const Maps& m, const Params& p, cudaStream_t st) {
+  switch (bits) {
+    case 2: return launch<AK, AV, 2, GROUP>(m, p, st);
+    case 3: return launch<AK, AV, 3, GROUP>(m, p, st);
+    case 4: return launch<AK, AV, 4, GROUP>(m, p, st);
+    case 8: return launch<AK, AV, 8, GROUP>(m, p, st);
+    default: return fail(XQ_ECONFIG, "unsupported bits %d", bits);
+  }
+}
+
+}  // namespace
+}  // namespace xq
+
+using namespace xq;
+using namespace xq::absorb;
+
+extern "C" {
+
+int64_t xq_absorbed_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q_heads,
+                                    int64_t kdim) {
+  return (int64_t)n_seqs * n_tiles_for(max_len) * n_q_heads * (kdim + 2) * (int64_t)sizeof(float);
+}
+
+int xq_arrange_weights_absorbed(const void* w_k, const void* w_v, int32_t w_dtype, int64_t kdim,
+                                int32_t n_kv_heads, int32_t a_mode_k, int32_t bits_k,
+                                int32_t a_mode_v, int32_t bits_v, void* wk_out, void* wv_out,
+                                void* stream) {
+  XQ_REQUIRE(kdim % 256 == 0 && kdim > 0, XQ_ESHAPE, "kdim must be a positive multiple of 256, got %lld",
+             (long long)kdim);
+  XQ_REQUIRE(dtype_size(w_dtype) > 0, XQ_ECONFIG, "unknown dtype");
+  XQ_REQUIRE(n_kv_heads >= 1, XQ_ESHAPE, "no KV heads");
+  if (a_mode_v == XQ_A_SAME) {
+    a_mode_v = a_mode_k;
+    bits_v = bits_k;
+  }
+  const int n_pass = (n_kv_heads + 1) / 2;
+  const int bs_k = perm_block(a_mode_k, bits_k), bs_v = perm_block(a_mode_v, bits_v);
+  const int64_t total = (int64_t)n_pass * 256 * kdim + (int64_t)n_kv_heads * kdim * 128;
+  const int64_t blocks = (total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16;
+  k_arrange_absorbed<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
+      w_k, w_v, w_dtype, kdim, n_kv_heads, n_pass, bs_k, bs_v, static_cast<__half*>(wk_out),
+      static_cast<__half*>(wv_out));
+  return check_launch("xq_arrange_weights_absorbed");
+}
+
+int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                              const float* ak_resid, const int32_t* ak_nflushed, int32_t ak_bits,
+                              int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
+                              const void* av_params, int32_t av_bits, int64_t av_row_bytes,
+                              int32_t group_size, int64_t L_max, int64_t kdim,
+                              const int32_t* seq_lens, int32_t n_seqs, int32_t max_len,
+                              const void* wk_arranged, const void* wv_arranged, int32_t n_kv_heads,
+                              int32_t group, const float* q_pre, const void* rope_cs,
+                              int64_t rope_n, float sm_scale, void* workspace,
+                              int64_t workspace_bytes, float* out, void* stream) {
+  XQ_REQUIRE(rope_n >= max_len, XQ_ESHAPE, "rope table shorter than max_len");
+  XQ_REQUIRE(kdim % 256 == 0 && kdim >= 256, XQ_ESHAPE,
+             "kdim must be a positive multiple of 256, got %lld", (long long)kdim);
+  XQ_REQUIRE(group_size == kG, XQ_ECONFIG,
+             "the fused kernel is specialised for group_size 128 (the reference default), got %d",
+             group_size);
+  XQ_REQUIRE(n_seqs >= 1 && n_kv_heads >= 1, XQ_ESHAPE, "empty batch");
+  XQ_REQUIRE(max_len <= L_max && max_len >= 1, XQ_ESHAPE, "max_len out of range");
+  const int n_q = n_kv_heads * group;
+  XQ_REQUIRE(n_q <= kMaxHeads, XQ_ECONFIG, "at most %d query heads per launch, got %d", kMaxHeads, n_q);
+  XQ_REQUIRE(workspace_bytes >= xq_absorbed_workspace_bytes(n_seqs, max_len, n_q, kdim), XQ_ESHAPE,
+             "workspace too small");
+  const bool mha = av_mode == XQ_A_SAME;
+  if (mha) {
+    av_mode = ak_mode;
+    av_src = ak_src;
+    av_params = ak_params;
+    av_bits = ak_bits;
+    av_row_bytes = ak_row_bytes;
+    XQ_REQUIRE(ak_mode == XQ_A_CODES_TOKEN || ak_mode == XQ_A_F16_ROWS, XQ_ECONFIG,
+               "shared A operand must be CODES_TOKEN or F16_ROWS");
+  } else {
+    XQ_REQUIRE(ak_mode == XQ_A_CODES_CHANNEL && av_mode == XQ_A_CODES_TOKEN, XQ_ECONFIG,
+               "split K/V A operands support (CODES_CHANNEL, CODES_TOKEN) only");
+    XQ_REQUIRE(ak_bits == av_bits, XQ_ECONFIG, "K and V latent bits must match");
+    XQ_REQUIRE(L_max % group_size == 0, XQ_ECONFIG, "per-channel K latent needs L_max % 128 == 0");
+  }
+  XQ_REQUIRE(ak_mode == XQ_A_F16_ROWS || valid_bits(ak_bits), XQ_ECONFIG, "bad bits %d", ak_bits);
+  const int n_pass = (n_kv_heads + 1) / 2;
+  const int64_t arena_rows = (int64_t)n_seqs * L_max;
+  Maps maps;
+  int st_;
+  if ((st_ = make_map(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wk_arranged, kdim,
+                      (uint64_t)n_pass * 256, kChunk, 128, CU_TENSOR_MAP_SWIZZLE_128B, "W_k")) != XQ_OK)
+    return st_;
+  if ((st_ = stream_maps(ak_mode, ak_bits, ak_src, ak_params, ak_row_bytes, kdim, group_size,
+                         arena_rows, 128, &maps.ka, &maps.kp)) != XQ_OK)
+    return st_;
+  if ((st_ = stream_maps(av_mode, av_bits, av_src, av_params, av_row_bytes, kdim, group_size,
+                         arena_rows, 64, &maps.va, &maps.vp)) != XQ_OK)
+    return st_;
+
+  Params p;
+  p.k_resid = ak_resid;
+  p.k_nflushed = ak_nflushed;
+  p.kdim = static_cast<int32_t>(kdim);
+  p.L_max = L_max;
+  p.seq_lens = seq_lens;
+  p.n_seqs = n_seqs;
+  p.n_tiles = static_cast<int32_t>(n_tiles_for(max_len));
+  p.n_units = n_seqs * p.n_tiles;
+  p.n_kv = n_kv_heads;
+  p.n_q = n_q;
+  p.nb = nb_for(n_q);
+  p.nbh = p.nb / 2;
+  p.n_pass = n_pass;
+  p.q_pre = q_pre;
+  p.rope = static_cast<const float2*>(rope_cs);
+  p.rope_n = rope_n;
+  p.q_scale = sm_scale * 1.4426950408889634f;
+  float* ws = static_cast<float*>(workspace);
+  p.part_o = ws;
+  p.part_ml = reinterpret_cast<float2*>(ws + (int64_t)n_seqs * p.n_tiles * n_q * kdim);
+  {
+    const char* e = getenv("XQ_W_HINT");
+    const int h = e ? atoi(e) : 1;
+    p.w_hint = h == 0 ? kEvictNormal : (h == 2 ? kEvictFirst : kEvictLast);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int status;
+  if (mha) {
+    XQ_REQUIRE(group == 1, XQ_ECONFIG, "MHA (shared A) needs group 1, got %d", group);
+    if (ak_mode == XQ_A_F16_ROWS)
+      status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 1>(maps, p, st);
+    else
+      status = dispatch_bits<XQ_A_CODES_TOKEN, XQ_A_CODES_TOKEN, 1>(ak_bits, maps, p, st);
+  } else {
+    switch (group) {
+      case 1: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 1>(ak_bits, maps, p, st); break;
+      case 2: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 2>(ak_bits, maps, p, st); break;
+      case 4: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 4>(ak_bits, maps, p, st); break;
+      default: return fail(XQ_ECONFIG, "unsupported GQA group %d (1, 2, 4)", group);
+    }
+  }
+  if (status != XQ_OK) return status;
+  const size_t vsmem = ((size_t)kdim + p.n_tiles) * sizeof(float);
+  if (vsmem > 48 * 1024) {
+    static size_t vconf = 0;
+    if (vconf < vsmem) {
+      if (cudaFuncSetAttribute(k_absorb_vproj, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)vsmem) != cudaSuccess)
+        return check_launch("cudaFuncSetAttribute(vproj)");
+      vconf = vsmem;
+    }
+  }
+  k_absorb_vproj<<<dim3(n_q, n_seqs), 256, vsmem, st>>>(p.part_o, p.part_ml, seq_lens, p.n_tiles, n_q,
+                                                         group, p.kdim,
+                                                         static_cast<const __half*>(wv_arranged), out);
+  return check_launch("k_absorb_vproj");
+}
+
+}  // extern "C"

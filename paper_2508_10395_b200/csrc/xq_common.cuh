@@ -281,6 +281,45 @@ XQ_DEVINL void tmem_ld32(uint32_t taddr, float (&v)[32]) {
       : "memory");
 }
 
+// 32 lanes x 16 consecutive 32-bit columns.
+XQ_DEVINL void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+// Store to the same-offset shared variable of another CTA of the cluster
+// (address from mapa_shared).
+XQ_DEVINL void st_cluster_f32(uint32_t cluster_addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
+}
+// Arrive with cluster-scope release: orders this thread's prior (remote) shared
+// stores before the arrival, for a consumer that waits with acquire.cluster.
+XQ_DEVINL void mbar_arrive_remote_release(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+// UMMA shared-memory descriptor for an MN-major operand in the canonical
+// SWIZZLE_128B layout: each K row holds 64 contiguous fp16 along M/N (128 B),
+// 8 K rows form a 1024-byte atom; `lbo` = byte stride between 64-element
+// M/N blocks, `sbo` = byte stride between 8-row K groups.
+XQ_DEVINL uint64_t sdesc_mn_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
 // UMMA shared-memory descriptor for a K-major operand stored in the canonical
 // SWIZZLE_128B layout: rows of 128 bytes (64 fp16 along K), 8-row atoms of
 // 1024 bytes, atoms contiguous along M/N. Start address must be 1024-aligned
@@ -304,12 +343,26 @@ __host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
          | (static_cast<uint32_t>(M >> 4) << 24); // M / 16
 }
 
+// The same with an MN-major ("transposed") A operand.
+__host__ __device__ constexpr uint32_t idesc_f16_f32_amn(int M, int N) {
+  return idesc_f16_f32(M, N) | (1u << 15);
+}
+
 // Byte offset of element (row, k) of a [rows x 64] fp16 tile in the SW128 K-major layout.
 XQ_DEVINL uint32_t sw128_offset(uint32_t row, uint32_t chunk16 /* 16-byte chunk 0..7 */) {
   return row * 128u + ((chunk16 ^ (row & 7u)) << 4);
 }
 
 // ---------------------------------------------------------------- misc
+XQ_DEVINL float load_as_f32(const void* base, int dt, int64_t i) {
+  switch (dt) {
+    case XQ_F32: return static_cast<const float*>(base)[i];
+    case XQ_BF16: return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]);
+    case XQ_F16: return __half2float(static_cast<const __half*>(base)[i]);
+    default: return static_cast<float>(static_cast<const double*>(base)[i]);
+  }
+}
+
 XQ_DEVINL float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -285,15 +285,6 @@ __global__ void k_rope_table(float2* __restrict__ cs, int64_t n_pos, int hd, dou
   }
 }
 
-XQ_DEVINL float load_as_f32(const void* base, int dt, int64_t i) {
-  switch (dt) {
-    case XQ_F32: return static_cast<const float*>(base)[i];
-    case XQ_BF16: return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[i]);
-    case XQ_F16: return __half2float(static_cast<const __half*>(base)[i]);
-    default: return static_cast<float>(static_cast<const double*>(base)[i]);
-  }
-}
-
 __global__ void k_arrange_weights(const void* __restrict__ w_k, const void* __restrict__ w_v,
                                   int dt, int64_t kdim, int n_kv, int bs_k, int bs_v,
                                   __half* __restrict__ out) {
