@@ -414,8 +414,14 @@ def run_xquant(args, cfg):
         return
     # ---------------- roofline of the dominant kernel ----------------
     peaks, peak_src = _peaks()
-    flops_launch = B * (S.remat_flops(cfg["variant"], l_avg, d, shape.kv_group)
-                        + S.attention_flops(l_avg, shape.n_heads)) / (world if heads else 1)
+    absorbed = os.environ.get("XQ_ABSORB", "1") != "0"
+    flops_unabsorbed = B * (S.remat_flops(cfg["variant"], l_avg, d, shape.kv_group)
+                            + S.attention_flops(l_avg, shape.n_heads)) / (world if heads else 1)
+    if absorbed:
+        flops_launch = B * S.absorbed_flops(cfg["variant"], l_avg, d, shape.kv_group,
+                                            shape.n_heads) / (world if heads else 1)
+    else:
+        flops_launch = flops_unabsorbed
     per_launch = kern_s / (args.steps * n_layers)
     achieved = flops_launch / per_launch / 1e12
     peak = peaks["bf16_tflops_sustained"]
@@ -457,8 +463,13 @@ def run_xquant(args, cfg):
         "speedup_vs_fp16_kv": (value / fp16["value"]) if fp16 and fp16.get("value") else None,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_decode_attend (+k_combine)",
+                     "kernel": ("k_decode_absorbed (+k_absorb_vproj)" if absorbed
+                                else "k_decode_attend (+k_combine)"),
                      "flops_per_launch": flops_launch, "launch_us": per_launch * 1e6,
+                     "flops_note": ("algorithmic FLOPs of the V-absorbed path (sysmodel.absorbed_flops); "
+                                    "the unabsorbed remat+attention count is flops_unabsorbed"
+                                    if absorbed else "sysmodel.remat_flops + attention_flops"),
+                     "flops_unabsorbed": flops_unabsorbed,
                      "peak_source": f"{peak_src} bf16_tflops_sustained (fp16 MMA, same rate)"},
         "remat_roofline_frac_step": t_roof / (ms_per_step / 1e3),
         "compression": {"factor": comp, "formula": "1/sysmodel.normalized_kv_size",

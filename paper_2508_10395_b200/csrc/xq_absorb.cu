@@ -52,7 +52,8 @@ constexpr int kThreads = 512;
 constexpr int kProdWarp0 = 4;
 constexpr int kEpiWarp0 = 12;
 constexpr int kG = 128;
-constexpr int kMaxStages = 6;
+constexpr int kStages = 4;      // A/B ring depth (power of two: index math is shifts)
+constexpr int kMaxStages = 4;
 constexpr int kMaxHeads = 64;
 constexpr uint32_t kABytes = kTileM * 128;  // [128 x 64] fp16 = 16 KB
 constexpr uint32_t kBBytes = 128 * 128;     // this CTA's 128 W rows x 64 channels
@@ -67,7 +68,7 @@ struct Params {
   const int32_t* seq_lens;
   int32_t n_seqs, n_tiles, n_units;
   int32_t n_kv, n_q, nb, nbh, n_pass;
-  int32_t stages, cstages;
+  int32_t stages, cstages, cstage_shift;  // cstages = 1 << cstage_shift
   uint32_t cstage_bytes;
   uint32_t k_code_bytes, k_tx, v_tx;  // codes ring: codes bytes / TMA bytes per stage
   const float* q_pre;
@@ -122,7 +123,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  const int STAGES = p.stages, CSTAGES = p.cstages;
+  constexpr int STAGES = kStages;
+  const int CSTAGES = p.cstages;
+  const uint32_t cshift = p.cstage_shift, cmask = (1u << cshift) - 1u;
   const int ngrp = p.kdim / kG;            // 128-channel groups
   const int nkc = p.kdim / kChunk;         // pass-1 stages per pass
   const int nblk = p.kdim / 256;           // V-side channel blocks (128 per CTA)
@@ -293,13 +296,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int b, t, len;
         if (!get_unit(p, u, b, t, len)) continue;
         const int32_t row_tile = static_cast<int32_t>((int64_t)b * p.L_max + t * kPairM);
+        int ps = 0, g = 0;  // K side: (pass, group); then V side: g = 2*bb + th
         for (int q = 0; q < ncs; ++q, ++ci) {
-          const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
+          const uint32_t cs = ci & cmask, cph = (ci >> cshift) & 1u;
           mbar_wait(&cempty[cs], cph ^ 1);
           if (elect_one()) {
             uint8_t* st = sC + cs * p.cstage_bytes;
-            if (q < p.n_pass * ngrp) {  // K side: group g of this CTA's 128 tokens
-              const int g = q % ngrp;
+            if (ps < p.n_pass) {  // K side: group g of this CTA's 128 tokens
               const int32_t arow = row_tile + rank * kTileM;
               mbar_arrive_expect_tx(&cfull[cs], p.k_tx);
               tma_load_2d(st, &tmap_ka, &cfull[cs], g * 16 * BITS, arow, kEvictNormal);
@@ -309,16 +312,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tma_load_2d(st + p.k_code_bytes, &tmap_kp, &cfull[cs], g * 128, 2 * (arow / kG),
                             kEvictNormal);
             } else {  // V side: group 2*bb + rank of token half th of the pair tile
-              const int qb = q - p.n_pass * ngrp;
-              const int g = 2 * (qb >> 1) + static_cast<int>(rank);
-              const int32_t arow = row_tile + (qb & 1) * kTileM;
+              const int gv = (g & ~1) + static_cast<int>(rank);
+              const int32_t arow = row_tile + (g & 1) * kTileM;
               mbar_arrive_expect_tx(&cfull[cs], p.v_tx);
-              tma_load_2d(st, &tmap_va, &cfull[cs], g * 16 * BITS, arow, kEvictNormal);
-              tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (g & ~3), arow,
+              tma_load_2d(st, &tmap_va, &cfull[cs], gv * 16 * BITS, arow, kEvictNormal);
+              tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (gv & ~3), arow,
                           kEvictNormal);
             }
           }
           __syncwarp();
+          if (++g == ngrp) {
+            g = 0;
+            ++ps;
+          }
         }
       }
     }
@@ -338,12 +344,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + b) : 0;
         const int tok_k = t * kPairM + rank * kTileM + r;
         const uint32_t ci0 = tcount * ncs;
-        for (int q = ((ci0 & 1) == static_cast<uint32_t>(gp)) ? 0 : 1; q < ncs; q += 2) {
+        const int q0 = ((ci0 & 1) == static_cast<uint32_t>(gp)) ? 0 : 1;
+        int g = q0, ps = 0;  // K side (pass ps, group g); V side (ps == n_pass): g = 2*bb + th
+        for (int q = q0; q < ncs; q += 2) {
           const uint32_t ci = ci0 + q;
-          const uint32_t cs = ci % CSTAGES, cph = (ci / CSTAGES) & 1;
+          const uint32_t cs = ci & cmask, cph = (ci >> cshift) & 1u;
           const uint32_t st = sC_a + cs * p.cstage_bytes;
           mbar_wait(&cfull[cs], cph);
-          const bool kside = q < p.n_pass * ngrp;
+          const bool kside = ps < p.n_pass;
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
             const uint32_t itn = 2 * ci + h;
@@ -351,17 +359,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&empty[s], ph ^ 1);
             const uint32_t tile = sAB_a + s * kABStage;
             if (kside) {
-              const int kc = 2 * (q % ngrp) + h;
               produce_chunk<AK, BITS>(tile, st, st + p.k_code_bytes, sw_k, r, tok_k < len, tok_k, b,
-                                      nfl, kc, nullptr, p.k_resid, p.kdim);
+                                      nfl, 2 * g + h, nullptr, p.k_resid, p.kdim);
             } else {
-              const int qb = q - p.n_pass * ngrp;
-              const int g = 2 * (qb >> 1) + static_cast<int>(rank);
+              const int gv = (g & ~1) + static_cast<int>(rank);
               const int crow = h * 64 + (r & 63);
-              const int tok = t * kPairM + (qb & 1) * kTileM + crow;
+              const int tok = t * kPairM + (g & 1) * kTileM + crow;
               if constexpr (AV == XQ_A_CODES_TOKEN)
                 produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
-                                        tok < len, tok, b, 1 << 30, 2 * g + hh, nullptr, nullptr,
+                                        tok < len, tok, b, 1 << 30, 2 * gv + hh, nullptr, nullptr,
                                         p.kdim);
             }
             fence_proxy_async_smem();
@@ -370,6 +376,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
           }
           mbar_arrive_if(&cempty[cs], lane == 0);
+          g += 2;
+          if (g >= ngrp) {
+            g -= ngrp;
+            ++ps;
+          }
         }
         ++tcount;
       }
@@ -738,13 +749,14 @@ int plan_smem(Params& p, size_t& total) {
                          + 512u * p.nbh                     // peer scores
                          + (4 * kMaxStages + 6) * 8 + 16;   // barriers + tmem slot
   const uint32_t budget = 227u * 1024u - 1024u;
-  int stages = 4, cstages = PROD ? 4 : 0;
+  const int stages = kStages;
+  int cstages = PROD ? 4 : 1;
   auto need = [&]() { return stages * kABStage + cstages * cst + fixed; };
-  while (need() > budget && cstages > 2) --cstages;
-  while (need() > budget && stages > 2) --stages;
-  XQ_REQUIRE(need() <= budget, XQ_ESHAPE, "shared memory plan does not fit (%u heads)", p.n_q);
+  if (need() > budget && PROD) cstages = 2;
+  XQ_REQUIRE(need() <= budget, XQ_ESHAPE, "shared memory plan does not fit (%d heads)", p.n_q);
   p.stages = stages;
   p.cstages = cstages;
+  p.cstage_shift = cstages == 4 ? 2 : (cstages == 2 ? 1 : 0);
   p.off_p = stages * kABStage;
   p.off_codes = p.off_p + 512u * p.nbh;
   p.off_q = p.off_codes + cstages * cst;

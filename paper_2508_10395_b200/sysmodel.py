@@ -31,6 +31,25 @@ def remat_flops(variant: str, seq_len: int, hidden_dim: int, kv_group: int = 1) 
     raise ValueError(variant)
 
 
+def absorbed_flops(variant: str, seq_len: int, hidden_dim: int, kv_group: int, n_heads: int,
+                   head_dim: int = 128) -> float:
+    """Tensor-core FLOPs per layer per sequence of the V-absorbed fused kernel
+    (csrc/xq_absorb.cu): K remat 2*l*kdim*d_kv, the V-side GEMM
+    sum_t p_t x_t 2*l*kdim*H, q.k 2*l*H*hd; the final per-head projection
+    through W_v (2*H*kdim*hd, independent of l) is included. kdim = d for the
+    X / CL caches, r = d_kv for the GQA latents."""
+    d = hidden_dim
+    kvw = d / kv_group
+    if variant in ("xq-mha", "xq-cl-mha"):
+        kdim = d
+    elif variant == "xq-gqa":
+        kdim = kvw
+    else:
+        raise ValueError(variant)
+    return (2.0 * seq_len * kdim * kvw + 2.0 * seq_len * kdim * n_heads
+            + 2.0 * seq_len * n_heads * head_dim + 2.0 * n_heads * kdim * head_dim)
+
+
 def attention_flops(seq_len: int, n_heads: int, head_dim: int = 128) -> float:
     """q.K^T and p.V for one decode token: 4 * l * H * hd."""
     return 4.0 * seq_len * n_heads * head_dim
