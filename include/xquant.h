@@ -183,7 +183,7 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
  * per-head projection through W_v at the end. kdim % 256 == 0. */
 
 /* Arranged weights of the absorbed kernel. wk_out: fp16
- * [ceil(n_kv/2)*256][kdim], row h*128+j = W_k[:, h*128+j]^T in the K-side
+ * [ceil(n_kv/4)*512][kdim], row h*128+j = W_k[:, h*128+j]^T in the K-side
  * producer channel order (zero rows pad an odd n_kv). wv_out: fp16
  * [n_kv][kdim][128], row c = W_v[perm_v(c), h*128 .. +128] with perm_v the
  * V-side producer order. a_mode_v may be XQ_A_SAME. */
@@ -209,6 +209,12 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
                               int32_t group, const float* q_pre, const void* rope_cs,
                               int64_t rope_n, float sm_scale, void* workspace,
                               int64_t workspace_bytes, float* out, void* stream);
+
+/* Debug: cycles each warp role of the absorbed kernel spent blocked per
+ * barrier (16 uint64 counters, see csrc/xq_absorb.cu); all zero unless the
+ * library was built with -DXQ_ROLE_PROFILE (tools/build_role_profile.sh).
+ * reset != 0 clears them after the read. */
+int xq_debug_role_profile(uint64_t* out, int32_t reset);
 
 /* Debug hook: when buf != NULL, xq_decode_attend also dumps the raw fp32
  * accumulator of every tile t < n_tiles to buf[b][kv_head][t][128][256]

@@ -13,7 +13,9 @@ import os
 from .errors import raise_for_status
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libxquant.so")
+# XQ_LIB selects an alternative build (e.g. the role-profiling library of
+# tools/build_role_profile.sh); the default is the in-tree libxquant.so
+LIB_PATH = os.environ.get("XQ_LIB") or os.path.join(_PKG, "libxquant.so")
 
 F32, BF16, F16, F64 = 0, 1, 2, 3
 A_CODES_TOKEN, A_CODES_CHANNEL, A_F16_ROWS, A_SAME = 0, 1, 2, 3
@@ -47,6 +49,7 @@ _SIGS = {
     "xq_cl_accumulate": [_I32, _P, _I64, _P, _I32, _I32, _I64, _P, _I32, _I32, _I64, _P, _P,
                          _P],
     "xq_debug_set_acc_dump": [_P, _I32],
+    "xq_debug_role_profile": [_P, _I32],
     "xq_kv_append": [_P, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P],
     "xq_kv_decode_attend": [_P, _P, _I64, _P, _I32, _I32, _I32, _I32, _P, _P, _F, _I32, _P,
                             _I64, _P, _P],

@@ -121,8 +121,8 @@ class LayerWeights:
             if width % HEAD_DIM:
                 raise ShapeError(f"kv width {width} not a multiple of {HEAD_DIM}")
             n_kv = width // HEAD_DIM
-            n_pass = (n_kv + 1) // 2
-            wk_out = torch.empty((n_pass * 256, kdim), dtype=torch.float16, device=wk.device)
+            wk_out = torch.empty(((n_kv + 3) // 4 * 512, kdim), dtype=torch.float16,
+                                 device=wk.device)
             wv_out = torch.empty((n_kv, kdim, HEAD_DIM), dtype=torch.float16, device=wk.device)
             wk_c, wv_c = wk.contiguous(), wv.contiguous()
             N.call("xq_arrange_weights_absorbed", N.ptr(wk_c), N.ptr(wv_c), _dtype_code(wk_c), kdim,

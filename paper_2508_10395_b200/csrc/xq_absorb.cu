@@ -45,6 +45,24 @@
 namespace xq {
 namespace absorb {
 
+// Role profile (built only with -DXQ_ROLE_PROFILE, tools/build_role_profile.sh):
+// cycles each role spends blocked on each barrier, summed over the grid.
+//  0 W-TMA empty   1 MMA tempty   2 MMA full(K)   3 MMA pready   4 MMA full(V)
+//  5 codes-TMA cempty   6 producer cfull   7 producer empty   8 epilogue tfull(K)
+//  9 epilogue xfull   10 epilogue tfull(V)   11 CTA cycles (thread 0)
+constexpr int kProfCounters = 16;
+__device__ unsigned long long g_role_prof[kProfCounters];
+#ifdef XQ_ROLE_PROFILE
+#define XQ_PROF(c, stmt)                                  \
+  do {                                                    \
+    const long long t0_ = clock64();                      \
+    stmt;                                                 \
+    prof_acc[c] += static_cast<unsigned long long>(clock64() - t0_); \
+  } while (0)
+#else
+#define XQ_PROF(c, stmt) stmt
+#endif
+
 constexpr int kTileM = 128;   // token rows per CTA (TMEM lanes)
 constexpr int kPairM = 256;   // token rows per CTA pair
 constexpr int kChunk = 64;    // channels per pass-1 stage
@@ -52,12 +70,23 @@ constexpr int kThreads = 512;
 constexpr int kProdWarp0 = 4;
 constexpr int kEpiWarp0 = 12;
 constexpr int kG = 128;
-constexpr int kStages = 4;      // A/B ring depth (power of two: index math is shifts)
 constexpr int kMaxStages = 4;
 constexpr int kMaxHeads = 64;
 constexpr uint32_t kABytes = kTileM * 128;  // [128 x 64] fp16 = 16 KB
-constexpr uint32_t kBBytes = 128 * 128;     // this CTA's 128 W rows x 64 channels
-constexpr uint32_t kABStage = kABytes + kBBytes;
+constexpr uint32_t kBSub = 128 * 128;       // 128 W rows x 64 channels (one KV head)
+// KV heads per K pass: 4 for MHA (two N=256 MMAs share each A stage: half the
+// dequant work per FLOP, one 512-column accumulator), 2 for GQA (one N=256
+// MMA, double-buffered accumulators: the GQA epilogue has 4x the score work
+// per MMA and must overlap the next pass).
+template <int GROUP>
+struct Cfg {
+  static constexpr int KH = GROUP == 1 ? 4 : 2;
+  static constexpr int NBUF = KH == 2 ? 2 : 1;         // accumulator buffers
+  static constexpr uint32_t kBBytes = (KH / 2) * kBSub;  // this CTA's W rows per stage
+  static constexpr uint32_t kABStage = kABytes + kBBytes;
+  static constexpr int kStages = KH == 2 ? 4 : 3;
+  static constexpr int kUseCols = 512 / NBUF;            // columns of one accumulator
+};
 constexpr uint32_t kMNHalf = 64 * 128;      // V-side A stage: [64 tok x 64 ch] per channel half
 
 struct Params {
@@ -123,14 +152,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  constexpr int STAGES = kStages;
+#ifdef XQ_ROLE_PROFILE
+  unsigned long long prof_acc[kProfCounters] = {};
+  const long long prof_t0 = clock64();
+#endif
+  using CF = Cfg<GROUP>;
+  constexpr int STAGES = CF::kStages;
+  constexpr int KH = CF::KH;
+  constexpr uint32_t kABStage = CF::kABStage;
+  constexpr uint32_t kBBytes = CF::kBBytes;
   const int CSTAGES = p.cstages;
   const uint32_t cshift = p.cstage_shift, cmask = (1u << cshift) - 1u;
   const int ngrp = p.kdim / kG;            // 128-channel groups
   const int nkc = p.kdim / kChunk;         // pass-1 stages per pass
   const int nblk = p.kdim / 256;           // V-side channel blocks (128 per CTA)
   const int ncs = (p.n_pass + 1) * ngrp;   // codes stages per tile (pass-1 + V side)
-  const int bpu = 256 / p.nb;              // V-side blocks per 256-column accumulator
+  const int bpu = CF::kUseCols / p.nb;     // V-side blocks per accumulator
   const int nuse = (nblk + bpu - 1) / bpu;
 
   if (threadIdx.x == 0) {
@@ -185,14 +222,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int ps = 0; ps < p.n_pass; ++ps) {
         for (int kc = 0; kc < nkc; ++kc, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+          XQ_PROF(0, mbar_wait(&empty[s], ph ^ 1));
           if (elect_one()) {
             uint8_t* st = sAB + s * kABStage;
             constexpr uint32_t kTx = 2 * (kBBytes + (PROD ? 0u : kABytes));
             if (leader) mbar_arrive_expect_tx(&full[s], kTx);
             else mbar_arrive_remote(full_leader0 + 8 * s);
-            tma_load_2d_pair(st + kABytes, &tmap_w, &full[s], kc * kChunk, ps * 256 + rank * 128,
-                             p.w_hint);
+#pragma unroll
+            for (int sub = 0; sub < KH / 2; ++sub)  // KV head KH*ps + 2*sub + rank
+              tma_load_2d_pair(st + kABytes + sub * kBSub, &tmap_w, &full[s], kc * kChunk,
+                               (KH * ps + 2 * sub + static_cast<int>(rank)) * 128, p.w_hint);
             if constexpr (!PROD)
               tma_load_2d_pair(st, &tmap_ka, &full[s], kc * kChunk, row_tile + rank * kTileM,
                                kEvictNormal);
@@ -203,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int bb = 0; bb < nblk; ++bb) {
         for (int j = 0; j < 4; ++j, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+          XQ_PROF(0, mbar_wait(&empty[s], ph ^ 1));
           if (elect_one()) {
             uint8_t* st = sAB + s * kABStage;
             if constexpr (PROD) {
@@ -236,20 +275,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int b, t, len;
         if (!get_unit(p, u, b, t, len)) continue;
         for (int ps = 0; ps < p.n_pass; ++ps, ++tc) {
-          const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-          mbar_wait_cluster(&tempty[a], aph ^ 1);
+          const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
+          const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
+          XQ_PROF(1, mbar_wait_cluster(&tempty[a], aph ^ 1));
           tc_fence_after();
           const uint32_t d = tmem + a * 256;
           for (int kc = 0; kc < nkc; ++kc, ++it) {
             const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-            mbar_wait_cluster(&full[s], ph);
+            XQ_PROF(2, mbar_wait_cluster(&full[s], ph));
             tc_fence_after();
             const uint64_t ad = desc0 + ((s * kABStage) >> 4);
             const uint64_t bd = ad + (kABytes >> 4);
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < kChunk / 16; ++k)
-                mma2_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdescK, (kc | k) != 0);
+#pragma unroll
+                for (int sub = 0; sub < KH / 2; ++sub)
+                  mma2_f16_ss(d + sub * 256, ad + 2 * k, bd + (sub * kBSub >> 4) + 2 * k, kIdescK,
+                              (kc | k) != 0);
               mma2_commit_both(&empty[s]);
             }
             __syncwarp();
@@ -258,18 +301,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
         // V side: needs this tile's P from both CTAs
-        mbar_wait_cluster(pready, ti & 1);
+        XQ_PROF(3, mbar_wait_cluster(pready, ti & 1));
         tc_fence_after();
         int blk = 0;
         for (int us = 0; us < nuse; ++us, ++tc) {
-          const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-          mbar_wait_cluster(&tempty[a], aph ^ 1);
+          const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
+          const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
+          XQ_PROF(1, mbar_wait_cluster(&tempty[a], aph ^ 1));
           tc_fence_after();
           for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
             const uint32_t d = tmem + a * 256 + bi * p.nb;
             for (int j = 0; j < 4; ++j, ++it) {
               const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-              mbar_wait_cluster(&full[s], ph);
+              XQ_PROF(4, mbar_wait_cluster(&full[s], ph));
               tc_fence_after();
               const uint64_t ad = descv0 + ((s * kABStage) >> 4);
               const uint64_t bd = descp0 + ((j * pstage) >> 4);
@@ -299,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int ps = 0, g = 0;  // K side: (pass, group); then V side: g = 2*bb + th
         for (int q = 0; q < ncs; ++q, ++ci) {
           const uint32_t cs = ci & cmask, cph = (ci >> cshift) & 1u;
-          mbar_wait(&cempty[cs], cph ^ 1);
+          XQ_PROF(5, mbar_wait(&cempty[cs], cph ^ 1));
           if (elect_one()) {
             uint8_t* st = sC + cs * p.cstage_bytes;
             if (ps < p.n_pass) {  // K side: group g of this CTA's 128 tokens
@@ -350,13 +394,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t ci = ci0 + q;
           const uint32_t cs = ci & cmask, cph = (ci >> cshift) & 1u;
           const uint32_t st = sC_a + cs * p.cstage_bytes;
-          mbar_wait(&cfull[cs], cph);
+          XQ_PROF(6, mbar_wait(&cfull[cs], cph));
           const bool kside = ps < p.n_pass;
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
             const uint32_t itn = 2 * ci + h;
             const uint32_t s = itn % STAGES, ph = (itn / STAGES) & 1;
-            mbar_wait(&empty[s], ph ^ 1);
+            XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
             const uint32_t tile = sAB_a + s * kABStage;
             if (kside) {
               produce_chunk<AK, BITS>(tile, st, st + p.k_code_bytes, sw_k, r, tok_k < len, tok_k, b,
@@ -415,50 +459,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int tok = t * kPairM + rank * kTileM + row;
       const bool valid = tok < len;
       const float2* rp = p.rope + (valid ? tok : 0);
-      // ---- K side: scores of every query head for this CTA's 128 tokens
+      // ---- K side: scores of every query head for this CTA's 128 tokens.
+      // The row's cos/sin (frequency-major table, L2-resident) are shared by
+      // the KH heads of a pass: loaded once per 16-frequency chunk, one chunk
+      // ahead, the first before the wait so the L2 latency hides under the MMA.
+      auto load_cs = [&](int c, float2(&dst)[16]) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dst[i] = __ldg(rp + (int64_t)(c * 16 + i) * p.rope_n);
+      };
       for (int ps = 0; ps < p.n_pass; ++ps, ++tc) {
-        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-        mbar_wait(&tfull[a], aph);
+        const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
+        const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
+        float2 csv[16];
+        load_cs(0, csv);
+        XQ_PROF(8, mbar_wait(&tfull[a], aph));
         tc_fence_after();
-#pragma unroll 1
-        for (int kh = 0; kh < 2; ++kh) {
-          const int kvh = 2 * ps + kh;
-          if (kvh >= p.n_kv) break;
-          float sc[GROUP];
+        float sc[KH][GROUP];
 #pragma unroll
-          for (int gi = 0; gi < GROUP; ++gi) sc[gi] = 0.f;
+        for (int kh = 0; kh < KH; ++kh)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float kb[32];
-            tmem_ld32(tmem + tlane + a * 256 + kh * 128 + c * 32, kb);
-            float2 csv[16];
+          for (int gi = 0; gi < GROUP; ++gi) sc[kh][gi] = 0.f;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) csv[i] = __ldg(rp + (int64_t)(c * 16 + i) * p.rope_n);
-            tmem_wait_ld();
+        for (int c = 0; c < 4; ++c) {
+          float2 nxt[16];
+          if (c < 3) load_cs(c + 1, nxt);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {  // RoPE (linalg.py:92-93)
-              const float2 cs = csv[i];
-              const float k0 = kb[2 * i], k1 = kb[2 * i + 1];
-              kb[2 * i] = k0 * cs.x - k1 * cs.y;
-              kb[2 * i + 1] = k0 * cs.y + k1 * cs.x;
-            }
+          for (int kh = 0; kh < KH; ++kh) {
+            const int kvh = KH * ps + kh;
+            if (kvh < p.n_kv) {
+              float kb[32];
+              tmem_ld32(tmem + tlane + a * 256 + kh * 128 + c * 32, kb);
+              tmem_wait_ld();
 #pragma unroll
-            for (int gi = 0; gi < GROUP; ++gi) {
-              const float4* qq =
-                  reinterpret_cast<const float4*>(q_s + (kvh * GROUP + gi) * kHeadDim + c * 32);
+              for (int i = 0; i < 16; ++i) {  // RoPE (linalg.py:92-93)
+                const float2 cs = csv[i];
+                const float k0 = kb[2 * i], k1 = kb[2 * i + 1];
+                kb[2 * i] = k0 * cs.x - k1 * cs.y;
+                kb[2 * i + 1] = k0 * cs.y + k1 * cs.x;
+              }
 #pragma unroll
-              for (int v4 = 0; v4 < 8; ++v4) {
-                const float4 q4 = qq[v4];
-                sc[gi] = fmaf(q4.x, kb[4 * v4], sc[gi]);
-                sc[gi] = fmaf(q4.y, kb[4 * v4 + 1], sc[gi]);
-                sc[gi] = fmaf(q4.z, kb[4 * v4 + 2], sc[gi]);
-                sc[gi] = fmaf(q4.w, kb[4 * v4 + 3], sc[gi]);
+              for (int gi = 0; gi < GROUP; ++gi) {
+                const float4* qq =
+                    reinterpret_cast<const float4*>(q_s + (kvh * GROUP + gi) * kHeadDim + c * 32);
+#pragma unroll
+                for (int v4 = 0; v4 < 8; ++v4) {
+                  const float4 q4 = qq[v4];
+                  sc[kh][gi] = fmaf(q4.x, kb[4 * v4], sc[kh][gi]);
+                  sc[kh][gi] = fmaf(q4.y, kb[4 * v4 + 1], sc[kh][gi]);
+                  sc[kh][gi] = fmaf(q4.z, kb[4 * v4 + 2], sc[kh][gi]);
+                  sc[kh][gi] = fmaf(q4.w, kb[4 * v4 + 3], sc[kh][gi]);
+                }
               }
             }
           }
+          if (c < 3) {
 #pragma unroll
-          for (int gi = 0; gi < GROUP; ++gi)
-            sc_s[(kvh * GROUP + gi) * kTileM + row] = valid ? sc[gi] : -INFINITY;
+            for (int i = 0; i < 16; ++i) csv[i] = nxt[i];
+          }
+        }
+#pragma unroll
+        for (int kh = 0; kh < KH; ++kh) {
+          const int kvh = KH * ps + kh;
+          if (kvh < p.n_kv) {
+#pragma unroll
+            for (int gi = 0; gi < GROUP; ++gi)
+              sc_s[(kvh * GROUP + gi) * kTileM + row] = valid ? sc[kh][gi] : -INFINITY;
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -473,8 +539,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         st_cluster_f32(x_peer + 4u * (hl * kTileM + row), h < p.n_q ? sc_s[h * kTileM + row] : -INFINITY);
       }
       mbar_arrive_remote_release(xfull_peer);
-      mbar_wait_cluster(xfull, ti & 1);
+      XQ_PROF(9, mbar_wait_cluster(xfull, ti & 1));
       // ---- softmax over the 256 tokens of the tile for this CTA's heads -> P
+      named_bar_sync(1, 128);  // every epilogue warp is done with q_s (P overwrites it)
       {
         const int seg = et & 7;  // tokens seg*32 .. +31 of the pair tile
         const int half = seg >> 2;
@@ -529,8 +596,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // ---- V side: drain O^T[channels x heads] of this tile
       int blk = 0;
       for (int us = 0; us < nuse; ++us, ++tc) {
-        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-        mbar_wait(&tfull[a], aph);
+        const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
+        const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
+        XQ_PROF(10, mbar_wait(&tfull[a], aph));
         tc_fence_after();
         for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
           const int ch = blk * 256 + static_cast<int>(rank) * 128 + row;  // storage channel
@@ -555,6 +623,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   }
+#ifdef XQ_ROLE_PROFILE
+  if (threadIdx.x == 0) prof_acc[11] = static_cast<unsigned long long>(clock64() - prof_t0);
+  if (lane == 0)
+    for (int c = 0; c < kProfCounters; ++c)
+      if (prof_acc[c]) atomicAdd(&g_role_prof[c], prof_acc[c]);
+#endif
   tc_fence_before();
   cluster_sync();
   if (warp == 1) {
@@ -627,7 +701,7 @@ __global__ void __launch_bounds__(256) k_absorb_vproj(const float* __restrict__ 
     out[((int64_t)b * n_q + h) * kHeadDim + tid] = acc4[0][tid] + acc4[1][tid] + acc4[2][tid] + acc4[3][tid];
 }
 
-// Arranged weights. wk_out: fp16 [n_pass*256][kdim], row kvh*128 + j =
+// Arranged weights. wk_out: fp16 [ceil(n_kv/4)*512][kdim], row kvh*128 + j =
 // W_k[:, kvh*128 + j]^T with the channels in the K-side producer order (zero
 // rows pad an odd n_kv). wv_out: fp16 [n_kv][kdim][128], row c = W_v[perm(c),
 // kvh*128 .. +128] with perm the V-side producer order.
@@ -635,7 +709,7 @@ __global__ void k_arrange_absorbed(const void* __restrict__ w_k, const void* __r
                                    int64_t kdim, int n_kv, int n_pass, int bs_k, int bs_v,
                                    __half* __restrict__ wk_out, __half* __restrict__ wv_out) {
   const int64_t ld = (int64_t)n_kv * 128;
-  const int64_t nk = (int64_t)n_pass * 256 * kdim;
+  const int64_t nk = (int64_t)n_pass * 512 * kdim;
   const int64_t nv = (int64_t)n_kv * kdim * 128;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nk + nv;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -733,7 +807,7 @@ int64_t n_tiles_for(int32_t max_len) {
 }
 
 // Shared-memory plan: [AB ring][P][codes ring][q][scores][peer scores][barriers]
-template <int AK, int AV, int BITS>
+template <int AK, int AV, int BITS, int GROUP>
 int plan_smem(Params& p, size_t& total) {
   constexpr bool PROD = AK != XQ_A_F16_ROWS;
   const uint32_t k_code = PROD ? 128u * 16u * BITS : 0u;
@@ -744,12 +818,18 @@ int plan_smem(Params& p, size_t& total) {
   p.v_tx = k_code + v_par;
   const uint32_t cst = PROD ? ((k_code + (k_par > v_par ? k_par : v_par) + 127) / 128 * 128) : 0u;
   p.cstage_bytes = cst;
-  const uint32_t fixed = 512u * p.nbh                      // P
-                         + 2u * 512u * p.n_q                // q, scores
+  // q (fp32 [n_q][128]) and P (fp16 [4][nbh][64]) share one region: P is
+  // written after the tile's last use of q, and q is rewritten only after the
+  // V-side MMAs that read P have completed
+  const uint32_t qp = ((512u * (p.n_q > p.nbh ? p.n_q : p.nbh)) + 1023u) / 1024u * 1024u;
+  const uint32_t fixed = qp                                 // q / P
+                         + 512u * p.n_q                     // scores
                          + 512u * p.nbh                     // peer scores
                          + (4 * kMaxStages + 6) * 8 + 16;   // barriers + tmem slot
   const uint32_t budget = 227u * 1024u - 1024u;
-  const int stages = kStages;
+  using CF = Cfg<GROUP>;
+  const int stages = CF::kStages;
+  constexpr uint32_t kABStage = CF::kABStage;
   int cstages = PROD ? 4 : 1;
   auto need = [&]() { return stages * kABStage + cstages * cst + fixed; };
   if (need() > budget && PROD) cstages = 2;
@@ -757,10 +837,10 @@ int plan_smem(Params& p, size_t& total) {
   p.stages = stages;
   p.cstages = cstages;
   p.cstage_shift = cstages == 4 ? 2 : (cstages == 2 ? 1 : 0);
-  p.off_p = stages * kABStage;
-  p.off_codes = p.off_p + 512u * p.nbh;
-  p.off_q = p.off_codes + cstages * cst;
-  p.off_sc = p.off_q + 512u * p.n_q;
+  p.off_q = stages * kABStage;
+  p.off_p = p.off_q;
+  p.off_codes = p.off_q + qp;
+  p.off_sc = p.off_codes + cstages * cst;
   p.off_x = p.off_sc + 512u * p.n_q;
   p.off_bar = (p.off_x + 512u * p.nbh + 7) / 8 * 8;
   total = 1024 + need();
@@ -769,8 +849,9 @@ int plan_smem(Params& p, size_t& total) {
 
 template <int AK, int AV, int BITS, int GROUP>
 int launch(const Maps& m, Params p, cudaStream_t st) {
+  p.n_pass = (p.n_kv + Cfg<GROUP>::KH - 1) / Cfg<GROUP>::KH;
   size_t smem = 0;
-  int status = plan_smem<AK, AV, BITS>(p, smem);
+  int status = plan_smem<AK, AV, BITS, GROUP>(p, smem);
   if (status != XQ_OK) return status;
   auto kern = k_decode_absorbed<AK, AV, BITS, GROUP>;
   static size_t configured = 0;
@@ -804,6 +885,20 @@ using namespace xq::absorb;
 
 extern "C" {
 
+/* Role profile of the absorbed kernel (zeros unless built with XQ_ROLE_PROFILE):
+ * reset != 0 clears the counters; out (if non-NULL) receives 16 uint64. */
+int xq_debug_role_profile(uint64_t* out, int32_t reset) {
+  if (out && cudaMemcpyFromSymbol(out, g_role_prof, sizeof(unsigned long long) * kProfCounters) !=
+                 cudaSuccess)
+    return check_launch("role profile read");
+  if (reset) {
+    static const unsigned long long zeros[kProfCounters] = {};
+    if (cudaMemcpyToSymbol(g_role_prof, zeros, sizeof(zeros)) != cudaSuccess)
+      return check_launch("role profile reset");
+  }
+  return XQ_OK;
+}
+
 int64_t xq_absorbed_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q_heads,
                                     int64_t kdim) {
   return (int64_t)n_seqs * n_tiles_for(max_len) * n_q_heads * (kdim + 2) * (int64_t)sizeof(float);
@@ -821,9 +916,9 @@ int xq_arrange_weights_absorbed(const void* w_k, const void* w_v, int32_t w_dtyp
     a_mode_v = a_mode_k;
     bits_v = bits_k;
   }
-  const int n_pass = (n_kv_heads + 1) / 2;
+  const int n_pass = (n_kv_heads + 3) / 4;  // rows padded to whole groups of 4 KV heads
   const int bs_k = perm_block(a_mode_k, bits_k), bs_v = perm_block(a_mode_v, bits_v);
-  const int64_t total = (int64_t)n_pass * 256 * kdim + (int64_t)n_kv_heads * kdim * 128;
+  const int64_t total = (int64_t)n_pass * 512 * kdim + (int64_t)n_kv_heads * kdim * 128;
   const int64_t blocks = (total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16;
   k_arrange_absorbed<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
       w_k, w_v, w_dtype, kdim, n_kv_heads, n_pass, bs_k, bs_v, static_cast<__half*>(wk_out),
@@ -869,12 +964,12 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
     XQ_REQUIRE(L_max % group_size == 0, XQ_ECONFIG, "per-channel K latent needs L_max % 128 == 0");
   }
   XQ_REQUIRE(ak_mode == XQ_A_F16_ROWS || valid_bits(ak_bits), XQ_ECONFIG, "bad bits %d", ak_bits);
-  const int n_pass = (n_kv_heads + 1) / 2;
+  const int64_t w_rows = (int64_t)(n_kv_heads + 3) / 4 * 512;
   const int64_t arena_rows = (int64_t)n_seqs * L_max;
   Maps maps;
   int st_;
   if ((st_ = make_map(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wk_arranged, kdim,
-                      (uint64_t)n_pass * 256, kChunk, 128, CU_TENSOR_MAP_SWIZZLE_128B, "W_k")) != XQ_OK)
+                      (uint64_t)w_rows, kChunk, 128, CU_TENSOR_MAP_SWIZZLE_128B, "W_k")) != XQ_OK)
     return st_;
   if ((st_ = stream_maps(ak_mode, ak_bits, ak_src, ak_params, ak_row_bytes, kdim, group_size,
                          arena_rows, 128, &maps.ka, &maps.kp)) != XQ_OK)
@@ -896,7 +991,6 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
   p.n_q = n_q;
   p.nb = nb_for(n_q);
   p.nbh = p.nb / 2;
-  p.n_pass = n_pass;
   p.q_pre = q_pre;
   p.rope = static_cast<const float2*>(rope_cs);
   p.rope_n = rope_n;
