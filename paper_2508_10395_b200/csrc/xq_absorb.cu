@@ -97,7 +97,7 @@ struct Params {
   const int32_t* seq_lens;
   int32_t n_seqs, n_tiles, n_units;
   int32_t n_kv, n_q, nb, nbh, n_pass;
-  int32_t stages, cstages, cstage_shift;  // cstages = 1 << cstage_shift
+  int32_t stages, cstages;
   uint32_t cstage_bytes;
   uint32_t k_code_bytes, k_tx, v_tx;  // codes ring: codes bytes / TMA bytes per stage
   const float* q_pre;
@@ -107,7 +107,7 @@ struct Params {
   float* part_o;       // [n_seqs][n_tiles][n_q][kdim]
   float2* part_ml;     // [n_seqs][n_tiles][n_q] (m, l), m in the log2 domain
   uint64_t w_hint;
-  uint32_t off_p, off_codes, off_q, off_sc, off_x, off_bar;
+  uint32_t off_p, off_codes, off_q, off_sc, off_x, off_rope, off_bar;
 };
 
 // work unit u -> (sequence, tile); false when the tile is past the sequence end
@@ -138,6 +138,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   float* q_s = reinterpret_cast<float*>(smem + p.off_q);    // [n_q][128]
   float* sc_s = reinterpret_cast<float*>(smem + p.off_sc);  // [n_q][128 rows]
   float* x_s = reinterpret_cast<float*>(smem + p.off_x);    // [nbh][128 rows] (peer's scores)
+  // RoPE of row r = 16*r1 + r0 of the tile: angle (t0 + 16*r1 + r0)*theta_j
+  // = base[r1][j] + off[j][r0], both from the float64-formed table
+  float2* rope_off = reinterpret_cast<float2*>(smem + p.off_rope);  // [64 j][16 r0]
+  float2* rope_base = rope_off + 64 * 16;                            // [8 r1][64 j]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* empty = full + kMaxStages;
   uint64_t* cfull = empty + kMaxStages;
@@ -162,7 +166,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr uint32_t kABStage = CF::kABStage;
   constexpr uint32_t kBBytes = CF::kBBytes;
   const int CSTAGES = p.cstages;
-  const uint32_t cshift = p.cstage_shift, cmask = (1u << cshift) - 1u;
   const int ngrp = p.kdim / kG;            // 128-channel groups
   const int nkc = p.kdim / kChunk;         // pass-1 stages per pass
   const int nblk = p.kdim / 256;           // V-side channel blocks (128 per CTA)
@@ -335,14 +338,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {
     // ------------------------------------------------ TMA: codes ring
     if constexpr (PROD) {
-      uint32_t ci = 0;
+      uint32_t ci = 0, cphase = 0;  // ring slot / phase of the next codes stage
       for (int u = cluster; u < p.n_units; u += n_clusters) {
         int b, t, len;
         if (!get_unit(p, u, b, t, len)) continue;
         const int32_t row_tile = static_cast<int32_t>((int64_t)b * p.L_max + t * kPairM);
         int ps = 0, g = 0;  // K side: (pass, group); then V side: g = 2*bb + th
-        for (int q = 0; q < ncs; ++q, ++ci) {
-          const uint32_t cs = ci & cmask, cph = (ci >> cshift) & 1u;
+        for (int q = 0; q < ncs; ++q) {
+          const uint32_t cs = ci, cph = cphase;
+          if (++ci == static_cast<uint32_t>(CSTAGES)) {
+            ci = 0;
+            cphase ^= 1u;
+          }
           XQ_PROF(5, mbar_wait(&cempty[cs], cph ^ 1));
           if (elect_one()) {
             uint8_t* st = sC + cs * p.cstage_bytes;
@@ -381,25 +388,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const RowSwizzle sw_v(r & 63);  // V side: row = token within a 64-token stage
       const int hh = r >> 6;          // V side: channel half of the group
       const uint32_t sAB_a = smem_u32(sAB), sC_a = smem_u32(sC);
-      uint32_t tcount = 0;
+      // this group's codes stages are the running indices == gp (mod 2); ring
+      // slot / phase advance by 2 per stage (ncs is even), A stages by 4
+      uint32_t cs = static_cast<uint32_t>(gp), cph = 0;
+      if (cs >= static_cast<uint32_t>(CSTAGES)) cs -= CSTAGES;  // (CSTAGES >= 2)
+      uint32_t as = static_cast<uint32_t>(2 * gp) % STAGES, aph = (2 * gp) / STAGES;
       for (int u = cluster; u < p.n_units; u += n_clusters) {
         int b, t, len;
         if (!get_unit(p, u, b, t, len)) continue;
         const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + b) : 0;
         const int tok_k = t * kPairM + rank * kTileM + r;
-        const uint32_t ci0 = tcount * ncs;
-        const int q0 = ((ci0 & 1) == static_cast<uint32_t>(gp)) ? 0 : 1;
-        int g = q0, ps = 0;  // K side (pass ps, group g); V side (ps == n_pass): g = 2*bb + th
-        for (int q = q0; q < ncs; q += 2) {
-          const uint32_t ci = ci0 + q;
-          const uint32_t cs = ci & cmask, cph = (ci >> cshift) & 1u;
+        int g = gp, ps = 0;  // K side (pass ps, group g); V side (ps == n_pass): g = 2*bb + th
+        for (int q = gp; q < ncs; q += 2) {
           const uint32_t st = sC_a + cs * p.cstage_bytes;
           XQ_PROF(6, mbar_wait(&cfull[cs], cph));
           const bool kside = ps < p.n_pass;
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
-            const uint32_t itn = 2 * ci + h;
-            const uint32_t s = itn % STAGES, ph = (itn / STAGES) & 1;
+            uint32_t s = as + h, ph = aph;
+            if (s >= STAGES) {
+              s -= STAGES;
+              ph ^= 1u;
+            }
             XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
             const uint32_t tile = sAB_a + s * kABStage;
             if (kside) {
@@ -425,8 +435,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             g -= ngrp;
             ++ps;
           }
+          cs += 2;
+          if (cs >= static_cast<uint32_t>(CSTAGES)) {
+            cs -= CSTAGES;
+            cph ^= 1u;
+          }
+          as += 4;
+          while (as >= STAGES) {
+            as -= STAGES;
+            aph ^= 1u;
+          }
         }
-        ++tcount;
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -440,12 +459,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t x_peer = mapa_shared(smem_u32(x_s), peer);
     const uint32_t xfull_peer = mapa_shared(smem_u32(xfull), peer);
     const uint32_t sP_a = smem_u32(sP);
+    // offsets table: cos/sin(r0*theta_j), r0 < 16 (table positions 0..15)
+    for (int i = et; i < 64 * 16; i += 128)
+      rope_off[i] = p.rope[(int64_t)(i >> 4) * p.rope_n + (i & 15)];
+    const int r0 = row & 15, r1 = row >> 4;
     uint32_t tc = 0, ti = 0;
     for (int u = cluster; u < p.n_units; u += n_clusters) {
       int b, t, len;
       if (!get_unit(p, u, b, t, len)) continue;
       const int pos = len - 1;
-      named_bar_sync(1, 128);  // previous tile's readers of q_s / sc_s are done
+      named_bar_sync(1, 128);  // previous tile's readers of q_s / sc_s / rope_base are done
+      for (int i = et; i < 8 * 64; i += 128) {  // base: cos/sin(t0 + 16*r1), t0 = tile row 0
+        const int64_t tp = (int64_t)t * kPairM + rank * kTileM + 16 * (i >> 6);
+        rope_base[i] = p.rope[(int64_t)(i & 63) * p.rope_n + (tp < p.rope_n ? tp : 0)];
+      }
       {
         const float2 cs = p.rope[(int64_t)(et >> 1) * p.rope_n + pos];
         for (int h = 0; h < p.n_q; ++h) {
@@ -458,21 +485,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 128);
       const int tok = t * kPairM + rank * kTileM + row;
       const bool valid = tok < len;
-      const float2* rp = p.rope + (valid ? tok : 0);
       // ---- K side: scores of every query head for this CTA's 128 tokens.
-      // The row's cos/sin (frequency-major table, L2-resident) are shared by
-      // the KH heads of a pass: loaded once per 16-frequency chunk, one chunk
-      // ahead, the first before the wait so the L2 latency hides under the MMA.
+      // cos/sin of (t0 + 16*r1 + r0)*theta_j by one angle addition from the two
+      // shared tables (shared by the KH heads of a pass)
       auto load_cs = [&](int c, float2(&dst)[16]) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) dst[i] = __ldg(rp + (int64_t)(c * 16 + i) * p.rope_n);
+        for (int i = 0; i < 16; ++i) {
+          const int j = c * 16 + i;
+          const float2 bs = rope_base[r1 * 64 + j], of = rope_off[j * 16 + r0];
+          dst[i] = make_float2(bs.x * of.x - bs.y * of.y, bs.y * of.x + bs.x * of.y);
+        }
       };
       for (int ps = 0; ps < p.n_pass; ++ps, ++tc) {
         const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
         const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
-        float2 csv[16];
-        load_cs(0, csv);
         XQ_PROF(8, mbar_wait(&tfull[a], aph));
+#ifdef XQ_ROLE_PROFILE
+        const long long pt_k = clock64();
+#endif
         tc_fence_after();
         float sc[KH][GROUP];
 #pragma unroll
@@ -481,8 +511,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int gi = 0; gi < GROUP; ++gi) sc[kh][gi] = 0.f;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          float2 nxt[16];
-          if (c < 3) load_cs(c + 1, nxt);
+          float2 csv[16];
+          load_cs(c, csv);
 #pragma unroll
           for (int kh = 0; kh < KH; ++kh) {
             const int kvh = KH * ps + kh;
@@ -512,10 +542,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
           }
-          if (c < 3) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) csv[i] = nxt[i];
-          }
         }
 #pragma unroll
         for (int kh = 0; kh < KH; ++kh) {
@@ -529,11 +555,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
+#ifdef XQ_ROLE_PROFILE
+        prof_acc[12] += clock64() - pt_k;
+#endif
           if (leader) mbar_arrive(&tempty[a]);
           else mbar_arrive_remote(tempty_leader0 + 8 * a);
         }
       }
       // ---- exchange: the peer owns query heads [peer*nbh, peer*nbh + nbh)
+#ifdef XQ_ROLE_PROFILE
+      const long long pt_x = clock64();
+#endif
       for (int hl = 0; hl < nbh; ++hl) {
         const int h = static_cast<int>(peer) * nbh + hl;
         st_cluster_f32(x_peer + 4u * (hl * kTileM + row), h < p.n_q ? sc_s[h * kTileM + row] : -INFINITY);
@@ -588,6 +620,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
+#ifdef XQ_ROLE_PROFILE
+        prof_acc[13] += clock64() - pt_x;
+#endif
           if (leader) mbar_arrive(pready);
           else mbar_arrive_remote(pready_leader);
         }
@@ -599,6 +634,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
         const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
         XQ_PROF(10, mbar_wait(&tfull[a], aph));
+#ifdef XQ_ROLE_PROFILE
+        const long long pt_v = clock64();
+#endif
         tc_fence_after();
         for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
           const int ch = blk * 256 + static_cast<int>(rank) * 128 + row;  // storage channel
@@ -617,6 +655,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
+#ifdef XQ_ROLE_PROFILE
+        prof_acc[14] += clock64() - pt_v;
+#endif
           if (leader) mbar_arrive(&tempty[a]);
           else mbar_arrive_remote(tempty_leader0 + 8 * a);
         }
@@ -825,24 +866,25 @@ int plan_smem(Params& p, size_t& total) {
   const uint32_t fixed = qp                                 // q / P
                          + 512u * p.n_q                     // scores
                          + 512u * p.nbh                     // peer scores
+                         + (64 * 16 + 8 * 64) * 8           // RoPE offset + base tables
                          + (4 * kMaxStages + 6) * 8 + 16;   // barriers + tmem slot
   const uint32_t budget = 227u * 1024u - 1024u;
   using CF = Cfg<GROUP>;
   const int stages = CF::kStages;
   constexpr uint32_t kABStage = CF::kABStage;
-  int cstages = PROD ? 4 : 1;
+  int cstages = PROD ? 4 : 2;
   auto need = [&]() { return stages * kABStage + cstages * cst + fixed; };
-  if (need() > budget && PROD) cstages = 2;
+  while (need() > budget && cstages > 2) --cstages;
   XQ_REQUIRE(need() <= budget, XQ_ESHAPE, "shared memory plan does not fit (%d heads)", p.n_q);
   p.stages = stages;
   p.cstages = cstages;
-  p.cstage_shift = cstages == 4 ? 2 : (cstages == 2 ? 1 : 0);
   p.off_q = stages * kABStage;
   p.off_p = p.off_q;
   p.off_codes = p.off_q + qp;
   p.off_sc = p.off_codes + cstages * cst;
   p.off_x = p.off_sc + 512u * p.n_q;
-  p.off_bar = (p.off_x + 512u * p.nbh + 7) / 8 * 8;
+  p.off_rope = p.off_x + 512u * p.nbh;
+  p.off_bar = p.off_rope + (64 * 16 + 8 * 64) * 8;
   total = 1024 + need();
   return XQ_OK;
 }
