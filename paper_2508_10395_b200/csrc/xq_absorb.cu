@@ -459,6 +459,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t x_peer = mapa_shared(smem_u32(x_s), peer);
     const uint32_t xfull_peer = mapa_shared(smem_u32(xfull), peer);
     const uint32_t sP_a = smem_u32(sP);
+    // 32-bit shared addresses: explicit ld/st.shared (a generic pointer into
+    // dynamic shared memory compiles to generic LD/ST)
+    const uint32_t q_a = smem_u32(q_s), sc_a = smem_u32(sc_s), x_a = smem_u32(x_s);
+    const uint32_t ro_a = smem_u32(rope_off), rb_a = smem_u32(rope_base);
     // offsets table: cos/sin(r0*theta_j), r0 < 16 (table positions 0..15)
     for (int i = et; i < 64 * 16; i += 128)
       rope_off[i] = p.rope[(int64_t)(i >> 4) * p.rope_n + (i & 15)];
@@ -479,7 +483,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const float* qp = p.q_pre + ((int64_t)b * p.n_q + h) * kHeadDim;
           const float e0 = qp[et & ~1], e1 = qp[et | 1];
           const float rr = (et & 1) ? (e0 * cs.y + e1 * cs.x) : (e0 * cs.x - e1 * cs.y);
-          q_s[h * kHeadDim + et] = rr * p.q_scale;
+          // split layout: even dims (first of each RoPE pair) then odd dims
+          sts_f32(q_a + 4u * (h * kHeadDim + ((et & 1) ? 64 : 0) + (et >> 1)), rr * p.q_scale);
         }
       }
       named_bar_sync(1, 128);
@@ -492,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int j = c * 16 + i;
-          const float2 bs = rope_base[r1 * 64 + j], of = rope_off[j * 16 + r0];
+          const float2 bs = lds_f2(rb_a + 8u * (r1 * 64 + j)), of = lds_f2(ro_a + 8u * (j * 16 + r0));
           dst[i] = make_float2(bs.x * of.x - bs.y * of.y, bs.y * of.x + bs.x * of.y);
         }
       };
@@ -504,40 +509,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long pt_k = clock64();
 #endif
         tc_fence_after();
-        float sc[KH][GROUP];
+        // K columns of a head come split (W_k rows arranged so): cols 0-63 hold
+        // the first element of each RoPE pair, cols 64-127 the second, so
+        // pairs of frequencies map to register pairs and the rotation + dot
+        // run as packed float2 FMAs (FFMA2)
+        float2 sc[KH][GROUP];
 #pragma unroll
         for (int kh = 0; kh < KH; ++kh)
 #pragma unroll
-          for (int gi = 0; gi < GROUP; ++gi) sc[kh][gi] = 0.f;
+          for (int gi = 0; gi < GROUP; ++gi) sc[kh][gi] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float2 csv[16];
-          load_cs(c, csv);
+        for (int c = 0; c < 4; ++c) {  // frequencies 16c .. 16c+15
+          float2 cc[8], ss[8], ns[8];
+          {
+            float2 csv[16];
+            load_cs(c, csv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              cc[i] = make_float2(csv[2 * i].x, csv[2 * i + 1].x);
+              ss[i] = make_float2(csv[2 * i].y, csv[2 * i + 1].y);
+              ns[i] = make_float2(-csv[2 * i].y, -csv[2 * i + 1].y);
+            }
+          }
 #pragma unroll
           for (int kh = 0; kh < KH; ++kh) {
             const int kvh = KH * ps + kh;
             if (kvh < p.n_kv) {
-              float kb[32];
-              tmem_ld32(tmem + tlane + a * 256 + kh * 128 + c * 32, kb);
+              float ke[16], ko[16];
+              tmem_ld16(tmem + tlane + a * 256 + kh * 128 + c * 16, ke);
+              tmem_ld16(tmem + tlane + a * 256 + kh * 128 + 64 + c * 16, ko);
               tmem_wait_ld();
+              float2 re[8], ro[8];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {  // RoPE (linalg.py:92-93)
-                const float2 cs = csv[i];
-                const float k0 = kb[2 * i], k1 = kb[2 * i + 1];
-                kb[2 * i] = k0 * cs.x - k1 * cs.y;
-                kb[2 * i + 1] = k0 * cs.y + k1 * cs.x;
+              for (int i = 0; i < 8; ++i) {  // RoPE (linalg.py:92-93)
+                const float2 e = make_float2(ke[2 * i], ke[2 * i + 1]);
+                const float2 o = make_float2(ko[2 * i], ko[2 * i + 1]);
+                re[i] = __ffma2_rn(e, cc[i], __fmul2_rn(o, ns[i]));
+                ro[i] = __ffma2_rn(e, ss[i], __fmul2_rn(o, cc[i]));
               }
 #pragma unroll
               for (int gi = 0; gi < GROUP; ++gi) {
-                const float4* qq =
-                    reinterpret_cast<const float4*>(q_s + (kvh * GROUP + gi) * kHeadDim + c * 32);
+                const uint32_t qe = q_a + 4u * ((kvh * GROUP + gi) * kHeadDim + c * 16);
 #pragma unroll
-                for (int v4 = 0; v4 < 8; ++v4) {
-                  const float4 q4 = qq[v4];
-                  sc[kh][gi] = fmaf(q4.x, kb[4 * v4], sc[kh][gi]);
-                  sc[kh][gi] = fmaf(q4.y, kb[4 * v4 + 1], sc[kh][gi]);
-                  sc[kh][gi] = fmaf(q4.z, kb[4 * v4 + 2], sc[kh][gi]);
-                  sc[kh][gi] = fmaf(q4.w, kb[4 * v4 + 3], sc[kh][gi]);
+                for (int v4 = 0; v4 < 4; ++v4) {
+                  const float4 a4 = lds_f4(qe + 16u * v4), b4 = lds_f4(qe + 256u + 16u * v4);
+                  float2 acc = sc[kh][gi];
+                  acc = __ffma2_rn(re[2 * v4], make_float2(a4.x, a4.y), acc);
+                  acc = __ffma2_rn(re[2 * v4 + 1], make_float2(a4.z, a4.w), acc);
+                  acc = __ffma2_rn(ro[2 * v4], make_float2(b4.x, b4.y), acc);
+                  acc = __ffma2_rn(ro[2 * v4 + 1], make_float2(b4.z, b4.w), acc);
+                  sc[kh][gi] = acc;
                 }
               }
             }
@@ -549,7 +570,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (kvh < p.n_kv) {
 #pragma unroll
             for (int gi = 0; gi < GROUP; ++gi)
-              sc_s[(kvh * GROUP + gi) * kTileM + row] = valid ? sc[kh][gi] : -INFINITY;
+              sts_f32(sc_a + 4u * ((kvh * GROUP + gi) * kTileM + row),
+                      valid ? sc[kh][gi].x + sc[kh][gi].y : -INFINITY);
           }
         }
         tc_fence_before();
@@ -568,7 +590,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
       for (int hl = 0; hl < nbh; ++hl) {
         const int h = static_cast<int>(peer) * nbh + hl;
-        st_cluster_f32(x_peer + 4u * (hl * kTileM + row), h < p.n_q ? sc_s[h * kTileM + row] : -INFINITY);
+        st_cluster_f32(x_peer + 4u * (hl * kTileM + row),
+                       h < p.n_q ? lds_f32(sc_a + 4u * (h * kTileM + row)) : -INFINITY);
       }
       mbar_arrive_remote_release(xfull_peer);
       XQ_PROF(9, mbar_wait_cluster(xfull, ti & 1));
@@ -579,11 +602,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int half = seg >> 2;
         for (int hl = et >> 3; hl < nbh; hl += 16) {
           const int h = static_cast<int>(rank) * nbh + hl;
-          const float* src = (half == static_cast<int>(rank)) ? (sc_s + h * kTileM) : (x_s + hl * kTileM);
+          const uint32_t src = ((half == static_cast<int>(rank)) ? (sc_a + 4u * h * kTileM)
+                                                                 : (x_a + 4u * hl * kTileM)) +
+                               4u * (seg & 3) * 32;
           float s[32];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 v = (h < p.n_q) ? reinterpret_cast<const float4*>(src + (seg & 3) * 32)[i]
+            const float4 v = (h < p.n_q) ? lds_f4(src + 16u * i)
                                          : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
             s[4 * i] = v.x; s[4 * i + 1] = v.y; s[4 * i + 2] = v.z; s[4 * i + 3] = v.w;
           }
@@ -648,7 +673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
               const int h = c16 * 16 + jj;
-              if (h < p.n_q) dst[(int64_t)h * p.kdim] = v[jj];
+              if (h < p.n_q) __stcg(dst + (int64_t)h * p.kdim, v[jj]);
             }
           }
         }
@@ -757,7 +782,10 @@ __global__ void k_arrange_absorbed(const void* __restrict__ w_k, const void* __r
     if (i < nk) {
       const int64_t pch = i % kdim, rowi = i / kdim;
       const int64_t k = (pch / bs_k) * bs_k + perm_channel(static_cast<int>(pch % bs_k), bs_k);
-      wk_out[i] = rowi < ld ? __float2half_rn(load_as_f32(w_k, dt, k * ld + rowi)) : __float2half_rn(0.f);
+      // within a head: rows 0-63 = even dims, 64-127 = odd dims (split RoPE pairs)
+      const int64_t cp = rowi & 127, dim = cp < 64 ? 2 * cp : 2 * (cp - 64) + 1;
+      const int64_t col = (rowi & ~int64_t(127)) + dim;
+      wk_out[i] = rowi < ld ? __float2half_rn(load_as_f32(w_k, dt, k * ld + col)) : __float2half_rn(0.f);
     } else {
       const int64_t e = i - nk;
       const int64_t j = e % 128, pch = (e / 128) % kdim, kvh = e / (128 * kdim);
