@@ -28,3 +28,11 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(params=["absorbed", "unabsorbed"])
+def kernel_path(request, monkeypatch):
+    """Run a fused-decode test through both kernels: the V-absorbed default
+    (csrc/xq_absorb.cu) and the unabsorbed remat kernel (csrc/xq_decode.cu)."""
+    monkeypatch.setenv("XQ_ABSORB", "1" if request.param == "absorbed" else "0")
+    return request.param

@@ -15,7 +15,7 @@ import pytest
 
 from _util import bf16f, fp16_round, golden, rel_err, torch_bf16
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("kernel_path")]
 
 FUSED_TOL = 2e-2
 F32_TOL = 1e-4

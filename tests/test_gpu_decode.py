@@ -6,7 +6,7 @@ import pytest
 
 from _util import rel_err
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("kernel_path")]
 
 TOL = 2e-2
 

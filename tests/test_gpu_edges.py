@@ -17,7 +17,7 @@ import pytest
 
 from _util import rel_err
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("kernel_path")]
 TOL = 2e-2
 
 
@@ -192,3 +192,58 @@ def test_full_c2_shape_against_independent_fp32():
     ref = torch.einsum("hn,nhd->hd", p, v.view(n, H, 128))
     err = (out - ref).abs().max().item() / ref.abs().max().item()
     assert err <= TOL, err
+
+
+@pytest.mark.parametrize("d,H", [(5120, 40, ), (768, 6), (512, 4)])
+def test_mha_head_layouts(d, H):
+    """Head counts that pad the absorbed kernel's V-side N (40 -> 48, 4 -> 16),
+    a partial 4-head K pass (6 heads) and the 13B width (kdim 5120)."""
+    import torch
+
+    lens = [300, 517]
+    st = _mha(3, len(lens), 640, d, H)
+    w = _weights(d, d, seed=H)
+    g = torch.Generator().manual_seed(11)
+    xs = [torch.randn(n, d, generator=g).to(torch.bfloat16) for n in lens]
+    for s, x in enumerate(xs):
+        st.prefill(x[:-1].cuda(), w, slot=s)
+    st.decode_append(torch.stack([x[-1] for x in xs]).cuda(), w)
+    q = torch.randn(len(lens), H, 128, generator=g)
+    out = st.decode_attend(q.cuda(), w).cpu().numpy()
+    wk, wv = w.w_k.double().cpu().numpy(), w.w_v.double().cpu().numpy()
+    for s, x in enumerate(xs):
+        ref = _oracle_mha(x.double().numpy(), wk, wv, q[s].double().numpy().reshape(-1), 3, H)
+        assert rel_err(out[s].reshape(-1), ref) <= TOL, (d, H, lens[s])
+
+
+@pytest.mark.parametrize("d,H,g", [(2048, 16, 4), (2048, 16, 2), (1024, 8, 8)])
+def test_gqa_group_layouts(d, H, g):
+    """xq-gqa with GROUP 4 / 2 / 8->1 KV heads: absorbed and unabsorbed kernels agree
+    (the unabsorbed one is pinned to the reference in test_gpu_cache)."""
+    import os
+
+    import torch
+
+    from paper_2508_10395_b200 import cache as M
+
+    r = d // g
+    if g not in (1, 2, 4):
+        pytest.skip("the fused kernels support query groups 1, 2, 4")
+    pol = M.LayerPolicy.uniform(4, 1)
+    st = M.make_cache("xq-gqa", 0, pol, 128, n_slots=2, max_len=768, hidden_dim=d, n_heads=H,
+                      kv_group=g, device="cuda")
+    gen = torch.Generator().manual_seed(5)
+    uk, _ = torch.linalg.qr(torch.randn(d, r, generator=gen, dtype=torch.float64))
+    uv, _ = torch.linalg.qr(torch.randn(d, r, generator=gen, dtype=torch.float64))
+    w = M.LayerWeights(u_k=uk.float().cuda(), u_v=uv.float().cuda(),
+                       fused_k=(torch.randn(r, r, generator=gen) / r ** 0.5).cuda(),
+                       fused_v=(torch.randn(r, r, generator=gen) / r ** 0.5).cuda())
+    for s, n in enumerate([300, 700]):
+        st.prefill(torch.randn(n, d, generator=gen).to(torch.bfloat16).cuda(), w, slot=s)
+    st.decode_append(torch.randn(2, d, generator=gen).to(torch.bfloat16).cuda(), w)
+    q = torch.randn(2, H, 128, generator=gen).cuda()
+    st.absorb = True
+    a = st.decode_attend(q, w).cpu().numpy()
+    st.absorb = False
+    b = st.decode_attend(q, w).cpu().numpy()
+    assert rel_err(a, b) <= 1e-2, rel_err(a, b)
