@@ -124,7 +124,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmap_ka,
                       const __grid_constant__ CUtensorMap tmap_kp,
                       const __grid_constant__ CUtensorMap tmap_va,
-                      const __grid_constant__ CUtensorMap tmap_vp, const Params p) {
+                      const __grid_constant__ CUtensorMap tmap_vp,
+                      const __grid_constant__ CUtensorMap tmap_o, const Params p) {
   constexpr bool PROD = AK != XQ_A_F16_ROWS;
   static_assert((AK == XQ_A_F16_ROWS) == (AV == XQ_A_F16_ROWS), "fp16 rows feed both sides or neither");
   static_assert(AV != XQ_A_CODES_CHANNEL, "the V side is per-token");
@@ -472,6 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int b, t, len;
       if (!get_unit(p, u, b, t, len)) continue;
       const int pos = len - 1;
+      if (et == 0) tma_store_wait_read<0>();  // previous tile's O stores have read q_s / sc_s
       named_bar_sync(1, 128);  // previous tile's readers of q_s / sc_s / rope_base are done
       for (int i = et; i < 8 * 64; i += 128) {  // base: cos/sin(t0 + 16*r1), t0 = tile row 0
         const int64_t tp = (int64_t)t * kPairM + rank * kTileM + 16 * (i >> 6);
@@ -663,9 +665,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long pt_v = clock64();
 #endif
         tc_fence_after();
+        // each [n_q x 128-channel] block is staged in shared memory (two
+        // buffers: the score region and the q/P region, both free here) and
+        // written by one TMA bulk store
         for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
-          const int ch = blk * 256 + static_cast<int>(rank) * 128 + row;  // storage channel
-          float* dst = p.part_o + ((int64_t)b * p.n_tiles + t) * p.n_q * (int64_t)p.kdim + ch;
+          const uint32_t stg = (blk & 1) ? q_a : sc_a;
+          if (et == 0) tma_store_wait_read<1>();  // the store that last read `stg` is done
+          named_bar_sync(1, 128);
           for (int c16 = 0; c16 < p.nb / 16; ++c16) {
             float v[16];
             tmem_ld16(tmem + tlane + a * 256 + bi * p.nb + c16 * 16, v);
@@ -673,8 +679,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
               const int h = c16 * 16 + jj;
-              if (h < p.n_q) __stcg(dst + (int64_t)h * p.kdim, v[jj]);
+              if (h < p.n_q) sts_f32(stg + 4u * (h * kTileM + row), v[jj]);
             }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (et == 0) {
+            tma_store_2d(&tmap_o, stg, blk * 256 + static_cast<int>(rank) * 128,
+                         static_cast<int32_t>(((int64_t)b * p.n_tiles + t) * p.n_q));
+            tma_store_commit();
           }
         }
         tc_fence_before();
@@ -689,6 +702,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (warp == kEpiWarp0 && lane == 0) tma_store_wait_all();
 #ifdef XQ_ROLE_PROFILE
   if (threadIdx.x == 0) prof_acc[11] = static_cast<unsigned long long>(clock64() - prof_t0);
   if (lane == 0)
@@ -862,7 +876,7 @@ int stream_maps(int mode, int bits, const void* src, const void* params, int64_t
 }
 
 struct Maps {
-  CUtensorMap w, ka, kp, va, vp;
+  CUtensorMap w, ka, kp, va, vp, o;
 };
 
 int nb_for(int n_q) {
@@ -932,7 +946,7 @@ int launch(const Maps& m, Params p, cudaStream_t st) {
     configured = 227 * 1024;
   }
   const int pairs = p.n_units < num_sms() / 2 ? p.n_units : num_sms() / 2;
-  kern<<<2 * pairs, kThreads, smem, st>>>(m.w, m.ka, m.kp, m.va, m.vp, p);
+  kern<<<2 * pairs, kThreads, smem, st>>>(m.w, m.ka, m.kp, m.va, m.vp, m.o, p);
   return check_launch("k_decode_absorbed");
 }
 
@@ -1048,6 +1062,11 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
                          arena_rows, 64, &maps.va, &maps.vp)) != XQ_OK)
     return st_;
 
+  const int64_t n_tiles = n_tiles_for(max_len);
+  if ((st_ = make_map(&maps.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, workspace, kdim,
+                      (uint64_t)n_seqs * n_tiles * n_q, 128, static_cast<uint32_t>(n_q),
+                      CU_TENSOR_MAP_SWIZZLE_NONE, "O partials")) != XQ_OK)
+    return st_;
   Params p;
   p.k_resid = ak_resid;
   p.k_nflushed = ak_nflushed;

@@ -18,7 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def launches(src, tag):
+def launches(src, tag, cfg):
     rows = list(csv.reader(open(src)))
     hdr, data = None, []
     for r in rows:
@@ -34,7 +34,7 @@ def launches(src, tag):
         agg[name][0] += 1
         agg[name][1] += float(d["Metric Value"]) * scale.get(d["Metric Unit"], 1.0)
     tot = sum(v[1] for v in agg.values())
-    lines = [f"# ncu launch list of `python bench.py --steps 2 --warmup 1 --no-fp16 --no-cpu-baseline`",
+    lines = [f"# ncu launch list of `python bench.py --config {cfg} --steps 2 --warmup 1 --no-fp16 --no-cpu-baseline`",
              "# (gpu__time_duration.sum, --clock-control none; cold-cache serialised: compare SHARES)",
              f"# {len(data)} launches, {tot / 1e3:.2f} ms total",
              f"{'total_ms':>10} {'share':>6} {'count':>6}  kernel"]
@@ -61,14 +61,15 @@ WANT = [
 ]
 
 
-def kernel(rep, tag, key):
+def kernel(rep, tag, key, cfg):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(raw.splitlines()))
     h, u, v = r[0], r[1], r[2]
     vals = {n: (v[i], u[i]) for i, n in enumerate(h)}
     lines = [f"# ncu --set full of {vals.get('Kernel Name', ('?', ''))[0]}",
-             "# one launch = one layer of the C2 step (B=8, l=32769, d=4096, 3-bit), --clock-control none"]
+             f"# one launch = one layer of the {cfg.upper()} bench step (tools/prof_step.py --config {cfg}, "
+             "layer 3 = first layer at the config's bit width), --clock-control none"]
     for n in WANT:
         if n in vals:
             lines.append(f"{n:80s} {vals[n][0]:>16} {vals[n][1]}")
@@ -88,6 +89,16 @@ def kernel(rep, tag, key):
     lines.append("# warp stall sampling (all warps, all roles)")
     for n, c in stalls.most_common(8):
         lines.append(f"{n:30s} {100 * c / tot:5.1f}%")
+    # hottest source lines (tools/ncu_lines.py over the cuda+sass source view)
+    mix = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    tmp = os.path.join(ROOT, "build", f"{tag}_mix.csv")
+    os.makedirs(os.path.dirname(tmp), exist_ok=True)
+    open(tmp, "w").write(mix)
+    hot = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), tmp, "25"],
+                         capture_output=True, text=True).stdout
+    lines.append("# hottest source lines (share of all warp-stall samples, top two stall reasons)")
+    lines.extend(hot.rstrip().splitlines())
     out = os.path.join(ROOT, "profiles", f"{tag}_decode_kernel.txt")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
@@ -109,9 +120,12 @@ def kernel(rep, tag, key):
     json.dump(js, open(js_path, "w"), indent=1)
 
 
+KEYS = {"c2": "xq-mha_3", "c3": "xq-cl-mha_2", "c4": "xq-gqa_3", "c1": "xq-mha_4"}
+
 if __name__ == "__main__":
+    # python tools/summarize_profiles.py gpurun_out r01 c2   (files of tools/profile_round.sh)
     src, tag = sys.argv[1], sys.argv[2]
-    key = sys.argv[3] if len(sys.argv) > 3 else "xq-mha_3"
+    cfg = sys.argv[3] if len(sys.argv) > 3 else "c2"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    launches(os.path.join(src, "launches_bench.csv"), tag)
-    kernel(os.path.join(src, "decode_full.ncu-rep"), tag, key)
+    launches(os.path.join(src, f"launches_bench_{cfg}.csv"), f"{tag}_{cfg}", cfg)
+    kernel(os.path.join(src, f"decode_full_{cfg}.ncu-rep"), f"{tag}_{cfg}", KEYS[cfg], cfg)
