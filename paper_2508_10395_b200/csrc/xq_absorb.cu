@@ -31,8 +31,8 @@
 //     M=256 channels over the pair (128 per CTA, MN-major A tiles written by
 //     the same producers), N = heads, K = tokens. O and (m, l) go to HBM as
 //     this tile's split partials.
-// k_absorb_vproj then merges the tile partials per (sequence, head) and
-// applies W_v[:, kv(h)].
+// k_absorb_combine then merges the tile partials per (sequence, head) and
+// k_absorb_project applies W_v[:, kv(h)].
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <stdlib.h>
@@ -717,34 +717,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
-// Merge the tile partials of one (sequence, query head) and project through
-// W_v: out = ((sum_i 2^(m_i-M) O_i) / (sum_i 2^(m_i-M) l_i)) @ W_v[:, kv(h)].
-// wv: fp16 [n_kv][kdim][128], rows in the storage channel order of O.
-__global__ void __launch_bounds__(256) k_absorb_vproj(const float* __restrict__ part_o,
-                                                      const float2* __restrict__ part_ml,
-                                                      const int32_t* __restrict__ seq_lens,
-                                                      int n_tiles, int n_q, int group, int kdim,
-                                                      const __half* __restrict__ wv,
-                                                      float* __restrict__ out) {
-  extern __shared__ float sm[];
-  float* x = sm;              // [kdim]
-  float* wts = sm + kdim;     // [n_tiles]
-  __shared__ float red[8];
-  __shared__ float acc4[4][128];
-  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+// Merge the tile partials: x[b][h][c] = (sum_i 2^(m_i-M) O_i[h][c]) / (sum_i 2^(m_i-M) l_i).
+// Grid (n_seqs*n_q, kdim/512), 128 threads x 4 channels (float4 loads, 8 tiles
+// in flight per thread: the partials are streamed once from HBM/L2).
+__global__ void __launch_bounds__(128) k_absorb_combine(const float* __restrict__ part_o,
+                                                        const float2* __restrict__ part_ml,
+                                                        const int32_t* __restrict__ seq_lens,
+                                                        int n_tiles, int n_q, int kdim,
+                                                        float* __restrict__ x_out) {
+  extern __shared__ float wts[];  // [n_tiles]
+  __shared__ float red[4];
+  const int bh = blockIdx.x, b = bh / n_q, h = bh % n_q, tid = threadIdx.x;
   const int len = seq_lens[b];
   const int nt = (len + kPairM - 1) / kPairM;
   const float2* ml = part_ml + (int64_t)b * n_tiles * n_q + h;
   float M = -INFINITY;
-  for (int i = tid; i < nt; i += 256) M = fmaxf(M, ml[(int64_t)i * n_q].x);
+  for (int i = tid; i < nt; i += 128) M = fmaxf(M, ml[(int64_t)i * n_q].x);
   M = warp_max(M);
   if ((tid & 31) == 0) red[tid >> 5] = M;
   __syncthreads();
-  M = red[0];
-  for (int w = 1; w < 8; ++w) M = fmaxf(M, red[w]);
+  M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
   __syncthreads();
   float L = 0.f;
-  for (int i = tid; i < nt; i += 256) {
+  for (int i = tid; i < nt; i += 128) {
     const float2 v = ml[(int64_t)i * n_q];
     const float wgt = (v.x == -INFINITY) ? 0.f : exp2f(v.x - M);
     wts[i] = wgt;
@@ -753,32 +748,78 @@ __global__ void __launch_bounds__(256) k_absorb_vproj(const float* __restrict__ 
   L = warp_sum(L);
   if ((tid & 31) == 0) red[tid >> 5] = L;
   __syncthreads();
-  L = 0.f;
-  for (int w = 0; w < 8; ++w) L += red[w];
+  L = red[0] + red[1] + red[2] + red[3];
   const float inv = L > 0.f ? 1.f / L : 0.f;
-  const float* po = part_o + (int64_t)b * n_tiles * n_q * kdim + (int64_t)h * kdim;
-  for (int c = tid; c < kdim; c += 256) {
-    float acc = 0.f;
-#pragma unroll 4
-    for (int i = 0; i < nt; ++i) acc = fmaf(wts[i], po[(int64_t)i * n_q * kdim + c], acc);
-    x[c] = acc * inv;
+  const int c = blockIdx.y * 512 + tid * 4;
+  if (c >= kdim) return;
+  const int64_t stride = (int64_t)n_q * kdim;  // tile stride of the partials
+  const float* po = part_o + (int64_t)b * n_tiles * stride + (int64_t)h * kdim + c;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int i = 0;
+  for (; i + 8 <= nt; i += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(reinterpret_cast<const float4*>(po + (int64_t)(i + k) * stride));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float w = wts[i + k];
+      acc.x = fmaf(w, v[k].x, acc.x); acc.y = fmaf(w, v[k].y, acc.y);
+      acc.z = fmaf(w, v[k].z, acc.z); acc.w = fmaf(w, v[k].w, acc.w);
+    }
+  }
+  for (; i < nt; ++i) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(po + (int64_t)i * stride));
+    const float w = wts[i];
+    acc.x = fmaf(w, v.x, acc.x); acc.y = fmaf(w, v.y, acc.y);
+    acc.z = fmaf(w, v.z, acc.z); acc.w = fmaf(w, v.w, acc.w);
+  }
+  *reinterpret_cast<float4*>(x_out + (int64_t)bh * kdim + c) =
+      make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+}
+
+// out[b][h][:] = x[b][h][:] @ W_v[:, kv(h)], wv fp16 [n_kv][kdim][128] (rows in the
+// storage channel order of x). Grid (n_q, ceil(n_seqs/8)): each CTA streams its
+// head's W_v slice once for up to 8 sequences (x staged in shared memory).
+__global__ void __launch_bounds__(256) k_absorb_project(const float* __restrict__ x,
+                                                        int n_seqs, int n_q, int group, int kdim,
+                                                        const __half* __restrict__ wv,
+                                                        float* __restrict__ out) {
+  extern __shared__ float xs[];  // [8][kdim]
+  __shared__ float red[4][8][128];
+  const int h = blockIdx.x, b0 = blockIdx.y * 8, tid = threadIdx.x;
+  const int nb = n_seqs - b0 < 8 ? n_seqs - b0 : 8;
+  for (int i = tid; i < 8 * kdim; i += 256) {
+    const int s = i / kdim, c = i % kdim;
+    xs[i] = s < nb ? x[((int64_t)(b0 + s) * n_q + h) * kdim + c] : 0.f;
   }
   __syncthreads();
   const int j2 = tid & 63, qtr = tid >> 6;
   const __half2* w2 = reinterpret_cast<const __half2*>(wv + (int64_t)(h / group) * kdim * 128) + j2;
   const int c0 = qtr * (kdim / 4), c1 = c0 + kdim / 4;
-  float a0 = 0.f, a1 = 0.f;
-#pragma unroll 8
+  float a0[8], a1[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) a0[s] = a1[s] = 0.f;
+#pragma unroll 4
   for (int c = c0; c < c1; ++c) {
     const float2 wf = __half22float2(w2[(int64_t)c * 64]);
-    a0 = fmaf(x[c], wf.x, a0);
-    a1 = fmaf(x[c], wf.y, a1);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const float xv = xs[s * kdim + c];
+      a0[s] = fmaf(xv, wf.x, a0[s]);
+      a1[s] = fmaf(xv, wf.y, a1[s]);
+    }
   }
-  acc4[qtr][2 * j2] = a0;
-  acc4[qtr][2 * j2 + 1] = a1;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    red[qtr][s][2 * j2] = a0[s];
+    red[qtr][s][2 * j2 + 1] = a1[s];
+  }
   __syncthreads();
-  if (tid < 128)
-    out[((int64_t)b * n_q + h) * kHeadDim + tid] = acc4[0][tid] + acc4[1][tid] + acc4[2][tid] + acc4[3][tid];
+  for (int i = tid; i < nb * 128; i += 256) {
+    const int s = i >> 7, j = i & 127;
+    out[((int64_t)(b0 + s) * n_q + h) * kHeadDim + j] =
+        red[0][s][j] + red[1][s][j] + red[2][s][j] + red[3][s][j];
+  }
 }
 
 // Arranged weights. wk_out: fp16 [ceil(n_kv/4)*512][kdim], row kvh*128 + j =
@@ -985,7 +1026,9 @@ int xq_debug_role_profile(uint64_t* out, int32_t reset) {
 
 int64_t xq_absorbed_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q_heads,
                                     int64_t kdim) {
-  return (int64_t)n_seqs * n_tiles_for(max_len) * n_q_heads * (kdim + 2) * (int64_t)sizeof(float);
+  // O partials + (m, l) per tile, then the merged x [n_seqs][n_q][kdim]
+  return (int64_t)n_seqs * n_q_heads *
+         ((int64_t)n_tiles_for(max_len) * (kdim + 2) + kdim) * (int64_t)sizeof(float);
 }
 
 int xq_arrange_weights_absorbed(const void* w_k, const void* w_v, int32_t w_dtype, int64_t kdim,
@@ -1109,20 +1152,24 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
     }
   }
   if (status != XQ_OK) return status;
-  const size_t vsmem = ((size_t)kdim + p.n_tiles) * sizeof(float);
-  if (vsmem > 48 * 1024) {
-    static size_t vconf = 0;
-    if (vconf < vsmem) {
-      if (cudaFuncSetAttribute(k_absorb_vproj, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)vsmem) != cudaSuccess)
-        return check_launch("cudaFuncSetAttribute(vproj)");
-      vconf = vsmem;
+  float* x_attn = reinterpret_cast<float*>(p.part_ml + (int64_t)n_seqs * p.n_tiles * n_q);
+  k_absorb_combine<<<dim3(n_seqs * n_q, static_cast<unsigned>((kdim + 511) / 512)), 128,
+                     p.n_tiles * sizeof(float), st>>>(p.part_o, p.part_ml, seq_lens, p.n_tiles,
+                                                      n_q, p.kdim, x_attn);
+  if ((status = check_launch("k_absorb_combine")) != XQ_OK) return status;
+  const size_t psmem = 8 * (size_t)kdim * sizeof(float);
+  {
+    static size_t pconf = 0;
+    if (psmem > 48 * 1024 && pconf < psmem) {
+      if (cudaFuncSetAttribute(k_absorb_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)psmem) != cudaSuccess)
+        return check_launch("cudaFuncSetAttribute(project)");
+      pconf = psmem;
     }
   }
-  k_absorb_vproj<<<dim3(n_q, n_seqs), 256, vsmem, st>>>(p.part_o, p.part_ml, seq_lens, p.n_tiles, n_q,
-                                                         group, p.kdim,
-                                                         static_cast<const __half*>(wv_arranged), out);
-  return check_launch("k_absorb_vproj");
+  k_absorb_project<<<dim3(n_q, (n_seqs + 7) / 8), 256, psmem, st>>>(
+      x_attn, n_seqs, n_q, group, p.kdim, static_cast<const __half*>(wv_arranged), out);
+  return check_launch("k_absorb_project");
 }
 
 }  // extern "C"
