@@ -465,7 +465,7 @@ def run_xquant(args, cfg):
         "speedup_vs_fp16_kv": (value / fp16["value"]) if fp16 and fp16.get("value") else None,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("k_decode_absorbed (+k_absorb_vproj)" if absorbed
+                     "kernel": ("k_decode_absorbed (+k_absorb_combine, k_absorb_project)" if absorbed
                                 else "k_decode_attend (+k_combine)"),
                      "flops_per_launch": flops_launch, "launch_us": per_launch * 1e6,
                      "flops_note": ("algorithmic FLOPs of the V-absorbed path (sysmodel.absorbed_flops); "

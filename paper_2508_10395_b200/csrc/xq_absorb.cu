@@ -665,12 +665,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long pt_v = clock64();
 #endif
         tc_fence_after();
-        // each [n_q x 128-channel] block is staged in shared memory (two
-        // buffers: the score region and the q/P region, both free here) and
-        // written by one TMA bulk store
+        // each [n_q x 128-channel] block is staged in shared memory and written
+        // by one TMA bulk store. Staging buffers: the score region, plus the
+        // q/P region when this is the tile's only V-side accumulator use (with
+        // more uses, later uses' MMAs still read P while this one drains).
+        const bool two_bufs = nuse == 1;
         for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
-          const uint32_t stg = (blk & 1) ? q_a : sc_a;
-          if (et == 0) tma_store_wait_read<1>();  // the store that last read `stg` is done
+          const uint32_t stg = (two_bufs && (blk & 1)) ? q_a : sc_a;
+          if (et == 0) {  // the store that last read `stg` is done
+            if (two_bufs) tma_store_wait_read<1>();
+            else tma_store_wait_read<0>();
+          }
           named_bar_sync(1, 128);
           for (int c16 = 0; c16 < p.nb / 16; ++c16) {
             float v[16];
@@ -778,29 +783,31 @@ __global__ void __launch_bounds__(128) k_absorb_combine(const float* __restrict_
 }
 
 // out[b][h][:] = x[b][h][:] @ W_v[:, kv(h)], wv fp16 [n_kv][kdim][128] (rows in the
-// storage channel order of x). Grid (n_q, ceil(n_seqs/8)): each CTA streams its
-// head's W_v slice once for up to 8 sequences (x staged in shared memory).
+// storage channel order of x). Grid (n_q, 4 column blocks of 32, ceil(n_seqs/8)):
+// a CTA streams its [kdim x 32] slice of W_v once for up to 8 sequences (x
+// staged in shared memory); 16 threads per row of the slice, 16 channel slices.
 __global__ void __launch_bounds__(256) k_absorb_project(const float* __restrict__ x,
                                                         int n_seqs, int n_q, int group, int kdim,
                                                         const __half* __restrict__ wv,
                                                         float* __restrict__ out) {
   extern __shared__ float xs[];  // [8][kdim]
-  __shared__ float red[4][8][128];
-  const int h = blockIdx.x, b0 = blockIdx.y * 8, tid = threadIdx.x;
+  __shared__ float red[16][8][33];
+  const int h = blockIdx.x, cb = blockIdx.y, b0 = blockIdx.z * 8, tid = threadIdx.x;
   const int nb = n_seqs - b0 < 8 ? n_seqs - b0 : 8;
   for (int i = tid; i < 8 * kdim; i += 256) {
     const int s = i / kdim, c = i % kdim;
     xs[i] = s < nb ? x[((int64_t)(b0 + s) * n_q + h) * kdim + c] : 0.f;
   }
   __syncthreads();
-  const int j2 = tid & 63, qtr = tid >> 6;
-  const __half2* w2 = reinterpret_cast<const __half2*>(wv + (int64_t)(h / group) * kdim * 128) + j2;
-  const int c0 = qtr * (kdim / 4), c1 = c0 + kdim / 4;
+  const int j2 = tid & 15, sl = tid >> 4;  // column pair of the block, channel slice
+  const __half2* w2 =
+      reinterpret_cast<const __half2*>(wv + (int64_t)(h / group) * kdim * 128 + cb * 32) + j2;
+  const int per = kdim / 16, c0 = sl * per;
   float a0[8], a1[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) a0[s] = a1[s] = 0.f;
 #pragma unroll 4
-  for (int c = c0; c < c1; ++c) {
+  for (int c = c0; c < c0 + per; ++c) {
     const float2 wf = __half22float2(w2[(int64_t)c * 64]);
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -811,14 +818,16 @@ __global__ void __launch_bounds__(256) k_absorb_project(const float* __restrict_
   }
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    red[qtr][s][2 * j2] = a0[s];
-    red[qtr][s][2 * j2 + 1] = a1[s];
+    red[sl][s][2 * j2] = a0[s];
+    red[sl][s][2 * j2 + 1] = a1[s];
   }
   __syncthreads();
-  for (int i = tid; i < nb * 128; i += 256) {
-    const int s = i >> 7, j = i & 127;
-    out[((int64_t)(b0 + s) * n_q + h) * kHeadDim + j] =
-        red[0][s][j] + red[1][s][j] + red[2][s][j] + red[3][s][j];
+  for (int i = tid; i < nb * 32; i += 256) {
+    const int s = i >> 5, j = i & 31;
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v += red[k][s][j];
+    out[((int64_t)(b0 + s) * n_q + h) * kHeadDim + cb * 32 + j] = v;
   }
 }
 
@@ -1159,15 +1168,15 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
   if ((status = check_launch("k_absorb_combine")) != XQ_OK) return status;
   const size_t psmem = 8 * (size_t)kdim * sizeof(float);
   {
-    static size_t pconf = 0;
-    if (psmem > 48 * 1024 && pconf < psmem) {
+    static size_t pconf = 0;  // (dynamic + the kernel's 17 KB static reduction buffer)
+    if (pconf < psmem) {
       if (cudaFuncSetAttribute(k_absorb_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)psmem) != cudaSuccess)
         return check_launch("cudaFuncSetAttribute(project)");
       pconf = psmem;
     }
   }
-  k_absorb_project<<<dim3(n_q, (n_seqs + 7) / 8), 256, psmem, st>>>(
+  k_absorb_project<<<dim3(n_q, 4, (n_seqs + 7) / 8), 256, psmem, st>>>(
       x_attn, n_seqs, n_q, group, p.kdim, static_cast<const __half*>(wv_arranged), out);
   return check_launch("k_absorb_project");
 }

@@ -83,6 +83,11 @@ def _svd_factors(w: torch.Tensor):
     return u.to(torch.bfloat16), fused.to(torch.bfloat16)
 
 
+def cache_kdim(cache) -> int:
+    """Channel count of the fused kernel's A operand (d, or the GQA latent rank)."""
+    return cache.latent if cache.variant == "xq-gqa" else cache.d
+
+
 class Decoder:
     """Per-layer caches of one model shape for ``n_slots`` sequences."""
 
@@ -192,13 +197,15 @@ class Decoder:
     def _launches_per_layer(self, cache) -> int:
         if self.variant == "fp16":
             return 3  # kv_append, kv_decode, combine
+        # fused decode + merge: absorbed = fused, combine, project; unabsorbed = fused, combine
+        attend = 3 if getattr(cache, "absorb", False) and cache_kdim(cache) % 256 == 0 else 2
         if self.variant == "xq-gqa":
-            return 3  # v-latent quantize, decode, combine (+ a flush every 128 steps)
+            return 1 + attend  # v-latent quantize (+ a K-latent flush every 128 steps)
         if self.variant == "xq-cl-mha":
             base = cache.layer_index < self.policy.base_layers
             seed = cache.layer_index == self.policy.base_layers - 1
-            return 3 + (0 if base and not seed else 1)
-        return 3  # quantize, decode, combine
+            return 1 + attend + (0 if base and not seed else 1)
+        return 1 + attend  # quantize
 
     # ------------------------------------------------------------- accounting
     def memory_bytes(self) -> dict:
