@@ -384,6 +384,9 @@ def run_xquant(args, cfg):
     t_e2e = _max_over_ranks(world, e0.elapsed_time(e1) / 1e3)
     e2e_value = tokens_per_step * args.steps / t_e2e
     mem = dec.memory_bytes()
+    last = dec.caches[-1]
+    dec_absorbed = (cfg["variant"] != "fp16"
+                    and last._use_absorbed(D.cache_kdim(last), int(last.n_tokens.max())))
     bits_per_layer = dec.policy.bits
     del dec
     for w in weights:
@@ -416,7 +419,7 @@ def run_xquant(args, cfg):
         return
     # ---------------- roofline of the dominant kernel ----------------
     peaks, peak_src = _peaks()
-    absorbed = os.environ.get("XQ_ABSORB", "1") != "0"
+    absorbed = dec_absorbed
     flops_unabsorbed = B * (S.remat_flops(cfg["variant"], l_avg, d, shape.kv_group)
                             + S.attention_flops(l_avg, shape.n_heads)) / (world if heads else 1)
     if absorbed:

@@ -308,8 +308,10 @@ class CacheBackend:
         self.device = torch.device(device)
         self.n_tokens = np.zeros(n_slots, dtype=np.int64)
         self.lens_dev = torch.zeros(n_slots, dtype=torch.int32, device=self.device)
-        # V absorption (xq_absorb.cu): exact reassociation p.(x W_v) = (p.x) W_v
-        self.absorb = os.environ.get("XQ_ABSORB", "1") != "0"
+        # V absorption (xq_absorb.cu): exact reassociation p.(x W_v) = (p.x) W_v.
+        # XQ_ABSORB: unset/"1" -> "auto" (by workload size), "force" -> True, "0" -> False
+        env = os.environ.get("XQ_ABSORB", "1")
+        self.absorb = False if env == "0" else (True if env == "force" else "auto")
 
     # -- interface ---------------------------------------------------------
     def prefill(self, x, weights: LayerWeights, acc: Accumulator | None = None, slot=None):
@@ -406,7 +408,7 @@ class CacheBackend:
         W_k, W_v) names the projection pair and the A operands that feed it."""
         key, mk, bk, mv, bv, wk, wv = w_spec
         rope = rope_table_t(max_len, self.device)
-        if self.absorb and kdim % 256 == 0:
+        if self._use_absorbed(kdim, max_len):
             wk_arr, wv_arr = weights.arranged_absorbed(key, mk, bk, mv, bv, wk, wv)
             nbytes = N.lib.xq_absorbed_workspace_bytes(self.n_slots, max_len, self.n_kv * group, kdim)
             ws = _scratch(self.device, nbytes)
@@ -426,6 +428,18 @@ class CacheBackend:
                N.ptr(w_arr), self.n_kv, group, N.ptr(q), N.ptr(rope), rope.shape[1] // 2,
                1.0 / math.sqrt(HEAD_DIM), tpc, N.ptr(ws), nbytes, N.ptr(out),
                N.stream_of(self.device))
+
+    def _use_absorbed(self, kdim: int, max_len: int) -> bool:
+        if kdim % 256 or self.absorb is False:
+            return False
+        return self.absorb is True or self._absorb_pays(max_len)
+
+    def _absorb_pays(self, max_len: int) -> bool:
+        """The absorbed kernel's work unit is a whole 256-token tile with all heads;
+        with fewer units than half the CTA pairs (e.g. one short sequence) the
+        unabsorbed kernel, which also splits by KV head, keeps more SMs busy."""
+        units = self.n_slots * max(1, -(-max_len // 256))
+        return units >= 37
 
     def _remat_f32(self, ak_mode, ak_src, ak_params, ak_resid, ak_nfl, ak_bits, ak_rb, av_mode,
                    av_src, av_params, av_bits, av_rb, kdim, wk, wv, slot, n):

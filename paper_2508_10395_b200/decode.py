@@ -198,7 +198,8 @@ class Decoder:
         if self.variant == "fp16":
             return 3  # kv_append, kv_decode, combine
         # fused decode + merge: absorbed = fused, combine, project; unabsorbed = fused, combine
-        attend = 3 if getattr(cache, "absorb", False) and cache_kdim(cache) % 256 == 0 else 2
+        absorbed = cache._use_absorbed(cache_kdim(cache), int(cache.n_tokens.max()))
+        attend = 3 if absorbed else 2
         if self.variant == "xq-gqa":
             return 1 + attend  # v-latent quantize (+ a K-latent flush every 128 steps)
         if self.variant == "xq-cl-mha":
