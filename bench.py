@@ -47,6 +47,10 @@ CONFIGS = {
                parallel="heads"),
     "c1": dict(workload="XQuant 4-bit, one Llama-2-7B layer, batch 1, 2K context",
                shape="llama2-7b", variant="xq-mha", bits=4, batch=1, ctx=2048, layers=1),
+    # C5 long-context sweep (8K-128K, batch 1-64 over 8 GPUs): one point per run, the
+    # per-GPU shard of a batch-sharded deployment; tools/sweep_c5.py drives --ctx/--batch
+    "c5": dict(workload="XQuant-CL 3-bit, Llama-2-13B shape (40 layers), batch 8 per GPU, 32K context",
+               shape="llama2-13b", variant="xq-cl-mha", bits=3, batch=8, ctx=32768),
 }
 
 
@@ -503,8 +507,15 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ctx", type=int, default=None, help="override the config's context")
+    ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.ctx or args.batch:
+        cfg["ctx"] = args.ctx or cfg["ctx"]
+        cfg["batch"] = args.batch or cfg["batch"]
+        cfg["workload"] = (cfg["workload"].split(", batch")[0] +
+                           f", batch {cfg['batch']} per GPU, {cfg['ctx'] // 1024}K context")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
