@@ -448,6 +448,64 @@ class XqClMhaStack:
         return accs, kvs
 
 
+class XqClGqaStack:
+    """DeltaLatentCacheGQA "xq-cl-gqa" over a layer stack (cache.py:538-604).
+
+    Every layer caches a per-channel (buffered) latent in the shared K|V
+    subspace U_kv of svd([W_k | W_v]) (model.py:135-142). Base layers cache
+    x @ U (cache.py:562-569); layer base-1 seeds the d-wide accumulator with
+    reconstruct() @ U^T (cache.py:571-572 via _DeltaBackend, :463-467). A
+    delta layer caches (x - acc[pos]) @ U (cache.py:574-586) and then adds
+    reconstruct() @ U^T to the accumulator (cache.py:588-589). Remat: base
+    kv = reconstruct() @ fused (cache.py:591-593); delta kv = (acc @ U) @ fused
+    (cache.py:595-598); K = RoPE(kv[:, :kvw]), V = kv[:, kvw:] (cache.py:600-604).
+    """
+
+    def __init__(self, bits_per_layer, base_layers, head_dim, group_size=128):
+        self.bits = list(bits_per_layer)
+        self.base = base_layers
+        self.hd = head_dim
+        self.g = group_size
+        self.streams = [None] * len(self.bits)
+        self.n_tokens = 0
+
+    def _stream(self, i, width):
+        if self.streams[i] is None:
+            self.streams[i] = Stream(self.bits[i], PER_CHANNEL, width, self.g, buffered=True)
+        return self.streams[i]
+
+    def step(self, xs, subspaces):
+        """Append rows ``xs[i]`` ([n_new, d]) to every layer in order.
+
+        ``subspaces[i]`` = (u, fused) of layer i (u: d x r, fused: r x 2*kvw).
+        Returns per-layer (latent rows quantized by this call, K, V, acc)."""
+        acc = None
+        out = []
+        for i, x in enumerate(xs):
+            x = np.atleast_2d(np.asarray(x, np.float64))
+            u, fused = subspaces[i]
+            st = self._stream(i, u.shape[1])
+            n_new = x.shape[0]
+            if i < self.base:
+                lat = x @ u
+                st.bulk(lat)
+                if i == self.base - 1:
+                    acc = st.reconstruct() @ u.T
+                kv = st.reconstruct() @ fused
+            else:
+                pos = self.n_tokens
+                lat = (x - acc[pos:pos + n_new]) @ u
+                st.bulk(lat)
+                acc = acc + st.reconstruct() @ u.T
+                kv = (acc @ u) @ fused
+            kvw = fused.shape[1] // 2
+            n = kv.shape[0]
+            out.append((lat, apply_rope(kv[:, :kvw], np.arange(n), self.hd), kv[:, kvw:],
+                        None if acc is None else acc.copy()))
+        self.n_tokens += np.atleast_2d(xs[0]).shape[0]
+        return out
+
+
 # ---------------------------------------------------------------------------
 # Performance / footprint model (sysmodel.py:85-196) -- metric definitions
 # ---------------------------------------------------------------------------

@@ -107,7 +107,7 @@ struct Params {
   float* part_o;       // [n_seqs][n_tiles][n_q][kdim]
   float2* part_ml;     // [n_seqs][n_tiles][n_q] (m, l), m in the log2 domain
   uint64_t w_hint;
-  uint32_t off_p, off_codes, off_q, off_sc, off_x, off_rope, off_bar;
+  uint32_t off_p, off_codes, off_q, off_sc, off_rope, off_bar;
 };
 
 // work unit u -> (sequence, tile); false when the tile is past the sequence end
@@ -137,8 +137,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sP = smem + p.off_p;
   uint8_t* sC = smem + p.off_codes;
   float* q_s = reinterpret_cast<float*>(smem + p.off_q);    // [n_q][128]
-  float* sc_s = reinterpret_cast<float*>(smem + p.off_sc);  // [n_q][128 rows]
-  float* x_s = reinterpret_cast<float*>(smem + p.off_x);    // [nbh][128 rows] (peer's scores)
+  // [nb][128 rows]: scores of this CTA's tokens; after the exchange the rows of
+  // the peer's heads hold the peer's tokens' scores for this CTA's heads
+  float* sc_s = reinterpret_cast<float*>(smem + p.off_sc);
   // RoPE of row r = 16*r1 + r0 of the tile: angle (t0 + 16*r1 + r0)*theta_j
   // = base[r1][j] + off[j][r0], both from the float64-formed table
   float2* rope_off = reinterpret_cast<float2*>(smem + p.off_rope);  // [64 j][16 r0]
@@ -151,7 +152,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* pready = tempty + 2;
   uint64_t* xfull = pready + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
+  uint64_t* xread = xfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xread + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -188,7 +190,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], 8);
     }
     mbar_init(pready, 8);   // leader's: 4 epilogue warps per CTA
-    mbar_init(xfull, 128);  // the peer's 128 epilogue threads
+    mbar_init(xfull, 128);  // the peer's 128 epilogue threads (their scores landed here)
+    mbar_init(xread, 128);  // the peer's 128 epilogue threads (they read out their landing rows)
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -457,12 +460,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tlane = static_cast<uint32_t>(ew * 32) << 16;
     const int nbh = p.nbh;
     const uint32_t peer = rank ^ 1u;
-    const uint32_t x_peer = mapa_shared(smem_u32(x_s), peer);
+    const uint32_t sc_peer = mapa_shared(smem_u32(sc_s), peer);
     const uint32_t xfull_peer = mapa_shared(smem_u32(xfull), peer);
+    const uint32_t xread_peer = mapa_shared(smem_u32(xread), peer);
     const uint32_t sP_a = smem_u32(sP);
     // 32-bit shared addresses: explicit ld/st.shared (a generic pointer into
     // dynamic shared memory compiles to generic LD/ST)
-    const uint32_t q_a = smem_u32(q_s), sc_a = smem_u32(sc_s), x_a = smem_u32(x_s);
+    const uint32_t q_a = smem_u32(q_s), sc_a = smem_u32(sc_s);
+    const uint32_t land_a = sc_a + 4u * (peer * nbh) * kTileM;  // rows of the peer's heads
     const uint32_t ro_a = smem_u32(rope_off), rb_a = smem_u32(rope_base);
     // offsets table: cos/sin(r0*theta_j), r0 < 16 (table positions 0..15)
     for (int i = et; i < 64 * 16; i += 128)
@@ -590,13 +595,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #ifdef XQ_ROLE_PROFILE
       const long long pt_x = clock64();
 #endif
-      for (int hl = 0; hl < nbh; ++hl) {
-        const int h = static_cast<int>(peer) * nbh + hl;
-        st_cluster_f32(x_peer + 4u * (hl * kTileM + row),
-                       h < p.n_q ? lds_f32(sc_a + 4u * (h * kTileM + row)) : -INFINITY);
+      // Each CTA's rows of the peer's heads are read out to registers, then
+      // receive the peer's tokens' scores for this CTA's heads (no extra buffer).
+      {
+        float outv[kMaxHeads / 2];
+#pragma unroll
+        for (int hl = 0; hl < kMaxHeads / 2; ++hl) {
+          const int h = static_cast<int>(peer) * nbh + hl;
+          outv[hl] = (hl < nbh && h < p.n_q) ? lds_f32(sc_a + 4u * (h * kTileM + row)) : -INFINITY;
+        }
+        mbar_arrive_remote_release(xread_peer);        // my landing rows may be overwritten
+        XQ_PROF(9, mbar_wait_cluster(xread, ti & 1));  // the peer's landing rows are free
+#pragma unroll
+        for (int hl = 0; hl < kMaxHeads / 2; ++hl)
+          if (hl < nbh)  // into the peer's landing row of my head hl
+            st_cluster_f32(sc_peer + 4u * ((static_cast<int>(rank) * nbh + hl) * kTileM + row),
+                           outv[hl]);
+        mbar_arrive_remote_release(xfull_peer);
+        XQ_PROF(9, mbar_wait_cluster(xfull, ti & 1));
       }
-      mbar_arrive_remote_release(xfull_peer);
-      XQ_PROF(9, mbar_wait_cluster(xfull, ti & 1));
       // ---- softmax over the 256 tokens of the tile for this CTA's heads -> P
       named_bar_sync(1, 128);  // every epilogue warp is done with q_s (P overwrites it)
       {
@@ -605,7 +622,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int hl = et >> 3; hl < nbh; hl += 16) {
           const int h = static_cast<int>(rank) * nbh + hl;
           const uint32_t src = ((half == static_cast<int>(rank)) ? (sc_a + 4u * h * kTileM)
-                                                                 : (x_a + 4u * hl * kTileM)) +
+                                                                 : (land_a + 4u * hl * kTileM)) +
                                4u * (seg & 3) * 32;
           float s[32];
 #pragma unroll
@@ -956,10 +973,9 @@ int plan_smem(Params& p, size_t& total) {
   // V-side MMAs that read P have completed
   const uint32_t qp = ((512u * (p.n_q > p.nbh ? p.n_q : p.nbh)) + 1023u) / 1024u * 1024u;
   const uint32_t fixed = qp                                 // q / P
-                         + 512u * p.n_q                     // scores
-                         + 512u * p.nbh                     // peer scores
+                         + 512u * p.nb                      // scores (+ the peer's, exchanged)
                          + (64 * 16 + 8 * 64) * 8           // RoPE offset + base tables
-                         + (4 * kMaxStages + 6) * 8 + 16;   // barriers + tmem slot
+                         + (4 * kMaxStages + 7) * 8 + 16;   // barriers + tmem slot
   const uint32_t budget = 227u * 1024u - 1024u;
   using CF = Cfg<GROUP>;
   const int stages = CF::kStages;
@@ -974,8 +990,7 @@ int plan_smem(Params& p, size_t& total) {
   p.off_p = p.off_q;
   p.off_codes = p.off_q + qp;
   p.off_sc = p.off_codes + cstages * cst;
-  p.off_x = p.off_sc + 512u * p.n_q;
-  p.off_rope = p.off_x + 512u * p.nbh;
+  p.off_rope = p.off_sc + 512u * p.nb;
   p.off_bar = p.off_rope + (64 * 16 + 8 * 64) * 8;
   total = 1024 + need();
   return XQ_OK;

@@ -244,6 +244,57 @@ def main():
         be[f"cl_codes{i}"] = states[i].stream.q.codes
         be[f"cl_scales{i}"] = states[i].stream.q.scales
         be[f"cl_zps{i}"] = states[i].stream.q.zero_points
+
+    # xq-cl-gqa: 5 layers (base 3, layers 0-2 at 4-bit, 3-bit deltas), d=1024, H=8,
+    # 2 KV heads (kv_group 4, kvw 256), shared K|V subspace r = 2*kvw = 512. U is an
+    # fp32-representable orthonormal basis, fused = U^T [W_k | W_v] with bf16 W
+    d, H, g, n_layers = 1024, 8, 4, 5
+    kvw = d // g
+    n_pre, n_dec = 250, 8  # decode crosses the 256-token per-channel flush
+    pol = LayerPolicy.for_bits(3, n_layers)
+    base = rng.normal(size=(n_pre + n_dec, d))
+    cx, cxb = [], []
+    for i in range(n_layers):
+        base = base + 0.03 * rng.normal(size=base.shape)
+        b_, f_ = bf16(base)
+        cxb.append(b_)
+        cx.append(f_)
+    us, fuseds, lws = [], [], []
+    for i in range(n_layers):
+        u = np.linalg.qr(rng.normal(size=(d, 2 * kvw)))[0].astype(np.float32).astype(np.float64)
+        fb, fused = bf16(rng.normal(size=(2 * kvw, 2 * kvw)) / np.sqrt(2 * kvw))
+        us.append(u.astype(np.float32))
+        fuseds.append(fb)
+        sub = SvdFactors(u=u, sigma=np.ones(2 * kvw), b_t=fused, fused=fused)
+        w = u @ fused
+        lws.append(dummy_lw(d, kvw, w[:, :kvw], w[:, kvw:], svd_kv=sub))
+    qb, q = bf16(rng.normal(size=(n_layers, d)))
+    states = [make_cache("xq-cl-gqa", i, pol, 128, group_size=128) for i in range(n_layers)]
+    acc = Accumulator()
+    for i in range(n_layers):
+        states[i].prefill(cx[i][:n_pre], lws[i], acc)
+    for t in range(n_dec):
+        acc = Accumulator()
+        ks, vs, attn = [], [], []
+        for i in range(n_layers):
+            states[i].decode_append(cx[i][n_pre + t], lws[i], acc)
+            k, v = states[i].rematerialize(lws[i], np.arange(n_pre + t + 1), acc)
+            ks.append(k)
+            vs.append(v)
+            qr = apply_rope(q[i:i + 1], np.array([n_pre + t]), 128)
+            attn.append(_attention(qr, k, v, H, g)[0])
+    be.update({
+        "clg_x": np.stack(cxb), "clg_u": np.stack(us), "clg_fused": np.stack(fuseds),
+        "clg_q": qb, "clg_bits": np.array(pol.bits), "clg_base": np.array(pol.base_layers),
+        "clg_k": np.stack([ks[2], ks[-1]]).astype(np.float32),
+        "clg_v": np.stack([vs[2], vs[-1]]).astype(np.float32), "clg_attn": np.stack(attn),
+        "clg_acc_last": acc.x_hat.astype(np.float32),
+    })
+    for i in range(n_layers):
+        be[f"clg_codes{i}"] = states[i].stream.q.codes
+        be[f"clg_scales{i}"] = states[i].stream.q.scales
+        be[f"clg_zps{i}"] = states[i].stream.q.zero_points
+        be[f"clg_buf{i}"] = np.asarray(states[i].stream.buf.tokens, np.float64)
     np.savez_compressed(os.path.join(HERE, "backends.npz"), **be)
 
     for f in ("quant", "pack", "rope", "backends"):
