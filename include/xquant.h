@@ -117,6 +117,12 @@ int xq_quantize_blocks_per_channel(const float* blocks, int64_t n_blocks, int64_
                                    int32_t bits, int32_t group_size, const int64_t* dst_row0,
                                    uint8_t* codes, int64_t row_bytes, void* params,
                                    int32_t* nonfinite_flag, void* stream);
+/* The same on float64 blocks (the xq-cl-gqa latents, formed in float64 like
+ * the reference's so the per-channel codes match it, cache.py:574-586). */
+int xq_quantize_blocks_per_channel_f64(const double* blocks, int64_t n_blocks, int64_t cols,
+                                       int32_t bits, int32_t group_size, const int64_t* dst_row0,
+                                       uint8_t* codes, int64_t row_bytes, void* params,
+                                       int32_t* nonfinite_flag, void* stream);
 
 /* Dequantize arena rows [row0, row0+n_rows) to float32 [n_rows, cols]
  * (quant.dequantize, quant.py:137-153). axis 0 per-token, 1 per-channel. */

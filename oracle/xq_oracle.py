@@ -245,7 +245,12 @@ class Stream:
     per-token payloads of xq-mha / xq-cl-mha / xq-gqa-V are unbuffered.
     """
 
-    def __init__(self, bits: int, axis: int, width: int, group_size: int, buffered: bool):
+    def __init__(self, bits: int, axis: int, width: int, group_size: int, buffered: bool,
+                 params_f16: bool = False):
+        """``params_f16``: dequantize with the scale / zero point rounded to fp16,
+        the storage format of the B200 arena (the reference charges 16+16 bits per
+        group, quant.py:44-45, but keeps float64 in memory)."""
+        self.params_f16 = params_f16
         self.bits, self.axis, self.width, self.g = bits, axis, width, group_size
         self.buffered = buffered or axis == PER_CHANNEL  # cache.py:173
         self.codes = np.zeros((0, width), np.uint8) if bits != 16 else np.zeros((0, width))
@@ -287,7 +292,10 @@ class Stream:
             self.buf = np.zeros((0, self.width))
 
     def reconstruct(self):  # cache.py:223-230
-        flushed = dequantize(self.codes, self.scales, self.zps, self.bits, self.axis, self.g)
+        sc, zp = self.scales, self.zps
+        if self.params_f16 and self.bits != 16:
+            sc, zp = sc.astype(np.float16).astype(np.float64), zp.astype(np.float16).astype(np.float64)
+        flushed = dequantize(self.codes, sc, zp, self.bits, self.axis, self.g)
         if len(self.buf):
             return np.vstack([flushed, self.buf])
         return flushed
@@ -461,17 +469,19 @@ class XqClGqaStack:
     (cache.py:595-598); K = RoPE(kv[:, :kvw]), V = kv[:, kvw:] (cache.py:600-604).
     """
 
-    def __init__(self, bits_per_layer, base_layers, head_dim, group_size=128):
+    def __init__(self, bits_per_layer, base_layers, head_dim, group_size=128, params_f16=False):
         self.bits = list(bits_per_layer)
         self.base = base_layers
         self.hd = head_dim
         self.g = group_size
+        self.params_f16 = params_f16
         self.streams = [None] * len(self.bits)
         self.n_tokens = 0
 
     def _stream(self, i, width):
         if self.streams[i] is None:
-            self.streams[i] = Stream(self.bits[i], PER_CHANNEL, width, self.g, buffered=True)
+            self.streams[i] = Stream(self.bits[i], PER_CHANNEL, width, self.g, buffered=True,
+                                     params_f16=self.params_f16)
         return self.streams[i]
 
     def step(self, xs, subspaces):

@@ -35,7 +35,7 @@ from .errors import ConfigError, DataError, ShapeError, UsageError
 
 VARIANTS = ("fp16", "kvq", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")  # cache.py:41
 CL_VARIANTS = ("xq-cl-mha", "xq-cl-gqa")
-SUPPORTED = ("fp16", "xq-mha", "xq-gqa", "xq-cl-mha")
+SUPPORTED = ("fp16", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")
 DEFAULT_GROUP_SIZE = 128
 HEAD_DIM = 128
 ROPE_THETA = 10000.0
@@ -98,6 +98,8 @@ class LayerWeights:
     u_v: torch.Tensor | None = None
     fused_k: torch.Tensor | None = None
     fused_v: torch.Tensor | None = None
+    u_kv: torch.Tensor | None = None      # xq-cl-gqa: shared K|V subspace, d x 2*kv_width
+    fused_kv: torch.Tensor | None = None  # xq-cl-gqa: diag(sigma) B^T, 2*kv_width x 2*kv_width
     _cache: dict = field(default_factory=dict, repr=False)
 
     def arranged(self, key, a_mode_k, bits_k, a_mode_v, bits_v, wk, wv) -> torch.Tensor:
@@ -210,7 +212,10 @@ class PackedStream:
     the rows of the current incomplete group (cache.py:203-208, 218-221).
     """
 
-    def __init__(self, bits, axis, width, group_size, n_slots, max_len, device):
+    def __init__(self, bits, axis, width, group_size, n_slots, max_len, device, resid_f64=False):
+        """``resid_f64``: per-channel only -- keep the residual rows in float64 as
+        well (quantized from float64, like the reference); ``resid`` is then
+        their float32 mirror read by the fused kernel."""
         if bits not in (2, 3, 4, 8):
             raise ConfigError(f"packed stream bits must be 2/3/4/8, got {bits}")
         if axis == CHANNEL and max_len % group_size:
@@ -227,6 +232,8 @@ class PackedStream:
             self.params = torch.zeros((n_slots * max_len // group_size, 2, width),
                                       dtype=torch.float16, device=device)
             self.resid = torch.zeros((n_slots, group_size, width), dtype=torch.float32, device=device)
+            self.resid64 = (torch.zeros((n_slots, group_size, width), dtype=torch.float64, device=device)
+                            if resid_f64 else None)
             self.n_flushed = np.zeros(n_slots, dtype=np.int64)
             self.nflushed_dev = torch.zeros(n_slots, dtype=torch.int32, device=device)
         self.flag = torch.zeros(1, dtype=torch.int32, device=device)
@@ -235,6 +242,8 @@ class PackedStream:
         out = {"codes": self.codes.numel(), "params": self.params.numel() * 2}
         if self.axis == CHANNEL:
             out["residual"] = self.resid.numel() * 4
+            if self.resid64 is not None:
+                out["residual_f64"] = self.resid64.numel() * 8
         return out
 
     # -- per-token ---------------------------------------------------------
@@ -257,9 +266,54 @@ class PackedStream:
     # -- per-channel -------------------------------------------------------
     def flush_blocks(self, blocks: torch.Tensor, dst_row0: list[int]):
         dst = torch.tensor(dst_row0, dtype=torch.int64, device=blocks.device)
-        N.call("xq_quantize_blocks_per_channel", N.ptr(blocks), len(dst_row0), self.width,
+        fn = ("xq_quantize_blocks_per_channel_f64" if blocks.dtype == torch.float64
+              else "xq_quantize_blocks_per_channel")
+        N.call(fn, N.ptr(blocks), len(dst_row0), self.width,
                self.bits, self.g, N.ptr(dst), N.ptr(self.codes), self.row_bytes,
                N.ptr(self.params), N.ptr(self.flag), N.stream_of(blocks.device))
+
+    def channel_bulk(self, slot: int, lat: torch.Tensor):
+        """Per-channel bulk (cache.py:191-208) into an empty slot: whole G-row
+        groups are quantized, the tail waits in the residual buffer."""
+        g, n = self.g, lat.shape[0]
+        n_full = n // g * g
+        if self.resid64 is not None:
+            lat = lat.double()
+        if n_full:
+            self.flush_blocks(lat[:n_full].contiguous(), [slot * self.L + i for i in range(0, n_full, g)])
+        self.resid[slot, :n - n_full] = lat[n_full:]
+        if self.resid64 is not None:
+            self.resid64[slot, :n - n_full] = lat[n_full:]
+        self.n_flushed[slot] = n_full
+        self.nflushed_dev[slot] = n_full
+
+    def channel_push(self, lat: torch.Tensor, n_tokens: np.ndarray):
+        """Per-channel push of one row per slot (cache.py:210-221); ``n_tokens``
+        counts the rows including this one. Full groups are flushed."""
+        dev = lat.device
+        buf_pos = torch.as_tensor(n_tokens - 1 - self.n_flushed, device=dev)
+        rows = torch.arange(self.n_slots, device=dev)
+        self.resid[rows, buf_pos] = lat.float()
+        if self.resid64 is not None:
+            self.resid64[rows, buf_pos] = lat.double()
+        full = np.nonzero(n_tokens - self.n_flushed >= self.g)[0]
+        if len(full):
+            src = self.resid64 if self.resid64 is not None else self.resid
+            blocks = src[torch.as_tensor(full, device=dev)].contiguous()
+            self.flush_blocks(blocks, [int(s) * self.L + int(self.n_flushed[s]) for s in full])
+            self.n_flushed[full] += self.g
+            self.nflushed_dev.copy_(torch.from_numpy(self.n_flushed.astype(np.int32)))
+
+    def channel_reconstruct(self, slot: int, n: int) -> torch.Tensor:
+        """float32 [n, width]: dequantized flushed rows + residual rows (cache.py:223-230)."""
+        out = torch.empty((n, self.width), dtype=torch.float32, device=self.codes.device)
+        nfl = int(self.n_flushed[slot])
+        if nfl:
+            N.call("xq_dequant_rows", N.ptr(self.codes), self.row_bytes, N.ptr(self.params), CHANNEL,
+                   self.bits, self.g, self.width, slot * self.L, nfl, N.ptr(out),
+                   N.stream_of(out.device))
+        out[nfl:] = self.resid[slot, :n - nfl]
+        return out
 
     def check_finite(self):
         """Raise DataError if any quantized input was NaN/Inf (quant.py:114-115).
@@ -403,12 +457,12 @@ class CacheBackend:
 
     def _fused(self, ak_mode, ak_src, ak_params, ak_resid, ak_nfl, ak_bits, ak_rb, av_mode,
                av_src, av_params, av_bits, av_rb, kdim, w_spec, weights, group, q, lens, max_len,
-               out, tpc):
+               out, tpc, force_absorbed=False):
         """One fused decode launch. ``w_spec`` = (key, a_mode_k, bits_k, a_mode_v, bits_v,
         W_k, W_v) names the projection pair and the A operands that feed it."""
         key, mk, bk, mv, bv, wk, wv = w_spec
         rope = rope_table_t(max_len, self.device)
-        if self._use_absorbed(kdim, max_len):
+        if force_absorbed or self._use_absorbed(kdim, max_len):
             wk_arr, wv_arr = weights.arranged_absorbed(key, mk, bk, mv, bv, wk, wv)
             nbytes = N.lib.xq_absorbed_workspace_bytes(self.n_slots, max_len, self.n_kv * group, kdim)
             ws = _scratch(self.device, nbytes)
@@ -624,28 +678,12 @@ class LatentInputCacheGQA(CacheBackend):
     def _prefill(self, slot, x, weights, acc):
         lat_k, lat_v = self._latents(x, weights)
         self.v_stream.fill_rows(lat_v.contiguous(), slot, 0)
-        ks, g = self.k_stream, self.group_size
-        n = x.shape[0]
-        n_full = n // g * g  # cache.py:203-208
-        if n_full:
-            blocks = lat_k[:n_full].contiguous()
-            ks.flush_blocks(blocks, [slot * self.L + i for i in range(0, n_full, g)])
-        ks.resid[slot, :n - n_full] = lat_k[n_full:]
-        ks.n_flushed[slot] = n_full
-        ks.nflushed_dev[slot] = n_full
+        self.k_stream.channel_bulk(slot, lat_k)  # cache.py:203-208
 
     def _decode(self, x, weights, acc, lens):
         lat_k, lat_v = self._latents(x, weights)
         self.v_stream.append_token_rows(lat_v.contiguous(), lens)
-        ks, g = self.k_stream, self.group_size
-        buf_pos = torch.as_tensor(self.n_tokens - 1 - ks.n_flushed, device=self.device)
-        ks.resid[torch.arange(self.n_slots, device=self.device), buf_pos] = lat_k
-        full = np.nonzero(self.n_tokens - ks.n_flushed >= g)[0]  # cache.py:218-221
-        if len(full):
-            blocks = ks.resid[torch.as_tensor(full, device=self.device)].contiguous()
-            ks.flush_blocks(blocks, [int(s) * self.L + int(ks.n_flushed[s]) for s in full])
-            ks.n_flushed[full] += g
-            ks.nflushed_dev.copy_(torch.from_numpy(ks.n_flushed.astype(np.int32)))
+        self.k_stream.channel_push(lat_k, self.n_tokens)  # cache.py:218-221
 
     def _rematerialize(self, weights, acc, slot, n):
         ks, vs = self.k_stream, self.v_stream
@@ -766,9 +804,146 @@ class DeltaInputCacheMHA(CacheBackend):
         return self.stream.nbytes()
 
 
+class DeltaLatentCacheGQA(CacheBackend):
+    """``xq-cl-gqa`` (cache.py:538-604): cross-layer deltas in the shared latent
+    subspace U_kv of svd([W_k | W_v]) (model.py:135-142), quantized per-channel
+    (buffered); the accumulator is d-wide (cache.py:124-146).
+
+    Base layers cache x @ U; layer base-1 seeds acc = reconstruct() @ U^T.
+    Delta layers cache (x - acc[pos]) @ U and add reconstruct() @ U^T to acc
+    (cache.py:574-589). Remat (cache.py:591-604): base kv = reconstruct() @ fused;
+    delta kv = (acc @ U) @ fused, run here as acc @ (U @ fused) -- the same
+    product reassociated, so the fused kernel reads the fp16 accumulator rows
+    like xq-cl-mha with W' = U @ fused_{k|v} (d x kv_width) precomputed once.
+    The accumulator update is a plain [l x r] @ [r x d] GEMM (cuBLAS).
+    """
+
+    variant = "xq-cl-gqa"
+    needs_accumulator = True
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        if self.policy.base_layers < 1:
+            raise ConfigError("cross-layer variants need at least one base layer")
+        if self.bits == 16:
+            raise ConfigError("xq-cl-gqa on the B200 path needs a quantized width (2/3/4/8)")
+        kv_width = self.d // self.g
+        if 2 * kv_width > self.d:  # model.py:135-142: the shared subspace only when 2*kvw <= d
+            raise ConfigError("xq-cl-gqa needs a shared K/V subspace (2*kv_width <= hidden_dim)")
+        self.rank = 2 * kv_width
+        self.kv_width = kv_width
+        # latents formed and quantized in float64 like the reference's (a base-layer
+        # code flip is a full quantization step, large against later deltas)
+        self.stream = PackedStream(self.bits, CHANNEL, self.rank, self.group_size, self.n_slots,
+                                   self.L, self.device, resid_f64=True)
+
+    @property
+    def is_base(self):
+        return self.layer_index < self.policy.base_layers
+
+    @property
+    def seeds_accumulator(self):
+        return self.layer_index == self.policy.base_layers - 1
+
+    @staticmethod
+    def _u64(weights):
+        key = ("f64", "u_kv")
+        if key not in weights._cache:
+            weights._cache[key] = weights.u_kv.double().contiguous()
+        return weights._cache[key]
+
+    @staticmethod
+    def _sub(weights):
+        if weights.u_kv is None or weights.fused_kv is None:
+            raise ConfigError("xq-cl-gqa needs the shared K/V subspace (u_kv, fused_kv)")
+        return weights.f32("u_kv"), weights.f32("fused_kv")
+
+    def _update_acc(self, acc, weights, slots, seed):
+        u, _ = self._sub(weights)
+        for s in slots:
+            n = int(self.n_tokens[s]) if self.n_tokens[s] else 0
+            if n == 0:
+                continue
+            rec = self.stream.channel_reconstruct(s, n)
+            rows = acc.x_hat[s, :n]
+            if seed:
+                torch.matmul(rec, u.t(), out=rows)  # cache.py:571-572
+            else:
+                rows.addmm_(rec, u.t())  # cache.py:588-589
+            acc.x16[s, :n] = rows.to(torch.float16)
+        acc.seeded = True
+
+    def _prefill(self, slot, x, weights, acc):
+        self._sub(weights)
+        n = x.shape[0]
+        xf = x.double()
+        if not self.is_base:
+            if not acc.seeded:
+                raise UsageError("accumulator used before the base layer seeded it")
+            xf = xf - acc.x_hat[slot, :n].double()  # cache.py:574-577 (delta = x - acc)
+        self.stream.channel_bulk(slot, xf @ self._u64(weights))
+        self.n_tokens[slot] = n  # the accumulator update reads the new length
+        if self.is_base and not self.seeds_accumulator:
+            return
+        self._update_acc(acc, weights, [slot], seed=self.is_base)
+
+    def _decode(self, x, weights, acc, lens):
+        self._sub(weights)
+        xf = x.double()
+        if not self.is_base:
+            if not acc.seeded:
+                raise UsageError("accumulator used before the base layer seeded it")
+            pos = torch.as_tensor(self.n_tokens - 1, device=self.device)
+            xf = xf - acc.x_hat[torch.arange(self.n_slots, device=self.device), pos].double()
+        self.stream.channel_push(xf @ self._u64(weights), self.n_tokens)
+        if self.is_base and not self.seeds_accumulator:
+            return
+        self._update_acc(acc, weights, range(self.n_slots), seed=self.is_base)
+
+    def _w_delta(self, weights):
+        key = ("clgqa_w", id(weights))
+        if key not in weights._cache:
+            u, fused = self._sub(weights)
+            w = u @ fused  # (acc @ U) @ fused == acc @ (U @ fused)
+            weights._cache[key] = (w[:, :self.kv_width].contiguous(), w[:, self.kv_width:].contiguous())
+        return weights._cache[key]
+
+    def _rematerialize(self, weights, acc, slot, n):
+        _, fused = self._sub(weights)
+        if self.is_base:
+            s = self.stream
+            return self._remat_f32(N.A_CODES_CHANNEL, s.codes, s.params, s.resid,
+                                   int(s.n_flushed[slot]), s.bits, s.row_bytes, N.A_SAME, None,
+                                   None, 0, 0, self.rank, fused[:, :self.kv_width].contiguous(),
+                                   fused[:, self.kv_width:].contiguous(), slot, n)
+        wk, wv = self._w_delta(weights)
+        return DeltaInputCacheMHA._remat_acc(self, acc, wk, wv, slot, n)
+
+    def _attend(self, q, weights, acc, lens, max_len, out, tpc):
+        _, fused = self._sub(weights)
+        if self.is_base:
+            s = self.stream
+            fk = weights._cache.setdefault(("clgqa_fk", id(weights)), fused[:, :self.kv_width].contiguous())
+            fv = weights._cache.setdefault(("clgqa_fv", id(weights)), fused[:, self.kv_width:].contiguous())
+            spec = (("clgqa-base", s.bits), N.A_CODES_CHANNEL, s.bits, N.A_SAME, s.bits, fk, fv)
+            self._fused(N.A_CODES_CHANNEL, s.codes, s.params, s.resid, s.nflushed_dev, s.bits,
+                        s.row_bytes, N.A_SAME, None, None, 0, 0, self.rank, spec, weights, self.g,
+                        q, lens, max_len, out, tpc, force_absorbed=True)
+        else:
+            wk, wv = self._w_delta(weights)
+            spec = (("clgqa-delta",), N.A_F16_ROWS, 16, N.A_SAME, 16, wk, wv)
+            self._fused(N.A_F16_ROWS, acc.x16, None, None, None, 16, 0, N.A_SAME, None, None, 0, 0,
+                        self.d, spec, weights, self.g, q, lens, max_len, out, tpc,
+                        force_absorbed=True)
+
+    def memory_bytes(self):
+        return self.stream.nbytes()
+
+
 _BACKENDS = {
     cls.variant: cls
-    for cls in (FullPrecisionCache, InputCacheMHA, LatentInputCacheGQA, DeltaInputCacheMHA)
+    for cls in (FullPrecisionCache, InputCacheMHA, LatentInputCacheGQA, DeltaInputCacheMHA,
+                DeltaLatentCacheGQA)
 }
 
 

@@ -128,7 +128,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmap_o, const Params p) {
   constexpr bool PROD = AK != XQ_A_F16_ROWS;
   static_assert((AK == XQ_A_F16_ROWS) == (AV == XQ_A_F16_ROWS), "fp16 rows feed both sides or neither");
-  static_assert(AV != XQ_A_CODES_CHANNEL, "the V side is per-token");
+  static_assert(AV != XQ_A_CODES_CHANNEL || AK == XQ_A_CODES_CHANNEL,
+                "a per-channel V side shares the K side's stream (xq-cl-gqa base layers)");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -371,8 +372,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const int32_t arow = row_tile + (g & 1) * kTileM;
               mbar_arrive_expect_tx(&cfull[cs], p.v_tx);
               tma_load_2d(st, &tmap_va, &cfull[cs], gv * 16 * BITS, arow, kEvictNormal);
-              tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (gv & ~3), arow,
-                          kEvictNormal);
+              if constexpr (AV == XQ_A_CODES_CHANNEL)  // [scales | zps] of this token group
+                tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], gv * 128, 2 * (arow / kG),
+                            kEvictNormal);
+              else
+                tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (gv & ~3), arow,
+                            kEvictNormal);
             }
           }
           __syncwarp();
@@ -426,6 +431,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if constexpr (AV == XQ_A_CODES_TOKEN)
                 produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
                                         tok < len, tok, b, 1 << 30, 2 * gv + hh, nullptr, nullptr,
+                                        p.kdim);
+              else if constexpr (AV == XQ_A_CODES_CHANNEL)  // same stream as the K side
+                produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
+                                        tok < len, tok, b, nfl, 2 * gv + hh, nullptr, p.k_resid,
                                         p.kdim);
             }
             fence_proxy_async_smem();
@@ -962,7 +971,7 @@ int plan_smem(Params& p, size_t& total) {
   constexpr bool PROD = AK != XQ_A_F16_ROWS;
   const uint32_t k_code = PROD ? 128u * 16u * BITS : 0u;
   const uint32_t k_par = AK == XQ_A_CODES_TOKEN ? 128u * 16u : (AK == XQ_A_CODES_CHANNEL ? 512u : 0u);
-  const uint32_t v_par = PROD ? 128u * 16u : 0u;
+  const uint32_t v_par = AV == XQ_A_CODES_TOKEN ? 128u * 16u : (AV == XQ_A_CODES_CHANNEL ? 512u : 0u);
   p.k_code_bytes = k_code;
   p.k_tx = k_code + k_par;
   p.v_tx = k_code + v_par;
@@ -1106,8 +1115,11 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
     av_params = ak_params;
     av_bits = ak_bits;
     av_row_bytes = ak_row_bytes;
-    XQ_REQUIRE(ak_mode == XQ_A_CODES_TOKEN || ak_mode == XQ_A_F16_ROWS, XQ_ECONFIG,
-               "shared A operand must be CODES_TOKEN or F16_ROWS");
+    XQ_REQUIRE(ak_mode == XQ_A_CODES_TOKEN || ak_mode == XQ_A_F16_ROWS ||
+                   ak_mode == XQ_A_CODES_CHANNEL,
+               XQ_ECONFIG, "shared A operand must be CODES_TOKEN, CODES_CHANNEL or F16_ROWS");
+    XQ_REQUIRE(ak_mode != XQ_A_CODES_CHANNEL || L_max % group_size == 0, XQ_ECONFIG,
+               "per-channel A operand needs L_max % 128 == 0");
   } else {
     XQ_REQUIRE(ak_mode == XQ_A_CODES_CHANNEL && av_mode == XQ_A_CODES_TOKEN, XQ_ECONFIG,
                "split K/V A operands support (CODES_CHANNEL, CODES_TOKEN) only");
@@ -1162,11 +1174,26 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int status;
   if (mha) {
-    XQ_REQUIRE(group == 1, XQ_ECONFIG, "MHA (shared A) needs group 1, got %d", group);
-    if (ak_mode == XQ_A_F16_ROWS)
-      status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 1>(maps, p, st);
-    else
+    // one A stream feeds K and V: X codes (xq-mha), the CL accumulator rows (F16),
+    // or the xq-cl-gqa base-layer latent (per-channel codes, any query group)
+    if (ak_mode == XQ_A_CODES_TOKEN) {
+      XQ_REQUIRE(group == 1, XQ_ECONFIG, "a per-token shared A operand needs group 1, got %d", group);
       status = dispatch_bits<XQ_A_CODES_TOKEN, XQ_A_CODES_TOKEN, 1>(ak_bits, maps, p, st);
+    } else if (ak_mode == XQ_A_F16_ROWS) {
+      switch (group) {
+        case 1: status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 1>(maps, p, st); break;
+        case 2: status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 2>(maps, p, st); break;
+        case 4: status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 4>(maps, p, st); break;
+        default: return fail(XQ_ECONFIG, "unsupported query group %d (1, 2, 4)", group);
+      }
+    } else {
+      switch (group) {
+        case 1: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_CHANNEL, 1>(ak_bits, maps, p, st); break;
+        case 2: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_CHANNEL, 2>(ak_bits, maps, p, st); break;
+        case 4: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_CHANNEL, 4>(ak_bits, maps, p, st); break;
+        default: return fail(XQ_ECONFIG, "unsupported query group %d (1, 2, 4)", group);
+      }
+    }
   } else {
     switch (group) {
       case 1: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 1>(ak_bits, maps, p, st); break;

@@ -172,7 +172,8 @@ __global__ void k_quantize_rows(const void* __restrict__ x, int dt, int64_t x_st
 }
 
 // One CTA per (block, 32-channel slice): per-channel min/max over the G rows.
-__global__ void k_quantize_blocks_per_channel(const float* __restrict__ blocks, int64_t cols,
+template <typename T>
+__global__ void k_quantize_blocks_per_channel(const T* __restrict__ blocks, int64_t cols,
                                               int bits, int G, const int64_t* __restrict__ dst0,
                                               uint8_t* __restrict__ codes, int64_t row_bytes,
                                               __half* __restrict__ params,
@@ -184,7 +185,7 @@ __global__ void k_quantize_blocks_per_channel(const float* __restrict__ blocks, 
   const int b = blockIdx.x, slice = blockIdx.y;
   const int c = threadIdx.x & 31, part = threadIdx.x >> 5;
   const int64_t ch = (int64_t)slice * 32 + c;
-  const float* blk = blocks + (int64_t)b * G * cols;
+  const T* blk = blocks + (int64_t)b * G * cols;
   if (threadIdx.x == 0) s_bad = 0;
   double mn = INFINITY, mx = -INFINITY;
   bool finite = true;
@@ -356,6 +357,28 @@ static int grid_for(int64_t n, int threads) {
 
 using namespace xq;
 
+namespace xq {
+template <typename T>
+static int quantize_blocks_per_channel(const T* blocks, int64_t n_blocks, int64_t cols, int32_t bits,
+                                       int32_t group_size, const int64_t* dst_row0, uint8_t* codes,
+                                       int64_t row_bytes, void* params, int32_t* nonfinite_flag,
+                                       void* stream) {
+  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bits must be one of (2, 3, 4, 8), got %d", bits);
+  XQ_REQUIRE(cols % 32 == 0, XQ_ESHAPE, "per-channel width must be a multiple of 32");
+  XQ_REQUIRE(group_size >= 1 && group_size <= 1024, XQ_ECONFIG, "bad group_size");
+  XQ_REQUIRE(row_bytes == row_bytes_for(cols, bits), XQ_ESHAPE, "bad row_bytes");
+  if (n_blocks == 0) return XQ_OK;
+  dim3 grid(static_cast<unsigned>(n_blocks), static_cast<unsigned>(cols / 32));
+  k_quantize_blocks_per_channel<T><<<grid, 128, static_cast<size_t>(group_size) * 32,
+                                     (cudaStream_t)stream>>>(blocks, cols, bits, group_size,
+                                                             dst_row0, codes, row_bytes,
+                                                             static_cast<__half*>(params),
+                                                             nonfinite_flag);
+  return check_launch("xq_quantize_blocks_per_channel");
+}
+
+}  // namespace xq
+
 extern "C" {
 
 const char* xq_version(void) { return "xquant-b200 0.1 (sm_100a)"; }
@@ -426,18 +449,16 @@ int xq_quantize_blocks_per_channel(const float* blocks, int64_t n_blocks, int64_
                                    int32_t bits, int32_t group_size, const int64_t* dst_row0,
                                    uint8_t* codes, int64_t row_bytes, void* params,
                                    int32_t* nonfinite_flag, void* stream) {
-  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bits must be one of (2, 3, 4, 8), got %d", bits);
-  XQ_REQUIRE(cols % 32 == 0, XQ_ESHAPE, "per-channel width must be a multiple of 32");
-  XQ_REQUIRE(group_size >= 1 && group_size <= 1024, XQ_ECONFIG, "bad group_size");
-  XQ_REQUIRE(row_bytes == row_bytes_for(cols, bits), XQ_ESHAPE, "bad row_bytes");
-  if (n_blocks == 0) return XQ_OK;
-  dim3 grid(static_cast<unsigned>(n_blocks), static_cast<unsigned>(cols / 32));
-  k_quantize_blocks_per_channel<<<grid, 128, static_cast<size_t>(group_size) * 32,
-                                  (cudaStream_t)stream>>>(blocks, cols, bits, group_size,
-                                                          dst_row0, codes, row_bytes,
-                                                          static_cast<__half*>(params),
-                                                          nonfinite_flag);
-  return check_launch("xq_quantize_blocks_per_channel");
+  return quantize_blocks_per_channel(blocks, n_blocks, cols, bits, group_size, dst_row0, codes,
+                                     row_bytes, params, nonfinite_flag, stream);
+}
+
+int xq_quantize_blocks_per_channel_f64(const double* blocks, int64_t n_blocks, int64_t cols,
+                                       int32_t bits, int32_t group_size, const int64_t* dst_row0,
+                                       uint8_t* codes, int64_t row_bytes, void* params,
+                                       int32_t* nonfinite_flag, void* stream) {
+  return quantize_blocks_per_channel(blocks, n_blocks, cols, bits, group_size, dst_row0, codes,
+                                     row_bytes, params, nonfinite_flag, stream);
 }
 
 int xq_dequant_rows(const uint8_t* codes, int64_t row_bytes, const void* params, int32_t axis,

@@ -68,11 +68,13 @@ def synthetic_weights(shape: ModelShape, variant: str, device, seed: int = 0,
         if variant == "xq-gqa":
             lw.u_k, lw.fused_k = _svd_factors(w_k)
             lw.u_v, lw.fused_v = _svd_factors(w_v)
+        if variant == "xq-cl-gqa":  # shared subspace of [W_k | W_v] (model.py:135-142)
+            lw.u_kv, lw.fused_kv = _svd_factors(torch.cat([w_k, w_v], dim=1), u_dtype=torch.float32)
         out.append(lw)
     return out, wq
 
 
-def _svd_factors(w: torch.Tensor):
+def _svd_factors(w: torch.Tensor, u_dtype=torch.bfloat16):
     u, s, vt = torch.linalg.svd(w.float(), full_matrices=False)
     idx = torch.argmax(u.abs(), dim=0)
     sign = torch.sign(u[idx, torch.arange(u.shape[1], device=u.device)])
@@ -80,7 +82,7 @@ def _svd_factors(w: torch.Tensor):
     u = u * sign[None, :]
     vt = vt * sign[:, None]
     fused = s[:, None] * vt
-    return u.to(torch.bfloat16), fused.to(torch.bfloat16)
+    return u.to(u_dtype), fused.to(torch.bfloat16)
 
 
 def cache_kdim(cache) -> int:
@@ -110,6 +112,8 @@ class Decoder:
         n_heads = shape.n_heads
         self.gather = None
         if head_shard is not None and head_shard[0] > 1:
+            if variant == "xq-cl-gqa":
+                raise ConfigError("xq-cl-gqa runs batch-sharded (no KV-head-group sharding)")
             world, rank = head_shard
             kv = P.head_shard(shape.n_heads // shape.kv_group, world, rank)
             weights = [P.shard_layer_weights(lw, variant, kv) for lw in weights]
@@ -202,6 +206,9 @@ class Decoder:
         attend = 3 if absorbed else 2
         if self.variant == "xq-gqa":
             return 1 + attend  # v-latent quantize (+ a K-latent flush every 128 steps)
+        if self.variant == "xq-cl-gqa":  # push (+ flush), fused + merge, acc GEMM per seq
+            upd = cache.layer_index >= self.policy.base_layers - 1
+            return 1 + attend + (2 * self.n_slots if upd else 0)
         if self.variant == "xq-cl-mha":
             base = cache.layer_index < self.policy.base_layers
             seed = cache.layer_index == self.policy.base_layers - 1

@@ -171,6 +171,33 @@ class TestBackendsGolden:
         assert rel(attn, z["cl_attn"]) <= 1e-12
 
 
+    def test_xq_cl_gqa(self):
+        z = load("backends")
+        xs = bf16f(z["clg_x"])
+        us = z["clg_u"].astype(np.float64)
+        fuseds, q = bf16f(z["clg_fused"]), bf16f(z["clg_q"])
+        bits, base = list(z["clg_bits"]), int(z["clg_base"])
+        assert bits == O.policy_for_bits(3, 5)[0]
+        n_pre, n_dec = 250, 8
+        st = O.XqClGqaStack(bits, base, 128, 128)
+        subs = list(zip(us, fuseds))
+        st.step([x[:n_pre] for x in xs], subs)
+        for t in range(n_dec):
+            out = st.step([x[n_pre + t] for x in xs], subs)
+        for i in range(5):
+            assert np.array_equal(st.streams[i].codes, z[f"clg_codes{i}"]), i
+            assert np.array_equal(st.streams[i].scales, z[f"clg_scales{i}"]), i
+            assert rel(st.streams[i].buf, z[f"clg_buf{i}"]) <= 1e-9, i
+        assert rel(out[-1][3], z["clg_acc_last"]) <= 1e-6
+        assert rel(out[2][1], z["clg_k"][0]) <= 1e-6
+        assert rel(out[-1][1], z["clg_k"][1]) <= 1e-6
+        assert rel(out[-1][2], z["clg_v"][1]) <= 1e-6
+        pos = [n_pre + n_dec - 1]
+        attn = np.stack([O.attention(O.apply_rope(q[i:i + 1], pos, 128), o[1], o[2], 8, 4)[0]
+                         for i, o in enumerate(out)])
+        assert rel(attn, z["clg_attn"]) <= 1e-10
+
+
 class TestSysmodel:
     def test_compression_factors(self):
         # PAPER.md:371/373/563-579 via sysmodel.normalized_kv_size
