@@ -102,3 +102,31 @@ def test_decoder_cl_step_matches_oracle():
             q = x[i, b, -1:] @ wq[i].double().cpu().numpy()
             ref = O.attention(O.apply_rope(q, [n1 - 1], 128), kvs[i][0], kvs[i][1], shape.n_heads, 1)[0]
             assert rel_err(out[i, b].reshape(-1), ref) <= TOL, (i, b)
+
+
+def test_decoder_cl_gqa_step_matches_oracle():
+    """xq-cl-gqa through the decode engine: 5 layers (base 3), 8 query heads on 2 KV
+    heads, the shared K|V subspace from the SVD of [W_k | W_v]; against the oracle
+    with the arena's fp16 scale/zero-point storage on the same inputs."""
+    import torch
+
+    import xq_oracle as O
+
+    shape, w, wq, xs, dev = _setup("xq-cl-gqa", 3, n_layers=5, d=1024, H=8, g=4, n=260)
+    base = xs[0].float()
+    drift = [base]
+    for i in range(1, xs.shape[0]):
+        drift.append(drift[-1] + 0.03 * xs[i].float())
+    xs = torch.stack(drift).to(torch.bfloat16)
+    out, dec = _run(shape, "xq-cl-gqa", 3, w, wq, xs, dev)
+    L, B, n1, d = xs.shape
+    x = xs.double().numpy()
+    subs = [(w[i].u_kv.double().cpu().numpy(), w[i].fused_kv.double().cpu().numpy()) for i in range(L)]
+    for b in range(B):
+        stack = O.XqClGqaStack(dec.policy.bits, dec.policy.base_layers, 128, 128, params_f16=True)
+        stack.step([x[i, b, :-1] for i in range(L)], subs)
+        o = stack.step([x[i, b, -1] for i in range(L)], subs)
+        for i in range(L):
+            q = x[i, b, -1:] @ wq[i].double().cpu().numpy()
+            ref = O.attention(O.apply_rope(q, [n1 - 1], 128), o[i][1], o[i][2], shape.n_heads, 4)[0]
+            assert rel_err(out[i, b].reshape(-1), ref) <= TOL, (i, b)
