@@ -315,6 +315,55 @@ class PackedStream:
         out[nfl:] = self.resid[slot, :n - nfl]
         return out
 
+    # -- XQT1 on-disk format (quant.py:232-291) ----------------------------
+    def _channel_perm(self) -> torch.Tensor:
+        """Storage position of each natural channel in the per-channel params
+        (the producer order of csrc/xq_layout.cuh)."""
+        bs = {2: 16, 3: 32, 4: 8, 8: 4}[self.bits]
+        h = bs // 2
+        c = np.arange(self.width)
+        j = c % bs
+        pos = (c // bs) * bs + np.where(j < h, 2 * j, 2 * (j - h) + 1)
+        return torch.as_tensor(pos, device=self.codes.device)
+
+    def _packed_rows(self, r0: int, n: int) -> bytes:
+        """One LSB-first bit stream over rows r0..r0+n (row-major elements)."""
+        rows = self.codes[r0:r0 + n]
+        if (self.width * self.bits) % 64 == 0:  # arena rows are u64-aligned: the bytes concatenate
+            return rows.contiguous().cpu().numpy().tobytes()
+        dev = self.codes.device
+        flat = torch.empty((n, self.width), dtype=torch.uint8, device=dev)
+        for i in range(n):
+            N.call("xq_unpack_codes", N.ptr(rows[i]), self.bits, self.width, N.ptr(flat[i]),
+                   N.stream_of(dev))
+        words = torch.empty(((n * self.width * self.bits + 63) // 64,), dtype=torch.int64, device=dev)
+        N.call("xq_pack_codes", N.ptr(flat), n * self.width, self.bits, N.ptr(words), N.stream_of(dev))
+        return words.cpu().numpy().tobytes()
+
+    def export_xqt1(self, slot: int, n_rows: int) -> bytes:
+        """XQT1 dump (quant.py:232-254) of one slot's quantized rows: the header,
+        the scale and zero-point grids (float64 of the stored fp16 values) and the
+        packed codes, which are byte-identical to the reference's for the same
+        codes. Per-token: rows 0..n_rows-1. Per-channel: the flushed rows (whole
+        groups; the residual buffer is not part of the quantized tensor)."""
+        import struct
+
+        r0 = slot * self.L
+        if self.axis == TOKEN:
+            n = int(n_rows)
+            ng = -(-self.width // self.g)
+            p = self.params[r0:r0 + n, :ng].double()
+            sc, zp = p[..., 0], p[..., 1]
+        else:
+            n = int(self.n_flushed[slot])
+            perm = self._channel_perm()
+            p = self.params[r0 // self.g:(r0 + n) // self.g].double()  # [groups, 2, width]
+            sc, zp = p[:, 0][:, perm], p[:, 1][:, perm]
+        head = b"XQT1" + struct.pack("<5i", n, self.width, self.bits, self.axis, self.g)
+        body = sc.contiguous().cpu().numpy().astype("<f8").tobytes() + \
+            zp.contiguous().cpu().numpy().astype("<f8").tobytes()
+        return head + body + self._packed_rows(r0, n)
+
     def check_finite(self):
         """Raise DataError if any quantized input was NaN/Inf (quant.py:114-115).
 

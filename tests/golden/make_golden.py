@@ -156,6 +156,8 @@ def main():
             be[key + "_codes"] = st.x_stream.q.codes
             be[key + "_scales"] = st.x_stream.q.scales
             be[key + "_zps"] = st.x_stream.q.zero_points
+            # XQT1 dump of the whole X cache (quant.py:232-254)
+            be[key + "_xqt1"] = np.frombuffer(dump_qtensor(st.x_stream.q), dtype=np.uint8)
 
     # fp16 baseline semantics (cache.py:302-323) on the same x
     lw = dummy_lw(d, d, from_bf16_bits(be["mha_b4_wk"]), from_bf16_bits(be["mha_b4_wv"]))
@@ -189,6 +191,7 @@ def main():
         qr = apply_rope(q[t:t + 1], np.array([n_pre + t]), 128)
         outs.append(_attention(qr, k, v, H, g)[0])
         bufs.append(len(st.k_stream.buf))
+    be["gqa_kxqt1"] = np.frombuffer(dump_qtensor(st.k_stream.q), dtype=np.uint8)
     be.update({
         "gqa_x": xb, "gqa_uk": ukb, "gqa_uv": uvb, "gqa_fk": fkb, "gqa_fv": fvb,
         "gqa_q": qb, "gqa_k": k.astype(np.float32), "gqa_v": v.astype(np.float32), "gqa_attn": np.stack(outs),

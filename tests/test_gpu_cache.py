@@ -256,3 +256,55 @@ def test_xq_cl_gqa_against_reference(M):
     kk, vv = sts[4].rematerialize(ws[4], np.arange(n), acc)
     assert rel_err(kk.cpu().numpy(), o[-1][1]) <= 2e-2
     assert rel_err(vv.cpu().numpy(), o[-1][2]) <= 2e-2
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_xqt1_export_matches_reference_dump(M, bits):
+    """XQT1 (quant.py:232-254) of the GPU X cache vs the reference's dump_qtensor:
+    header and packed codes byte-identical, scale/zp grids = the stored fp16
+    values (the reference's float64 grids rounded to fp16)."""
+    import torch
+
+    z = golden("backends")
+    key = f"mha_b{bits}"
+    x = torch_bf16(z[key + "_x"])
+    st = M.make_cache("xq-mha", 0, M.LayerPolicy.uniform(bits, 1), 128, 128, n_slots=2,
+                      max_len=512, hidden_dim=256, n_heads=2)
+    st.prefill(x[:300], M.LayerWeights(), slot=1)
+    got = np.frombuffer(st.stream.export_xqt1(1, 300), dtype=np.uint8)
+    ref = z[key + "_xqt1"]
+    assert got.shape == ref.shape
+    n_grid = 300 * 2 * 8  # scales + zps, float64
+    assert np.array_equal(got[:24], ref[:24])  # magic + header
+    assert np.array_equal(got[24 + 2 * n_grid:], ref[24 + 2 * n_grid:])  # packed codes
+    gs = got[24:24 + 2 * n_grid].view(np.float64)
+    rs = ref[24:24 + 2 * n_grid].view(np.float64)
+    assert np.array_equal(gs, fp16_round(rs))
+
+
+def test_xqt1_export_per_channel(M):
+    """Per-channel (xq-gqa K latent) export: flushed groups only, params back in
+    natural channel order; codes byte-identical with the reference's dump."""
+    import torch
+
+    z = golden("backends")
+    x = torch_bf16(z["gqa_x"])
+    w = _weights(M, u_k=torch_bf16(z["gqa_uk"]), u_v=torch_bf16(z["gqa_uv"]),
+                 fused_k=torch_bf16(z["gqa_fk"]), fused_v=torch_bf16(z["gqa_fv"]))
+    st = M.make_cache("xq-gqa", 0, M.LayerPolicy.uniform(3, 1), 128, 128, n_slots=1,
+                      max_len=512, hidden_dim=1024, n_heads=8, kv_group=4)
+    st.prefill(x[:250], w)
+    for t in range(12):
+        st.decode_append(x[250 + t][None], w)
+    got = np.frombuffer(st.k_stream.export_xqt1(0, 262), dtype=np.uint8)
+    ref = z["gqa_kxqt1"]
+    assert got.shape == ref.shape
+    n_grid = 2 * 256 * 8
+    assert np.array_equal(got[:24], ref[:24])
+    # latents are fp32 GEMVs here (float64 in the reference): codes agree except at
+    # rounding boundaries; the grids to fp16 rounding of the fp32-vs-fp64 latents
+    gc, rc = got[24 + 2 * n_grid:], ref[24 + 2 * n_grid:]
+    assert np.mean(gc != rc) <= 1e-3
+    gs = got[24:24 + 2 * n_grid].view(np.float64)
+    rs = ref[24:24 + 2 * n_grid].view(np.float64)
+    assert np.max(np.abs(gs - rs) / np.maximum(np.abs(rs), 1e-3)) <= 2e-3
