@@ -174,6 +174,17 @@ def _rope(n_pos: int, device, j_major: int) -> torch.Tensor:
     return cur
 
 
+def _rope_rows(m: torch.Tensor, pos0: int, device) -> torch.Tensor:
+    """RoPE (linalg.py:58-95) of rows m [n, heads*128] at positions pos0..pos0+n-1."""
+    n = m.shape[0]
+    rope = rope_table(pos0 + n, device)
+    cos, sin = rope[pos0:pos0 + n, 0::2], rope[pos0:pos0 + n, 1::2]
+    mm = m.view(n, -1, HEAD_DIM // 2, 2)
+    e, o = mm[..., 0], mm[..., 1]
+    c, s = cos[:, None, :], sin[:, None, :]
+    return torch.stack([e * c - o * s, e * s + o * c], dim=-1).view(n, -1)
+
+
 def rope_table(n_pos: int, device) -> torch.Tensor:
     """cos/sin table [n_pos, 64] float2 (angle formed in float64, linalg.py:84-88)."""
     return _rope(n_pos, device, 0)
@@ -472,6 +483,49 @@ class CacheBackend:
         self._attend(q, weights, acc, self.lens_dev, int(self.n_tokens.max()), out, tiles_per_chunk)
         return out
 
+    def prefill_attend(self, x, q_pre, weights: LayerWeights, acc: Accumulator | None = None,
+                       slot: int = 0):
+        """Prefill of one slot and its causal attention (the attention block of
+        ``_Session.prefill``, model.py:205-221): cache the prompt x [n, d]
+        (``prefill``), rebuild K/V of all n positions from the cache just written
+        (``rematerialize``, cache.py:271-281), rotate q_pre [n, n_heads*128] to
+        positions 0..n-1 and attend causally (model.py:150-182).
+
+        Prefill is GEMM-shaped: K/V are materialized (fp16) by cuBLAS GEMMs on the
+        dequantized cache rows and attention runs through PyTorch's fused causal
+        SDPA (a library kernel). Returns float32 [n, n_heads, 128]."""
+        self._check_acc(acc)
+        x = torch.as_tensor(x, device=self.device)
+        n = x.shape[0]
+        self.prefill(x, weights, acc, slot=slot)
+        k, v = self._prefill_kv(weights, acc, slot, n)  # fp16, K rotated, [n, kvw]
+        q = q_pre.reshape(n, self.n_heads, self.head_dim).float()
+        q = _rope_rows(q.reshape(n, -1), 0, self.device).view(n, self.n_heads, self.head_dim)
+        qh = q.permute(1, 0, 2)[None].to(torch.float16)
+        kh = k.view(n, self.n_kv, self.head_dim).permute(1, 0, 2)[None]
+        vh = v.view(n, self.n_kv, self.head_dim).permute(1, 0, 2)[None]
+        ctx = torch.nn.functional.scaled_dot_product_attention(
+            qh, kh, vh, is_causal=True, scale=1.0 / math.sqrt(self.head_dim),
+            enable_gqa=self.g > 1)
+        return ctx[0].permute(1, 0, 2).float().contiguous()
+
+    def _prefill_kv(self, weights, acc, slot, n):  # pragma: no cover
+        raise NotImplementedError
+
+    def _dequant_rows(self, stream, slot, n):
+        """float32 [n, width] of a per-token stream's rows of one slot."""
+        out = torch.empty((n, stream.width), dtype=torch.float32, device=self.device)
+        N.call("xq_dequant_rows", N.ptr(stream.codes), stream.row_bytes, N.ptr(stream.params), TOKEN,
+               stream.bits, stream.g, stream.width, slot * self.L, n, N.ptr(out),
+               N.stream_of(self.device))
+        return out
+
+    def _kv_from(self, a_k, a_v, wk, wv, n):
+        """K (rotated to 0..n-1) and V in fp16 from A operands and weights (cuBLAS)."""
+        k = a_k.to(torch.float16) @ wk.to(torch.float16)
+        v = a_v.to(torch.float16) @ wv.to(torch.float16)
+        return _rope_rows(k.float(), 0, self.device).to(torch.float16), v
+
     # -- helpers -------------------------------------------------------------
     def _sync_lens(self):
         self.lens_dev.copy_(torch.from_numpy(self.n_tokens.astype(np.int32)), non_blocking=False)
@@ -632,6 +686,10 @@ class FullPrecisionCache(CacheBackend):
         base = slot * self.L
         return self.k[base:base + n].float(), self.v[base:base + n].float()
 
+    def _prefill_kv(self, weights, acc, slot, n):
+        base = slot * self.L
+        return self.k[base:base + n].to(torch.float16), self.v[base:base + n].to(torch.float16)
+
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         chunk = tpc * 128 if tpc else kv_chunk_tokens(self.n_slots, max_len, self.n_kv)
         nbytes = N.lib.xq_kv_decode_workspace_bytes(self.n_slots, max_len, self.n_kv, self.g, chunk)
@@ -687,6 +745,11 @@ class InputCacheMHA(CacheBackend):
         s = self.stream
         return N.A_CODES_TOKEN, s.codes, s.params, s.bits, s.row_bytes
 
+    def _prefill_kv(self, weights, acc, slot, n):
+        a = (self.x16[slot * self.L:slot * self.L + n] if self.passthrough
+             else self._dequant_rows(self.stream, slot, n))
+        return self._kv_from(a, a, weights.w_k, weights.w_v, n)
+
     def _rematerialize(self, weights, acc, slot, n):
         mode, src, params, bits, rb = self._a_operand()
         return self._remat_f32(mode, src, params, None, 0, bits, rb, N.A_SAME, None, None, 0, 0,
@@ -733,6 +796,11 @@ class LatentInputCacheGQA(CacheBackend):
         lat_k, lat_v = self._latents(x, weights)
         self.v_stream.append_token_rows(lat_v.contiguous(), lens)
         self.k_stream.channel_push(lat_k, self.n_tokens)  # cache.py:218-221
+
+    def _prefill_kv(self, weights, acc, slot, n):
+        lat_k = self.k_stream.channel_reconstruct(slot, n)
+        lat_v = self._dequant_rows(self.v_stream, slot, n)
+        return self._kv_from(lat_k, lat_v, weights.fused_k, weights.fused_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
         ks, vs = self.k_stream, self.v_stream
@@ -814,6 +882,10 @@ class DeltaInputCacheMHA(CacheBackend):
             raise UsageError("accumulator used before the base layer seeded it")
         self.stream.append_token_rows(x.contiguous(), lens, sub=acc.x_hat.view(-1, self.d))
         self._accumulate(acc, False, max_len, lens)
+
+    def _prefill_kv(self, weights, acc, slot, n):
+        a = self._dequant_rows(self.stream, slot, n) if self.is_base else acc.x_hat[slot, :n]
+        return self._kv_from(a, a, weights.w_k, weights.w_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
         wk, wv = weights.f32("w_k"), weights.f32("w_v")
@@ -956,6 +1028,15 @@ class DeltaLatentCacheGQA(CacheBackend):
             w = u @ fused  # (acc @ U) @ fused == acc @ (U @ fused)
             weights._cache[key] = (w[:, :self.kv_width].contiguous(), w[:, self.kv_width:].contiguous())
         return weights._cache[key]
+
+    def _prefill_kv(self, weights, acc, slot, n):
+        _, fused = self._sub(weights)
+        if self.is_base:
+            a = self.stream.channel_reconstruct(slot, n)
+            return self._kv_from(a, a, fused[:, :self.kv_width], fused[:, self.kv_width:], n)
+        wk, wv = self._w_delta(weights)
+        a = acc.x_hat[slot, :n]
+        return self._kv_from(a, a, wk, wv, n)
 
     def _rematerialize(self, weights, acc, slot, n):
         _, fused = self._sub(weights)
