@@ -273,6 +273,30 @@ int xq_kv_decode_attend(const void* k_cache, const void* v_cache, int64_t L_max,
                         const void* rope_cs, float sm_scale, int32_t chunk_tokens,
                         void* workspace, int64_t workspace_bytes, float* out, void* stream);
 
+/* ======================================================================
+ * Quantized-KV decode baseline "kvq" (QuantizedKvCache, cache.py:326-360)
+ * ====================================================================== */
+
+/* Workspace (bytes) of xq_kvq_decode_attend's split partials. */
+int64_t xq_kvq_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q_heads,
+                               int32_t chunk_tokens);
+
+/* Decode attention over a quantized K/V cache: K pre-RoPE per-channel codes
+ * (planar params in the producer order, residual rows k_resid for tokens >=
+ * k_nflushed[b]), V per-token codes + half2 params (residual rows v_resid for
+ * tokens >= v_nflushed[b]); width n_kv_heads*128, both arenas row_bytes wide.
+ * K is rotated at its cached positions (cache.py:357-360), q at
+ * seq_lens[b]-1; rope_cs is the position-major table. out: float32
+ * [n_seqs, n_kv_heads*group, 128]. */
+int xq_kvq_decode_attend(const uint8_t* k_codes, const void* k_params, const float* k_resid,
+                         const uint8_t* v_codes, const void* v_params, const float* v_resid,
+                         const int32_t* k_nflushed, const int32_t* v_nflushed, int32_t bits,
+                         int32_t group_size, int64_t row_bytes, int64_t L_max,
+                         const int32_t* seq_lens, int32_t n_seqs, int32_t max_len,
+                         int32_t n_kv_heads, int32_t group, const float* q_pre,
+                         const void* rope_cs, float sm_scale, int32_t chunk_tokens,
+                         void* workspace, int64_t workspace_bytes, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

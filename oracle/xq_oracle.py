@@ -325,6 +325,36 @@ class Fp16Cache:
         return apply_rope(self.k_pre, np.arange(n), self.hd), self.v.copy()
 
 
+class KvqCache:
+    """QuantizedKvCache "kvq" (cache.py:326-360): pre-RoPE K per-channel and V
+    per-token, both buffered (cache.py:336-342); K/V given pre-projected."""
+
+    def __init__(self, bits, head_dim, group_size=128):
+        self.hd = head_dim
+        self.bits, self.g = bits, group_size
+        self.k = None
+        self.v = None
+
+    def _ensure(self, width):
+        if self.k is None:
+            self.k = Stream(self.bits, PER_CHANNEL, width, self.g, buffered=True)
+            self.v = Stream(self.bits, PER_TOKEN, width, self.g, buffered=True)
+
+    def prefill(self, k, v):  # cache.py:344-349
+        self._ensure(k.shape[1])
+        self.k.bulk(k)
+        self.v.bulk(v)
+
+    def push(self, k_row, v_row):  # cache.py:351-354
+        self._ensure(np.asarray(k_row).reshape(-1).shape[0])
+        self.k.push(k_row)
+        self.v.push(v_row)
+
+    def remat(self):  # cache.py:356-360
+        k = self.k.reconstruct()
+        return apply_rope(k, np.arange(k.shape[0]), self.hd), self.v.reconstruct()
+
+
 class XqMhaCache:
     """InputCacheMHA "xq-mha" (cache.py:363-387): per-token X, unbuffered."""
 

@@ -52,12 +52,15 @@ _SIGS = {
     "xq_debug_set_acc_dump": [_P, _I32],
     "xq_debug_role_profile": [_P, _I32],
     "xq_kv_append": [_P, _P, _P, _I32, _I32, _I64, _P, _P, _P, _P],
+    "xq_kvq_decode_attend": [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I64, _I64, _P, _I32,
+                             _I32, _I32, _I32, _P, _P, _F, _I32, _P, _I64, _P, _P],
     "xq_kv_decode_attend": [_P, _P, _I64, _P, _I32, _I32, _I32, _I32, _P, _P, _F, _I32, _P,
                             _I64, _P, _P],
 }
 _I64_RET = {"xq_decode_workspace_bytes": [_I32, _I32, _I32, _I32, _I32],
             "xq_kv_decode_workspace_bytes": [_I32, _I32, _I32, _I32, _I32],
-            "xq_absorbed_workspace_bytes": [_I32, _I32, _I32, _I64]}
+            "xq_absorbed_workspace_bytes": [_I32, _I32, _I32, _I64],
+            "xq_kvq_workspace_bytes": [_I32, _I32, _I32, _I32]}
 
 
 def _load():

@@ -35,7 +35,7 @@ from .errors import ConfigError, DataError, ShapeError, UsageError
 
 VARIANTS = ("fp16", "kvq", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")  # cache.py:41
 CL_VARIANTS = ("xq-cl-mha", "xq-cl-gqa")
-SUPPORTED = ("fp16", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")
+SUPPORTED = ("fp16", "kvq", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")
 DEFAULT_GROUP_SIZE = 128
 HEAD_DIM = 128
 ROPE_THETA = 10000.0
@@ -223,7 +223,8 @@ class PackedStream:
     the rows of the current incomplete group (cache.py:203-208, 218-221).
     """
 
-    def __init__(self, bits, axis, width, group_size, n_slots, max_len, device, resid_f64=False):
+    def __init__(self, bits, axis, width, group_size, n_slots, max_len, device, resid_f64=False,
+                 buffered=False):
         """``resid_f64``: per-channel only -- keep the residual rows in float64 as
         well (quantized from float64, like the reference); ``resid`` is then
         their float32 mirror read by the fused kernel."""
@@ -239,6 +240,11 @@ class PackedStream:
             ng = -(-width // group_size)
             ngp = -(-ng // 4) * 4  # row stride padded to 16-byte quads (include/xquant.h)
             self.params = torch.zeros((n_slots * max_len, ngp, 2), dtype=torch.float16, device=device)
+            if buffered:  # per-token with a residual buffer (kvq V, cache.py:340-341)
+                self.resid = torch.zeros((n_slots, group_size, width), dtype=torch.float32,
+                                         device=device)
+                self.n_flushed = np.zeros(n_slots, dtype=np.int64)
+                self.nflushed_dev = torch.zeros(n_slots, dtype=torch.int32, device=device)
         else:
             self.params = torch.zeros((n_slots * max_len // group_size, 2, width),
                                       dtype=torch.float16, device=device)
@@ -251,6 +257,8 @@ class PackedStream:
 
     def nbytes(self) -> dict:
         out = {"codes": self.codes.numel(), "params": self.params.numel() * 2}
+        if self.axis == TOKEN and hasattr(self, "resid"):
+            out["residual"] = self.resid.numel() * 4
         if self.axis == CHANNEL:
             out["residual"] = self.resid.numel() * 4
             if self.resid64 is not None:
@@ -273,6 +281,23 @@ class PackedStream:
                self.bits, self.g, None, slot * self.L + pos0, self.L, N.ptr(sub),
                N.ptr(self.codes), self.row_bytes, N.ptr(self.params), N.ptr(x_eff),
                N.ptr(self.flag), N.stream_of(x.device))
+
+    def token_bulk(self, slot: int, x: torch.Tensor):
+        """Buffered per-token bulk (cache.py:191-201): every row is quantized."""
+        self.fill_rows(x.contiguous(), slot, 0)
+        self.n_flushed[slot] = x.shape[0]
+        self.nflushed_dev[slot] = x.shape[0]
+
+    def token_push(self, x: torch.Tensor, n_tokens: np.ndarray):
+        """Buffered per-token push (cache.py:210-221): the row waits in the
+        residual buffer; a full buffer of G rows is quantized at once."""
+        dev = x.device
+        buf_pos = torch.as_tensor(n_tokens - 1 - self.n_flushed, device=dev)
+        self.resid[torch.arange(self.n_slots, device=dev), buf_pos] = x.float()
+        for s in np.nonzero(n_tokens - self.n_flushed >= self.g)[0]:
+            self.fill_rows(self.resid[int(s)], int(s), int(self.n_flushed[s]))
+            self.n_flushed[s] += self.g
+        self.nflushed_dev.copy_(torch.from_numpy(self.n_flushed.astype(np.int32)))
 
     # -- per-channel -------------------------------------------------------
     def flush_blocks(self, blocks: torch.Tensor, dst_row0: list[int]):
@@ -711,6 +736,79 @@ def kv_chunk_tokens(n_slots, max_len, n_kv, n_sm=148):
     return max(512, -(-max_len // chunks))
 
 
+class QuantizedKvCache(CacheBackend):
+    """``kvq`` (cache.py:326-360): the quantized K/V baseline at equal bits.
+    Pre-RoPE K quantized per channel, V per token, both buffered while decoding
+    (prefill quantizes V whole and K by whole groups); K/V from one bf16 GEMM
+    per token as in the fp16 baseline. Decode attention dequantizes the K/V
+    tiles in shared memory (csrc/xq_kvq.cu)."""
+
+    variant = "kvq"
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        if self.bits == 16:
+            raise ConfigError("kvq needs a quantized width (2/3/4/8)")
+        self.k_stream = PackedStream(self.bits, CHANNEL, self.kvw, self.group_size, self.n_slots,
+                                     self.L, self.device)
+        self.v_stream = PackedStream(self.bits, TOKEN, self.kvw, self.group_size, self.n_slots,
+                                     self.L, self.device, buffered=True)
+
+    def _project(self, x, weights):
+        # float32 GEMMs: K/V are quantized here, so their rounding picks codes
+        xf = x.float()
+        return xf @ weights.f32("w_k"), xf @ weights.f32("w_v")
+
+    def _prefill(self, slot, x, weights, acc):
+        k, v = self._project(x, weights)  # cache.py:344-349
+        self.k_stream.channel_bulk(slot, k)
+        self.v_stream.token_bulk(slot, v)
+
+    def _decode(self, x, weights, acc, lens):
+        k, v = self._project(x, weights)  # cache.py:351-354
+        self.k_stream.channel_push(k, self.n_tokens)
+        self.v_stream.token_push(v, self.n_tokens)
+
+    def _kv_rows(self, slot, n):
+        k = self.k_stream.channel_reconstruct(slot, n)
+        vs = self.v_stream
+        nfl = int(vs.n_flushed[slot])
+        v = torch.empty((n, self.kvw), dtype=torch.float32, device=self.device)
+        if nfl:
+            v[:nfl] = self._dequant_rows(vs, slot, nfl)
+        v[nfl:] = vs.resid[slot, :n - nfl]
+        return k, v
+
+    def _rematerialize(self, weights, acc, slot, n):  # cache.py:356-360
+        k, v = self._kv_rows(slot, n)
+        return _rope_rows(k, 0, self.device), v
+
+    def _prefill_kv(self, weights, acc, slot, n):
+        k, v = self._rematerialize(weights, acc, slot, n)
+        return k.to(torch.float16), v.to(torch.float16)
+
+    def _attend(self, q, weights, acc, lens, max_len, out, tpc):
+        ks, vs = self.k_stream, self.v_stream
+        # one CTA per (sequence, chunk), all heads: ~2 CTAs per SM in total
+        chunks = max(1, -(-2 * 148 // self.n_slots))
+        per = -(-max_len // chunks)
+        chunk = tpc * 128 if tpc else max(64, (per + 63) // 64 * 64)
+        nbytes = N.lib.xq_kvq_workspace_bytes(self.n_slots, max_len, self.n_heads, chunk)
+        ws = _scratch(self.device, nbytes)
+        rope = rope_table(max_len, self.device)
+        N.call("xq_kvq_decode_attend", N.ptr(ks.codes), N.ptr(ks.params), N.ptr(ks.resid),
+               N.ptr(vs.codes), N.ptr(vs.params), N.ptr(vs.resid), N.ptr(ks.nflushed_dev),
+               N.ptr(vs.nflushed_dev), self.bits, self.group_size, ks.row_bytes, self.L,
+               N.ptr(lens), self.n_slots, max_len, self.n_kv, self.g, N.ptr(q), N.ptr(rope),
+               1.0 / math.sqrt(HEAD_DIM), chunk, N.ptr(ws), nbytes, N.ptr(out),
+               N.stream_of(self.device))
+
+    def memory_bytes(self):
+        out = {f"k_{k}": v for k, v in self.k_stream.nbytes().items()}
+        out.update({f"v_{k}": v for k, v in self.v_stream.nbytes().items()})
+        return out
+
+
 class InputCacheMHA(CacheBackend):
     """``xq-mha`` (cache.py:363-387): per-token X codes; K/V rebuilt from X."""
 
@@ -1072,7 +1170,7 @@ class DeltaLatentCacheGQA(CacheBackend):
 
 _BACKENDS = {
     cls.variant: cls
-    for cls in (FullPrecisionCache, InputCacheMHA, LatentInputCacheGQA, DeltaInputCacheMHA,
+    for cls in (FullPrecisionCache, QuantizedKvCache, InputCacheMHA, LatentInputCacheGQA, DeltaInputCacheMHA,
                 DeltaLatentCacheGQA)
 }
 

@@ -298,6 +298,32 @@ def main():
         be[f"clg_scales{i}"] = states[i].stream.q.scales
         be[f"clg_zps{i}"] = states[i].stream.q.zero_points
         be[f"clg_buf{i}"] = np.asarray(states[i].stream.buf.tokens, np.float64)
+
+    # kvq: d=512, 4 heads on 2 KV heads (kvw 256), 3-bit; prefill 250 + 12 decodes
+    # (crosses the 256-token K flush; V buffers 12 rows after the whole-V prefill)
+    d, H, g = 512, 4, 2
+    kvw = d // g
+    n_pre, n_dec = 250, 12
+    xb, x = bf16(rng.normal(size=(n_pre + n_dec, d)))
+    wkb, w_k = bf16(rng.normal(size=(d, kvw)) / np.sqrt(d))
+    wvb, w_v = bf16(rng.normal(size=(d, kvw)) / np.sqrt(d))
+    qb, q = bf16(rng.normal(size=(n_dec, d)))
+    lw = dummy_lw(d, kvw, w_k, w_v)
+    st = make_cache("kvq", 0, LayerPolicy.uniform(3, 1), 128, group_size=128)
+    st.prefill(x[:n_pre], lw)
+    outs = []
+    for t in range(n_dec):
+        st.decode_append(x[n_pre + t], lw)
+        k, v = st.rematerialize(lw, np.arange(n_pre + t + 1))
+        qr = apply_rope(q[t:t + 1], np.array([n_pre + t]), 128)
+        outs.append(_attention(qr, k, v, H, g)[0])
+    be.update({
+        "kvq_x": xb, "kvq_wk": wkb, "kvq_wv": wvb, "kvq_q": qb, "kvq_attn": np.stack(outs),
+        "kvq_k": k.astype(np.float32), "kvq_v": v.astype(np.float32),
+        "kvq_kcodes": st.k_stream.q.codes, "kvq_kscales": st.k_stream.q.scales,
+        "kvq_vcodes": st.v_stream.q.codes, "kvq_vscales": st.v_stream.q.scales,
+        "kvq_vbuf": np.asarray(st.v_stream.buf.tokens, np.float64),
+    })
     np.savez_compressed(os.path.join(HERE, "backends.npz"), **be)
 
     for f in ("quant", "pack", "rope", "backends"):

@@ -198,6 +198,27 @@ class TestBackendsGolden:
         assert rel(attn, z["clg_attn"]) <= 1e-10
 
 
+    def test_kvq(self):
+        z = load("backends")
+        x, q = bf16f(z["kvq_x"]), bf16f(z["kvq_q"])
+        wk, wv = bf16f(z["kvq_wk"]), bf16f(z["kvq_wv"])
+        st = O.KvqCache(3, 128, 128)
+        n_pre = 250
+        st.prefill(x[:n_pre] @ wk, x[:n_pre] @ wv)
+        outs = []
+        for t in range(12):
+            st.push(x[n_pre + t] @ wk, x[n_pre + t] @ wv)
+            k, v = st.remat()
+            outs.append(O.attention(O.apply_rope(q[t:t + 1], [n_pre + t], 128), k, v, 4, 2)[0])
+        assert np.array_equal(st.k.codes, z["kvq_kcodes"])
+        assert np.array_equal(st.k.scales, z["kvq_kscales"])
+        assert np.array_equal(st.v.codes, z["kvq_vcodes"])
+        assert np.array_equal(st.v.scales, z["kvq_vscales"])
+        assert rel(st.v.buf, z["kvq_vbuf"]) <= 1e-12
+        assert rel(k, z["kvq_k"]) <= 1e-6 and rel(v, z["kvq_v"]) <= 1e-6
+        assert rel(np.stack(outs), z["kvq_attn"]) <= 1e-12
+
+
 class TestSysmodel:
     def test_compression_factors(self):
         # PAPER.md:371/373/563-579 via sysmodel.normalized_kv_size
