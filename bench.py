@@ -419,6 +419,27 @@ def run_xquant(args, cfg):
         except torch.OutOfMemoryError as e:
             fp16 = {"value": None, "note": f"fp16 KV cache does not fit one B200: {str(e)[:120]}"}
 
+    # ------- quantized-KV baseline at equal bits (kvq, cache.py:326-360; opt-in) -------
+    kvq = None
+    if args.kvq:
+        try:
+            qdec, _ = make("kvq")
+            for k in range(args.warmup):
+                qdec.step(xs[k])
+            tq = _time_steps(qdec, xs[args.warmup:], args.steps, world)
+            tq = _max_over_ranks(world, tq)
+            qbytes = sum(S.cache_bytes("kvq", l_avg, d, b, shape.kv_group) for b in qdec.policy.bits) * B
+            kvq = {"value": tokens_per_step * args.steps / tq, "unit": "tokens/s",
+                   "ms_per_step": tq / args.steps * 1e3,
+                   "hbm_gbs_achieved": qbytes / (tq / args.steps) / 1e9,
+                   "compression": S.compression_factor("kvq", qdec.policy.bits, shape.kv_group),
+                   "kernel": "xq_kvq_decode_attend (shared-memory dequant flash-decode)"}
+            del qdec
+            gc.collect()
+            torch.cuda.empty_cache()
+        except torch.OutOfMemoryError as e:
+            kvq = {"value": None, "note": f"kvq cache does not fit one B200: {str(e)[:120]}"}
+
     if rank != 0:
         return
     # ---------------- roofline of the dominant kernel ----------------
@@ -470,6 +491,7 @@ def run_xquant(args, cfg):
                    "l2": "no flush: per-step inputs (packed caches, GBs) exceed the 126 MB L2"},
         "fp16_kv": fp16,
         "speedup_vs_fp16_kv": (value / fp16["value"]) if fp16 and fp16.get("value") else None,
+        "kvq": kvq,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": ("k_decode_absorbed (+k_absorb_combine, k_absorb_project)" if absorbed
@@ -507,6 +529,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kvq", action="store_true", help="also time the kvq baseline at equal bits")
     ap.add_argument("--ctx", type=int, default=None, help="override the config's context")
     ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
     args = ap.parse_args()

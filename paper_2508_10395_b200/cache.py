@@ -294,10 +294,12 @@ class PackedStream:
         dev = x.device
         buf_pos = torch.as_tensor(n_tokens - 1 - self.n_flushed, device=dev)
         self.resid[torch.arange(self.n_slots, device=dev), buf_pos] = x.float()
-        for s in np.nonzero(n_tokens - self.n_flushed >= self.g)[0]:
+        full = np.nonzero(n_tokens - self.n_flushed >= self.g)[0]
+        for s in full:
             self.fill_rows(self.resid[int(s)], int(s), int(self.n_flushed[s]))
             self.n_flushed[s] += self.g
-        self.nflushed_dev.copy_(torch.from_numpy(self.n_flushed.astype(np.int32)))
+        if len(full):
+            self.nflushed_dev.copy_(torch.from_numpy(self.n_flushed.astype(np.int32)))
 
     # -- per-channel -------------------------------------------------------
     def flush_blocks(self, blocks: torch.Tensor, dst_row0: list[int]):
@@ -789,10 +791,8 @@ class QuantizedKvCache(CacheBackend):
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         ks, vs = self.k_stream, self.v_stream
-        # one CTA per (sequence, chunk), all heads: ~2 CTAs per SM in total
-        chunks = max(1, -(-2 * 148 // self.n_slots))
-        per = -(-max_len // chunks)
-        chunk = tpc * 128 if tpc else max(64, (per + 63) // 64 * 64)
+        # one CTA per (sequence, KV head, chunk of whole 128-token groups)
+        chunk = tpc * 128 if tpc else -(-kv_chunk_tokens(self.n_slots, max_len, self.n_kv) // 128) * 128
         nbytes = N.lib.xq_kvq_workspace_bytes(self.n_slots, max_len, self.n_heads, chunk)
         ws = _scratch(self.device, nbytes)
         rope = rope_table(max_len, self.device)

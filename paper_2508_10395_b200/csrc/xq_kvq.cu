@@ -3,14 +3,11 @@
 // channel, V per token, both with residual buffers while decoding
 // (cache.py:336-342, the newest < G tokens of each stay in float32).
 //
-// One CTA per (sequence, chunk of tokens). Per 64-token tile the CTA stages
-// the tile's cos/sin rows once, then for each KV head dequantizes the K tile
-// into shared memory, rotates it (RoPE at the cached positions,
-// cache.py:357-360 + linalg.py:58-95), scores it against the head's query
-// heads, updates the per-head online softmax, dequantizes the V tile and
-// accumulates p.V. Split partials (m, l, o) per (sequence, query head, chunk)
-// are merged by k_combine. HBM traffic per token: 2*kv_width*(bits/8) code
-// bytes + the scale / zero-point grids.
+// A split-K flash-decode that streams the codes once: one CTA per (sequence,
+// KV head, chunk of tokens), half-warps on tokens, dequantization and RoPE of
+// K in registers (k_kvq_decode below), split partials merged by k_combine.
+// HBM traffic per token and layer: 2*kv_width*bits/8 code bytes + the scale /
+// zero-point grids.
 #include <math.h>
 
 #include "xq_common.cuh"
@@ -23,10 +20,9 @@ __global__ void k_combine(const float* __restrict__ partials, int n_parts, float
 
 namespace kvq {
 
-constexpr int kT = 64;          // tokens per tile
+constexpr int kT = 128;  // token chunks are whole K groups (G = 128)
 constexpr int kThreads = 256;
 constexpr int kPart = 2 + kHeadDim;
-constexpr int kPad = kHeadDim + 4;  // row stride of the K/V tiles (floats)
 
 struct Params {
   const uint8_t* k_codes;  // [n_seqs*L_max][row_bytes]
@@ -48,191 +44,229 @@ struct Params {
   float* partials;  // [n_seqs*n_q][n_chunks][130]
 };
 
-// 16 consecutive codes starting at element c0 of a packed row (c0*bits % 8 == 0).
-XQ_DEVINL void load16(const uint8_t* row, int64_t c0, int bits, uint32_t (&out)[16]) {
-  const uint8_t* p = row + (c0 * bits) / 8;
-  uint64_t lo = 0, hi = 0;
-  const int nbytes = 2 * bits;  // 16 codes
-  for (int i = 0; i < nbytes && i < 8; ++i) lo |= static_cast<uint64_t>(p[i]) << (8 * i);
-  for (int i = 8; i < nbytes; ++i) hi |= static_cast<uint64_t>(p[i]) << (8 * (i - 8));
-  const uint32_t mask = (1u << bits) - 1u;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int b = i * bits;
-    uint32_t v;
-    if (b + bits <= 64) v = static_cast<uint32_t>(lo >> b);
-    else if (b >= 64) v = static_cast<uint32_t>(hi >> (b - 64));
-    else v = static_cast<uint32_t>((lo >> b) | (hi << (64 - b)));
-    out[i] = v & mask;
-  }
+// `nbits` (<= 32) bits of a packed row starting at byte `off` (any alignment;
+// rows are 8-byte aligned): two aligned 32-bit loads and a funnel shift.
+XQ_DEVINL uint32_t load_bits(const uint8_t* row, int64_t off) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row + (off & ~int64_t(3)));
+  const uint32_t lo = __ldg(w), hi = __ldg(w + 1);
+  return __funnelshift_r(lo, hi, static_cast<uint32_t>(off & 3) * 8u);
 }
 
-__global__ void __launch_bounds__(kThreads) k_kvq_decode(const Params p) {
-  extern __shared__ float sm[];
-  const int n_q = p.n_kv * p.group;
-  float* q_s = sm;                                          // [n_q][128]
-  float* o_s = q_s + n_q * kHeadDim;                        // [n_q][128]
-  float2* cs_s = reinterpret_cast<float2*>(o_s + n_q * kHeadDim);  // [kT][64]
-  __half2* kp_s = reinterpret_cast<__half2*>(cs_s + kT * 64);      // [kvw] (scale, zp), natural order
-  float* kt_s = reinterpret_cast<float*>(kp_s + p.kvw);     // [kT][kPad]
-  float* vt_s = kt_s + kT * kPad;                           // [kT][kPad]
-  float* sc_s = vt_s + kT * kPad;                           // [group][kT]
-  float* al_s = sc_s + p.group * kT;                        // [group] tile rescale
-  float* m_s = al_s + p.group;                              // [n_q]
-  float* l_s = m_s + n_q;                                   // [n_q]
+// The 8 codes of channels 8*hl .. 8*hl+7 of head h in a packed row, raw
+// (BITS*8 bits; for 8-bit two words).
+template <int BITS>
+XQ_DEVINL uint2 raw8(const uint8_t* row, int h, int hl) {
+  const int64_t off = (int64_t)(h * kHeadDim + 8 * hl) * BITS / 8;  // byte-aligned: 8 codes
+  if constexpr (BITS == 8) return __ldg(reinterpret_cast<const uint2*>(row + off));
+  return make_uint2(load_bits(row, off), 0u);
+}
+template <int BITS>
+XQ_DEVINL uint32_t code_j(uint2 raw, int j) {
+  if constexpr (BITS == 8) return ((j < 4 ? raw.x : raw.y) >> (8 * (j & 3))) & 0xFFu;
+  return (raw.x >> (BITS * j)) & ((1u << BITS) - 1u);
+}
 
-  const int b = blockIdx.x / p.n_chunks, chunk = blockIdx.x % p.n_chunks;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+// One CTA per (sequence, KV head, chunk of tokens); each half-warp streams its
+// own tokens (lane hl owns dims 8hl..8hl+7, kUnroll tokens in flight), like the
+// fp16-KV kernel but on codes: K dequantized with the per-channel (scale, zp)
+// of the token's group, rotated at its position by angle addition
+// cos/sin((t0 + r) theta) from the 16-token block base (global table, one
+// coalesced row per block) and a shared offset table r < 16; V dequantized
+// with its per-token (scale, zp).
+constexpr int kNw = kThreads / 32;
+constexpr int kStreams = 2 * kNw;
+
+template <int BITS, int GROUP>
+__global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
+  constexpr int kUnroll = GROUP >= 4 ? 4 : 8;  // tokens in flight per half-warp (registers)
+  const int unit = blockIdx.x;
+  const int chunk = unit % p.n_chunks;
+  const int h = (unit / p.n_chunks) % p.n_kv;
+  const int b = unit / (p.n_chunks * p.n_kv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  const int stream = warp * 2 + half;
   const int len = p.seq_lens[b];
-  const int t_begin = chunk * p.chunk_tokens;
-  const int t_end = min(len, t_begin + p.chunk_tokens);
+  const int t0 = chunk * p.chunk_tokens;
+  const int t1 = min(t0 + p.chunk_tokens, len);
+  const int n_q = p.n_kv * GROUP;
   const int nfl = p.k_nflushed[b], vnfl = p.v_nflushed[b];
-  const int pos = len - 1;
-  // q rotated to position len-1 (model.py:234), scaled into the log2 domain
-  for (int i = tid; i < n_q * kHeadDim; i += kThreads) {
-    const int h = i / kHeadDim, dd = i % kHeadDim;
-    const float* qp = p.q_pre + ((int64_t)b * n_q + h) * kHeadDim;
-    const float2 cs = p.rope[(int64_t)(pos < 0 ? 0 : pos) * 64 + dd / 2];
-    const float e0 = qp[dd & ~1], e1 = qp[dd | 1];
-    q_s[i] = ((dd & 1) ? (e0 * cs.y + e1 * cs.x) : (e0 * cs.x - e1 * cs.y)) * p.q_scale;
-    o_s[i] = 0.f;
-  }
-  for (int h = tid; h < n_q; h += kThreads) {
-    m_s[h] = -INFINITY;
-    l_s[h] = 0.f;
-  }
-  int kp_group = -1;
-  const int bs = perm_block(XQ_A_CODES_CHANNEL, p.bits);
-  for (int t0 = t_begin; t0 < t_end; t0 += kT) {
-    __syncthreads();
-    for (int i = tid; i < kT * 64; i += kThreads) {  // the tile's cos/sin rows
-      const int r = i >> 6, j = i & 63;
-      const int t = min(t0 + r, len - 1);
-      cs_s[i] = p.rope[(int64_t)t * 64 + j];
-    }
-    const int grp = t0 / p.G;  // tiles never straddle a group (G % kT == 0)
-    if (grp != kp_group && t0 < nfl) {
-      const __half* prow = p.k_params + ((int64_t)b * p.L_max / p.G + grp) * 2 * p.kvw;
-      for (int c = tid; c < p.kvw; c += kThreads) {
-        const int ppos = (c / bs) * bs + perm_position(c % bs, bs);
-        kp_s[c] = __halves2half2(prow[ppos], prow[p.kvw + ppos]);
+
+  __shared__ float2 s_off[16][64];  // cos/sin(r theta_j), r < 16
+  for (int i = threadIdx.x; i < 16 * 64; i += kThreads) s_off[i >> 6][i & 63] = p.rope[i];
+  float q[GROUP][8];
+  {
+    const int pos = len - 1;
+#pragma unroll
+    for (int gi = 0; gi < GROUP; ++gi) {
+      const float* qp = p.q_pre + ((int64_t)b * n_q + h * GROUP + gi) * kHeadDim + 8 * hl;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 cs = p.rope[(int64_t)pos * 64 + 4 * hl + j];
+        const float e0 = qp[2 * j], e1 = qp[2 * j + 1];
+        q[gi][2 * j] = (e0 * cs.x - e1 * cs.y) * p.q_scale;
+        q[gi][2 * j + 1] = (e0 * cs.y + e1 * cs.x) * p.q_scale;
       }
-      kp_group = grp;
-    }
-    __syncthreads();
-    const int r = tid >> 2, part = tid & 3;  // token row of the tile, 32-channel quarter
-    const int t = t0 + r;
-    const bool valid = t < t_end;
-    const int64_t arow = (int64_t)b * p.L_max + t;
-    for (int kvh = 0; kvh < p.n_kv; ++kvh) {
-      // ---- K tile: dequant (per-channel params) or residual row, then RoPE
-      const int c0 = kvh * kHeadDim + part * 32;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float v[16];
-        const int cc = c0 + half * 16;
-        if (valid && t < nfl) {
-          uint32_t code[16];
-          load16(p.k_codes + arow * p.row_bytes, cc, p.bits, code);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 sz = __half22float2(kp_s[cc + i]);
-            v[i] = fmaf(static_cast<float>(code[i]), sz.x, sz.y);
-          }
-        } else if (valid) {
-          const float* rr = p.k_resid + ((int64_t)b * p.G + (t - nfl)) * p.kvw + cc;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = rr[i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        }
-        const int d0 = part * 32 + half * 16;  // dim within the head
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const float2 cs = cs_s[r * 64 + (d0 + i) / 2];
-          kt_s[r * kPad + d0 + i] = v[i] * cs.x - v[i + 1] * cs.y;
-          kt_s[r * kPad + d0 + i + 1] = v[i] * cs.y + v[i + 1] * cs.x;
-        }
-      }
-      // ---- V tile: per-token params of this head's 128-channel group (G = 128)
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float v[16];
-        const int cc = c0 + half * 16;
-        if (valid && t < vnfl) {
-          uint32_t code[16];
-          load16(p.v_codes + arow * p.row_bytes, cc, p.bits, code);
-          const float2 sz = __half22float2(p.v_params[arow * p.vp_stride + cc / p.G]);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = fmaf(static_cast<float>(code[i]), sz.x, sz.y);
-        } else if (valid) {
-          const float* rr = p.v_resid + ((int64_t)b * p.G + (t - vnfl)) * p.kvw + cc;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = rr[i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        }
-        const int d0 = part * 32 + half * 16;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) vt_s[r * kPad + d0 + i] = v[i];
-      }
-      __syncthreads();
-      // ---- scores of the head's query heads (4 threads per token)
-      for (int gi = 0; gi < p.group; ++gi) {
-        const float* qh = q_s + (kvh * p.group + gi) * kHeadDim + part * 32;
-        const float* kr = kt_s + r * kPad + part * 32;
-        float s = 0.f;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s = fmaf(qh[i], kr[i], s);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (part == 0) sc_s[gi * kT + r] = valid ? s : -INFINITY;
-      }
-      __syncthreads();
-      // ---- online softmax per query head (one warp each, 2 tokens per lane)
-      for (int gi = warp; gi < p.group; gi += kThreads / 32) {
-        const int h = kvh * p.group + gi;
-        const float s0 = sc_s[gi * kT + lane], s1 = sc_s[gi * kT + 32 + lane];
-        const float mo = m_s[h];
-        const float mn = fmaxf(mo, warp_max(fmaxf(s0, s1)));
-        const float p0 = (s0 == -INFINITY) ? 0.f : exp2f(s0 - mn);
-        const float p1 = (s1 == -INFINITY) ? 0.f : exp2f(s1 - mn);
-        const float alpha = (mo == -INFINITY) ? 0.f : exp2f(mo - mn);
-        const float ls = warp_sum(p0 + p1);
-        sc_s[gi * kT + lane] = p0;
-        sc_s[gi * kT + 32 + lane] = p1;
-        if (lane == 0) {
-          al_s[gi] = alpha;
-          m_s[h] = mn;
-          l_s[h] = l_s[h] * alpha + ls;
-        }
-      }
-      __syncthreads();
-      // ---- o = o*alpha + p.V (thread = (query head, channel))
-      for (int i = tid; i < p.group * kHeadDim; i += kThreads) {
-        const int gi = i / kHeadDim, c = i % kHeadDim;
-        const float* pp = sc_s + gi * kT;
-        float acc = 0.f;
-#pragma unroll 8
-        for (int rr = 0; rr < kT; ++rr) acc = fmaf(pp[rr], vt_s[rr * kPad + c], acc);
-        float* o = o_s + (kvh * p.group + gi) * kHeadDim + c;
-        *o = *o * al_s[gi] + acc;
-      }
-      __syncthreads();
     }
   }
   __syncthreads();
-  for (int i = tid; i < n_q * kHeadDim; i += kThreads) {
-    const int h = i / kHeadDim, c = i % kHeadDim;
-    float* dst = p.partials + (((int64_t)b * n_q + h) * p.n_chunks + chunk) * kPart;
-    if (c == 0) {
-      dst[0] = m_s[h];
-      dst[1] = l_s[h];
-    }
-    dst[2 + c] = o_s[i];
+  float m[GROUP], l[GROUP], o[GROUP][8];
+#pragma unroll
+  for (int gi = 0; gi < GROUP; ++gi) {
+    m[gi] = -INFINITY;
+    l[gi] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[gi][j] = 0.f;
   }
+  const int64_t row0 = (int64_t)b * p.L_max;
+  const int bs = perm_block(XQ_A_CODES_CHANNEL, BITS);
+  int cur_grp = -1;
+  float2 kp[8];  // (scale, zp) of this lane's 8 K channels for the current token group
+  // warp w takes blocks of 2*kUnroll = 16 tokens (16-aligned: one RoPE base,
+  // one K group); half-warp `half` the tokens 2u + half
+  for (int wbase = t0 + warp * 2 * kUnroll; wbase < t1; wbase += kNw * 2 * kUnroll) {
+    const int grp = wbase / p.G;
+    if (grp != cur_grp && wbase < nfl) {
+      const __half* prow = p.k_params + (row0 / p.G + grp) * 2 * p.kvw;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = h * kHeadDim + 8 * hl + j;
+        const int ppos = (c / bs) * bs + perm_position(c % bs, bs);
+        kp[j] = make_float2(__half2float(prow[ppos]), __half2float(prow[p.kvw + ppos]));
+      }
+      cur_grp = grp;
+    }
+    float2 base[4];  // cos/sin(wbase theta_j) of this lane's 4 frequencies
+#pragma unroll
+    for (int j = 0; j < 4; ++j) base[j] = __ldg(p.rope + (int64_t)wbase * 64 + 4 * hl + j);
+    // load phase: raw codes (and V's per-token scale/zp) of kUnroll tokens in flight
+    uint2 kraw[kUnroll], vraw[kUnroll];
+    __half2 vsz[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int t = min(wbase + 2 * u + half, t1 - 1);
+      kraw[u] = raw8<BITS>(p.k_codes + (row0 + t) * p.row_bytes, h, hl);
+      vraw[u] = raw8<BITS>(p.v_codes + (row0 + t) * p.row_bytes, h, hl);
+      vsz[u] = p.v_params[(row0 + t) * p.vp_stride + h];  // G = 128: one group per head
+    }
+    // K phase: dequant + RoPE in registers, scores of the group's query heads
+    float sc[GROUP][kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int r = 2 * u + half;
+      const int t = min(wbase + r, t1 - 1);
+      float kv[8];
+      if (t < nfl) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          kv[j] = fmaf(static_cast<float>(code_j<BITS>(kraw[u], j)), kp[j].x, kp[j].y);
+      } else {
+        const float4* rr = reinterpret_cast<const float4*>(
+            p.k_resid + ((int64_t)b * p.G + (t - nfl)) * p.kvw + h * kHeadDim + 8 * hl);
+        const float4 a0 = rr[0], a1 = rr[1];
+        kv[0] = a0.x; kv[1] = a0.y; kv[2] = a0.z; kv[3] = a0.w;
+        kv[4] = a1.x; kv[5] = a1.y; kv[6] = a1.z; kv[7] = a1.w;
+      }
+      float kf[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // RoPE at position wbase + r (linalg.py:92-93)
+        const float2 of = s_off[r][4 * hl + j];
+        const float cs = base[j].x * of.x - base[j].y * of.y;
+        const float sn = base[j].y * of.x + base[j].x * of.y;
+        kf[2 * j] = kv[2 * j] * cs - kv[2 * j + 1] * sn;
+        kf[2 * j + 1] = kv[2 * j] * sn + kv[2 * j + 1] * cs;
+      }
+#pragma unroll
+      for (int gi = 0; gi < GROUP; ++gi) {
+        float d = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d = fmaf(q[gi][j], kf[j], d);
+#pragma unroll
+        for (int off = 8; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+        sc[gi][u] = (wbase + r < t1) ? d : -INFINITY;
+      }
+    }
+    float mn[GROUP];
+#pragma unroll
+    for (int gi = 0; gi < GROUP; ++gi) {
+      float mt = -INFINITY;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) mt = fmaxf(mt, sc[gi][u]);
+      mn[gi] = fmaxf(m[gi], mt);
+      const float alpha = (m[gi] == -INFINITY) ? 0.f : exp2f(m[gi] - mn[gi]);
+      l[gi] *= alpha;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[gi][j] *= alpha;
+      m[gi] = mn[gi];
+    }
+    // V phase: dequant once per token, p.V for every query head of the group
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int t = min(wbase + 2 * u + half, t1 - 1);
+      float vf[8];
+      if (t < vnfl) {
+        const float2 sz = __half22float2(vsz[u]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vf[j] = fmaf(static_cast<float>(code_j<BITS>(vraw[u], j)), sz.x, sz.y);
+      } else {
+        const float4* rr = reinterpret_cast<const float4*>(
+            p.v_resid + ((int64_t)b * p.G + (t - vnfl)) * p.kvw + h * kHeadDim + 8 * hl);
+        const float4 a0 = rr[0], a1 = rr[1];
+        vf[0] = a0.x; vf[1] = a0.y; vf[2] = a0.z; vf[3] = a0.w;
+        vf[4] = a1.x; vf[5] = a1.y; vf[6] = a1.z; vf[7] = a1.w;
+      }
+#pragma unroll
+      for (int gi = 0; gi < GROUP; ++gi) {
+        const float pr = (sc[gi][u] == -INFINITY) ? 0.f : exp2f(sc[gi][u] - mn[gi]);
+        l[gi] += pr;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[gi][j] = fmaf(pr, vf[j], o[gi][j]);
+      }
+    }
+  }
+  // merge the half-warp streams, one partial per CTA
+  __shared__ float s_m[kStreams][GROUP], s_l[kStreams][GROUP], s_o[kStreams][GROUP][kHeadDim];
+#pragma unroll
+  for (int gi = 0; gi < GROUP; ++gi) {
+    if (hl == 0) {
+      s_m[stream][gi] = m[gi];
+      s_l[stream][gi] = l[gi];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s_o[stream][gi][8 * hl + j] = o[gi][j];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < GROUP * kHeadDim; idx += kThreads) {
+    const int gi = idx / kHeadDim, d = idx % kHeadDim;
+    float M = -INFINITY;
+    for (int w = 0; w < kStreams; ++w) M = fmaxf(M, s_m[w][gi]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY)
+      for (int w = 0; w < kStreams; ++w) {
+        if (s_m[w][gi] == -INFINITY) continue;
+        const float wgt = exp2f(s_m[w][gi] - M);
+        L = fmaf(wgt, s_l[w][gi], L);
+        O = fmaf(wgt, s_o[w][gi][d], O);
+      }
+    float* dst = p.partials + (((int64_t)b * n_q + h * GROUP + gi) * p.n_chunks + chunk) * kPart;
+    if (d == 0) {
+      dst[0] = M;
+      dst[1] = L;
+    }
+    dst[2 + d] = O;
+  }
+}
+
+template <int GROUP>
+static int launch_bits(int bits, const Params& p, int grid, cudaStream_t st) {
+  switch (bits) {
+    case 2: k_kvq_decode<2, GROUP><<<grid, kThreads, 0, st>>>(p); break;
+    case 3: k_kvq_decode<3, GROUP><<<grid, kThreads, 0, st>>>(p); break;
+    case 4: k_kvq_decode<4, GROUP><<<grid, kThreads, 0, st>>>(p); break;
+    case 8: k_kvq_decode<8, GROUP><<<grid, kThreads, 0, st>>>(p); break;
+    default: return fail(XQ_ECONFIG, "bad bits %d", bits);
+  }
+  return check_launch("k_kvq_decode");
 }
 
 }  // namespace kvq
@@ -246,6 +280,7 @@ extern "C" {
 int64_t xq_kvq_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q_heads,
                                int32_t chunk_tokens) {
   if (chunk_tokens < kT) chunk_tokens = kT;
+  chunk_tokens = (chunk_tokens + 127) / 128 * 128;
   const int64_t n_chunks = max_len <= 0 ? 1 : (max_len + chunk_tokens - 1) / chunk_tokens;
   return (int64_t)n_seqs * n_q_heads * n_chunks * kPart * (int64_t)sizeof(float);
 }
@@ -264,7 +299,7 @@ int xq_kvq_decode_attend(const uint8_t* k_codes, const void* k_params, const flo
   XQ_REQUIRE(n_seqs >= 1 && n_kv_heads >= 1 && group >= 1, XQ_ESHAPE, "empty batch");
   XQ_REQUIRE(max_len >= 1 && max_len <= L_max, XQ_ESHAPE, "max_len out of range");
   if (chunk_tokens < kT) chunk_tokens = kT;
-  chunk_tokens = (chunk_tokens + kT - 1) / kT * kT;
+  chunk_tokens = (chunk_tokens + 127) / 128 * 128;  // blocks of 16 never straddle a K group
   XQ_REQUIRE(workspace_bytes >= xq_kvq_workspace_bytes(n_seqs, max_len, n_kv_heads * group,
                                                        chunk_tokens),
              XQ_ESHAPE, "workspace too small");
@@ -295,19 +330,15 @@ int xq_kvq_decode_attend(const uint8_t* k_codes, const void* k_params, const flo
   p.n_chunks = (max_len + chunk_tokens - 1) / chunk_tokens;
   p.partials = static_cast<float*>(workspace);
   const int n_q = n_kv_heads * group;
-  const size_t smem = sizeof(float) * (2 * (size_t)n_q * kHeadDim + 2 * kT * 64 + kvw +
-                                       2 * kT * kPad + (size_t)group * kT + group + 2 * n_q);
-  XQ_REQUIRE(smem <= 227 * 1024, XQ_ESHAPE, "kvq decode: shared memory plan does not fit");
-  static size_t configured = 0;
-  if (configured < smem) {
-    if (cudaFuncSetAttribute(k_kvq_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(kvq)");
-    configured = smem;
-  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  k_kvq_decode<<<n_seqs * p.n_chunks, kThreads, smem, st>>>(p);
-  int status = check_launch("k_kvq_decode");
+  const int grid = n_seqs * n_kv_heads * p.n_chunks;
+  int status;
+  switch (group) {
+    case 1: status = launch_bits<1>(bits, p, grid, st); break;
+    case 2: status = launch_bits<2>(bits, p, grid, st); break;
+    case 4: status = launch_bits<4>(bits, p, grid, st); break;
+    default: return fail(XQ_ECONFIG, "unsupported query group %d (1, 2, 4)", group);
+  }
   if (status != XQ_OK) return status;
   k_combine<<<static_cast<unsigned>(n_seqs) * n_q, kHeadDim, 0, st>>>(p.partials, p.n_chunks, out);
   return check_launch("k_combine(kvq)");

@@ -201,6 +201,8 @@ class Decoder:
     def _launches_per_layer(self, cache) -> int:
         if self.variant == "fp16":
             return 3  # kv_append, kv_decode, combine
+        if self.variant == "kvq":
+            return 2  # kvq decode, combine (+ quantizer launches on flushes)
         # fused decode + merge: absorbed = fused, combine, project; unabsorbed = fused, combine
         absorbed = cache._use_absorbed(cache_kdim(cache), int(cache.n_tokens.max()))
         attend = 3 if absorbed else 2

@@ -66,7 +66,7 @@ def cache_bytes(variant: str, seq_len: int, hidden_dim: int, bits: int, kv_group
         return 2.0 * 2.0 * seq_len * kvw
     if variant in ("xq-mha", "xq-cl-mha"):
         return pe * seq_len * d
-    if variant == "xq-gqa":
+    if variant in ("xq-gqa", "kvq"):
         return 2.0 * pe * seq_len * kvw
     raise ValueError(variant)
 
