@@ -107,7 +107,7 @@ struct Params {
   float* part_o;       // [n_seqs][n_tiles][n_q][kdim]
   float2* part_ml;     // [n_seqs][n_tiles][n_q] (m, l), m in the log2 domain
   uint64_t w_hint;
-  uint32_t off_p, off_codes, off_q, off_sc, off_rope, off_bar;
+  uint32_t off_p, off_codes, off_q, off_sc, off_rope, off_stg, off_bar;
 };
 
 // work unit u -> (sequence, tile); false when the tile is past the sequence end
@@ -116,6 +116,41 @@ XQ_DEVINL bool get_unit(const Params& p, int u, int& b, int& t, int& len) {
   t = u / p.n_seqs;
   len = __ldg(p.seq_lens + b);
   return t * kPairM < len;
+}
+
+struct Tile {
+  int b, t, len;
+};
+
+// Visit this cluster's tiles in the order the pipeline consumes them: the K
+// passes (kfn(tile, pass)) and the V side (vfn(tile)) of each tile. With PIPE
+// (double-buffered accumulators) the first K pass of the next tile is issued
+// before the V side of the current one, so the tensor cores have work while
+// the epilogue finishes the current tile's softmax. Every role walks the same
+// order, so the stage / accumulator counters stay in lock step.
+template <bool PIPE, typename KF, typename VF>
+XQ_DEVINL void walk(const Params& p, int cluster, int n_clusters, KF&& kfn, VF&& vfn) {
+  auto next_valid = [&](int u, Tile& tl) {
+    for (; u < p.n_units; u += n_clusters)
+      if (get_unit(p, u, tl.b, tl.t, tl.len)) return u;
+    return p.n_units;
+  };
+  Tile cur, nxt;
+  int u = next_valid(cluster, cur);
+  bool first = true;
+  while (u < p.n_units) {
+    const int nu = PIPE ? next_valid(u + n_clusters, nxt) : 0;
+    for (int ps = (PIPE && !first) ? 1 : 0; ps < p.n_pass; ++ps) kfn(cur, ps);
+    if (PIPE && nu < p.n_units) kfn(nxt, 0);
+    vfn(cur);
+    first = false;
+    if (PIPE) {
+      u = nu;
+      cur = nxt;
+    } else {
+      u = next_valid(u + n_clusters, cur);
+    }
+  }
 }
 
 template <int AK, int AV, int BITS, int GROUP>
@@ -173,7 +208,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int ngrp = p.kdim / kG;            // 128-channel groups
   const int nkc = p.kdim / kChunk;         // pass-1 stages per pass
   const int nblk = p.kdim / 256;           // V-side channel blocks (128 per CTA)
-  const int ncs = (p.n_pass + 1) * ngrp;   // codes stages per tile (pass-1 + V side)
   const int bpu = CF::kUseCols / p.nb;     // V-side blocks per accumulator
   const int nuse = (nblk + bpu - 1) / bpu;
 
@@ -220,14 +254,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
   const uint32_t pready_leader = mapa_shared(smem_u32(pready), 0);
 
+  constexpr bool PIPE = Cfg<GROUP>::NBUF == 2;  // see walk(): overlap tile k+1's first K pass with tile k's softmax
   if (warp == 0) {
     // ------------------------------------------------ TMA: W_k halves (+ fp16 A rows)
     uint32_t it = 0;
-    for (int u = cluster; u < p.n_units; u += n_clusters) {
-      int b, t, len;
-      if (!get_unit(p, u, b, t, len)) continue;
-      const int32_t row_tile = static_cast<int32_t>((int64_t)b * p.L_max + t * kPairM);
-      for (int ps = 0; ps < p.n_pass; ++ps) {
+    walk<PIPE>(p, cluster, n_clusters,
+      [&](const Tile& tl, int ps) {
+        const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
         for (int kc = 0; kc < nkc; ++kc, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           XQ_PROF(0, mbar_wait(&empty[s], ph ^ 1));
@@ -246,7 +279,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
         }
-      }
+      },
+      [&](const Tile& tl) {
+        const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
       for (int bb = 0; bb < nblk; ++bb) {
         for (int j = 0; j < 4; ++j, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
@@ -268,7 +303,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
       }
-    }
+      });
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader CTA only)
     if (leader) {
@@ -279,10 +314,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint64_t descp0 = sdesc_sw128(smem_u32(sP));
       const uint32_t pstage = p.nbh * 128;  // bytes of one 64-token P stage
       uint32_t it = 0, tc = 0, ti = 0;
-      for (int u = cluster; u < p.n_units; u += n_clusters) {
-        int b, t, len;
-        if (!get_unit(p, u, b, t, len)) continue;
-        for (int ps = 0; ps < p.n_pass; ++ps, ++tc) {
+      walk<PIPE>(p, cluster, n_clusters,
+        [&](const Tile&, int) {
           const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
           const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
           XQ_PROF(1, mbar_wait_cluster(&tempty[a], aph ^ 1));
@@ -307,7 +340,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           if (elect_one()) mma2_commit_both(&tfull[a]);
           __syncwarp();
-        }
+          ++tc;
+        },
+        [&](const Tile&) {
         // V side: needs this tile's P from both CTAs
         XQ_PROF(3, mbar_wait_cluster(pready, ti & 1));
         tc_fence_after();
@@ -338,28 +373,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
         ++ti;
-      }
+        });
     }
   } else if (warp == 2) {
     // ------------------------------------------------ TMA: codes ring
     if constexpr (PROD) {
       uint32_t ci = 0, cphase = 0;  // ring slot / phase of the next codes stage
-      for (int u = cluster; u < p.n_units; u += n_clusters) {
-        int b, t, len;
-        if (!get_unit(p, u, b, t, len)) continue;
-        const int32_t row_tile = static_cast<int32_t>((int64_t)b * p.L_max + t * kPairM);
-        int ps = 0, g = 0;  // K side: (pass, group); then V side: g = 2*bb + th
-        for (int q = 0; q < ncs; ++q) {
-          const uint32_t cs = ci, cph = cphase;
-          if (++ci == static_cast<uint32_t>(CSTAGES)) {
-            ci = 0;
-            cphase ^= 1u;
-          }
-          XQ_PROF(5, mbar_wait(&cempty[cs], cph ^ 1));
-          if (elect_one()) {
-            uint8_t* st = sC + cs * p.cstage_bytes;
-            if (ps < p.n_pass) {  // K side: group g of this CTA's 128 tokens
-              const int32_t arow = row_tile + rank * kTileM;
+      auto next_slot = [&](uint32_t& cs, uint32_t& cph) {
+        cs = ci;
+        cph = cphase;
+        if (++ci == static_cast<uint32_t>(CSTAGES)) {
+          ci = 0;
+          cphase ^= 1u;
+        }
+      };
+      walk<PIPE>(p, cluster, n_clusters,
+        [&](const Tile& tl, int) {  // K side: group g of this CTA's 128 tokens
+          const int32_t arow = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM) +
+                               static_cast<int32_t>(rank) * kTileM;
+          for (int g = 0; g < ngrp; ++g) {
+            uint32_t cs, cph;
+            next_slot(cs, cph);
+            XQ_PROF(5, mbar_wait(&cempty[cs], cph ^ 1));
+            if (elect_one()) {
+              uint8_t* st = sC + cs * p.cstage_bytes;
               mbar_arrive_expect_tx(&cfull[cs], p.k_tx);
               tma_load_2d(st, &tmap_ka, &cfull[cs], g * 16 * BITS, arow, kEvictNormal);
               if constexpr (AK == XQ_A_CODES_TOKEN)
@@ -367,7 +404,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               else
                 tma_load_2d(st + p.k_code_bytes, &tmap_kp, &cfull[cs], g * 128, 2 * (arow / kG),
                             kEvictNormal);
-            } else {  // V side: group 2*bb + rank of token half th of the pair tile
+            }
+            __syncwarp();
+          }
+        },
+        [&](const Tile& tl) {  // V side: group 2*bb + rank of token half th of the pair tile
+          const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
+          for (int g = 0; g < ngrp; ++g) {
+            uint32_t cs, cph;
+            next_slot(cs, cph);
+            XQ_PROF(5, mbar_wait(&cempty[cs], cph ^ 1));
+            if (elect_one()) {
+              uint8_t* st = sC + cs * p.cstage_bytes;
               const int gv = (g & ~1) + static_cast<int>(rank);
               const int32_t arow = row_tile + (g & 1) * kTileM;
               mbar_arrive_expect_tx(&cfull[cs], p.v_tx);
@@ -379,14 +427,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (gv & ~3), arow,
                             kEvictNormal);
             }
+            __syncwarp();
           }
-          __syncwarp();
-          if (++g == ngrp) {
-            g = 0;
-            ++ps;
-          }
-        }
-      }
+        });
     }
   } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
     // ------------------------------------------------ dequant producers
@@ -397,69 +440,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const RowSwizzle sw_v(r & 63);  // V side: row = token within a 64-token stage
       const int hh = r >> 6;          // V side: channel half of the group
       const uint32_t sAB_a = smem_u32(sAB), sC_a = smem_u32(sC);
-      // this group's codes stages are the running indices == gp (mod 2); ring
-      // slot / phase advance by 2 per stage (ncs is even), A stages by 4
+      // this group's codes stages are the running indices == gp (mod 2) (every
+      // K or V item has an even number ngrp of them); ring slot / phase advance
+      // by 2 per stage, A stages by 4
       uint32_t cs = static_cast<uint32_t>(gp), cph = 0;
       if (cs >= static_cast<uint32_t>(CSTAGES)) cs -= CSTAGES;  // (CSTAGES >= 2)
       uint32_t as = static_cast<uint32_t>(2 * gp) % STAGES, aph = (2 * gp) / STAGES;
-      for (int u = cluster; u < p.n_units; u += n_clusters) {
-        int b, t, len;
-        if (!get_unit(p, u, b, t, len)) continue;
-        const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + b) : 0;
-        const int tok_k = t * kPairM + rank * kTileM + r;
-        int g = gp, ps = 0;  // K side (pass ps, group g); V side (ps == n_pass): g = 2*bb + th
-        for (int q = gp; q < ncs; q += 2) {
-          const uint32_t st = sC_a + cs * p.cstage_bytes;
-          XQ_PROF(6, mbar_wait(&cfull[cs], cph));
-          const bool kside = ps < p.n_pass;
+      auto advance = [&]() {
+        cs += 2;
+        if (cs >= static_cast<uint32_t>(CSTAGES)) {
+          cs -= CSTAGES;
+          cph ^= 1u;
+        }
+        as += 4;
+        while (as >= STAGES) {
+          as -= STAGES;
+          aph ^= 1u;
+        }
+      };
+      // two A stages per codes stage; fill(tile address, h) writes stage h
+      auto stages2 = [&](auto&& fill) {
+        const uint32_t st = sC_a + cs * p.cstage_bytes;
+        XQ_PROF(6, mbar_wait(&cfull[cs], cph));
 #pragma unroll 1
-          for (int h = 0; h < 2; ++h) {
-            uint32_t s = as + h, ph = aph;
-            if (s >= STAGES) {
-              s -= STAGES;
-              ph ^= 1u;
-            }
-            XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
-            const uint32_t tile = sAB_a + s * kABStage;
-            if (kside) {
-              produce_chunk<AK, BITS>(tile, st, st + p.k_code_bytes, sw_k, r, tok_k < len, tok_k, b,
-                                      nfl, 2 * g + h, nullptr, p.k_resid, p.kdim);
-            } else {
+        for (int h = 0; h < 2; ++h) {
+          uint32_t s = as + h, ph = aph;
+          if (s >= STAGES) {
+            s -= STAGES;
+            ph ^= 1u;
+          }
+          XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
+          fill(sAB_a + s * kABStage, st, h);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (leader) mbar_arrive_if(&full[s], lane == 0);
+          else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
+        }
+        mbar_arrive_if(&cempty[cs], lane == 0);
+        advance();
+      };
+      walk<PIPE>(p, cluster, n_clusters,
+        [&](const Tile& tl, int) {
+          const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
+          const int tok_k = tl.t * kPairM + static_cast<int>(rank) * kTileM + r;
+          for (int g = gp; g < ngrp; g += 2)
+            stages2([&](uint32_t tile, uint32_t st, int h) {
+              produce_chunk<AK, BITS>(tile, st, st + p.k_code_bytes, sw_k, r, tok_k < tl.len,
+                                      tok_k, tl.b, nfl, 2 * g + h, nullptr, p.k_resid, p.kdim);
+            });
+        },
+        [&](const Tile& tl) {
+          const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
+          for (int g = gp; g < ngrp; g += 2)
+            stages2([&](uint32_t tile, uint32_t st, int h) {
               const int gv = (g & ~1) + static_cast<int>(rank);
               const int crow = h * 64 + (r & 63);
-              const int tok = t * kPairM + (g & 1) * kTileM + crow;
+              const int tok = tl.t * kPairM + (g & 1) * kTileM + crow;
               if constexpr (AV == XQ_A_CODES_TOKEN)
                 produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
-                                        tok < len, tok, b, 1 << 30, 2 * gv + hh, nullptr, nullptr,
-                                        p.kdim);
+                                        tok < tl.len, tok, tl.b, 1 << 30, 2 * gv + hh, nullptr,
+                                        nullptr, p.kdim);
               else if constexpr (AV == XQ_A_CODES_CHANNEL)  // same stream as the K side
                 produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
-                                        tok < len, tok, b, nfl, 2 * gv + hh, nullptr, p.k_resid,
-                                        p.kdim);
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (leader) mbar_arrive_if(&full[s], lane == 0);
-            else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
-          }
-          mbar_arrive_if(&cempty[cs], lane == 0);
-          g += 2;
-          if (g >= ngrp) {
-            g -= ngrp;
-            ++ps;
-          }
-          cs += 2;
-          if (cs >= static_cast<uint32_t>(CSTAGES)) {
-            cs -= CSTAGES;
-            cph ^= 1u;
-          }
-          as += 4;
-          while (as >= STAGES) {
-            as -= STAGES;
-            aph ^= 1u;
-          }
-        }
-      }
+                                        tok < tl.len, tok, tl.b, nfl, 2 * gv + hh, nullptr,
+                                        p.k_resid, p.kdim);
+            });
+        });
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------ epilogue (this CTA's 128 rows)
@@ -482,12 +528,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = et; i < 64 * 16; i += 128)
       rope_off[i] = p.rope[(int64_t)(i >> 4) * p.rope_n + (i & 15)];
     const int r0 = row & 15, r1 = row >> 4;
+    const uint32_t stg_a = smem_u32(smem + p.off_stg);
     uint32_t tc = 0, ti = 0;
-    for (int u = cluster; u < p.n_units; u += n_clusters) {
-      int b, t, len;
-      if (!get_unit(p, u, b, t, len)) continue;
+    walk<PIPE>(p, cluster, n_clusters,
+      [&](const Tile& tl, int ps) {
+      const int b = tl.b, t = tl.t, len = tl.len;
+      if (ps == 0) {  // tile setup: q rotated to len-1, the RoPE base rows
       const int pos = len - 1;
-      if (et == 0) tma_store_wait_read<0>();  // previous tile's O stores have read q_s / sc_s
+      if (!PIPE && et == 0) tma_store_wait_read<0>();  // previous tile's O stores have read q_s / sc_s
       named_bar_sync(1, 128);  // previous tile's readers of q_s / sc_s / rope_base are done
       for (int i = et; i < 8 * 64; i += 128) {  // base: cos/sin(t0 + 16*r1), t0 = tile row 0
         const int64_t tp = (int64_t)t * kPairM + rank * kTileM + 16 * (i >> 6);
@@ -504,6 +552,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       named_bar_sync(1, 128);
+      }
       const int tok = t * kPairM + rank * kTileM + row;
       const bool valid = tok < len;
       // ---- K side: scores of every query head for this CTA's 128 tokens.
@@ -517,7 +566,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           dst[i] = make_float2(bs.x * of.x - bs.y * of.y, bs.y * of.x + bs.x * of.y);
         }
       };
-      for (int ps = 0; ps < p.n_pass; ++ps, ++tc) {
         const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
         const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
         XQ_PROF(8, mbar_wait(&tfull[a], aph));
@@ -599,7 +647,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (leader) mbar_arrive(&tempty[a]);
           else mbar_arrive_remote(tempty_leader0 + 8 * a);
         }
-      }
+        ++tc;
+      if (ps == p.n_pass - 1) {
       // ---- exchange: the peer owns query heads [peer*nbh, peer*nbh + nbh)
 #ifdef XQ_ROLE_PROFILE
       const long long pt_x = clock64();
@@ -681,6 +730,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       ++ti;
+      }
+      },
+      [&](const Tile& tl) {
+      const int b = tl.b, t = tl.t;
       // ---- V side: drain O^T[channels x heads] of this tile
       int blk = 0;
       for (int us = 0; us < nuse; ++us, ++tc) {
@@ -695,9 +748,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // by one TMA bulk store. Staging buffers: the score region, plus the
         // q/P region when this is the tile's only V-side accumulator use (with
         // more uses, later uses' MMAs still read P while this one drains).
-        const bool two_bufs = nuse == 1;
+        // (pipelined: the next tile's scores and q already live there -> a
+        // dedicated staging buffer)
+        const bool two_bufs = !PIPE && nuse == 1;
         for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
-          const uint32_t stg = (two_bufs && (blk & 1)) ? q_a : sc_a;
+          const uint32_t stg = PIPE ? stg_a : ((two_bufs && (blk & 1)) ? q_a : sc_a);
           if (et == 0) {  // the store that last read `stg` is done
             if (two_bufs) tma_store_wait_read<1>();
             else tma_store_wait_read<0>();
@@ -731,7 +786,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           else mbar_arrive_remote(tempty_leader0 + 8 * a);
         }
       }
-    }
+      });
   }
   if (warp == kEpiWarp0 && lane == 0) tma_store_wait_all();
 #ifdef XQ_ROLE_PROFILE
@@ -980,8 +1035,14 @@ int plan_smem(Params& p, size_t& total) {
   // q (fp32 [n_q][128]) and P (fp16 [4][nbh][64]) share one region: P is
   // written after the tile's last use of q, and q is rewritten only after the
   // V-side MMAs that read P have completed
-  const uint32_t qp = ((512u * (p.n_q > p.nbh ? p.n_q : p.nbh)) + 1023u) / 1024u * 1024u;
-  const uint32_t fixed = qp                                 // q / P
+  // pipelined (double-buffered) configs keep P and a V staging buffer apart,
+  // the next tile's q and scores are live while this tile's V side drains
+  constexpr bool PIPE = Cfg<GROUP>::NBUF == 2;
+  const uint32_t qp = PIPE ? (512u * p.n_q + 1023u) / 1024u * 1024u
+                           : ((512u * (p.n_q > p.nbh ? p.n_q : p.nbh)) + 1023u) / 1024u * 1024u;
+  const uint32_t pbytes = PIPE ? (512u * p.nbh + 1023u) / 1024u * 1024u : 0u;
+  const uint32_t stg = PIPE ? 512u * p.n_q : 0u;
+  const uint32_t fixed = qp + pbytes + stg                  // q / P (+ P, staging)
                          + 512u * p.nb                      // scores (+ the peer's, exchanged)
                          + (64 * 16 + 8 * 64) * 8           // RoPE offset + base tables
                          + (4 * kMaxStages + 7) * 8 + 16;   // barriers + tmem slot
@@ -996,10 +1057,11 @@ int plan_smem(Params& p, size_t& total) {
   p.stages = stages;
   p.cstages = cstages;
   p.off_q = stages * kABStage;
-  p.off_p = p.off_q;
-  p.off_codes = p.off_q + qp;
+  p.off_p = PIPE ? p.off_q + qp : p.off_q;
+  p.off_codes = p.off_q + qp + pbytes;
   p.off_sc = p.off_codes + cstages * cst;
-  p.off_rope = p.off_sc + 512u * p.nb;
+  p.off_stg = p.off_sc + 512u * p.nb;
+  p.off_rope = p.off_stg + stg;
   p.off_bar = p.off_rope + (64 * 16 + 8 * 64) * 8;
   total = 1024 + need();
   return XQ_OK;
