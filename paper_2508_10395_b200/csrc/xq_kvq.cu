@@ -44,11 +44,12 @@ struct Params {
   float* partials;  // [n_seqs*n_q][n_chunks][130]
 };
 
-// `nbits` (<= 32) bits of a packed row starting at byte `off` (any alignment;
+// `nbytes` (<= 4) bytes of a packed row starting at byte `off` (any alignment;
 // rows are 8-byte aligned): two aligned 32-bit loads and a funnel shift.
-XQ_DEVINL uint32_t load_bits(const uint8_t* row, int64_t off) {
+XQ_DEVINL uint32_t load_bits(const uint8_t* row, int64_t off, int nbytes) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(row + (off & ~int64_t(3)));
-  const uint32_t lo = __ldg(w), hi = __ldg(w + 1);
+  // the second word only when the bits cross into it (never past the row end)
+  const uint32_t lo = __ldg(w), hi = ((off & 3) + nbytes > 4) ? __ldg(w + 1) : 0u;
   return __funnelshift_r(lo, hi, static_cast<uint32_t>(off & 3) * 8u);
 }
 
@@ -58,7 +59,7 @@ template <int BITS>
 XQ_DEVINL uint2 raw8(const uint8_t* row, int h, int hl) {
   const int64_t off = (int64_t)(h * kHeadDim + 8 * hl) * BITS / 8;  // byte-aligned: 8 codes
   if constexpr (BITS == 8) return __ldg(reinterpret_cast<const uint2*>(row + off));
-  return make_uint2(load_bits(row, off), 0u);
+  return make_uint2(load_bits(row, off, BITS), 0u);
 }
 template <int BITS>
 XQ_DEVINL uint32_t code_j(uint2 raw, int j) {

@@ -304,20 +304,40 @@ __global__ void k_arrange_weights(const void* __restrict__ w_k, const void* __re
   }
 }
 
-// XQuant-CL accumulator: one CTA per (slot, token); each thread 8 channels.
-__global__ void k_cl_accumulate(int seed, const uint8_t* __restrict__ codes, int64_t row_bytes,
-                                const __half2* __restrict__ params, int bits, int G, int64_t cols,
-                                const int32_t* __restrict__ lens, int32_t max_len, int64_t L_max,
-                                float* __restrict__ acc, __half* __restrict__ x16) {
-  const int b = blockIdx.x / max_len, t = blockIdx.x % max_len;
-  if (t >= lens[b]) return;
-  const int64_t r = (int64_t)b * L_max + t;
+// XQuant-CL accumulator (cache.py:139-146, :481): a grid-stride stream over
+// (slot, token, 8-channel chunk) items -- 32 B of fp32 acc in and out, 16 B of
+// fp16 copy out, bits bytes of codes and one (scale, zp) in per item, all as
+// whole-word loads; HBM-bound.
+__global__ void __launch_bounds__(256) k_cl_accumulate(
+    int seed, const uint8_t* __restrict__ codes, int64_t row_bytes,
+    const __half2* __restrict__ params, int bits, int G, int64_t cols,
+    const int32_t* __restrict__ lens, int32_t n_seqs, int32_t max_len, int64_t L_max,
+    float* __restrict__ acc, __half* __restrict__ x16) {
+  const int64_t per_row = cols / 8;
+  const int64_t total = (int64_t)n_seqs * max_len * per_row;
   const int64_t ng = param_stride(cols, G);
-  const uint8_t* crow = codes + r * row_bytes;
-  for (int64_t c0 = (int64_t)threadIdx.x * 8; c0 < cols; c0 += (int64_t)blockDim.x * 8) {
-    uint64_t packed = 0;  // 8 codes = `bits` bytes, starting at byte bits*c0/8
-    const uint8_t* src = crow + (c0 / 8) * bits;
-    for (int k = 0; k < bits; ++k) packed |= static_cast<uint64_t>(src[k]) << (8 * k);
+  const uint32_t mask = (1u << bits) - 1u;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rowi = i / per_row;
+    const int b = static_cast<int>(rowi / max_len), t = static_cast<int>(rowi % max_len);
+    if (t >= __ldg(lens + b)) continue;
+    const int64_t c0 = (i % per_row) * 8;
+    const int64_t r = (int64_t)b * L_max + t;
+    // 8 codes = `bits` bytes at byte bits*c0/8 of the row (8-byte aligned rows)
+    const uint8_t* crow = codes + r * row_bytes;
+    const int64_t off = (c0 / 8) * bits;
+    uint64_t packed;
+    {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(crow + (off & ~int64_t(3)));
+      // the second word only when the codes cross into it (never past the row)
+      const uint64_t lo = __ldg(w), hi = ((off & 3) + bits > 4) ? __ldg(w + 1) : 0u;
+      packed = (lo | (hi << 32)) >> ((off & 3) * 8);
+      if (bits == 8) {  // 8 bytes, 8-aligned: the two words are exactly the codes
+        packed = lo | (hi << 32);
+      }
+    }
+    const float2 sz = __half22float2(__ldg(params + r * ng + c0 / G));  // one group: 8 | G
     float4* a4 = reinterpret_cast<float4*>(acc + r * cols + c0);
     float v[8];
     if (seed) {
@@ -328,13 +348,9 @@ __global__ void k_cl_accumulate(int seed, const uint8_t* __restrict__ codes, int
       v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
       v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
     }
-    const uint32_t mask = (1u << bits) - 1;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const __half2 p = params[r * ng + (c0 + k) / G];
-      const float code = static_cast<float>((packed >> (k * bits)) & mask);
-      v[k] += fmaf(code, __low2float(p), __high2float(p));
-    }
+    for (int k = 0; k < 8; ++k)
+      v[k] += fmaf(static_cast<float>((packed >> (k * bits)) & mask), sz.x, sz.y);
     a4[0] = make_float4(v[0], v[1], v[2], v[3]);
     a4[1] = make_float4(v[4], v[5], v[6], v[7]);
     if (x16) {
@@ -506,10 +522,13 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
   XQ_REQUIRE(cols % 8 == 0, XQ_ESHAPE, "cols must be a multiple of 8");
   XQ_REQUIRE(max_len <= L_max, XQ_ESHAPE, "max_len > L_max");
   if (n_seqs == 0 || max_len == 0) return XQ_OK;
-  const int threads = static_cast<int>(cols / 8 < 512 ? cols / 8 : 512);
-  k_cl_accumulate<<<static_cast<unsigned>(n_seqs) * max_len, threads, 0, (cudaStream_t)stream>>>(
+  XQ_REQUIRE(group_size % 8 == 0, XQ_ECONFIG, "group_size must be a multiple of 8");
+  const int64_t items = (int64_t)n_seqs * max_len * (cols / 8);
+  int64_t blocks = (items + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_cl_accumulate<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
       seed, codes, row_bytes, static_cast<const __half2*>(params), bits, group_size, cols,
-      seq_lens, max_len, L_max, acc, static_cast<__half*>(x16_out));
+      seq_lens, n_seqs, max_len, L_max, acc, static_cast<__half*>(x16_out));
   return check_launch("xq_cl_accumulate");
 }
 
