@@ -204,9 +204,12 @@ int64_t xq_absorbed_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q
 
 /* Arguments as xq_decode_attend, with the two arranged weight buffers of
  * xq_arrange_weights_absorbed in place of w_arranged. out: float32
- * [n_seqs, n_kv_heads*group, 128]. */
+ * [n_seqs, n_kv_heads*group, 128]. ak_first (nullable, CODES_CHANNEL K side
+ * only): float32 per arena row, the full-precision channel 0 of the flushed
+ * K-latent rows -- the fp16 outlier channel of cache.py:406-411 / :653-658. */
 int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* ak_params,
-                              const float* ak_resid, const int32_t* ak_nflushed, int32_t ak_bits,
+                              const float* ak_resid, const int32_t* ak_nflushed,
+                              const float* ak_first, int32_t ak_bits,
                               int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
                               const void* av_params, int32_t av_bits, int64_t av_row_bytes,
                               int32_t group_size, int64_t L_max, int64_t kdim,

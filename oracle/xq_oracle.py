@@ -246,15 +246,19 @@ class Stream:
     """
 
     def __init__(self, bits: int, axis: int, width: int, group_size: int, buffered: bool,
-                 params_f16: bool = False):
+                 params_f16: bool = False, keep_first_channel: bool = False):
         """``params_f16``: dequantize with the scale / zero point rounded to fp16,
         the storage format of the B200 arena (the reference charges 16+16 bits per
         group, quant.py:44-45, but keeps float64 in memory)."""
         self.params_f16 = params_f16
+        # channel 0 verbatim, the rest quantized (cache.py:174-177, 184-189, 223-230)
+        self.keep_first = keep_first_channel and bits != 16
+        self.first = np.zeros(0)
         self.bits, self.axis, self.width, self.g = bits, axis, width, group_size
+        stored = width - 1 if self.keep_first else width
         self.buffered = buffered or axis == PER_CHANNEL  # cache.py:173
-        self.codes = np.zeros((0, width), np.uint8) if bits != 16 else np.zeros((0, width))
-        ngrid = (0, -(-width // group_size)) if axis == PER_TOKEN else (0, width)
+        self.codes = np.zeros((0, stored), np.uint8) if bits != 16 else np.zeros((0, stored))
+        ngrid = (0, -(-stored // group_size)) if axis == PER_TOKEN else (0, stored)
         self.scales = np.zeros(ngrid)
         self.zps = np.zeros(ngrid)
         self.buf = np.zeros((0, width))
@@ -263,6 +267,9 @@ class Stream:
         return self.codes.shape[0] + self.buf.shape[0]
 
     def _flush(self, block):  # cache.py:184-189 -> quant.append_rows (quant.py:210-228)
+        if self.keep_first:
+            self.first = np.concatenate([self.first, block[:, 0]])
+            block = np.ascontiguousarray(block[:, 1:])
         c, s, z = quantize(block, self.bits, self.axis, self.g)
         self.codes = np.vstack([self.codes, c])
         if s is not None:
@@ -296,6 +303,8 @@ class Stream:
         if self.params_f16 and self.bits != 16:
             sc, zp = sc.astype(np.float16).astype(np.float64), zp.astype(np.float16).astype(np.float64)
         flushed = dequantize(self.codes, sc, zp, self.bits, self.axis, self.g)
+        if self.keep_first:
+            flushed = np.hstack([self.first[:, None], flushed])
         if len(self.buf):
             return np.vstack([flushed, self.buf])
         return flushed
@@ -382,15 +391,17 @@ class XqGqaCache:
     V latent = x @ U_v per-token. Remat through fused = diag(sigma) B^T.
     """
 
-    def __init__(self, bits, head_dim, group_size=128):
+    def __init__(self, bits, head_dim, group_size=128, fp16_first_channel=False):
         self.hd = head_dim
         self.bits, self.g = bits, group_size
+        self.first = fp16_first_channel  # cache.py:403-409
         self.k_stream = None
         self.v_stream = None
 
     def _ensure(self, r):
         if self.k_stream is None:
-            self.k_stream = Stream(self.bits, PER_CHANNEL, r, self.g, buffered=True)
+            self.k_stream = Stream(self.bits, PER_CHANNEL, r, self.g, buffered=True,
+                                   keep_first_channel=self.first)
             self.v_stream = Stream(self.bits, PER_TOKEN, r, self.g, buffered=False)
 
     def prefill(self, lat_k, lat_v):  # cache.py:422-427 (latents precomputed)

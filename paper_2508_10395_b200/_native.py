@@ -42,7 +42,7 @@ _SIGS = {
                          _I64, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _I64, _F, _I32, _P, _I64,
                          _P, _P],
     "xq_arrange_weights_absorbed": [_P, _P, _I32, _I64, _I32, _I32, _I32, _I32, _I32, _P, _P, _P],
-    "xq_decode_attend_absorbed": [_I32, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32,
+    "xq_decode_attend_absorbed": [_I32, _P, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32,
                                   _I64, _I64, _P, _I32, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _F,
                                   _P, _I64, _P, _P],
     "xq_remat_f32": [_I32, _P, _P, _P, _I32, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32, _I64,

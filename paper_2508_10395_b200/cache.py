@@ -224,7 +224,7 @@ class PackedStream:
     """
 
     def __init__(self, bits, axis, width, group_size, n_slots, max_len, device, resid_f64=False,
-                 buffered=False):
+                 buffered=False, keep_first=False):
         """``resid_f64``: per-channel only -- keep the residual rows in float64 as
         well (quantized from float64, like the reference); ``resid`` is then
         their float32 mirror read by the fused kernel."""
@@ -251,6 +251,10 @@ class PackedStream:
             self.resid = torch.zeros((n_slots, group_size, width), dtype=torch.float32, device=device)
             self.resid64 = (torch.zeros((n_slots, group_size, width), dtype=torch.float64, device=device)
                             if resid_f64 else None)
+            # fp16 outlier channel (cache.py:406-411): channel 0 of the flushed rows
+            # kept in full precision (float32 per arena row) beside the codes
+            self.first = (torch.zeros(n_slots * max_len, dtype=torch.float32, device=device)
+                          if keep_first else None)
             self.n_flushed = np.zeros(n_slots, dtype=np.int64)
             self.nflushed_dev = torch.zeros(n_slots, dtype=torch.int32, device=device)
         self.flag = torch.zeros(1, dtype=torch.int32, device=device)
@@ -263,6 +267,8 @@ class PackedStream:
             out["residual"] = self.resid.numel() * 4
             if self.resid64 is not None:
                 out["residual_f64"] = self.resid64.numel() * 8
+            if self.first is not None:
+                out["first_channel_f32"] = self.first.numel() * 4
         return out
 
     # -- per-token ---------------------------------------------------------
@@ -304,6 +310,9 @@ class PackedStream:
     # -- per-channel -------------------------------------------------------
     def flush_blocks(self, blocks: torch.Tensor, dst_row0: list[int]):
         dst = torch.tensor(dst_row0, dtype=torch.int64, device=blocks.device)
+        if getattr(self, "first", None) is not None:
+            rows = dst[:, None] + torch.arange(self.g, device=blocks.device)[None, :]
+            self.first[rows.reshape(-1)] = blocks.reshape(-1, self.width)[:, 0].float()
         fn = ("xq_quantize_blocks_per_channel_f64" if blocks.dtype == torch.float64
               else "xq_quantize_blocks_per_channel")
         N.call(fn, N.ptr(blocks), len(dst_row0), self.width,
@@ -350,6 +359,8 @@ class PackedStream:
             N.call("xq_dequant_rows", N.ptr(self.codes), self.row_bytes, N.ptr(self.params), CHANNEL,
                    self.bits, self.g, self.width, slot * self.L, nfl, N.ptr(out),
                    N.stream_of(out.device))
+        if nfl and self.first is not None:
+            out[:nfl, 0] = self.first[slot * self.L:slot * self.L + nfl]
         out[nfl:] = self.resid[slot, :n - nfl]
         return out
 
@@ -587,7 +598,7 @@ class CacheBackend:
 
     def _fused(self, ak_mode, ak_src, ak_params, ak_resid, ak_nfl, ak_bits, ak_rb, av_mode,
                av_src, av_params, av_bits, av_rb, kdim, w_spec, weights, group, q, lens, max_len,
-               out, tpc, force_absorbed=False):
+               out, tpc, force_absorbed=False, ak_first=None):
         """One fused decode launch. ``w_spec`` = (key, a_mode_k, bits_k, a_mode_v, bits_v,
         W_k, W_v) names the projection pair and the A operands that feed it."""
         key, mk, bk, mv, bv, wk, wv = w_spec
@@ -597,7 +608,7 @@ class CacheBackend:
             nbytes = N.lib.xq_absorbed_workspace_bytes(self.n_slots, max_len, self.n_kv * group, kdim)
             ws = _scratch(self.device, nbytes)
             N.call("xq_decode_attend_absorbed", ak_mode, N.ptr(ak_src), N.ptr(ak_params),
-                   N.ptr(ak_resid), N.ptr(ak_nfl), ak_bits, ak_rb, av_mode, N.ptr(av_src),
+                   N.ptr(ak_resid), N.ptr(ak_nfl), N.ptr(ak_first), ak_bits, ak_rb, av_mode, N.ptr(av_src),
                    N.ptr(av_params), av_bits, av_rb, self.group_size, self.L, kdim, N.ptr(lens),
                    self.n_slots, max_len, N.ptr(wk_arr), N.ptr(wv_arr), self.n_kv, group, N.ptr(q),
                    N.ptr(rope), rope.shape[1] // 2, 1.0 / math.sqrt(HEAD_DIM), N.ptr(ws), nbytes,
@@ -876,10 +887,19 @@ class LatentInputCacheGQA(CacheBackend):
         if self.bits == 16:
             raise ConfigError("xq-gqa on the B200 path needs a quantized width (2/3/4/8)")
         r = self.latent  # the latent cache is whole even when heads are sharded
+        self.fp16_first_channel = False
         self.k_stream = PackedStream(self.bits, CHANNEL, r, self.group_size, self.n_slots, self.L,
                                      self.device)
         self.v_stream = PackedStream(self.bits, TOKEN, r, self.group_size, self.n_slots, self.L,
                                      self.device)
+
+    def set_fp16_first_channel(self, enable: bool) -> None:
+        """Pin channel 0 of the K latent to full precision (cache.py:403-409)."""
+        if np.any(self.n_tokens):
+            raise UsageError("toggle the full-precision channel before caching")
+        self.fp16_first_channel = bool(enable)
+        self.k_stream = PackedStream(self.bits, CHANNEL, self.latent, self.group_size, self.n_slots,
+                                     self.L, self.device, keep_first=self.fp16_first_channel)
 
     def _latents(self, x, weights):
         xf = x.float()
@@ -902,6 +922,10 @@ class LatentInputCacheGQA(CacheBackend):
 
     def _rematerialize(self, weights, acc, slot, n):
         ks, vs = self.k_stream, self.v_stream
+        if ks.first is not None:  # float32 torch path (the SIMT debug kernel has no outlier channel)
+            k = ks.channel_reconstruct(slot, n) @ weights.f32("fused_k")
+            v = self._dequant_rows(vs, slot, n) @ weights.f32("fused_v")
+            return _rope_rows(k, 0, self.device), v
         return self._remat_f32(N.A_CODES_CHANNEL, ks.codes, ks.params, ks.resid,
                                int(ks.n_flushed[slot]), ks.bits, ks.row_bytes, N.A_CODES_TOKEN,
                                vs.codes, vs.params, vs.bits, vs.row_bytes, self.latent,
@@ -913,7 +937,8 @@ class LatentInputCacheGQA(CacheBackend):
                 weights.fused_k, weights.fused_v)
         self._fused(N.A_CODES_CHANNEL, ks.codes, ks.params, ks.resid, ks.nflushed_dev, ks.bits,
                     ks.row_bytes, N.A_CODES_TOKEN, vs.codes, vs.params, vs.bits, vs.row_bytes,
-                    self.latent, spec, weights, self.g, q, lens, max_len, out, tpc)
+                    self.latent, spec, weights, self.g, q, lens, max_len, out, tpc,
+                    force_absorbed=ks.first is not None, ak_first=ks.first)
 
     def memory_bytes(self):
         out = {f"k_{k}": v for k, v in self.k_stream.nbytes().items()}
@@ -1173,6 +1198,14 @@ _BACKENDS = {
     for cls in (FullPrecisionCache, QuantizedKvCache, InputCacheMHA, LatentInputCacheGQA, DeltaInputCacheMHA,
                 DeltaLatentCacheGQA)
 }
+
+
+def fp16_outlier_channel_variant(state: CacheBackend, enable: bool) -> CacheBackend:
+    """Pin channel 0 of the K latent to full precision (cache.py:653-658; xq-gqa only)."""
+    if not isinstance(state, LatentInputCacheGQA):
+        raise UsageError("full-precision outlier channel applies to xq-gqa only")
+    state.set_fp16_first_channel(enable)
+    return state
 
 
 def make_cache(variant: str, layer_index: int, policy: LayerPolicy, head_dim: int,

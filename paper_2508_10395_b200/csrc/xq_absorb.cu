@@ -92,6 +92,7 @@ constexpr uint32_t kMNHalf = 64 * 128;      // V-side A stage: [64 tok x 64 ch] 
 struct Params {
   const float* k_resid;        // CODES_CHANNEL: fp32 residual rows [n_seqs][128][kdim]
   const int32_t* k_nflushed;   // CODES_CHANNEL: flushed token count per sequence
+  const float* k_first;        // CODES_CHANNEL: fp32 channel 0 per arena row (outlier channel) or null
   int32_t kdim;
   int64_t L_max;
   const int32_t* seq_lens;
@@ -486,7 +487,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int g = gp; g < ngrp; g += 2)
             stages2([&](uint32_t tile, uint32_t st, int h) {
               produce_chunk<AK, BITS>(tile, st, st + p.k_code_bytes, sw_k, r, tok_k < tl.len,
-                                      tok_k, tl.b, nfl, 2 * g + h, nullptr, p.k_resid, p.kdim);
+                                      tok_k, tl.b, nfl, 2 * g + h,
+                                      p.k_first ? p.k_first + (int64_t)tl.b * p.L_max + tok_k : nullptr,
+                                      p.k_resid, p.kdim);
             });
         },
         [&](const Tile& tl) {
@@ -1149,7 +1152,8 @@ int xq_arrange_weights_absorbed(const void* w_k, const void* w_v, int32_t w_dtyp
 }
 
 int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* ak_params,
-                              const float* ak_resid, const int32_t* ak_nflushed, int32_t ak_bits,
+                              const float* ak_resid, const int32_t* ak_nflushed,
+                              const float* ak_first, int32_t ak_bits,
                               int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
                               const void* av_params, int32_t av_bits, int64_t av_row_bytes,
                               int32_t group_size, int64_t L_max, int64_t kdim,
@@ -1210,6 +1214,9 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
     return st_;
   Params p;
   p.k_resid = ak_resid;
+  XQ_REQUIRE(ak_first == nullptr || (ak_mode == XQ_A_CODES_CHANNEL && !mha), XQ_ECONFIG,
+             "the full-precision first channel applies to the per-channel K latent (xq-gqa)");
+  p.k_first = ak_first;
   p.k_nflushed = ak_nflushed;
   p.kdim = static_cast<int32_t>(kdim);
   p.L_max = L_max;

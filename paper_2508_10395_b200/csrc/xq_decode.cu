@@ -364,10 +364,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               mbar_wait(&empty[s], ph ^ 1);
               const uint32_t tile = sAB_a + s * R::kABStage;
               produce_chunk<AK, BITS>(tile, st + R::code_off(0), st + R::param_off(0), sw, row,
-                                      valid, tok, w.b, nfl, kc, p.ak_params, p.ak_resid, p.kdim);
+                                      valid, tok, w.b, nfl, kc, nullptr, p.ak_resid, p.kdim);
               if constexpr (A_TILES == 2)
                 produce_chunk<AVM, BITS>(tile + kABytes, st + R::code_off(1), st + R::param_off(1),
-                                         sw, row, valid, tok, w.b, 1 << 30, kc, p.av_params,
+                                         sw, row, valid, tok, w.b, 1 << 30, kc, nullptr,
                                          nullptr, p.kdim);
               fence_proxy_async_smem();
               __syncwarp();

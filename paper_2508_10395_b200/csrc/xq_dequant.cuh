@@ -116,8 +116,8 @@ struct RowSwizzle {
 // tile / cstage / pstage are 32-bit shared addresses.
 template <int MODE, int BITS>
 XQ_DEVINL void produce_chunk(uint32_t tile, uint32_t cstage, uint32_t pstage, const RowSwizzle& sw,
-                             int row, bool valid, int tok, int b, int nflushed, int kc, const void* gparams, const float* resid,
-                             int kdim) {
+                             int row, bool valid, int tok, int b, int nflushed, int kc,
+                             const float* first_row, const float* resid, int kdim) {
   uint32_t v[32];
   if (!valid) {
 #pragma unroll
@@ -152,6 +152,10 @@ XQ_DEVINL void produce_chunk(uint32_t tile, uint32_t cstage, uint32_t pstage, co
         z2[4 * c + 2] = from_u32<__half2>(z.z); z2[4 * c + 3] = from_u32<__half2>(z.w);
       }
       convert_raw<BITS, true>(raw, s2, z2, v);
+      // fp16 outlier channel (cache.py:406-411): channel 0 (position 0 of the
+      // first block in producer order) kept in full precision beside the codes
+      if (first_row != nullptr && kc == 0)
+        v[0] = as_u32(__halves2half2(__float2half_rn(*first_row), __high2half(from_u32<__half2>(v[0]))));
     } else {  // residual full-precision row (cache.py:228-229)
       const float* r = resid + ((int64_t)b * kDqG + (tok - nflushed)) * kdim + kc * kDqChunk;
 #pragma unroll

@@ -324,6 +324,31 @@ def main():
         "kvq_vcodes": st.v_stream.q.codes, "kvq_vscales": st.v_stream.q.scales,
         "kvq_vbuf": np.asarray(st.v_stream.buf.tokens, np.float64),
     })
+
+    # xq-gqa with the fp16 outlier channel (cache.py:403-409, 653-658): the same
+    # inputs as the xq-gqa case above, channel 0 of the K latent in full precision
+    from xcache.cache import fp16_outlier_channel_variant
+    d, H, g = 1024, 8, 4
+    r = d // g
+    x = from_bf16_bits(be["gqa_x"])
+    u_k, u_v = from_bf16_bits(be["gqa_uk"]), from_bf16_bits(be["gqa_uv"])
+    f_k, f_v = from_bf16_bits(be["gqa_fk"]), from_bf16_bits(be["gqa_fv"])
+    q = from_bf16_bits(be["gqa_q"])
+    svd_k = SvdFactors(u=u_k, sigma=np.ones(r), b_t=f_k, fused=f_k)
+    svd_v = SvdFactors(u=u_v, sigma=np.ones(r), b_t=f_v, fused=f_v)
+    lw = dummy_lw(d, r, u_k @ f_k, u_v @ f_v, svd_k=svd_k, svd_v=svd_v)
+    st = fp16_outlier_channel_variant(make_cache("xq-gqa", 0, LayerPolicy.uniform(3, 1), 128,
+                                                 group_size=128), True)
+    st.prefill(x[:250], lw)
+    outs = []
+    for t in range(12):
+        st.decode_append(x[250 + t], lw)
+        k, v = st.rematerialize(lw, np.arange(250 + t + 1))
+        qr = apply_rope(q[t:t + 1], np.array([250 + t]), 128)
+        outs.append(_attention(qr, k, v, H, g)[0])
+    be.update({"gqa1_attn": np.stack(outs), "gqa1_k": k.astype(np.float32),
+               "gqa1_kcodes": st.k_stream.q.codes, "gqa1_kscales": st.k_stream.q.scales,
+               "gqa1_first": np.asarray(st.k_stream.first_channel, np.float64)})
     np.savez_compressed(os.path.join(HERE, "backends.npz"), **be)
 
     for f in ("quant", "pack", "rope", "backends"):

@@ -308,3 +308,37 @@ def test_xqt1_export_per_channel(M):
     gs = got[24:24 + 2 * n_grid].view(np.float64)
     rs = ref[24:24 + 2 * n_grid].view(np.float64)
     assert np.max(np.abs(gs - rs) / np.maximum(np.abs(rs), 1e-3)) <= 2e-3
+
+
+def test_xq_gqa_fp16_outlier_channel_against_reference(M):
+    """fp16 outlier channel (cache.py:403-409, 653-658): channel 0 of the K latent
+    in full precision. The reference's run on the xq-gqa golden inputs; codes of
+    channels 1..r-1 bit-exact (stage-wise: the GPU latent is an fp32 GEMV)."""
+    import torch
+
+    import xq_oracle as O
+
+    z = golden("backends")
+    x = torch_bf16(z["gqa_x"])
+    q = torch_bf16(z["gqa_q"]).float()
+    w = _weights(M, u_k=torch_bf16(z["gqa_uk"]), u_v=torch_bf16(z["gqa_uv"]),
+                 fused_k=torch_bf16(z["gqa_fk"]), fused_v=torch_bf16(z["gqa_fv"]))
+    st = M.make_cache("xq-gqa", 0, M.LayerPolicy.uniform(3, 1), 128, 128, n_slots=1,
+                      max_len=512, hidden_dim=1024, n_heads=8, kv_group=4)
+    M.fp16_outlier_channel_variant(st, True)
+    st.prefill(x[:250], w)
+    errs = []
+    for t in range(12):
+        st.decode_append(x[250 + t][None], w)
+        out = st.decode_attend(q[t][None], w)
+        errs.append(rel_err(out.reshape(-1).cpu().numpy(), z["gqa1_attn"][t]))
+    assert max(errs) <= FUSED_TOL, errs
+    kk, _ = st.rematerialize(w, np.arange(262))
+    assert rel_err(kk.cpu().numpy(), z["gqa1_k"]) <= 2e-2
+    ks = st.k_stream
+    got = ks.codes[:256].cpu().numpy()
+    un = np.stack([O.unpack_codes(got[r].view(np.uint64), 3, 256) for r in range(256)])
+    assert np.mean(un[:, 1:] != z["gqa1_kcodes"]) <= 1e-3
+    assert rel_err(ks.first[:256].cpu().numpy(), z["gqa1_first"]) <= 1e-5
+    with pytest.raises(M.UsageError):
+        M.fp16_outlier_channel_variant(st, False)  # not on a non-empty cache

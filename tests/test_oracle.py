@@ -219,6 +219,25 @@ class TestBackendsGolden:
         assert rel(np.stack(outs), z["kvq_attn"]) <= 1e-12
 
 
+    def test_xq_gqa_fp16_first_channel(self):
+        z = load("backends")
+        x, q = bf16f(z["gqa_x"]), bf16f(z["gqa_q"])
+        uk, uv = bf16f(z["gqa_uk"]), bf16f(z["gqa_uv"])
+        fk, fv = bf16f(z["gqa_fk"]), bf16f(z["gqa_fv"])
+        st = O.XqGqaCache(3, 128, 128, fp16_first_channel=True)
+        st.prefill(x[:250] @ uk, x[:250] @ uv)
+        outs = []
+        for t in range(12):
+            st.push(x[250 + t] @ uk, x[250 + t] @ uv)
+            kk, vv = st.remat(fk, fv)
+            outs.append(O.attention(O.apply_rope(q[t:t + 1], [250 + t], 128), kk, vv, 8, 4)[0])
+        assert np.array_equal(st.k_stream.codes, z["gqa1_kcodes"])
+        assert np.array_equal(st.k_stream.scales, z["gqa1_kscales"])
+        assert rel(st.k_stream.first, z["gqa1_first"]) <= 1e-12
+        assert rel(kk, z["gqa1_k"]) <= 1e-6
+        assert rel(np.stack(outs), z["gqa1_attn"]) <= 1e-12
+
+
 class TestSysmodel:
     def test_compression_factors(self):
         # PAPER.md:371/373/563-579 via sysmodel.normalized_kv_size
