@@ -902,8 +902,13 @@ class LatentInputCacheGQA(CacheBackend):
                                      self.L, self.device, keep_first=self.fp16_first_channel)
 
     def _latents(self, x, weights):
-        xf = x.float()
-        return xf @ weights.f32("u_k"), xf @ weights.f32("u_v")
+        # one float32 GEMM against [U_k | U_v] (cache.py:429-432)
+        key = ("f32", "u_kv_cat")
+        if key not in weights._cache:
+            weights._cache[key] = torch.cat([weights.f32("u_k"), weights.f32("u_v")], dim=1).contiguous()
+        lat = x.float() @ weights._cache[key]
+        r = self.latent
+        return lat[:, :r], lat[:, r:]
 
     def _prefill(self, slot, x, weights, acc):
         lat_k, lat_v = self._latents(x, weights)
