@@ -250,7 +250,9 @@ int xq_remat_f32(int32_t ak_mode, const void* ak_src, const void* ak_params,
  *   seed != 0 : acc = deq(codes)          (base layer seeds, cache.py:473-477)
  *   seed == 0 : acc = acc + deq(codes)    (delta layer, cache.py:481)
  * and, if x16_out != NULL, x16_out = fp16(acc) for the remat A operand.
- * acc/x16_out: [n_slots*L_max][cols]. */
+ * acc == NULL: fp16-storage accumulator -- x16_out is the accumulator itself
+ * (read, updated, written back in fp16; the reference's accounting charges the
+ * accumulator 4 bits, cache.py:45, 129-133). acc/x16_out: [n_slots*L_max][cols]. */
 int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, const void* params,
                      int32_t bits, int32_t group_size, int64_t cols, const int32_t* seq_lens,
                      int32_t n_seqs, int32_t max_len, int64_t L_max, float* acc, void* x16_out,

@@ -203,10 +203,21 @@ class Accumulator:
     base layer re-seeds it every step (model.py:228); the memory is reused.
     """
 
-    def __init__(self, n_slots: int, max_len: int, width: int, device="cuda"):
-        self.x_hat = torch.zeros((n_slots, max_len, width), dtype=torch.float32, device=device)
+    def __init__(self, n_slots: int, max_len: int, width: int, device="cuda", precision="fp32"):
+        """precision "fp16": the fp16 copy is the accumulator (``x_hat`` is None),
+        which halves the per-layer accumulate traffic twice over (xq-cl-mha
+        only; the reference charges the accumulator 4 bits, cache.py:45)."""
+        if precision not in ("fp32", "fp16"):
+            raise ConfigError(f"accumulator precision {precision!r}")
+        self.precision = precision
+        self.x_hat = (torch.zeros((n_slots, max_len, width), dtype=torch.float32, device=device)
+                      if precision == "fp32" else None)
         self.x16 = torch.zeros((n_slots, max_len, width), dtype=torch.float16, device=device)
         self.seeded = False
+
+    def rows(self, slot, n) -> torch.Tensor:
+        """float32 view/copy of the accumulator rows 0..n-1 of a slot."""
+        return self.x_hat[slot, :n] if self.x_hat is not None else self.x16[slot, :n].float()
 
 
 # ---------------------------------------------------------------------------
@@ -979,9 +990,10 @@ class DeltaInputCacheMHA(CacheBackend):
 
     def _accumulate(self, acc, seed, max_len, lens):
         s = self.stream
+        x16 = acc.x16 if (acc.x_hat is None or not seed) else None
         N.call("xq_cl_accumulate", 1 if seed else 0, N.ptr(s.codes), s.row_bytes, N.ptr(s.params),
                s.bits, self.group_size, self.d, N.ptr(lens), self.n_slots, max_len, self.L,
-               N.ptr(acc.x_hat), None if seed else N.ptr(acc.x16), N.stream_of(self.device))
+               N.ptr(acc.x_hat), N.ptr(x16), N.stream_of(self.device))
         acc.seeded = True
 
     def _prefill(self, slot, x, weights, acc):
@@ -995,8 +1007,10 @@ class DeltaInputCacheMHA(CacheBackend):
             return
         if not acc.seeded:
             raise UsageError("accumulator used before the base layer seeded it")
-        sub = acc.x_hat.view(-1, self.d)
-        self.stream.fill_rows(x.contiguous(), slot, 0, sub=sub)
+        if acc.x_hat is None:  # fp16 accumulator: the delta in float32 here
+            self.stream.fill_rows((x.float() - acc.x16[slot, :n].float()).contiguous(), slot, 0)
+        else:
+            self.stream.fill_rows(x.contiguous(), slot, 0, sub=acc.x_hat.view(-1, self.d))
         self._accumulate(acc, False, n, lens)
 
     def _decode(self, x, weights, acc, lens):
@@ -1008,11 +1022,16 @@ class DeltaInputCacheMHA(CacheBackend):
             return
         if not acc.seeded:
             raise UsageError("accumulator used before the base layer seeded it")
-        self.stream.append_token_rows(x.contiguous(), lens, sub=acc.x_hat.view(-1, self.d))
+        if acc.x_hat is None:  # fp16 accumulator: x - acc[pos] in float32 here
+            pos = torch.as_tensor(self.n_tokens - 1, device=self.device)
+            rows = acc.x16[torch.arange(self.n_slots, device=self.device), pos].float()
+            self.stream.append_token_rows((x.float() - rows).contiguous(), lens)
+        else:
+            self.stream.append_token_rows(x.contiguous(), lens, sub=acc.x_hat.view(-1, self.d))
         self._accumulate(acc, False, max_len, lens)
 
     def _prefill_kv(self, weights, acc, slot, n):
-        a = self._dequant_rows(self.stream, slot, n) if self.is_base else acc.x_hat[slot, :n]
+        a = self._dequant_rows(self.stream, slot, n) if self.is_base else acc.rows(slot, n)
         return self._kv_from(a, a, weights.w_k, weights.w_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
@@ -1025,7 +1044,7 @@ class DeltaInputCacheMHA(CacheBackend):
 
     def _remat_acc(self, acc, wk, wv, slot, n):
         # parity path from the float32 accumulator itself (cache.py:531-535)
-        xh = acc.x_hat[slot, :n]
+        xh = acc.rows(slot, n)
         k = xh @ wk
         v = xh @ wv
         rope = rope_table(n, self.device)

@@ -338,21 +338,32 @@ __global__ void __launch_bounds__(256) k_cl_accumulate(
       }
     }
     const float2 sz = __half22float2(__ldg(params + r * ng + c0 / G));  // one group: 8 | G
-    float4* a4 = reinterpret_cast<float4*>(acc + r * cols + c0);
+    float4* a4 = acc ? reinterpret_cast<float4*>(acc + r * cols + c0) : nullptr;
     float v[8];
     if (seed) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = 0.f;
-    } else {
+    } else if (a4) {
       const float4 p0 = a4[0], p1 = a4[1];
       v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
       v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
+    } else {  // fp16-storage accumulator: the fp16 copy is the accumulator
+      const uint4 u = *reinterpret_cast<const uint4*>(x16 + r * cols + c0);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+        v[2 * k] = f.x;
+        v[2 * k + 1] = f.y;
+      }
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       v[k] += fmaf(static_cast<float>((packed >> (k * bits)) & mask), sz.x, sz.y);
-    a4[0] = make_float4(v[0], v[1], v[2], v[3]);
-    a4[1] = make_float4(v[4], v[5], v[6], v[7]);
+    if (a4) {
+      a4[0] = make_float4(v[0], v[1], v[2], v[3]);
+      a4[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
     if (x16) {
       __half2 h[4];
 #pragma unroll
@@ -523,6 +534,7 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
   XQ_REQUIRE(max_len <= L_max, XQ_ESHAPE, "max_len > L_max");
   if (n_seqs == 0 || max_len == 0) return XQ_OK;
   XQ_REQUIRE(group_size % 8 == 0, XQ_ECONFIG, "group_size must be a multiple of 8");
+  XQ_REQUIRE(acc != nullptr || x16_out != nullptr, XQ_EUSAGE, "no accumulator buffer");
   const int64_t items = (int64_t)n_seqs * max_len * (cols / 8);
   int64_t blocks = (items + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;

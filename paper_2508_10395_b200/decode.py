@@ -127,7 +127,10 @@ class Decoder:
                   device=self.device)
         self.caches = [C.make_cache(variant, i, self.policy, shape.head_dim, **kw)
                        for i in range(len(weights))]
-        self.acc = (C.Accumulator(n_slots, max_len, shape.hidden_dim, self.device)
+        # xq-cl-mha: fp16-storage accumulator (the remat operand itself); xq-cl-gqa
+        # keeps float32 (its delta latents are formed in float64)
+        self.acc = (C.Accumulator(n_slots, max_len, shape.hidden_dim, self.device,
+                                  precision="fp16" if variant == "xq-cl-mha" else "fp32")
                     if variant in C.CL_VARIANTS else None)
         # one shared length vector (host + device) for all layers
         self.n_tokens = np.zeros(n_slots, dtype=np.int64)
@@ -224,7 +227,8 @@ class Decoder:
             for k, v in c.memory_bytes().items():
                 tot[k] = tot.get(k, 0) + v
         if self.acc is not None:
-            tot["cl_accumulator_f32"] = self.acc.x_hat.numel() * 4
+            if self.acc.x_hat is not None:
+                tot["cl_accumulator_f32"] = self.acc.x_hat.numel() * 4
             tot["cl_accumulator_f16"] = self.acc.x16.numel() * 2
         return tot
 

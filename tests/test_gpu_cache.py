@@ -169,7 +169,8 @@ def test_xq_gqa_against_reference(M):
     assert rel_err(vv.cpu().numpy(), z["gqa_v"]) <= 2e-2
 
 
-def test_xq_cl_mha_against_reference(M):
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+def test_xq_cl_mha_against_reference(M, precision):
     import torch
 
     z = golden("backends")
@@ -181,7 +182,7 @@ def test_xq_cl_mha_against_reference(M):
           for i in range(6)]
     kw = dict(n_slots=1, max_len=256, hidden_dim=256, n_heads=2)
     sts = [M.make_cache("xq-cl-mha", i, pol, 128, 128, **kw) for i in range(6)]
-    acc = M.Accumulator(1, 256, 256)
+    acc = M.Accumulator(1, 256, 256, precision=precision)
     n_pre, n_dec = 140, 3
     for i in range(6):
         sts[i].prefill(xs[i, :n_pre], ws[i], acc)
@@ -193,7 +194,7 @@ def test_xq_cl_mha_against_reference(M):
     for i in range(6):
         assert rel_err(outs[i], z["cl_attn"][i]) <= FUSED_TOL, i
     n = n_pre + n_dec
-    assert rel_err(acc.x_hat[0, :n].cpu().numpy(), z["cl_acc_last"]) <= 3e-2
+    assert rel_err(acc.rows(0, n).cpu().numpy(), z["cl_acc_last"]) <= 3e-2
 
 
 def test_xq_cl_gqa_against_reference(M):
