@@ -373,6 +373,63 @@ __global__ void __launch_bounds__(256) k_cl_accumulate(
   }
 }
 
+// The same update for the fp16-storage accumulator after seeding -- the engine's
+// per-delta-layer hot case. Each thread owns 32 consecutive channels of one row: 64 B
+// of accumulator in flight as four 16-byte loads, `BITS` whole words of codes and
+// four (scale, zp) loads, with 32-bit index math. Per element the arithmetic is the
+// generic kernel's (fp32 add of the fp32 dequantized delta, one fp16 rounding).
+template <int BITS>
+__global__ void __launch_bounds__(256) k_cl_accumulate_h(
+    const uint8_t* __restrict__ codes, int64_t row_bytes, const __half2* __restrict__ params,
+    int G, int cols, const int32_t* __restrict__ lens, int max_len, int64_t L_max,
+    uint32_t total, __half* __restrict__ x16) {
+  constexpr uint32_t kMask = (1u << BITS) - 1u;
+  const uint32_t per_row = static_cast<uint32_t>(cols) / 32;
+  const int64_t ng = param_stride(cols, G);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += gridDim.x * blockDim.x) {
+    const uint32_t rowi = i / per_row;
+    const uint32_t b = rowi / static_cast<uint32_t>(max_len);
+    const int t = static_cast<int>(rowi - b * static_cast<uint32_t>(max_len));
+    if (t >= __ldg(lens + b)) continue;
+    const int c0 = static_cast<int>(i - rowi * per_row) * 32;
+    const int64_t r = static_cast<int64_t>(b) * L_max + t;
+    uint4* xp = reinterpret_cast<uint4*>(x16 + r * cols + c0);
+    uint4 q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = xp[k];
+    // 32 codes = BITS words at byte 4*BITS*(c0/32) of the row
+    const uint32_t* cw = reinterpret_cast<const uint32_t*>(codes + r * row_bytes) + (c0 / 32) * BITS;
+    uint32_t w[BITS + 1];
+#pragma unroll
+    for (int k = 0; k < BITS; ++k) w[k] = __ldg(cw + k);
+    w[BITS] = 0u;
+    __half2 sz[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sz[k] = __ldg(params + r * ng + (c0 + 8 * k) / G);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(sz[k]);
+      uint32_t hw[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = 8 * k + 2 * j + e, bit = m * BITS, wi = bit / 32, sh = bit % 32;
+          const uint32_t code =
+              static_cast<uint32_t>(((static_cast<uint64_t>(w[wi + 1]) << 32) | w[wi]) >> sh) & kMask;
+          v[e] = fmaf(static_cast<float>(code), f.x, f.y);
+        }
+        const float2 old = __half22float2(*reinterpret_cast<const __half2*>(&hw[j]));
+        const __half2 h = __floats2half2_rn(old.x + v[0], old.y + v[1]);
+        hw[j] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      xp[k] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    }
+  }
+}
+
 static int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 32) g = 148 * 32;
@@ -535,6 +592,24 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
   if (n_seqs == 0 || max_len == 0) return XQ_OK;
   XQ_REQUIRE(group_size % 8 == 0, XQ_ECONFIG, "group_size must be a multiple of 8");
   XQ_REQUIRE(acc != nullptr || x16_out != nullptr, XQ_EUSAGE, "no accumulator buffer");
+  const int64_t items32 = (int64_t)n_seqs * max_len * (cols / 32);
+  if (!seed && acc == nullptr && cols % 32 == 0 && cols < (int64_t(1) << 30) &&
+      items32 + (int64_t)148 * 6 * 256 < (int64_t(1) << 32)) {
+    const int64_t blocks = std::min<int64_t>((items32 + 255) / 256, 148 * 6);  // 38 regs: 6 CTAs per SM
+    auto launch = [&](auto kern) {
+      kern<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
+          codes, row_bytes, static_cast<const __half2*>(params), group_size,
+          static_cast<int>(cols), seq_lens, max_len, L_max, static_cast<uint32_t>(items32),
+          static_cast<__half*>(x16_out));
+    };
+    switch (bits) {
+      case 2: launch(k_cl_accumulate_h<2>); break;
+      case 3: launch(k_cl_accumulate_h<3>); break;
+      case 4: launch(k_cl_accumulate_h<4>); break;
+      default: launch(k_cl_accumulate_h<8>); break;
+    }
+    return check_launch("xq_cl_accumulate");
+  }
   const int64_t items = (int64_t)n_seqs * max_len * (cols / 8);
   int64_t blocks = (items + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
