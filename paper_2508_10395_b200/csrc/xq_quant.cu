@@ -373,15 +373,15 @@ __global__ void __launch_bounds__(256) k_cl_accumulate(
   }
 }
 
-// The same update for the fp16-storage accumulator after seeding -- the engine's
-// per-delta-layer hot case. Each thread owns 32 consecutive channels of one row: 64 B
+// The same update for the fp16-storage accumulator -- the engine's per-delta-layer
+// hot case (seed: the accumulator starts at zero and is not read). Each thread owns 32 consecutive channels of one row: 64 B
 // of accumulator in flight as four 16-byte loads, `BITS` whole words of codes and
 // four (scale, zp) loads, with 32-bit index math. Per element the arithmetic is the
 // generic kernel's (fp32 add of the fp32 dequantized delta, one fp16 rounding).
 template <int BITS>
 __global__ void __launch_bounds__(256) k_cl_accumulate_h(
-    const uint8_t* __restrict__ codes, int64_t row_bytes, const __half2* __restrict__ params,
-    int G, int cols, const int32_t* __restrict__ lens, int max_len, int64_t L_max,
+    int seed, const uint8_t* __restrict__ codes, int64_t row_bytes,
+    const __half2* __restrict__ params, int G, int cols, const int32_t* __restrict__ lens, int max_len, int64_t L_max,
     uint32_t total, __half* __restrict__ x16) {
   constexpr uint32_t kMask = (1u << BITS) - 1u;
   const uint32_t per_row = static_cast<uint32_t>(cols) / 32;
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256) k_cl_accumulate_h(
     uint4* xp = reinterpret_cast<uint4*>(x16 + r * cols + c0);
     uint4 q[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = xp[k];
+    for (int k = 0; k < 4; ++k) q[k] = seed ? make_uint4(0u, 0u, 0u, 0u) : xp[k];
     // 32 codes = BITS words at byte 4*BITS*(c0/32) of the row
     const uint32_t* cw = reinterpret_cast<const uint32_t*>(codes + r * row_bytes) + (c0 / 32) * BITS;
     uint32_t w[BITS + 1];
@@ -593,12 +593,12 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
   XQ_REQUIRE(group_size % 8 == 0, XQ_ECONFIG, "group_size must be a multiple of 8");
   XQ_REQUIRE(acc != nullptr || x16_out != nullptr, XQ_EUSAGE, "no accumulator buffer");
   const int64_t items32 = (int64_t)n_seqs * max_len * (cols / 32);
-  if (!seed && acc == nullptr && cols % 32 == 0 && cols < (int64_t(1) << 30) &&
+  if (acc == nullptr && cols % 32 == 0 && cols < (int64_t(1) << 30) &&
       items32 + (int64_t)148 * 6 * 256 < (int64_t(1) << 32)) {
     const int64_t blocks = std::min<int64_t>((items32 + 255) / 256, 148 * 6);  // 38 regs: 6 CTAs per SM
     auto launch = [&](auto kern) {
       kern<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
-          codes, row_bytes, static_cast<const __half2*>(params), group_size,
+          seed, codes, row_bytes, static_cast<const __half2*>(params), group_size,
           static_cast<int>(cols), seq_lens, max_len, L_max, static_cast<uint32_t>(items32),
           static_cast<__half*>(x16_out));
     };
