@@ -740,7 +740,8 @@ class FullPrecisionCache(CacheBackend):
         return self.k[base:base + n].to(torch.float16), self.v[base:base + n].to(torch.float16)
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
-        chunk = tpc * 128 if tpc else kv_chunk_tokens(self.n_slots, max_len, self.n_kv)
+        chunk = tpc * 128 if tpc else kv_chunk_tokens(self.n_slots, max_len, self.n_kv,
+                                                       ctas_per_sm=4 if self.g == 1 else 24)
         nbytes = N.lib.xq_kv_decode_workspace_bytes(self.n_slots, max_len, self.n_kv, self.g, chunk)
         ws = torch.empty(nbytes // 4 + 1, dtype=torch.float32, device=self.device)
         rope = rope_table(max_len, self.device)
@@ -753,10 +754,13 @@ class FullPrecisionCache(CacheBackend):
         return {"kv_cache": 2 * self.k.numel() * 2}
 
 
-def kv_chunk_tokens(n_slots, max_len, n_kv, n_sm=148):
-    """Tokens per CTA of the fp16-KV flash-decode: >= ~4 CTAs per SM in total."""
+def kv_chunk_tokens(n_slots, max_len, n_kv, n_sm=148, ctas_per_sm=4):
+    """Tokens per CTA of the fp16-KV flash-decode: >= ~ctas_per_sm CTAs per SM in total.
+
+    The grouped-query kernel keeps 3 CTAs resident per SM; 24 per SM (8 waves) keeps its
+    tail short."""
     units_per_chunk = max(1, n_slots * n_kv)
-    chunks = max(1, -(-4 * n_sm // units_per_chunk))
+    chunks = max(1, -(-ctas_per_sm * n_sm // units_per_chunk))
     return max(512, -(-max_len // chunks))
 
 
