@@ -433,7 +433,7 @@ def run_xquant(args, cfg):
                    "ms_per_step": tq / args.steps * 1e3,
                    "hbm_gbs_achieved": qbytes / (tq / args.steps) / 1e9,
                    "compression": S.compression_factor("kvq", qdec.policy.bits, shape.kv_group),
-                   "kernel": "xq_kvq_decode_attend (shared-memory dequant flash-decode)"}
+                   "kernel": "xq_kvq_decode_attend (cp.async-staged codes, register dequant + RoPE flash-decode)"}
             del qdec
             gc.collect()
             torch.cuda.empty_cache()

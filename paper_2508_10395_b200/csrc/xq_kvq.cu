@@ -76,10 +76,47 @@ XQ_DEVINL uint32_t code_j(uint2 raw, int j) {
 // with its per-token (scale, zp).
 constexpr int kNw = kThreads / 32;
 constexpr int kStreams = 2 * kNw;
+constexpr int kStages = 3;  // per-warp cp.async ring of token blocks
+
+template <int GROUP>
+constexpr int unroll_for() { return GROUP >= 4 ? 4 : 8; }  // tokens per half-warp per block
+// one ring stage: a block's K code rows, V code rows (16*BITS bytes per token for
+// one head) and V (scale, zp)
+template <int BITS, int GROUP>
+constexpr uint32_t stage_bytes() { return 2u * 2 * unroll_for<GROUP>() * (16 * BITS + 2); }
+template <int BITS, int GROUP>
+constexpr uint32_t smem_bytes() { return kNw * kStages * stage_bytes<BITS, GROUP>(); }
+
+XQ_DEVINL void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+XQ_DEVINL void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+XQ_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+XQ_DEVINL void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+XQ_DEVINL __half2 from_u32h2(uint32_t u) { return *reinterpret_cast<const __half2*>(&u); }
+
+// raw8 from a staged row (shared address of the head's 16*BITS code bytes)
+template <int BITS>
+XQ_DEVINL uint2 raw8_s(uint32_t row, int hl) {
+  if constexpr (BITS == 8) return lds64(row + 8u * hl);
+  const uint32_t off = static_cast<uint32_t>(BITS * hl);
+  const uint32_t a = row + (off & ~3u);
+  const uint32_t lo = lds32(a), hi = ((off & 3u) + BITS > 4u) ? lds32(a + 4u) : 0u;
+  return make_uint2(__funnelshift_r(lo, hi, (off & 3u) * 8u), 0u);
+}
 
 template <int BITS, int GROUP>
 __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
-  constexpr int kUnroll = GROUP >= 4 ? 4 : 8;  // tokens in flight per half-warp (registers)
+  constexpr int kUnroll = unroll_for<GROUP>();
+  constexpr int kBlk = 2 * kUnroll;
+  constexpr uint32_t kRowB = 16 * BITS;
+  constexpr uint32_t kStageB = stage_bytes<BITS, GROUP>();
   const int unit = blockIdx.x;
   const int chunk = unit % p.n_chunks;
   const int h = (unit / p.n_chunks) % p.n_kv;
@@ -123,9 +160,33 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
   const int bs = perm_block(XQ_A_CODES_CHANNEL, BITS);
   int cur_grp = -1;
   float2 kp[8];  // (scale, zp) of this lane's 8 K channels for the current token group
-  // warp w takes blocks of 2*kUnroll = 16 tokens (16-aligned: one RoPE base,
-  // one K group); half-warp `half` the tokens 2u + half
-  for (int wbase = t0 + warp * 2 * kUnroll; wbase < t1; wbase += kNw * 2 * kUnroll) {
+  // warp w takes blocks of kBlk = 2*kUnroll tokens (16-aligned: one RoPE base,
+  // one K group); half-warp `half` the tokens 2u + half. Codes arrive through a
+  // per-warp cp.async ring (rows past t1 clamp to t1 - 1 and are masked).
+  extern __shared__ __align__(16) uint8_t kvq_smem[];
+  const uint32_t ring = smem_u32(kvq_smem) + warp * kStages * kStageB;
+  auto issue = [&](int wb, int stg) {
+    if (wb < t1) {
+      const uint32_t sa = ring + stg * kStageB;
+      for (int i = lane; i < kBlk * BITS; i += 32) {  // BITS 16-byte chunks per row
+        const int r = i / BITS, qq = i % BITS;
+        const int64_t t = min(wb + r, t1 - 1);
+        const int64_t src = (row0 + t) * p.row_bytes + (int64_t)h * kRowB + 16 * qq;
+        cp_async16(sa + r * kRowB + 16u * qq, p.k_codes + src);
+        cp_async16(sa + kBlk * kRowB + r * kRowB + 16u * qq, p.v_codes + src);
+      }
+      if (lane < kBlk) {
+        const int64_t t = min(wb + lane, t1 - 1);
+        cp_async4(sa + 2 * kBlk * kRowB + 4u * lane, p.v_params + (row0 + t) * p.vp_stride + h);
+      }
+    }
+    cp_async_commit();
+  };
+  const int wfirst = t0 + warp * kBlk;
+#pragma unroll
+  for (int k = 0; k < kStages - 1; ++k) issue(wfirst + k * kNw * kBlk, k);
+  int stage = 0;
+  for (int wbase = wfirst; wbase < t1; wbase += kNw * kBlk) {
     const int grp = wbase / p.G;
     if (grp != cur_grp && wbase < nfl) {
       const __half* prow = p.k_params + (row0 / p.G + grp) * 2 * p.kvw;
@@ -140,15 +201,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
     float2 base[4];  // cos/sin(wbase theta_j) of this lane's 4 frequencies
 #pragma unroll
     for (int j = 0; j < 4; ++j) base[j] = __ldg(p.rope + (int64_t)wbase * 64 + 4 * hl + j);
-    // load phase: raw codes (and V's per-token scale/zp) of kUnroll tokens in flight
+    cp_async_wait<kStages - 2>();
+    __syncwarp();
+    const uint32_t sa = ring + stage * kStageB;
     uint2 kraw[kUnroll], vraw[kUnroll];
     __half2 vsz[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int t = min(wbase + 2 * u + half, t1 - 1);
-      kraw[u] = raw8<BITS>(p.k_codes + (row0 + t) * p.row_bytes, h, hl);
-      vraw[u] = raw8<BITS>(p.v_codes + (row0 + t) * p.row_bytes, h, hl);
-      vsz[u] = p.v_params[(row0 + t) * p.vp_stride + h];  // G = 128: one group per head
+      const int r = 2 * u + half;
+      kraw[u] = raw8_s<BITS>(sa + r * kRowB, hl);
+      vraw[u] = raw8_s<BITS>(sa + kBlk * kRowB + r * kRowB, hl);
+      vsz[u] = from_u32h2(lds32(sa + 2 * kBlk * kRowB + 4u * r));
     }
     // K phase: dequant + RoPE in registers, scores of the group's query heads
     float sc[GROUP][kUnroll];
@@ -224,7 +287,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
         for (int j = 0; j < 8; ++j) o[gi][j] = fmaf(pr, vf[j], o[gi][j]);
       }
     }
+    __syncwarp();  // every lane has read this stage before it is refilled
+    issue(wbase + (kStages - 1) * kNw * kBlk, stage == 0 ? kStages - 1 : stage - 1);
+    stage = stage + 1 == kStages ? 0 : stage + 1;
   }
+  cp_async_wait<0>();
   // merge the half-warp streams, one partial per CTA
   __shared__ float s_m[kStreams][GROUP], s_l[kStreams][GROUP], s_o[kStreams][GROUP][kHeadDim];
 #pragma unroll
@@ -258,16 +325,29 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
   }
 }
 
+template <int BITS, int GROUP>
+static int launch_one(const Params& p, int grid, cudaStream_t st) {
+  constexpr uint32_t smem = smem_bytes<BITS, GROUP>();
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(k_kvq_decode<BITS, GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem) != cudaSuccess)
+      return check_launch("cudaFuncSetAttribute(kvq_decode)");
+    configured = true;
+  }
+  k_kvq_decode<BITS, GROUP><<<grid, kThreads, smem, st>>>(p);
+  return check_launch("k_kvq_decode");
+}
+
 template <int GROUP>
 static int launch_bits(int bits, const Params& p, int grid, cudaStream_t st) {
   switch (bits) {
-    case 2: k_kvq_decode<2, GROUP><<<grid, kThreads, 0, st>>>(p); break;
-    case 3: k_kvq_decode<3, GROUP><<<grid, kThreads, 0, st>>>(p); break;
-    case 4: k_kvq_decode<4, GROUP><<<grid, kThreads, 0, st>>>(p); break;
-    case 8: k_kvq_decode<8, GROUP><<<grid, kThreads, 0, st>>>(p); break;
+    case 2: return launch_one<2, GROUP>(p, grid, st);
+    case 3: return launch_one<3, GROUP>(p, grid, st);
+    case 4: return launch_one<4, GROUP>(p, grid, st);
+    case 8: return launch_one<8, GROUP>(p, grid, st);
     default: return fail(XQ_ECONFIG, "bad bits %d", bits);
   }
-  return check_launch("k_kvq_decode");
 }
 
 }  // namespace kvq
