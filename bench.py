@@ -341,7 +341,7 @@ def run_xquant(args, cfg):
 
     def make(variant):
         dec = D.Decoder(shape, variant, cfg["bits"], B, L_max, weights, w_q, device=dev,
-                        head_shard=shard)
+                        head_shard=shard, gather=args.gather)
         t0 = time.perf_counter()
         dec.fill_synthetic(ctx, seed=1 + wseed)
         return dec, time.perf_counter() - t0
@@ -486,7 +486,10 @@ def run_xquant(args, cfg):
         "config": {"workload": cfg["workload"], "shape": cfg["shape"], "variant": cfg["variant"],
                    "bits": cfg["bits"], "policy_bits": bits_per_layer[:4] + ["..."],
                    "batch_per_gpu": B, "context": ctx + 1, "layers": n_layers,
-                   "parallelism": (f"kv-head-group x{world} (NCCL all-gather of attention outputs)"
+                   "parallelism": (f"kv-head-group x{world} ("
+                                   + ("peer-store gather from the projection kernel into symmetric memory"
+                                      if args.gather == "peer" else "NCCL all-gather of attention outputs")
+                                   + ")"
                                    if heads else f"batch-sharded x{world} (no data-path collective)"),
                    "l2": "no flush: per-step inputs (packed caches, GBs) exceed the 126 MB L2"},
         "fp16_kv": fp16,
@@ -530,6 +533,9 @@ def main():
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kvq", action="store_true", help="also time the kvq baseline at equal bits")
+    ap.add_argument("--gather", choices=["nccl", "peer"], default="nccl",
+                    help="KV-head-group sharding (c4 under torchrun): NCCL all-gather, or the "
+                         "fused kernel's peer stores into torch symmetric memory")
     ap.add_argument("--ctx", type=int, default=None, help="override the config's context")
     ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
     args = ap.parse_args()

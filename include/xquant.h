@@ -219,6 +219,26 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
                               int64_t rope_n, float sm_scale, void* workspace,
                               int64_t workspace_bytes, float* out, void* stream);
 
+/* xq_decode_attend_absorbed with the projected output [n_seqs][H][128] stored
+ * to each of n_outs (1..9) destinations. Under KV-head-group sharding
+ * (paper_2508_10395_b200/parallel.py) these are this rank's slot
+ * in every rank's gather buffer (peer pointers, e.g. torch symmetric memory over
+ * NVLink): the all-gather of attention outputs becomes the projection kernel's
+ * own stores, followed by a device-side barrier instead of an NCCL call. outs is
+ * a host array of device (or peer) pointers. */
+int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                                    const float* ak_resid, const int32_t* ak_nflushed,
+                                    const float* ak_first, int32_t ak_bits,
+                                    int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
+                                    const void* av_params, int32_t av_bits, int64_t av_row_bytes,
+                                    int32_t group_size, int64_t L_max, int64_t kdim,
+                                    const int32_t* seq_lens, int32_t n_seqs, int32_t max_len,
+                                    const void* wk_arranged, const void* wv_arranged,
+                                    int32_t n_kv_heads, int32_t group, const float* q_pre,
+                                    const void* rope_cs, int64_t rope_n, float sm_scale,
+                                    void* workspace, int64_t workspace_bytes,
+                                    float* const* outs, int32_t n_outs, void* stream);
+
 /* Debug: cycles each warp role of the absorbed kernel spent blocked per
  * barrier (16 uint64 counters, see csrc/xq_absorb.cu); all zero unless the
  * library was built with -DXQ_ROLE_PROFILE (tools/build_role_profile.sh).

@@ -45,6 +45,9 @@ _SIGS = {
     "xq_decode_attend_absorbed": [_I32, _P, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32,
                                   _I64, _I64, _P, _I32, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _F,
                                   _P, _I64, _P, _P],
+    "xq_decode_attend_absorbed_peers": [_I32, _P, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32,
+                                        _I64, _I32, _I64, _I64, _P, _I32, _I32, _P, _P, _I32,
+                                        _I32, _P, _P, _I64, _F, _P, _I64, _P, _I32, _P],
     "xq_remat_f32": [_I32, _P, _P, _P, _I32, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32, _I64,
                      _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P],
     "xq_cl_accumulate": [_I32, _P, _I64, _P, _I32, _I32, _I64, _P, _I32, _I32, _I64, _P, _P,

@@ -23,6 +23,7 @@ scope table and raise ``ConfigError`` here.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass, field
@@ -618,12 +619,19 @@ class CacheBackend:
             wk_arr, wv_arr = weights.arranged_absorbed(key, mk, bk, mv, bv, wk, wv)
             nbytes = N.lib.xq_absorbed_workspace_bytes(self.n_slots, max_len, self.n_kv * group, kdim)
             ws = _scratch(self.device, nbytes)
-            N.call("xq_decode_attend_absorbed", ak_mode, N.ptr(ak_src), N.ptr(ak_params),
-                   N.ptr(ak_resid), N.ptr(ak_nfl), N.ptr(ak_first), ak_bits, ak_rb, av_mode, N.ptr(av_src),
-                   N.ptr(av_params), av_bits, av_rb, self.group_size, self.L, kdim, N.ptr(lens),
-                   self.n_slots, max_len, N.ptr(wk_arr), N.ptr(wv_arr), self.n_kv, group, N.ptr(q),
-                   N.ptr(rope), rope.shape[1] // 2, 1.0 / math.sqrt(HEAD_DIM), N.ptr(ws), nbytes,
-                   N.ptr(out), N.stream_of(self.device))
+            args = (ak_mode, N.ptr(ak_src), N.ptr(ak_params), N.ptr(ak_resid), N.ptr(ak_nfl),
+                    N.ptr(ak_first), ak_bits, ak_rb, av_mode, N.ptr(av_src), N.ptr(av_params), av_bits,
+                    av_rb, self.group_size, self.L, kdim, N.ptr(lens), self.n_slots, max_len,
+                    N.ptr(wk_arr), N.ptr(wv_arr), self.n_kv, group, N.ptr(q), N.ptr(rope),
+                    rope.shape[1] // 2, 1.0 / math.sqrt(HEAD_DIM), N.ptr(ws), nbytes)
+            peers = getattr(self, "peer_outs", None)
+            if peers:  # head-sharded engine: the projection stores into every rank's gather slot
+                arr = (ctypes.c_void_p * len(peers))(*peers)
+                N.call("xq_decode_attend_absorbed_peers", *args, ctypes.cast(arr, ctypes.c_void_p),
+                       len(peers), N.stream_of(self.device))
+                self.peer_stored = True
+                return
+            N.call("xq_decode_attend_absorbed", *args, N.ptr(out), N.stream_of(self.device))
             return
         w_arr = weights.arranged(key, mk, bk, mv, bv, wk, wv)
         tpc = tpc or default_tiles_per_chunk(self.n_slots, max_len, self.n_kv)

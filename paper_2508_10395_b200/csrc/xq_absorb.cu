@@ -870,10 +870,19 @@ __global__ void __launch_bounds__(128) k_absorb_combine(const float* __restrict_
 // storage channel order of x). Grid (n_q, 4 column blocks of 32, ceil(n_seqs/8)):
 // a CTA streams its [kdim x 32] slice of W_v once for up to 8 sequences (x
 // staged in shared memory); 16 threads per row of the slice, 16 channel slices.
+// Destinations of the projected output: this GPU's buffer, or under KV-head-group
+// sharding this rank's slot in every rank's gather buffer (peer pointers over
+// NVLink), so the all-gather is the projection's own stores.
+constexpr int kMaxOuts = 9;  // 8 ranks + a local copy
+struct OutPtrs {
+  float* p[kMaxOuts];
+  int n;
+};
+
 __global__ void __launch_bounds__(256) k_absorb_project(const float* __restrict__ x,
                                                         int n_seqs, int n_q, int group, int kdim,
                                                         const __half* __restrict__ wv,
-                                                        float* __restrict__ out) {
+                                                        const OutPtrs outs) {
   extern __shared__ float xs[];  // [8][kdim]
   __shared__ float red[16][8][33];
   const int h = blockIdx.x, cb = blockIdx.y, b0 = blockIdx.z * 8, tid = threadIdx.x;
@@ -911,7 +920,8 @@ __global__ void __launch_bounds__(256) k_absorb_project(const float* __restrict_
     float v = 0.f;
 #pragma unroll
     for (int k = 0; k < 16; ++k) v += red[k][s][j];
-    out[((int64_t)(b0 + s) * n_q + h) * kHeadDim + cb * 32 + j] = v;
+    const int64_t o = ((int64_t)(b0 + s) * n_q + h) * kHeadDim + cb * 32 + j;
+    for (int k = 0; k < outs.n; ++k) outs.p[k][o] = v;
   }
 }
 
@@ -1162,6 +1172,33 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
                               int32_t group, const float* q_pre, const void* rope_cs,
                               int64_t rope_n, float sm_scale, void* workspace,
                               int64_t workspace_bytes, float* out, void* stream) {
+  return xq_decode_attend_absorbed_peers(
+      ak_mode, ak_src, ak_params, ak_resid, ak_nflushed, ak_first, ak_bits, ak_row_bytes, av_mode,
+      av_src, av_params, av_bits, av_row_bytes, group_size, L_max, kdim, seq_lens, n_seqs, max_len,
+      wk_arranged, wv_arranged, n_kv_heads, group, q_pre, rope_cs, rope_n, sm_scale, workspace,
+      workspace_bytes, &out, 1, stream);
+}
+
+int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const void* ak_params,
+                                    const float* ak_resid, const int32_t* ak_nflushed,
+                                    const float* ak_first, int32_t ak_bits,
+                                    int64_t ak_row_bytes, int32_t av_mode, const void* av_src,
+                                    const void* av_params, int32_t av_bits, int64_t av_row_bytes,
+                                    int32_t group_size, int64_t L_max, int64_t kdim,
+                                    const int32_t* seq_lens, int32_t n_seqs, int32_t max_len,
+                                    const void* wk_arranged, const void* wv_arranged,
+                                    int32_t n_kv_heads, int32_t group, const float* q_pre,
+                                    const void* rope_cs, int64_t rope_n, float sm_scale,
+                                    void* workspace, int64_t workspace_bytes,
+                                    float* const* outs, int32_t n_outs, void* stream) {
+  XQ_REQUIRE(outs != nullptr && n_outs >= 1 && n_outs <= kMaxOuts, XQ_EUSAGE,
+             "need 1..%d output pointers, got %d", kMaxOuts, n_outs);
+  OutPtrs op{};
+  op.n = n_outs;
+  for (int i = 0; i < n_outs; ++i) {
+    XQ_REQUIRE(outs[i] != nullptr, XQ_EUSAGE, "output pointer %d is null", i);
+    op.p[i] = outs[i];
+  }
   XQ_REQUIRE(rope_n >= max_len, XQ_ESHAPE, "rope table shorter than max_len");
   XQ_REQUIRE(kdim % 256 == 0 && kdim >= 256, XQ_ESHAPE,
              "kdim must be a positive multiple of 256, got %lld", (long long)kdim);
@@ -1288,7 +1325,7 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
     }
   }
   k_absorb_project<<<dim3(n_q, 4, (n_seqs + 7) / 8), 256, psmem, st>>>(
-      x_attn, n_seqs, n_q, group, p.kdim, static_cast<const __half*>(wv_arranged), out);
+      x_attn, n_seqs, n_q, group, p.kdim, static_cast<const __half*>(wv_arranged), op);
   return check_launch("k_absorb_project");
 }
 

@@ -96,10 +96,12 @@ class Decoder:
     def __init__(self, shape: ModelShape, variant: str, bits: int, n_slots: int, max_len: int,
                  weights, w_q, device="cuda", policy: C.LayerPolicy | None = None,
                  tiles_per_chunk: int | None = None, head_shard: tuple[int, int] | None = None,
-                 group=None):
+                 group=None, gather: str = "nccl"):
         """``head_shard=(world, rank)``: KV-head-group sharding (parallel.py).
         This rank serves KV heads parallel.head_shard(...) with column-sliced
-        weights; step() all-gathers the attention outputs of all ranks."""
+        weights; step() all-gathers the attention outputs of all ranks, by
+        ``all_gather_into_tensor`` (``gather="nccl"``) or by the fused kernel's
+        peer stores into symmetric memory (``gather="peer"``)."""
         from . import parallel as P
 
         if variant not in C.SUPPORTED:
@@ -119,7 +121,12 @@ class Decoder:
             weights = [P.shard_layer_weights(lw, variant, kv) for lw in weights]
             w_q = [P.shard_wq(w, kv, shape.kv_group) for w in w_q]
             n_heads = len(kv) * shape.kv_group
-            self.gather = P.HeadGather(n_slots, n_heads, world, self.device, group)
+            if gather == "peer":
+                self.gather = P.PeerHeadGather(n_slots, n_heads, world, rank, self.device, group)
+            elif gather == "nccl":
+                self.gather = P.HeadGather(n_slots, n_heads, world, self.device, group)
+            else:
+                raise ConfigError(f"gather must be 'nccl' or 'peer', got {gather!r}")
         self.n_heads_local = n_heads
         self.weights, self.w_q = weights, w_q
         kw = dict(n_slots=n_slots, max_len=max_len, hidden_dim=shape.hidden_dim,
@@ -192,12 +199,22 @@ class Decoder:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-            cache._attend(q, lw, self.acc, self.lens_dev, max_len, out, self.tpc)
+            peer = self.gather is not None and getattr(self.gather, "peer", False)
+            if peer:  # the absorbed kernel stores into every rank's gather slot
+                cache.peer_outs = self.gather.out_ptrs(i) + [out.data_ptr()]  # + the local copy
+                cache.peer_stored = False
+            try:
+                cache._attend(q, lw, self.acc, self.lens_dev, max_len, out, self.tpc)
+            finally:
+                if peer:
+                    cache.peer_outs = None
             if timers is not None:
                 e1.record()
                 timers.append((e0, e1))
             self.launches += self._launches_per_layer(cache)
-            if self.gather is not None:  # KV-head-group sharding: [B, H_local, 128] -> [B, H, 128]
+            if peer:  # [B, H_local, 128] -> [B, H, 128]
+                out = self.gather.finish(i) if cache.peer_stored else self.gather(out, i)
+            elif self.gather is not None:
                 out = self.gather(out)
         return out
 

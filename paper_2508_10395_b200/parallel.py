@@ -10,6 +10,12 @@
   channels of X (cache.py:385-387, 434-437), so every rank quantizes the same
   row. After the fused attention each rank holds [B, H/world, 128]; one
   all-gather per layer assembles [B, H, 128] for the replicated W_o.
+  * ``HeadGather``: ``all_gather_into_tensor`` (NCCL on GPUs, gloo in tests).
+  * ``PeerHeadGather``: torch symmetric memory. The fused kernel's projection
+    stores this rank's [B, H/world, 128] straight into its slot of every rank's
+    buffer through peer pointers (NVLink), then one device-side barrier. There is
+    no separate collective launch. The buffers alternate per layer, so the next
+    layer's stores never land in a buffer a slower rank is still reading.
 
 One process per GPU, torch.distributed (NCCL on GPUs, gloo on CPU in tests).
 """
@@ -88,3 +94,51 @@ class HeadGather:
         dist.all_gather_into_tensor(self.buf.view(-1), local.view(-1), group=self.group)
         # [world, B, H_local, 128] -> [B, world*H_local, 128]
         return self.buf.permute(1, 0, 2, 3).reshape(local.shape[0], self.world * self.h, HEAD_DIM)
+
+
+class PeerHeadGather:
+    """KV-head-group gather by peer stores (torch symmetric memory over NVLink).
+
+    ``out_ptrs(i)`` are the device addresses of this rank's slot in every rank's
+    buffer for layer i. The decoder hands them to the fused kernel
+    (``xq_decode_attend_absorbed_peers``), and ``finish(i)`` is the barrier plus
+    the [B, H, 128] view. ``__call__`` covers the unabsorbed kernel: the local
+    output is copied into the peers' slots and then the same barrier runs.
+    """
+
+    peer = True
+
+    def __init__(self, n_seqs: int, n_heads_local: int, world: int, rank: int, device,
+                 group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        self.world, self.rank, self.h, self.n_seqs = world, rank, n_heads_local, n_seqs
+        self.shape = (world, n_seqs, n_heads_local, HEAD_DIM)
+        name = (group or dist.group.WORLD).group_name
+        self.bufs = [symm.empty(self.shape, dtype=torch.float32, device=device) for _ in range(2)]
+        self.hdls = [symm.rendezvous(b, name) for b in self.bufs]
+        slot = n_seqs * n_heads_local * HEAD_DIM * 4
+        self._ptrs = []
+        for b, hdl in zip(self.bufs, self.hdls):
+            off = b.data_ptr() - hdl.buffer_ptrs[rank]  # the tensor inside its allocation
+            self._ptrs.append([hdl.buffer_ptrs[p] + off + rank * slot for p in range(world)])
+
+    def out_ptrs(self, layer: int) -> list[int]:
+        return self._ptrs[layer % 2]
+
+    def finish(self, layer: int) -> torch.Tensor:
+        self.hdls[layer % 2].barrier(channel=0)
+        return gathered_view(self.bufs[layer % 2])
+
+    def __call__(self, local: torch.Tensor, layer: int = 0) -> torch.Tensor:
+        hdl = self.hdls[layer % 2]
+        for p in range(self.world):
+            hdl.get_buffer(p, self.shape, torch.float32)[self.rank].copy_(local)
+        return self.finish(layer)
+
+
+def gathered_view(buf: torch.Tensor) -> torch.Tensor:
+    """[world, B, H_local, 128] -> [B, world*H_local, 128] (rank r's heads at r*H_local)."""
+    world, n, h, d = buf.shape
+    return buf.permute(1, 0, 2, 3).reshape(n, world * h, d)

@@ -1,6 +1,8 @@
 """Decode engine (decode.Decoder) on the GPU: a multi-layer step against the
 CPU oracle, and KV-head-group shards reassembling the unsharded output."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -130,3 +132,71 @@ def test_decoder_cl_gqa_step_matches_oracle():
             q = x[i, b, -1:] @ wq[i].double().cpu().numpy()
             ref = O.attention(O.apply_rope(q, [n1 - 1], 128), o[i][1], o[i][2], shape.n_heads, 4)[0]
             assert rel_err(out[i, b].reshape(-1), ref) <= TOL, (i, b)
+
+
+class _LocalPeers:
+    """Stand-in for parallel.PeerHeadGather with every rank's decoder in this process:
+    the "peer" buffers are ordinary device tensors. The fused kernel's peer stores and
+    the decoder's plumbing run exactly as over NVLink. Only the pointers come from
+    elsewhere, and the barrier is a no-op because the ranks run in stream order."""
+
+    peer = True
+
+    def __init__(self, bufs, rank):
+        self.bufs, self.rank = bufs, rank  # bufs[rank][parity]: [world, B, H_local, 128]
+
+    def out_ptrs(self, layer):
+        slot = self.bufs[0][0][0].numel() * 4
+        return [b[layer % 2].data_ptr() + self.rank * slot for b in self.bufs]
+
+    def finish(self, layer):
+        from paper_2508_10395_b200 import parallel as P
+
+        return P.gathered_view(self.bufs[self.rank][layer % 2])
+
+    def __call__(self, local, layer=0):
+        for b in self.bufs:
+            b[layer % 2][self.rank].copy_(local)
+        return self.finish(layer)
+
+
+@pytest.mark.parametrize("variant,g", [("xq-mha", 1), ("xq-gqa", 2)])
+def test_peer_store_gather(variant, g):
+    """KV-head-group sharding with the gather done by the projection kernel's peer
+    stores (xq_decode_attend_absorbed_peers): every rank's buffer holds the unsharded
+    output, and attn_out keeps the local heads."""
+    import torch
+
+    from paper_2508_10395_b200 import decode as D
+
+    world = 2
+    shape, w, wq, xs, dev = _setup(variant, 3, n_layers=3, d=1024, H=8, g=g)
+    full, _ = _run(shape, variant, 3, w, wq, xs, dev)
+    L, B, n1, d = xs.shape
+    h_loc = shape.n_heads // world
+    bufs = [[torch.full((world, B, h_loc, 128), float("nan"), device=dev) for _ in range(2)]
+            for _ in range(world)]
+    locals_ = []
+    for r in range(world):
+        dec = D.Decoder(shape, variant, 3, B, 512, w, wq, device=dev, head_shard=(world, r))
+        dec.gather = _LocalPeers(bufs, r)
+        for s in range(B):
+            for i, c in enumerate(dec.caches):
+                c._prefill(s, xs[i, s, :-1].to(dev), dec.weights[i], dec.acc)
+        dec.n_tokens[:] = n1 - 1
+        dec.lens_dev.fill_(n1 - 1)
+        out = torch.empty((L, B, h_loc, 128), dtype=torch.float32, device=dev)
+        last = dec.step(xs[:, :, -1].to(dev).contiguous(), attn_out=out)
+        torch.cuda.synchronize()
+        locals_.append(out.cpu().numpy())
+        assert last.shape == (B, shape.n_heads, 128)
+        if os.environ.get("XQ_ABSORB") == "force":  # the absorbed kernel did the peer stores
+            assert all(c.peer_stored for c in dec.caches)
+    scale = np.max(np.abs(full))
+    np.testing.assert_allclose(np.concatenate(locals_, axis=2), full, atol=1e-5 * scale, rtol=0)
+    for r in range(world):  # the last two layers' buffers (parity L-1, L-2) on every rank
+        for i in (L - 1, L - 2):
+            from paper_2508_10395_b200 import parallel as P
+
+            got = P.gathered_view(bufs[r][i % 2]).cpu().numpy()
+            np.testing.assert_allclose(got, full[i], atol=1e-5 * scale, rtol=0)
