@@ -182,11 +182,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
     }
     cp_async_commit();
   };
-  const int wfirst = t0 + warp * kBlk;
+  // block k of this warp: warp w takes whole K groups (128 tokens, 128/kBlk blocks)
+  // w, w + nw, ...: the per-channel K params load once per group
+  constexpr int kBpg = 128 / kBlk;
+  auto wb_of = [&](int k) { return t0 + ((k / kBpg) * kNw + warp) * 128 + (k % kBpg) * kBlk; };
 #pragma unroll
-  for (int k = 0; k < kStages - 1; ++k) issue(wfirst + k * kNw * kBlk, k);
+  for (int k = 0; k < kStages - 1; ++k) issue(wb_of(k), k);
   int stage = 0;
-  for (int wbase = wfirst; wbase < t1; wbase += kNw * kBlk) {
+  for (int kb = 0, wbase = wb_of(0); wbase < t1; wbase = wb_of(++kb)) {
     const int grp = wbase / p.G;
     if (grp != cur_grp && wbase < nfl) {
       const __half* prow = p.k_params + (row0 / p.G + grp) * 2 * p.kvw;
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
       }
     }
     __syncwarp();  // every lane has read this stage before it is refilled
-    issue(wbase + (kStages - 1) * kNw * kBlk, stage == 0 ? kStages - 1 : stage - 1);
+    issue(wb_of(kb + kStages - 1), stage == 0 ? kStages - 1 : stage - 1);
     stage = stage + 1 == kStages ? 0 : stage + 1;
   }
   cp_async_wait<0>();
