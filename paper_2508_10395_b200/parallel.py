@@ -115,6 +115,7 @@ class PeerHeadGather:
 
         self.world, self.rank, self.h, self.n_seqs = world, rank, n_heads_local, n_seqs
         self.shape = (world, n_seqs, n_heads_local, HEAD_DIM)
+        torch.cuda.set_device(device)  # symmetric allocations land on the current device
         name = (group or dist.group.WORLD).group_name
         self.bufs = [symm.empty(self.shape, dtype=torch.float32, device=device) for _ in range(2)]
         self.hdls = [symm.rendezvous(b, name) for b in self.bufs]
