@@ -81,8 +81,14 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (a fork/exec, ~100 ms of CPU) stays outside the timed
+            # region: wait for its first sample, then mark where the region's samples begin
+            t_end = time.perf_counter() + 3.0
+            while not self.lines and time.perf_counter() < t_end and self.proc.poll() is None:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
+        self.mark = len(self.lines)
         return self
 
     def _read(self):
@@ -100,7 +106,13 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        mark = getattr(self, "mark", 0)
+        lines = self.lines[mark:]
+        note = None
+        if not lines and mark > 0:  # region shorter than the 200 ms sampling period
+            lines = self.lines[mark - 1:mark]
+            note = "timed region shorter than the 200 ms sampling period: nearest sample before it"
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -112,8 +124,11 @@ class ClockSampler:
             for n, v in zip(names, parts[3:7]):
                 if v.lower() == "active":
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+               "reasons": sorted(reasons), "samples": 0 if note else len(sm)}
+        if note:
+            out["note"] = note
+        return out
 
 
 # ---------------------------------------------------------------------------
