@@ -476,6 +476,11 @@ class CacheBackend:
         # XQ_ABSORB: unset/"1" -> "auto" (by workload size), "force" -> True, "0" -> False
         env = os.environ.get("XQ_ABSORB", "1")
         self.absorb = False if env == "0" else (True if env == "force" else "auto")
+        # KV-head-group sharding (decode.Decoder with parallel.PeerHeadGather): device
+        # addresses the absorbed kernel's projection stores to, set around one _attend
+        # call; peer_stored tells the decoder whether that launch did the gather
+        self.peer_outs: list[int] | None = None
+        self.peer_stored = False
 
     # -- interface ---------------------------------------------------------
     def prefill(self, x, weights: LayerWeights, acc: Accumulator | None = None, slot=None):
@@ -624,7 +629,7 @@ class CacheBackend:
                     av_rb, self.group_size, self.L, kdim, N.ptr(lens), self.n_slots, max_len,
                     N.ptr(wk_arr), N.ptr(wv_arr), self.n_kv, group, N.ptr(q), N.ptr(rope),
                     rope.shape[1] // 2, 1.0 / math.sqrt(HEAD_DIM), N.ptr(ws), nbytes)
-            peers = getattr(self, "peer_outs", None)
+            peers = self.peer_outs
             if peers:  # head-sharded engine: the projection stores into every rank's gather slot
                 arr = (ctypes.c_void_p * len(peers))(*peers)
                 N.call("xq_decode_attend_absorbed_peers", *args, ctypes.cast(arr, ctypes.c_void_p),
