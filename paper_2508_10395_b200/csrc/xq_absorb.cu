@@ -72,6 +72,10 @@ constexpr int kEpiWarp0 = 12;
 constexpr int kG = 128;
 constexpr int kMaxStages = 4;
 constexpr int kMaxHeads = 64;
+#ifndef XQ_SERPENTINE
+#define XQ_SERPENTINE 1
+#endif
+constexpr bool kSerpentine = XQ_SERPENTINE != 0;  // fp16-row K passes alternate chunk direction
 constexpr uint32_t kABytes = kTileM * 128;  // [128 x 64] fp16 = 16 KB
 constexpr uint32_t kBSub = 128 * 128;       // 128 W rows x 64 channels (one KV head)
 // KV heads per K pass: 4 for MHA (two N=256 MMAs share each A stage: half the
@@ -262,8 +266,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     walk<PIPE>(p, cluster, n_clusters,
       [&](const Tile& tl, int ps) {
         const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
+        // fp16 A rows: odd passes walk the channel chunks backwards, so a pass
+        // starts on the chunks the previous one read last (still in L2). The
+        // 74 clusters' 2 MB tiles exceed L2, and a forward-only walk re-reads
+        // every pass from HBM. The MMA accumulates in issue order, so only the
+        // fp32 summation order changes. Code-fed passes keep the forward order
+        // (the producers' chunk mapping; their codes tiles fit L2).
+        const bool rev = !PROD && kSerpentine && (ps & 1);
         for (int kc = 0; kc < nkc; ++kc, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          const int kcc = rev ? nkc - 1 - kc : kc;
           XQ_PROF(0, mbar_wait(&empty[s], ph ^ 1));
           if (elect_one()) {
             uint8_t* st = sAB + s * kABStage;
@@ -272,10 +284,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             else mbar_arrive_remote(full_leader0 + 8 * s);
 #pragma unroll
             for (int sub = 0; sub < KH / 2; ++sub)  // KV head KH*ps + 2*sub + rank
-              tma_load_2d_pair(st + kABytes + sub * kBSub, &tmap_w, &full[s], kc * kChunk,
+              tma_load_2d_pair(st + kABytes + sub * kBSub, &tmap_w, &full[s], kcc * kChunk,
                                (KH * ps + 2 * sub + static_cast<int>(rank)) * 128, p.w_hint);
             if constexpr (!PROD)
-              tma_load_2d_pair(st, &tmap_ka, &full[s], kc * kChunk, row_tile + rank * kTileM,
+              tma_load_2d_pair(st, &tmap_ka, &full[s], kcc * kChunk, row_tile + rank * kTileM,
                                kEvictNormal);
           }
           __syncwarp();
