@@ -112,6 +112,8 @@ struct Params {
   float* part_o;       // [n_seqs][n_tiles][n_q][kdim]
   float2* part_ml;     // [n_seqs][n_tiles][n_q] (m, l), m in the log2 domain
   uint64_t w_hint;
+  int32_t a_hint;   // fp16-row A: 0 evict-normal, 1 split (see the K-pass TMA loop), 2 evict-last
+  int32_t a_split;  // split: chunks at the start of each sweep loaded evict-first
   uint32_t off_p, off_codes, off_q, off_sc, off_rope, off_stg, off_bar;
 };
 
@@ -287,8 +289,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tma_load_2d_pair(st + kABytes + sub * kBSub, &tmap_w, &full[s], kcc * kChunk,
                                (KH * ps + 2 * sub + static_cast<int>(rank)) * 128, p.w_hint);
             if constexpr (!PROD)
+              // split: the first half of a sweep is the part the previous
+              // sweep left in L2 (demote it), the second half is what the next
+              // sweep reads first (keep it)
               tma_load_2d_pair(st, &tmap_ka, &full[s], kcc * kChunk, row_tile + rank * kTileM,
-                               kEvictNormal);
+                               p.a_hint == 1 ? (kc < p.a_split ? kEvictFirst : kEvictLast)
+                                             : (p.a_hint == 2 ? kEvictLast : kEvictNormal));
           }
           __syncwarp();
         }
@@ -310,7 +316,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh)
                 tma_load_2d_pair(st + hh * kMNHalf, &tmap_va, &full[s],
-                                 bb * 256 + rank * 128 + hh * 64, row_tile + 64 * j, kEvictNormal);
+                                 bb * 256 + rank * 128 + hh * 64, row_tile + 64 * j,
+                                 p.a_hint != 0 ? kEvictFirst : kEvictNormal);  // last use
             }
           }
           __syncwarp();
@@ -1288,6 +1295,13 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
     const char* e = getenv("XQ_W_HINT");
     const int h = e ? atoi(e) : 1;
     p.w_hint = h == 0 ? kEvictNormal : (h == 2 ? kEvictFirst : kEvictLast);
+    // fp16-row A operand (XQuant-CL delta layers): the serpentine sweeps keep
+    // the trailing (16 - split)/16 of each sweep evict-last for the next one
+    // (C3: 30.7 -> 23.9 GB of DRAM reads per launch, profiles/r01_c3_l2_policy.txt)
+    const char* a = getenv("XQ_A_HINT");
+    p.a_hint = a ? atoi(a) : 1;
+    const char* sp = getenv("XQ_A_SPLIT16");
+    p.a_split = (p.kdim / kChunk) * (sp ? atoi(sp) : 8) / 16;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int status;
