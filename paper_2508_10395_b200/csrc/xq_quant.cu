@@ -378,9 +378,9 @@ __global__ void __launch_bounds__(256) k_cl_accumulate(
 // of accumulator in flight as four 16-byte loads, `BITS` whole words of codes and
 // four (scale, zp) loads, with 32-bit index math. Per element the arithmetic is the
 // generic kernel's (fp32 add of the fp32 dequantized delta, one fp16 rounding).
-template <int BITS>
+template <int BITS, bool SEED>
 __global__ void __launch_bounds__(256) k_cl_accumulate_h(
-    int seed, const uint8_t* __restrict__ codes, int64_t row_bytes,
+    const uint8_t* __restrict__ codes, int64_t row_bytes,
     const __half2* __restrict__ params, int G, int cols, const int32_t* __restrict__ lens, int max_len, int64_t L_max,
     uint32_t total, __half* __restrict__ x16) {
   constexpr uint32_t kMask = (1u << BITS) - 1u;
@@ -397,7 +397,9 @@ __global__ void __launch_bounds__(256) k_cl_accumulate_h(
     uint4* xp = reinterpret_cast<uint4*>(x16 + r * cols + c0);
     uint4 q[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = seed ? make_uint4(0u, 0u, 0u, 0u) : xp[k];
+    // SEED is a template flag: as a runtime flag here it halved the kernel's
+    // bandwidth (C3 shape: 3.49 vs 1.77 ms, tools/bench_accumulate.py)
+    for (int k = 0; k < 4; ++k) q[k] = SEED ? make_uint4(0u, 0u, 0u, 0u) : xp[k];
     // 32 codes = BITS words at byte 4*BITS*(c0/32) of the row
     const uint32_t* cw = reinterpret_cast<const uint32_t*>(codes + r * row_bytes) + (c0 / 32) * BITS;
     uint32_t w[BITS + 1];
@@ -596,17 +598,17 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
   if (acc == nullptr && cols % 32 == 0 && cols < (int64_t(1) << 30) &&
       items32 + (int64_t)148 * 6 * 256 < (int64_t(1) << 32)) {
     const int64_t blocks = std::min<int64_t>((items32 + 255) / 256, 148 * 6);  // 38 regs: 6 CTAs per SM
-    auto launch = [&](auto kern) {
+    auto launch2 = [&](auto kern) {
       kern<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
-          seed, codes, row_bytes, static_cast<const __half2*>(params), group_size,
+          codes, row_bytes, static_cast<const __half2*>(params), group_size,
           static_cast<int>(cols), seq_lens, max_len, L_max, static_cast<uint32_t>(items32),
           static_cast<__half*>(x16_out));
     };
     switch (bits) {
-      case 2: launch(k_cl_accumulate_h<2>); break;
-      case 3: launch(k_cl_accumulate_h<3>); break;
-      case 4: launch(k_cl_accumulate_h<4>); break;
-      default: launch(k_cl_accumulate_h<8>); break;
+      case 2: seed ? launch2(k_cl_accumulate_h<2, true>) : launch2(k_cl_accumulate_h<2, false>); break;
+      case 3: seed ? launch2(k_cl_accumulate_h<3, true>) : launch2(k_cl_accumulate_h<3, false>); break;
+      case 4: seed ? launch2(k_cl_accumulate_h<4, true>) : launch2(k_cl_accumulate_h<4, false>); break;
+      default: seed ? launch2(k_cl_accumulate_h<8, true>) : launch2(k_cl_accumulate_h<8, false>); break;
     }
     return check_launch("xq_cl_accumulate");
   }
