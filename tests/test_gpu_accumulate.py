@@ -63,3 +63,34 @@ def test_fp16_accumulate_matches_generic(seed, bits, d, G):
         assert torch.equal(x_fast[rows], want[rows]), (b, n)
         rest = slice(b * L + n, (b + 1) * L)
         assert torch.equal(x_fast[rest], x0[rest])  # untouched past the sequence length
+
+
+def test_fp16_accumulate_bandwidth_floor():
+    """Performance guard: the fp16 update streams at about 5.2 TB/s of algorithmic
+    traffic. A regression that serialised its accumulator loads ran
+    at 2.6 TB/s and passed every bit-exact test. The floor here, 3.5 TB/s, sits between
+    the two. The shape is B=4 x 32K x 4096 at 2 bits, 2.3 GB per launch, so well past L2."""
+    import torch
+
+    from paper_2508_10395_b200 import _native as N
+
+    dev = torch.device("cuda", 0)
+    B, L, d, bits, G = 4, 32768, 4096, 2, 128
+    row_bytes = -(-d * bits // 64) * 8
+    codes = torch.randint(0, 255, (B * L, row_bytes), dtype=torch.uint8, device=dev)
+    params = (torch.rand(B * L, d // G, 2, device=dev) * 0.01).to(torch.float16)
+    lens = torch.full((B,), L, dtype=torch.int32, device=dev)
+    x16 = torch.zeros(B * L, d, dtype=torch.float16, device=dev)
+    for _ in range(3):
+        _run(N, 0, codes, row_bytes, params, bits, G, d, lens, B, L, L, None, x16)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 10
+    e0.record()
+    for _ in range(n):
+        _run(N, 0, codes, row_bytes, params, bits, G, d, lens, B, L, L, None, x16)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    tbs = B * L * d * (4.0 + bits / 8 + 4.0 / G) / 1e9 / ms
+    assert tbs > 3.5, f"xq_cl_accumulate at {tbs:.2f} TB/s ({ms:.3f} ms)"
