@@ -378,6 +378,15 @@ __global__ void __launch_bounds__(256) k_cl_accumulate(
 // of accumulator in flight as four 16-byte loads, `BITS` whole words of codes and
 // four (scale, zp) loads, with 32-bit index math. Per element the arithmetic is the
 // generic kernel's (fp32 add of the fp32 dequantized delta, one fp16 rounding).
+#ifndef XQ_ACC_CS
+#define XQ_ACC_CS 0
+#endif
+#ifndef XQ_ACC_CTAS
+#define XQ_ACC_CTAS 6
+#endif
+#ifndef XQ_ACC_COALESCED
+#define XQ_ACC_COALESCED 1
+#endif
 template <int BITS, bool SEED>
 __global__ void __launch_bounds__(256) k_cl_accumulate_h(
     const uint8_t* __restrict__ codes, int64_t row_bytes,
@@ -399,7 +408,11 @@ __global__ void __launch_bounds__(256) k_cl_accumulate_h(
 #pragma unroll
     // SEED is a template flag: as a runtime flag here it halved the kernel's
     // bandwidth (C3 shape: 3.49 vs 1.77 ms, tools/bench_accumulate.py)
+#if XQ_ACC_CS
+    for (int k = 0; k < 4; ++k) q[k] = SEED ? make_uint4(0u, 0u, 0u, 0u) : __ldcs(xp + k);
+#else
     for (int k = 0; k < 4; ++k) q[k] = SEED ? make_uint4(0u, 0u, 0u, 0u) : xp[k];
+#endif
     // 32 codes = BITS words at byte 4*BITS*(c0/32) of the row
     const uint32_t* cw = reinterpret_cast<const uint32_t*>(codes + r * row_bytes) + (c0 / 32) * BITS;
     uint32_t w[BITS + 1];
@@ -427,7 +440,72 @@ __global__ void __launch_bounds__(256) k_cl_accumulate_h(
         const __half2 h = __floats2half2_rn(old.x + v[0], old.y + v[1]);
         hw[j] = *reinterpret_cast<const uint32_t*>(&h);
       }
+#if XQ_ACC_CS
+      __stcs(xp + k, make_uint4(hw[0], hw[1], hw[2], hw[3]));
+#else
       xp[k] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+#endif
+    }
+  }
+}
+
+// Warp-coalesced form of the fp16 update for BITS 2/4/8 and cols % 1024 == 0: a
+// warp owns 1024 channels of one row, lane l channels 256k + 8l .. +7 (k < 4), so
+// every 16-byte accumulator load and store instruction covers 512 contiguous bytes
+// (the per-thread-contiguous form touches a quarter of each 64-byte span per
+// instruction and leans on L1 to merge them). A lane's 8 codes are BITS whole bytes.
+// Same arithmetic per element as k_cl_accumulate_h.
+template <int BITS, bool SEED>
+__global__ void __launch_bounds__(256) k_cl_accumulate_w(
+    const uint8_t* __restrict__ codes, int64_t row_bytes, const __half2* __restrict__ params,
+    int G, int cols, const int32_t* __restrict__ lens, int max_len, int64_t L_max,
+    uint32_t total_spans, __half* __restrict__ x16) {
+  constexpr uint32_t kMask = (1u << BITS) - 1u;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t spans = static_cast<uint32_t>(cols) / 1024u;
+  const int64_t ng = param_stride(cols, G);
+  const uint32_t nw = gridDim.x * (blockDim.x / 32u);
+  for (uint32_t w = blockIdx.x * (blockDim.x / 32u) + (threadIdx.x >> 5); w < total_spans; w += nw) {
+    const uint32_t rowi = w / spans;
+    const uint32_t b = rowi / static_cast<uint32_t>(max_len);
+    const int t = static_cast<int>(rowi - b * static_cast<uint32_t>(max_len));
+    if (t >= __ldg(lens + b)) continue;  // warp-uniform
+    const int64_t r = static_cast<int64_t>(b) * L_max + t;
+    const int cbase = static_cast<int>(w - rowi * spans) * 1024 + 8 * static_cast<int>(lane);
+    uint4* xp = reinterpret_cast<uint4*>(x16 + r * cols + cbase);  // + 32 uint4 per k
+    uint4 q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = SEED ? make_uint4(0u, 0u, 0u, 0u) : xp[32 * k];
+    uint2 cw[4];
+    __half2 sz[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c0 = cbase + 256 * k;
+      const uint8_t* cp = codes + r * row_bytes + c0 * BITS / 8;
+      if constexpr (BITS == 2) cw[k] = make_uint2(__ldg(reinterpret_cast<const unsigned short*>(cp)), 0u);
+      else if constexpr (BITS == 4) cw[k] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(cp)), 0u);
+      else cw[k] = __ldg(reinterpret_cast<const uint2*>(cp));
+      sz[k] = __ldg(params + r * ng + c0 / G);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(sz[k]);
+      uint32_t hw[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = 2 * j + e;
+          const uint32_t word = (BITS == 8 && m >= 4) ? cw[k].y : cw[k].x;
+          const uint32_t code = (word >> ((m * BITS) % 32)) & kMask;
+          v[e] = fmaf(static_cast<float>(code), f.x, f.y);
+        }
+        const float2 old = __half22float2(*reinterpret_cast<const __half2*>(&hw[j]));
+        const __half2 h = __floats2half2_rn(old.x + v[0], old.y + v[1]);
+        hw[j] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      xp[32 * k] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
     }
   }
 }
@@ -595,9 +673,26 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
   XQ_REQUIRE(group_size % 8 == 0, XQ_ECONFIG, "group_size must be a multiple of 8");
   XQ_REQUIRE(acc != nullptr || x16_out != nullptr, XQ_EUSAGE, "no accumulator buffer");
   const int64_t items32 = (int64_t)n_seqs * max_len * (cols / 32);
+  const int64_t spans = (int64_t)n_seqs * max_len * (cols / 1024);
+  if (XQ_ACC_COALESCED && acc == nullptr && cols % 1024 == 0 && bits != 3 && group_size % 8 == 0 &&
+      cols < (int64_t(1) << 30) && spans + (int64_t)148 * XQ_ACC_CTAS * 8 < (int64_t(1) << 32)) {
+    const int64_t blocks = std::min<int64_t>((spans + 7) / 8, 148 * XQ_ACC_CTAS);
+    auto launchw = [&](auto kern) {
+      kern<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
+          codes, row_bytes, static_cast<const __half2*>(params), group_size,
+          static_cast<int>(cols), seq_lens, max_len, L_max, static_cast<uint32_t>(spans),
+          static_cast<__half*>(x16_out));
+    };
+    switch (bits) {
+      case 2: seed ? launchw(k_cl_accumulate_w<2, true>) : launchw(k_cl_accumulate_w<2, false>); break;
+      case 4: seed ? launchw(k_cl_accumulate_w<4, true>) : launchw(k_cl_accumulate_w<4, false>); break;
+      default: seed ? launchw(k_cl_accumulate_w<8, true>) : launchw(k_cl_accumulate_w<8, false>); break;
+    }
+    return check_launch("xq_cl_accumulate");
+  }
   if (acc == nullptr && cols % 32 == 0 && cols < (int64_t(1) << 30) &&
-      items32 + (int64_t)148 * 6 * 256 < (int64_t(1) << 32)) {
-    const int64_t blocks = std::min<int64_t>((items32 + 255) / 256, 148 * 6);  // 38 regs: 6 CTAs per SM
+      items32 + (int64_t)148 * XQ_ACC_CTAS * 256 < (int64_t(1) << 32)) {
+    const int64_t blocks = std::min<int64_t>((items32 + 255) / 256, 148 * XQ_ACC_CTAS);  // 38 regs
     auto launch2 = [&](auto kern) {
       kern<<<static_cast<unsigned>(blocks), 256, 0, (cudaStream_t)stream>>>(
           codes, row_bytes, static_cast<const __half2*>(params), group_size,
