@@ -449,11 +449,12 @@ __global__ void __launch_bounds__(256) k_cl_accumulate_h(
   }
 }
 
-// Warp-coalesced form of the fp16 update for BITS 2/4/8 and cols % 1024 == 0: a
+// Warp-coalesced form of the fp16 update for cols % 1024 == 0: a
 // warp owns 1024 channels of one row, lane l channels 256k + 8l .. +7 (k < 4), so
 // every 16-byte accumulator load and store instruction covers 512 contiguous bytes
 // (the per-thread-contiguous form touches a quarter of each 64-byte span per
-// instruction and leans on L1 to merge them). A lane's 8 codes are BITS whole bytes.
+// instruction and leans on L1 to merge them). A lane's 8 codes are BITS whole bytes
+// (for 3 bits at any byte alignment).
 // Same arithmetic per element as k_cl_accumulate_h.
 template <int BITS, bool SEED>
 __global__ void __launch_bounds__(256) k_cl_accumulate_w(
@@ -482,7 +483,14 @@ __global__ void __launch_bounds__(256) k_cl_accumulate_w(
     for (int k = 0; k < 4; ++k) {
       const int c0 = cbase + 256 * k;
       const uint8_t* cp = codes + r * row_bytes + c0 * BITS / 8;
-      if constexpr (BITS == 2) cw[k] = make_uint2(__ldg(reinterpret_cast<const unsigned short*>(cp)), 0u);
+      if constexpr (BITS == 3) {  // 3 bytes at any alignment: one or two aligned words
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(cp) & ~uintptr_t(3));
+        const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(cp) & 3u);
+        // the second word only when the field crosses into it (never past the row end:
+        // rows are 8-byte multiples and the field ends at or before it)
+        const uint32_t lo = __ldg(wp), hi = sh >= 2u ? __ldg(wp + 1) : 0u;
+        cw[k] = make_uint2(__funnelshift_r(lo, hi, 8u * sh), 0u);
+      } else if constexpr (BITS == 2) cw[k] = make_uint2(__ldg(reinterpret_cast<const unsigned short*>(cp)), 0u);
       else if constexpr (BITS == 4) cw[k] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(cp)), 0u);
       else cw[k] = __ldg(reinterpret_cast<const uint2*>(cp));
       sz[k] = __ldg(params + r * ng + c0 / G);
@@ -674,7 +682,7 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
   XQ_REQUIRE(acc != nullptr || x16_out != nullptr, XQ_EUSAGE, "no accumulator buffer");
   const int64_t items32 = (int64_t)n_seqs * max_len * (cols / 32);
   const int64_t spans = (int64_t)n_seqs * max_len * (cols / 1024);
-  if (XQ_ACC_COALESCED && acc == nullptr && cols % 1024 == 0 && bits != 3 && group_size % 8 == 0 &&
+  if (XQ_ACC_COALESCED && acc == nullptr && cols % 1024 == 0 && group_size % 8 == 0 &&
       cols < (int64_t(1) << 30) && spans + (int64_t)148 * XQ_ACC_CTAS * 8 < (int64_t(1) << 32)) {
     const int64_t blocks = std::min<int64_t>((spans + 7) / 8, 148 * XQ_ACC_CTAS);
     auto launchw = [&](auto kern) {
@@ -685,6 +693,7 @@ int xq_cl_accumulate(int32_t seed, const uint8_t* codes, int64_t row_bytes, cons
     };
     switch (bits) {
       case 2: seed ? launchw(k_cl_accumulate_w<2, true>) : launchw(k_cl_accumulate_w<2, false>); break;
+      case 3: seed ? launchw(k_cl_accumulate_w<3, true>) : launchw(k_cl_accumulate_w<3, false>); break;
       case 4: seed ? launchw(k_cl_accumulate_w<4, true>) : launchw(k_cl_accumulate_w<4, false>); break;
       default: seed ? launchw(k_cl_accumulate_w<8, true>) : launchw(k_cl_accumulate_w<8, false>); break;
     }
