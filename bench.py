@@ -37,11 +37,22 @@ sys.path.insert(0, ROOT)
 
 METRIC = "decode tokens/s at 32K ctx vs fp16 KV-cache; remat roofline %; memory compression"
 
+# model shapes (d, heads, kv group, layers) -- the same table as
+# paper_2508_10395_b200.decode.SHAPES, inlined so the reference arm never imports
+# the package (its process must load no library of ours)
+REF_SHAPES = {
+    "llama2-7b": dict(hidden_dim=4096, n_heads=32, kv_group=1, n_layers=32),
+    "llama3.1-8b": dict(hidden_dim=4096, n_heads=32, kv_group=4, n_layers=32),
+    "llama2-13b": dict(hidden_dim=5120, n_heads=40, kv_group=1, n_layers=40),
+}
+
 CONFIGS = {
     "c2": dict(workload="XQuant 3-bit, Llama-2-7B shape (32 layers), batch 8, 32K context",
                shape="llama2-7b", variant="xq-mha", bits=3, batch=8, ctx=32768),
+    # configs[2]: one global batch of 16 split by sequence over the ranks (16/n per GPU)
     "c3": dict(workload="XQuant-CL 2-bit, Llama-2-7B shape, batch 16, 32K context",
-               shape="llama2-7b", variant="xq-cl-mha", bits=2, batch=16, ctx=32768),
+               shape="llama2-7b", variant="xq-cl-mha", bits=2, batch=16, ctx=32768,
+               parallel="batch"),
     "c4": dict(workload="xq-gqa 3-bit latent, Llama-3.1-8B shape, batch 32, 16K context",
                shape="llama3.1-8b", variant="xq-gqa", bits=3, batch=32, ctx=16384,
                parallel="heads"),
@@ -52,6 +63,46 @@ CONFIGS = {
     "c5": dict(workload="XQuant-CL 3-bit, Llama-2-13B shape (40 layers), batch 8 per GPU, 32K context",
                shape="llama2-13b", variant="xq-cl-mha", bits=3, batch=8, ctx=32768),
 }
+
+
+def _split(cfg, world: int, rank: int) -> tuple[int, int, int]:
+    """(sequences on this rank, sequences per step over all ranks, first sequence).
+
+    "batch": configs[2]'s one global batch split by sequence (16/n per GPU, strong
+    scaling); "heads": every rank serves the whole batch for its KV heads; else
+    every rank decodes its own batch (weak scaling)."""
+    B, mode = cfg["batch"], cfg.get("parallel")
+    if mode == "batch" and world > 1:
+        per, extra = divmod(B, world)
+        start = rank * per + min(rank, extra)
+        return per + (1 if rank < extra else 0), B, start
+    if mode == "heads" and world > 1:
+        return B, B, 0
+    return B, world * B, rank * B
+
+
+def _config_dict(cfg, world: int, gather: str = "nccl") -> dict:
+    """The workload description both arms print (identical keys and values)."""
+    sh = REF_SHAPES[cfg["shape"]]
+    n_layers = cfg.get("layers", sh["n_layers"])
+    bits = cfg["bits"]
+    policy = [max(bits, 4) if i < 3 else bits for i in range(n_layers)]  # LayerPolicy.for_bits
+    mode = cfg.get("parallel")
+    if world == 1:
+        par = "single GPU"
+    elif mode == "heads":
+        par = f"kv-head-group x{world} (" + (
+            "peer-store gather from the projection kernel into symmetric memory" if gather == "peer"
+            else "NCCL all-gather of attention outputs") + ")"
+    elif mode == "batch":
+        par = f"batch-split x{world} ({cfg['batch']} sequences over {world} GPUs, no data-path collective)"
+    else:
+        par = f"batch-sharded x{world} ({cfg['batch']} sequences per GPU, no data-path collective)"
+    return {"workload": cfg["workload"], "shape": cfg["shape"], "variant": cfg["variant"],
+            "bits": bits, "policy_bits": policy[:4] + ["..."], "global_batch": _split(cfg, world, 0)[1],
+            "batch_per_gpu": _split(cfg, world, 0)[0],
+            "context": cfg["ctx"] + 1, "layers": n_layers, "parallelism": par,
+            "l2": "no flush: per-step inputs (packed caches, GBs) exceed the 126 MB L2"}
 
 
 def _peaks():
@@ -155,11 +206,9 @@ class CpuReferenceStep:
         import numpy as np
 
         self.kind = _import_reference()
-        from paper_2508_10395_b200.decode import SHAPES
-
-        sh = SHAPES[cfg["shape"]]
-        self.d, self.H, self.g = sh.hidden_dim, sh.n_heads, sh.kv_group
-        self.L = sh.n_layers if "layers" not in cfg else cfg["layers"]
+        sh = REF_SHAPES[cfg["shape"]]
+        self.d, self.H, self.g = sh["hidden_dim"], sh["n_heads"], sh["kv_group"]
+        self.L = sh["n_layers"] if "layers" not in cfg else cfg["layers"]
         self.variant, self.bits, self.ctx, self.batch = cfg["variant"], cfg["bits"], cfg["ctx"], cfg["batch"]
         rng = np.random.default_rng(seed)
         d, kvw = self.d, self.d // self.g
@@ -254,16 +303,19 @@ def run_reference(args, cfg):
     times = [ref.step() for _ in range(args.steps)]
     per = statistics.mean(times)
     val = ref.tokens_per_s(per)
+    # a reference "step" is the bounded sample: one layer x one sequence of the
+    # full-context decode step; value extrapolates it to tokens/s of the workload
+    # (L layer-samples per token of a sequence; sequences run one after another)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per * 1e3 * ref.L * cfg["batch"], "higher_is_better": True,
+        "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "variant": cfg["variant"], "bits": cfg["bits"],
-                   "batch_per_gpu": cfg["batch"], "context": cfg["ctx"] + 1},
+        "config": _config_dict(cfg, args.gpus, args.gather),
         "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": os.cpu_count(),
                          "kind": ref.kind, "sample": ref.sample_desc(),
-                         "seconds_per_layer_seq": per, "setup_s": build_s},
+                         "seconds_per_layer_seq": per, "setup_s": build_s,
+                         "ms_per_full_step_extrapolated": per * 1e3 * ref.L * cfg["batch"]},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -284,6 +336,9 @@ def _dist():
     if world > 1:
         import torch.distributed as dist
 
+        # communicator-init lines on stderr: the rank count is checkable from the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
@@ -343,14 +398,17 @@ def run_xquant(args, cfg):
     dev = torch.device("cuda", local)
     shape = D.SHAPES[cfg["shape"]]
     n_layers = cfg.get("layers", shape.n_layers)
-    B, ctx = cfg["batch"], cfg["ctx"]
+    B, tokens_per_step, _ = _split(cfg, world, rank)
+    ctx = cfg["ctx"]
     total_steps = args.warmup + 2 * args.steps + 2
     L_max = -(-(ctx + total_steps) // 128) * 128
     # "heads": KV-head-group sharding of one global batch (strong scaling, one
-    # all-gather of attention outputs per layer); otherwise every rank decodes
+    # all-gather of attention outputs per layer); "batch": the global batch split
+    # by sequence (strong scaling, no collective); otherwise every rank decodes
     # its own batch (weak scaling, no collective)
     heads = cfg.get("parallel") == "heads" and world > 1
-    wseed = 0 if heads else rank
+    strong = heads or (cfg.get("parallel") == "batch" and world > 1)
+    wseed = 0 if strong else rank  # one model; batch-split ranks fill their own sequences
     weights, w_q = D.synthetic_weights(shape, cfg["variant"], dev, seed=wseed, layers=n_layers)
     shard = (world, rank) if heads else None
 
@@ -358,10 +416,10 @@ def run_xquant(args, cfg):
         dec = D.Decoder(shape, variant, cfg["bits"], B, L_max, weights, w_q, device=dev,
                         head_shard=shard, gather=args.gather)
         t0 = time.perf_counter()
-        dec.fill_synthetic(ctx, seed=1 + wseed)
+        dec.fill_synthetic(ctx, seed=1 + (rank if not heads else 0))
         return dec, time.perf_counter() - t0
 
-    g = torch.Generator(device=dev).manual_seed(100 + wseed)
+    g = torch.Generator(device=dev).manual_seed(100 + (rank if not heads else 0))
     d = shape.hidden_dim
     n_in = args.warmup + args.steps
     xs = [torch.randn(n_layers, B, d, generator=g, device=dev).to(torch.bfloat16) for _ in range(n_in)]
@@ -380,7 +438,6 @@ def run_xquant(args, cfg):
     t = _max_over_ranks(world, t)
     kern_s = sum(a.elapsed_time(b) for a, b in timers) / 1e3
     kern_s = _max_over_ranks(world, kern_s)
-    tokens_per_step = B if heads else world * B
     value = tokens_per_step * args.steps / t
     ms_per_step = t / args.steps * 1e3
     l_avg = ctx_before + (args.steps + 1) / 2.0
@@ -495,18 +552,10 @@ def run_xquant(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong" if heads else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": "f16",
         "data": "synthetic (random-init weights, N(0,1) activations)",
-        "config": {"workload": cfg["workload"], "shape": cfg["shape"], "variant": cfg["variant"],
-                   "bits": cfg["bits"], "policy_bits": bits_per_layer[:4] + ["..."],
-                   "batch_per_gpu": B, "context": ctx + 1, "layers": n_layers,
-                   "parallelism": (f"kv-head-group x{world} ("
-                                   + ("peer-store gather from the projection kernel into symmetric memory"
-                                      if args.gather == "peer" else "NCCL all-gather of attention outputs")
-                                   + ")"
-                                   if heads else f"batch-sharded x{world} (no data-path collective)"),
-                   "l2": "no flush: per-step inputs (packed caches, GBs) exceed the 126 MB L2"},
+        "config": _config_dict(cfg, world, args.gather),
         "fp16_kv": fp16,
         "speedup_vs_fp16_kv": (value / fp16["value"]) if fp16 and fp16.get("value") else None,
         "kvq": kvq,
@@ -554,6 +603,23 @@ def main():
     ap.add_argument("--ctx", type=int, default=None, help="override the config's context")
     ap.add_argument("--batch", type=int, default=None, help="override the per-GPU batch")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        # not under torchrun: start one rank per GPU ourselves (same launch as the driver's)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if world and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     cfg = dict(CONFIGS[args.config])
     if args.ctx or args.batch:
         cfg["ctx"] = args.ctx or cfg["ctx"]

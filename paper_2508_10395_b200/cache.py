@@ -16,16 +16,15 @@ differences are the ones the hot path needs:
   output without materialising K/V; ``rematerialize`` stays for parity and
   returns float32 K/V (SIMT debug kernel).
 
-Variants on the hot path: ``fp16`` (baseline semantics), ``xq-mha``,
-``xq-gqa`` and ``xq-cl-mha``. ``kvq`` and ``xq-cl-gqa`` are "next" rows of the
-scope table and raise ``ConfigError`` here.
+All six variants (``cache.py:41``) have a GPU backend: ``fp16`` (baseline
+semantics), ``xq-mha``, ``xq-gqa``, ``xq-cl-mha`` on the hot path, and the
+"next" rows ``kvq`` and ``xq-cl-gqa``.
 """
 
 from __future__ import annotations
 
 import ctypes
 import math
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -41,6 +40,10 @@ DEFAULT_GROUP_SIZE = 128
 HEAD_DIM = 128
 ROPE_THETA = 10000.0
 TOKEN, CHANNEL = 0, 1
+# fused decode kernel: "auto" (the V-absorbed kernel when the workload has enough
+# 256-token tiles, else the unabsorbed one), "absorbed" or "unabsorbed"; read
+# when a backend is constructed
+FUSED_KERNEL = "auto"
 
 
 # ---------------------------------------------------------------------------
@@ -473,9 +476,8 @@ class CacheBackend:
         self.n_tokens = np.zeros(n_slots, dtype=np.int64)
         self.lens_dev = torch.zeros(n_slots, dtype=torch.int32, device=self.device)
         # V absorption (xq_absorb.cu): exact reassociation p.(x W_v) = (p.x) W_v.
-        # XQ_ABSORB: unset/"1" -> "auto" (by workload size), "force" -> True, "0" -> False
-        env = os.environ.get("XQ_ABSORB", "1")
-        self.absorb = False if env == "0" else (True if env == "force" else "auto")
+        # FUSED_KERNEL "auto" picks by workload size; the tests pin both kernels
+        self.absorb = {"auto": "auto", "absorbed": True, "unabsorbed": False}[FUSED_KERNEL]
         # KV-head-group sharding (decode.Decoder with parallel.PeerHeadGather): device
         # addresses the absorbed kernel's projection stores to, set around one _attend
         # call; peer_stored tells the decoder whether that launch did the gather

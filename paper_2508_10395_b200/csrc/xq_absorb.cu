@@ -1106,13 +1106,9 @@ int launch(const Maps& m, Params p, cudaStream_t st) {
   int status = plan_smem<AK, AV, BITS, GROUP>(p, smem);
   if (status != XQ_OK) return status;
   auto kern = k_decode_absorbed<AK, AV, BITS, GROUP>;
-  static size_t configured = 0;
-  if (configured < smem) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-        cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(decode_absorbed)");
-    configured = 227 * 1024;
-  }
+  if ((status = ensure_smem(reinterpret_cast<const void*>(kern), 227 * 1024,
+                            "cudaFuncSetAttribute(decode_absorbed)")) != XQ_OK)
+    return status;
   const int pairs = p.n_units < num_sms() / 2 ? p.n_units : num_sms() / 2;
   kern<<<2 * pairs, kThreads, smem, st>>>(m.w, m.ka, m.kp, m.va, m.vp, m.o, p);
   return check_launch("k_decode_absorbed");
@@ -1291,18 +1287,13 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
   float* ws = static_cast<float*>(workspace);
   p.part_o = ws;
   p.part_ml = reinterpret_cast<float2*>(ws + (int64_t)n_seqs * p.n_tiles * n_q * kdim);
-  {
-    const char* e = getenv("XQ_W_HINT");
-    const int h = e ? atoi(e) : 1;
-    p.w_hint = h == 0 ? kEvictNormal : (h == 2 ? kEvictFirst : kEvictLast);
-    // fp16-row A operand (XQuant-CL delta layers): the serpentine sweeps keep
-    // the trailing (16 - split)/16 of each sweep evict-last for the next one
-    // (C3: 30.7 -> 23.9 GB of DRAM reads per launch, profiles/r01_c3_l2_policy.txt)
-    const char* a = getenv("XQ_A_HINT");
-    p.a_hint = a ? atoi(a) : 1;
-    const char* sp = getenv("XQ_A_SPLIT16");
-    p.a_split = (p.kdim / kChunk) * (sp ? atoi(sp) : 8) / 16;
-  }
+  // W_k stays L2-resident across the CTA pairs (evict_last). fp16-row A operand
+  // (XQuant-CL delta layers): the serpentine sweeps keep the trailing half of each
+  // sweep evict-last for the next one (C3: 30.7 -> 23.9 GB of DRAM reads per
+  // launch, profiles/r01_c3_l2_policy.txt; 6-8 sixteenths measured best).
+  p.w_hint = kEvictLast;
+  p.a_hint = 1;
+  p.a_split = (p.kdim / kChunk) / 2;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int status;
   if (mha) {
@@ -1341,15 +1332,10 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
                                                       n_q, p.kdim, x_attn);
   if ((status = check_launch("k_absorb_combine")) != XQ_OK) return status;
   const size_t psmem = 8 * (size_t)kdim * sizeof(float);
-  {
-    static size_t pconf = 0;  // (dynamic + the kernel's 17 KB static reduction buffer)
-    if (pconf < psmem) {
-      if (cudaFuncSetAttribute(k_absorb_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)psmem) != cudaSuccess)
-        return check_launch("cudaFuncSetAttribute(project)");
-      pconf = psmem;
-    }
-  }
+  // (dynamic; the kernel's 17 KB static reduction buffer comes on top)
+  if ((status = ensure_smem(reinterpret_cast<const void*>(k_absorb_project), psmem,
+                            "cudaFuncSetAttribute(project)")) != XQ_OK)
+    return status;
   k_absorb_project<<<dim3(n_q, 4, (n_seqs + 7) / 8), 256, psmem, st>>>(
       x_attn, n_seqs, n_q, group, p.kdim, static_cast<const __half*>(wv_arranged), op);
   return check_launch("k_absorb_project");

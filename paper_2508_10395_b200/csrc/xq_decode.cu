@@ -671,13 +671,8 @@ static int launch_decode(const Maps& m, const DecodeParams& p, cudaStream_t st) 
   static_assert(R::kABStage % 1024 == 0, "stages must keep 1024-byte swizzle alignment");
   static_assert(smem <= 227 * 1024, "shared memory budget");
   auto kern = k_decode_attend<AK, AV, BITS, GROUP>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(decode)");
-    configured = true;
-  }
+  if (int s = ensure_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(decode)"))
+    return s;
   // one CTA pair per unit in flight; an even grid of at most one CTA per SM
   const int pairs = p.n_units < num_sms() / 2 ? p.n_units : num_sms() / 2;
   kern<<<2 * pairs, kThreads, smem, st>>>(m.w, m.ca, m.pa, m.cb, m.pb, p);
@@ -829,8 +824,6 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
     // on both dies (measured: 6.5 -> 1.4 GB of DRAM per C2 layer launch)
     int hb = n_kv_heads;
     while (hb > 1 && ((int64_t)hb * 512 * kdim > (32ll << 20) || n_kv_heads % hb)) --hb;
-    const char* e = getenv("XQ_HEAD_BLOCK");  // experiment override
-    if (e && atoi(e) >= 1 && n_kv_heads % atoi(e) == 0) hb = atoi(e);
     p.head_block = hb;
   }
   p.q_pre = q_pre;
@@ -840,11 +833,7 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
   p.partials = static_cast<float*>(workspace);
   p.dbg_acc = g_dbg_acc;
   p.dbg_tiles = g_dbg_tiles;
-  {
-    const char* e = getenv("XQ_W_HINT");  // experiment knob: 0 normal, 1 evict_last, 2 evict_first
-    const int h = e ? atoi(e) : 1;
-    p.w_hint = h == 0 ? kEvictNormal : (h == 2 ? kEvictFirst : kEvictLast);
-  }
+  p.w_hint = kEvictLast;  // the W slice of the pairs in flight stays L2-resident
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   int status;
@@ -886,8 +875,9 @@ int xq_remat_f32(int32_t ak_mode, const void* ak_src, const void* ak_params,
   p.L_max = L_max; p.kdim = kdim; p.n_out = n_out; p.w_k = w_k; p.w_v = w_v;
   p.rope = static_cast<const float2*>(rope_cs); p.k_out = k_out; p.v_out = v_out;
   const size_t smem = (2 * kdim + n_out) * sizeof(float);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_remat_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (int s = ensure_smem(reinterpret_cast<const void*>(k_remat_f32), smem,
+                         "cudaFuncSetAttribute(remat_f32)"))
+    return s;
   k_remat_f32<<<n_tok, 256, smem, static_cast<cudaStream_t>(stream)>>>(p);
   return check_launch("k_remat_f32");
 }

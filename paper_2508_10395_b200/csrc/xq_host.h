@@ -7,6 +7,9 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "../../include/xquant.h"
 
 namespace xq {
@@ -26,6 +29,26 @@ inline int fail(int status, const char* fmt, ...) {
 inline int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(XQ_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return XQ_OK;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (kernel, device): one
+// process may drive several GPUs (Decoder(device=...)), so the "already raised"
+// record is keyed by both, under a lock.
+inline int ensure_smem(const void* kern, size_t bytes, const char* what) {
+  if (bytes <= 48 * 1024) return XQ_OK;
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = reinterpret_cast<uint64_t>(kern) * 64 + static_cast<uint64_t>(dev & 63);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return XQ_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(bytes)) != cudaSuccess)
+    return check_launch(what);
+  done[key] = bytes;
   return XQ_OK;
 }
 

@@ -405,13 +405,9 @@ static int launch_kv(const __nv_bfloat16* K, const __nv_bfloat16* V, int64_t L_m
     k_kv_decode<GROUP><<<static_cast<unsigned>(n_seqs) * n_kv * n_chunks, kKvThreads, 0, st>>>(
         K, V, L_max, lens, n_kv, chunk_tokens, n_chunks, q_pre, rope, q_scale, partials);
   } else {
-    static bool configured = false;
-    if (!configured) {
-      if (cudaFuncSetAttribute(k_kv_decode_gqa<GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kGqaSmem) != cudaSuccess)
-        return check_launch("cudaFuncSetAttribute(kv_decode_gqa)");
-      configured = true;
-    }
+    if (int s = ensure_smem(reinterpret_cast<const void*>(k_kv_decode_gqa<GROUP>), kGqaSmem,
+                           "cudaFuncSetAttribute(kv_decode_gqa)"))
+      return s;
     k_kv_decode_gqa<GROUP><<<static_cast<unsigned>(n_seqs) * n_kv * n_chunks, 32 * kGqaWarps,
                              kGqaSmem, st>>>(K, V, L_max, lens, n_kv, chunk_tokens, n_chunks, q_pre, rope,
                                    q_scale, partials);

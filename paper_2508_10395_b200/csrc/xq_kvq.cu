@@ -331,13 +331,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
 template <int BITS, int GROUP>
 static int launch_one(const Params& p, int grid, cudaStream_t st) {
   constexpr uint32_t smem = smem_bytes<BITS, GROUP>();
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(k_kvq_decode<BITS, GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem) != cudaSuccess)
-      return check_launch("cudaFuncSetAttribute(kvq_decode)");
-    configured = true;
-  }
+  if (int s = ensure_smem(reinterpret_cast<const void*>(k_kvq_decode<BITS, GROUP>), smem,
+                         "cudaFuncSetAttribute(kvq_decode)"))
+    return s;
   k_kvq_decode<BITS, GROUP><<<grid, kThreads, smem, st>>>(p);
   return check_launch("k_kvq_decode");
 }

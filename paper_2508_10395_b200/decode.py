@@ -181,7 +181,8 @@ class Decoder:
 
         Returns the last layer's attention output [n_slots, n_heads, 128]
         (all layers' outputs when ``attn_out`` [n_layers, n_slots, H, 128]
-        is given). ``timers``: optional list that receives (start, end) CUDA
+        is given). With head sharding the gathered output is a copy: the
+        gather buffers are rewritten by every rank at the next step. ``timers``: optional list that receives (start, end) CUDA
         event pairs around every fused attention launch."""
         if np.any(self.n_tokens >= self.L):
             raise ConfigError("cache full")
@@ -216,6 +217,8 @@ class Decoder:
                 out = self.gather.finish(i) if cache.peer_stored else self.gather(out, i)
             elif self.gather is not None:
                 out = self.gather(out)
+        if self.gather is not None:
+            out = out.clone()
         return out
 
     def _launches_per_layer(self, cache) -> int:

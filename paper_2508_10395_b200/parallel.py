@@ -120,9 +120,10 @@ class PeerHeadGather:
         self.bufs = [symm.empty(self.shape, dtype=torch.float32, device=device) for _ in range(2)]
         self.hdls = [symm.rendezvous(b, name) for b in self.bufs]
         slot = n_seqs * n_heads_local * HEAD_DIM * 4
-        self._ptrs = []
+        self._ptrs, self._offs = [], []
         for b, hdl in zip(self.bufs, self.hdls):
             off = b.data_ptr() - hdl.buffer_ptrs[rank]  # the tensor inside its allocation
+            self._offs.append(off // 4)
             self._ptrs.append([hdl.buffer_ptrs[p] + off + rank * slot for p in range(world)])
 
     def out_ptrs(self, layer: int) -> list[int]:
@@ -133,9 +134,9 @@ class PeerHeadGather:
         return gathered_view(self.bufs[layer % 2])
 
     def __call__(self, local: torch.Tensor, layer: int = 0) -> torch.Tensor:
-        hdl = self.hdls[layer % 2]
-        for p in range(self.world):
-            hdl.get_buffer(p, self.shape, torch.float32)[self.rank].copy_(local)
+        hdl, off = self.hdls[layer % 2], self._offs[layer % 2]
+        for p in range(self.world):  # the same addresses out_ptrs() hands the kernel
+            hdl.get_buffer(p, self.shape, torch.float32, storage_offset=off)[self.rank].copy_(local)
         return self.finish(layer)
 
 

@@ -34,5 +34,7 @@ def pytest_collection_modifyitems(config, items):
 def kernel_path(request, monkeypatch):
     """Run a fused-decode test through both kernels: the V-absorbed default
     (csrc/xq_absorb.cu) and the unabsorbed remat kernel (csrc/xq_decode.cu)."""
-    monkeypatch.setenv("XQ_ABSORB", "force" if request.param == "absorbed" else "0")
+    from paper_2508_10395_b200 import cache
+
+    monkeypatch.setattr(cache, "FUSED_KERNEL", request.param)
     return request.param

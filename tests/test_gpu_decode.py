@@ -1,7 +1,6 @@
 """Decode engine (decode.Decoder) on the GPU: a multi-layer step against the
 CPU oracle, and KV-head-group shards reassembling the unsharded output."""
 
-import os
 
 import numpy as np
 import pytest
@@ -161,7 +160,7 @@ class _LocalPeers:
 
 
 @pytest.mark.parametrize("variant,g", [("xq-mha", 1), ("xq-gqa", 2)])
-def test_peer_store_gather(variant, g):
+def test_peer_store_gather(variant, g, kernel_path):
     """KV-head-group sharding with the gather done by the projection kernel's peer
     stores (xq_decode_attend_absorbed_peers): every rank's buffer holds the unsharded
     output, and attn_out keeps the local heads."""
@@ -190,7 +189,7 @@ def test_peer_store_gather(variant, g):
         torch.cuda.synchronize()
         locals_.append(out.cpu().numpy())
         assert last.shape == (B, shape.n_heads, 128)
-        if os.environ.get("XQ_ABSORB") == "force":  # the absorbed kernel did the peer stores
+        if kernel_path == "absorbed":  # the absorbed kernel did the peer stores
             assert all(c.peer_stored for c in dec.caches)
     scale = np.max(np.abs(full))
     np.testing.assert_allclose(np.concatenate(locals_, axis=2), full, atol=1e-5 * scale, rtol=0)
