@@ -109,6 +109,21 @@ int xq_quantize_rows(const void* x, int32_t x_dtype, int64_t x_row_stride, int64
                      int64_t row_bytes, void* params, double* x_eff_out, int32_t* nonfinite_flag,
                      void* stream);
 
+/* XQuant-CL quantize-and-append with the running accumulator row in float64
+ * (replaces _DeltaBackend._prefill/_decode, cache.py:460-481, with
+ * Accumulator.seed/add, cache.py:124-146). Rows as xq_quantize_rows; row i of
+ * acc_rows [n_rows, cols] (float64) is the accumulator at that token.
+ * acc_mode 1 (delta layer): quantize x - acc, then acc += code*scale + zp.
+ * acc_mode 2 (seeding base layer): quantize x, then acc = code*scale + zp.
+ * The reconstruction uses the float64 scale/zero point before their fp16
+ * storage, so the delta codes of every later layer are bit-exact with the
+ * reference's. */
+int xq_quantize_rows_cl(const void* x, int32_t x_dtype, int64_t x_row_stride, int64_t n_rows,
+                        int64_t cols, int32_t bits, int32_t group_size, const int32_t* seq_lens,
+                        int64_t row0, int64_t L_max, double* acc_rows, int32_t acc_mode,
+                        uint8_t* codes, int64_t row_bytes, void* params, int32_t* nonfinite_flag,
+                        void* stream);
+
 /* Per-channel quantization of whole token groups (quant.py:124-134): block b
  * is float32 [group_size, cols] at blocks + b*group_size*cols; its codes go to
  * arena rows dst_row0[b] .. +group_size-1 and its params to param row

@@ -391,18 +391,20 @@ class XqGqaCache:
     V latent = x @ U_v per-token. Remat through fused = diag(sigma) B^T.
     """
 
-    def __init__(self, bits, head_dim, group_size=128, fp16_first_channel=False):
+    def __init__(self, bits, head_dim, group_size=128, fp16_first_channel=False, params_f16=False):
         self.hd = head_dim
         self.bits, self.g = bits, group_size
         self.first = fp16_first_channel  # cache.py:403-409
+        self.params_f16 = params_f16
         self.k_stream = None
         self.v_stream = None
 
     def _ensure(self, r):
         if self.k_stream is None:
             self.k_stream = Stream(self.bits, PER_CHANNEL, r, self.g, buffered=True,
-                                   keep_first_channel=self.first)
-            self.v_stream = Stream(self.bits, PER_TOKEN, r, self.g, buffered=False)
+                                   keep_first_channel=self.first, params_f16=self.params_f16)
+            self.v_stream = Stream(self.bits, PER_TOKEN, r, self.g, buffered=False,
+                                   params_f16=self.params_f16)
 
     def prefill(self, lat_k, lat_v):  # cache.py:422-427 (latents precomputed)
         self._ensure(lat_k.shape[1])
@@ -450,28 +452,34 @@ class XqClMhaStack:
     (model.py:228).
     """
 
-    def __init__(self, bits_per_layer, base_layers, head_dim, group_size=128):
+    def __init__(self, bits_per_layer, base_layers, head_dim, group_size=128, params_f16=False):
         self.bits = list(bits_per_layer)
         self.base = base_layers
         self.hd = head_dim
         self.g = group_size
+        self.params_f16 = params_f16
         self.streams = [None] * len(self.bits)
         self.n_tokens = 0
 
     def _stream(self, i, width):
         if self.streams[i] is None:
-            self.streams[i] = Stream(self.bits[i], PER_TOKEN, width, self.g, buffered=False)
+            self.streams[i] = Stream(self.bits[i], PER_TOKEN, width, self.g, buffered=False,
+                                     params_f16=self.params_f16)
         return self.streams[i]
 
-    def step(self, xs, weights=None):
+    def step(self, xs, weights=None, on_layer=None, keep=True):
         """Append rows ``xs[i]`` ([n_new, d]) to every layer in order.
 
         Returns the per-layer accumulator snapshots (None for base layers
         before the seed) and, when ``weights`` (list of (w_k, w_v)) is
-        given, the per-layer remat (K, V).
+        given, the per-layer remat (K, V). ``xs`` may be an iterable that
+        produces the layers one at a time; ``on_layer(i, src)`` receives each
+        layer's remat source (x_hat or the accumulator) as it is formed, and
+        ``keep=False`` skips the snapshots (full-size runs).
         """
         acc = None
         accs, kvs = [], []
+        n_new = None
         for i, x in enumerate(xs):
             x = np.atleast_2d(np.asarray(x, np.float64))
             st = self._stream(i, x.shape[1])
@@ -480,20 +488,25 @@ class XqClMhaStack:
                 x_hat = st.reconstruct()
                 if i == self.base - 1:
                     acc = x_hat.copy()  # cache.py:463-467 / 473-477
-                accs.append(acc.copy() if acc is not None else None)
+                if keep:
+                    accs.append(acc.copy() if acc is not None else None)
                 src = x_hat
             else:
                 pos = self.n_tokens
                 delta = x - acc[pos:pos + x.shape[0]]  # cache.py:468, 478-479
                 st.bulk(delta)
                 acc = acc + st.reconstruct()  # cache.py:470, 481
-                accs.append(acc.copy())
+                if keep:
+                    accs.append(acc.copy())
                 src = acc
+            n_new = x.shape[0]
+            if on_layer is not None:
+                on_layer(i, src)
             if weights is not None:
                 w_k, w_v = weights[i]
                 n = src.shape[0]
                 kvs.append((apply_rope(src @ w_k, np.arange(n), self.hd), src @ w_v))
-        self.n_tokens += np.atleast_2d(xs[0]).shape[0]
+        self.n_tokens += n_new
         return accs, kvs
 
 

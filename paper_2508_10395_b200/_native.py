@@ -33,6 +33,8 @@ _SIGS = {
     "xq_unpack_codes": [_P, _I32, _I64, _P, _P],
     "xq_quantize_rows": [_P, _I32, _I64, _I64, _I64, _I32, _I32, _P, _I64, _I64, _P, _P, _I64,
                          _P, _P, _P, _P],
+    "xq_quantize_rows_cl": [_P, _I32, _I64, _I64, _I64, _I32, _I32, _P, _I64, _I64, _P, _I32, _P,
+                            _I64, _P, _P, _P],
     "xq_quantize_blocks_per_channel": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P],
     "xq_quantize_blocks_per_channel_f64": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P],
     "xq_dequant_rows": [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _I64, _P, _P],

@@ -202,9 +202,18 @@ def rope_table_t(n_pos: int, device) -> torch.Tensor:
 class Accumulator:
     """XQuant-CL running reconstruction (cache.py:124-146) on the device.
 
-    ``x_hat`` float32 [n_slots, L_max, d] plus its fp16 copy ``x16`` (the
-    remat A operand of the delta layers). Transient per forward pass: the
-    base layer re-seeds it every step (model.py:228); the memory is reused.
+    Two parts with two jobs:
+
+    * the remat operand of the delta layers, for every cached token: ``x16``
+      (fp16 [n_slots, L_max, d]) and, with precision "fp32", ``x_hat`` (float32).
+      It is rebuilt every step from the arenas (the base layer re-seeds it,
+      model.py:228) by the accumulate kernel;
+    * the accumulator at the tokens being appended, in float64 like the
+      reference's: ``row64`` [n_slots, d] at decode, and per prefilled slot a
+      [n, d] block (``prefill_rows``). The quantize kernel forms each delta
+      against it and adds the float64 reconstruction of the codes it just wrote
+      (``xq_quantize_rows_cl``), so delta codes are bit-exact with the
+      reference's whatever precision the remat operand is stored in.
     """
 
     def __init__(self, n_slots: int, max_len: int, width: int, device="cuda", precision="fp32"):
@@ -214,14 +223,35 @@ class Accumulator:
         if precision not in ("fp32", "fp16"):
             raise ConfigError(f"accumulator precision {precision!r}")
         self.precision = precision
+        self.width = width
         self.x_hat = (torch.zeros((n_slots, max_len, width), dtype=torch.float32, device=device)
                       if precision == "fp32" else None)
         self.x16 = torch.zeros((n_slots, max_len, width), dtype=torch.float16, device=device)
+        self.row64 = torch.zeros((n_slots, width), dtype=torch.float64, device=device)
+        self._prefill64: dict = {}
         self.seeded = False
 
     def rows(self, slot, n) -> torch.Tensor:
         """float32 view/copy of the accumulator rows 0..n-1 of a slot."""
         return self.x_hat[slot, :n] if self.x_hat is not None else self.x16[slot, :n].float()
+
+    def prefill_rows(self, slot: int, n: int, seed: bool) -> torch.Tensor:
+        """The float64 accumulator of a slot's n prefilled tokens (allocated by the
+        seeding base layer, reused by the delta layers of the same prefill)."""
+        cur = self._prefill64.get(slot)
+        if seed or cur is None or cur.shape[0] != n:
+            if not seed:
+                raise UsageError("accumulator used before the base layer seeded it")
+            cur = torch.empty((n, self.width), dtype=torch.float64, device=self.x16.device)
+            self._prefill64[slot] = cur
+        return cur
+
+    def release_prefill(self, slot: int | None = None) -> None:
+        """Drop the float64 prefill blocks (all slots, or one)."""
+        if slot is None:
+            self._prefill64.clear()
+        else:
+            self._prefill64.pop(slot, None)
 
 
 # ---------------------------------------------------------------------------
@@ -287,6 +317,25 @@ class PackedStream:
         return out
 
     # -- per-token ---------------------------------------------------------
+    def append_token_rows_cl(self, x: torch.Tensor, lens_dev: torch.Tensor, acc64: torch.Tensor,
+                             seed: bool):
+        """XQuant-CL append of one row per slot against / into the float64
+        accumulator rows ``acc64`` [n_slots, width] (xq_quantize_rows_cl)."""
+        N.call("xq_quantize_rows_cl", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.width,
+               self.bits, self.g, N.ptr(lens_dev), 0, self.L, N.ptr(acc64), 2 if seed else 1,
+               N.ptr(self.codes), self.row_bytes, N.ptr(self.params), N.ptr(self.flag),
+               N.stream_of(x.device))
+
+    def fill_rows_cl(self, x: torch.Tensor, slot: int, pos0: int, acc64: torch.Tensor, seed: bool):
+        """Bulk XQuant-CL quantization of x [n, width] into slot rows pos0.. against /
+        into the float64 accumulator block ``acc64`` [n, width]."""
+        if x.shape[0] == 0:
+            return
+        N.call("xq_quantize_rows_cl", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.width,
+               self.bits, self.g, None, slot * self.L + pos0, self.L, N.ptr(acc64),
+               2 if seed else 1, N.ptr(self.codes), self.row_bytes, N.ptr(self.params),
+               N.ptr(self.flag), N.stream_of(x.device))
+
     def append_token_rows(self, x: torch.Tensor, lens_dev: torch.Tensor, sub=None, x_eff=None):
         """Quantize one row per slot and store it at position lens[b]-1."""
         N.call("xq_quantize_rows", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.width,
@@ -1019,35 +1068,31 @@ class DeltaInputCacheMHA(CacheBackend):
         n = x.shape[0]
         lens = torch.zeros(self.n_slots, dtype=torch.int32, device=self.device)
         lens[slot] = n
-        if self.is_base:
-            self.stream.fill_rows(x.contiguous(), slot, 0)
-            if self.seeds_accumulator:
-                self._accumulate(acc, True, n, lens)
+        x = x.contiguous()
+        if self.is_base and not self.seeds_accumulator:
+            self.stream.fill_rows(x, slot, 0)
             return
-        if not acc.seeded:
+        if not self.is_base and not acc.seeded:
             raise UsageError("accumulator used before the base layer seeded it")
-        if acc.x_hat is None:  # fp16 accumulator: the delta in float32 here
-            self.stream.fill_rows((x.float() - acc.x16[slot, :n].float()).contiguous(), slot, 0)
-        else:
-            self.stream.fill_rows(x.contiguous(), slot, 0, sub=acc.x_hat.view(-1, self.d))
-        self._accumulate(acc, False, n, lens)
+        # codes against the float64 accumulator (cache.py:463-470), then the
+        # remat operand of all n rows from the arena (cache.py:139-146)
+        acc64 = acc.prefill_rows(slot, n, seed=self.is_base)
+        self.stream.fill_rows_cl(x, slot, 0, acc64, seed=self.is_base)
+        self._accumulate(acc, self.is_base, n, lens)
 
     def _decode(self, x, weights, acc, lens):
         max_len = int(self.n_tokens.max())
-        if self.is_base:
-            self.stream.append_token_rows(x.contiguous(), lens)
-            if self.seeds_accumulator:
-                self._accumulate(acc, True, max_len, lens)
+        x = x.contiguous()
+        if self.is_base and not self.seeds_accumulator:
+            self.stream.append_token_rows(x, lens)
             return
-        if not acc.seeded:
+        if not self.is_base and not acc.seeded:
             raise UsageError("accumulator used before the base layer seeded it")
-        if acc.x_hat is None:  # fp16 accumulator: x - acc[pos] in float32 here
-            pos = torch.as_tensor(self.n_tokens - 1, device=self.device)
-            rows = acc.x16[torch.arange(self.n_slots, device=self.device), pos].float()
-            self.stream.append_token_rows((x.float() - rows).contiguous(), lens)
-        else:
-            self.stream.append_token_rows(x.contiguous(), lens, sub=acc.x_hat.view(-1, self.d))
-        self._accumulate(acc, False, max_len, lens)
+        if self.is_base:
+            acc.release_prefill()
+        # the new token's delta against the float64 accumulator row (cache.py:473-481)
+        self.stream.append_token_rows_cl(x, lens, acc.row64, seed=self.is_base)
+        self._accumulate(acc, self.is_base, max_len, lens)
 
     def _prefill_kv(self, weights, acc, slot, n):
         a = self._dequant_rows(self.stream, slot, n) if self.is_base else acc.rows(slot, n)

@@ -35,8 +35,8 @@ inline int check_launch(const char* what) {
 // cudaFuncAttributeMaxDynamicSharedMemorySize is per (kernel, device): one
 // process may drive several GPUs (Decoder(device=...)), so the "already raised"
 // record is keyed by both, under a lock.
+// (Always set: a kernel's static shared memory counts against the default 48 KB.)
 inline int ensure_smem(const void* kern, size_t bytes, const char* what) {
-  if (bytes <= 48 * 1024) return XQ_OK;
   static std::mutex mu;
   static std::unordered_map<uint64_t, size_t> done;
   int dev = 0;

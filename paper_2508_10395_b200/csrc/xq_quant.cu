@@ -40,10 +40,16 @@ XQ_DEVINL double shfl_xor_d(double v, int o) { return __shfl_xor_sync(0xffffffff
 // Quantize one row (block-cooperative: warps over groups, lanes over
 // elements). Codes land in `codes_out` (shared or global bytes); the group
 // parameters are handed to `sink(g, scale, zp)` by lane 0 of the owning warp.
+// XQuant-CL running row (`acc`, float64): with `acc_mode` 1 the quantized value
+// is x - acc and the row then becomes acc + code*scale + zp (cache.py:478-481
+// with Accumulator.add, cache.py:139-146); with `acc_mode` 2 (the seeding base
+// layer, cache.py:463-467) it becomes code*scale + zp. The reconstruction is the
+// reference's float64 dequantize (fallback.py:134-146: one multiply, one add),
+// so every later delta is formed exactly as the reference forms it.
 template <class Sink>
 __device__ void quantize_row(const void* x, int dt, int64_t x_off, int64_t cols, int G, int bits,
                              const float* sub, uint8_t* codes_out, double* x_eff, int* bad,
-                             Sink sink) {
+                             Sink sink, double* acc = nullptr, int acc_mode = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int64_t ngroups = (cols + G - 1) / G;
   const double qmax = static_cast<double>((1 << bits) - 1);
@@ -55,6 +61,7 @@ __device__ void quantize_row(const void* x, int dt, int64_t x_off, int64_t cols,
     for (int64_t j = lo + lane; j < hi; j += 32) {
       double v = load_as_f64(x, dt, x_off + j);
       if (sub) v = __dsub_rn(v, static_cast<double>(sub[j]));
+      if (acc_mode == 1) v = __dsub_rn(v, acc[j]);
       finite &= isfinite(v);
       mn = fmin(mn, v);
       mx = fmax(mx, v);
@@ -71,10 +78,16 @@ __device__ void quantize_row(const void* x, int dt, int64_t x_off, int64_t cols,
     for (int64_t j = lo + lane; j < hi; j += 32) {
       double v = load_as_f64(x, dt, x_off + j);
       if (sub) v = __dsub_rn(v, static_cast<double>(sub[j]));
+      const double a = acc_mode == 1 ? acc[j] : 0.0;
+      if (acc_mode == 1) v = __dsub_rn(v, a);
       double q = floor(__dadd_rn(__ddiv_rn(__dsub_rn(v, mn), scale), 0.5));
       q = q < 0.0 ? 0.0 : (q > qmax ? qmax : q);
       codes_out[j] = static_cast<uint8_t>(q);
       if (x_eff) x_eff[j] = v;
+      if (acc_mode) {
+        const double r = __dadd_rn(__dmul_rn(q, scale), mn);
+        acc[j] = acc_mode == 1 ? __dadd_rn(a, r) : r;
+      }
     }
   }
 }
@@ -149,7 +162,8 @@ __global__ void k_quantize_rows(const void* __restrict__ x, int dt, int64_t x_st
                                 int64_t row0, int64_t L_max, const float* __restrict__ sub_rows,
                                 uint8_t* __restrict__ codes, int64_t row_bytes,
                                 __half2* __restrict__ params, double* __restrict__ x_eff,
-                                int32_t* __restrict__ flag) {
+                                int32_t* __restrict__ flag, double* __restrict__ acc = nullptr,
+                                int acc_mode = 0) {
   extern __shared__ uint8_t s_codes[];
   __shared__ int s_bad;
   if (threadIdx.x == 0) s_bad = 0;
@@ -162,7 +176,8 @@ __global__ void k_quantize_rows(const void* __restrict__ x, int dt, int64_t x_st
                s_codes, x_eff ? x_eff + i * cols : nullptr, &bad,
                [&](int64_t g, double s, double z) {
                  params[dst * ng + g] = __halves2half2(__double2half(s), __double2half(z));
-               });
+               },
+               acc ? acc + i * cols : nullptr, acc_mode);
   if (bad) s_bad = 1;
   __syncthreads();
   uint32_t* out = reinterpret_cast<uint32_t*>(codes + dst * row_bytes);
@@ -615,6 +630,30 @@ int xq_quantize_rows(const void* x, int32_t x_dtype, int64_t x_row_stride, int64
                                             static_cast<__half2*>(params), x_eff_out,
                                             nonfinite_flag);
   return check_launch("xq_quantize_rows");
+}
+
+int xq_quantize_rows_cl(const void* x, int32_t x_dtype, int64_t x_row_stride, int64_t n_rows,
+                        int64_t cols, int32_t bits, int32_t group_size, const int32_t* seq_lens,
+                        int64_t row0, int64_t L_max, double* acc_rows, int32_t acc_mode,
+                        uint8_t* codes, int64_t row_bytes, void* params, int32_t* nonfinite_flag,
+                        void* stream) {
+  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bits must be one of (2, 3, 4, 8), got %d", bits);
+  XQ_REQUIRE(group_size >= 1, XQ_ECONFIG, "group_size must be >= 1");
+  XQ_REQUIRE(dtype_size(x_dtype) > 0, XQ_ECONFIG, "unknown dtype %d", x_dtype);
+  XQ_REQUIRE(acc_rows != nullptr, XQ_EUSAGE, "acc_rows is required");
+  XQ_REQUIRE(acc_mode == 1 || acc_mode == 2, XQ_ECONFIG,
+             "acc_mode must be 1 (delta) or 2 (seed), got %d", acc_mode);
+  XQ_REQUIRE(row_bytes == row_bytes_for(cols, bits), XQ_ESHAPE,
+             "row_bytes %lld != ceil(cols*bits/64)*8 = %lld", (long long)row_bytes,
+             (long long)row_bytes_for(cols, bits));
+  XQ_REQUIRE(cols <= 48 * 1024, XQ_ESHAPE, "cols %lld too wide for one CTA", (long long)cols);
+  if (n_rows == 0 || cols == 0) return XQ_OK;
+  k_quantize_rows<<<static_cast<unsigned>(n_rows), 128, static_cast<size_t>(cols),
+                    (cudaStream_t)stream>>>(x, x_dtype, x_row_stride, cols, group_size, bits,
+                                            seq_lens, row0, L_max, nullptr, codes, row_bytes,
+                                            static_cast<__half2*>(params), nullptr,
+                                            nonfinite_flag, acc_rows, acc_mode);
+  return check_launch("xq_quantize_rows_cl");
 }
 
 int xq_quantize_blocks_per_channel(const float* blocks, int64_t n_blocks, int64_t cols,

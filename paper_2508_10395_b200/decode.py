@@ -96,7 +96,7 @@ class Decoder:
     def __init__(self, shape: ModelShape, variant: str, bits: int, n_slots: int, max_len: int,
                  weights, w_q, device="cuda", policy: C.LayerPolicy | None = None,
                  tiles_per_chunk: int | None = None, head_shard: tuple[int, int] | None = None,
-                 group=None, gather: str = "nccl"):
+                 group=None, gather: str = "nccl", acc_precision: str | None = None):
         """``head_shard=(world, rank)``: KV-head-group sharding (parallel.py).
         This rank serves KV heads parallel.head_shard(...) with column-sliced
         weights; step() all-gathers the attention outputs of all ranks, by
@@ -134,10 +134,12 @@ class Decoder:
                   device=self.device)
         self.caches = [C.make_cache(variant, i, self.policy, shape.head_dim, **kw)
                        for i in range(len(weights))]
-        # xq-cl-mha: fp16-storage accumulator (the remat operand itself); xq-cl-gqa
-        # keeps float32 (its delta latents are formed in float64)
+        # xq-cl-mha: fp16-storage accumulator (the remat operand itself) by default;
+        # xq-cl-gqa keeps float32 (its delta latents are formed in float64)
+        if acc_precision is None:
+            acc_precision = "fp16" if variant == "xq-cl-mha" else "fp32"
         self.acc = (C.Accumulator(n_slots, max_len, shape.hidden_dim, self.device,
-                                  precision="fp16" if variant == "xq-cl-mha" else "fp32")
+                                  precision=acc_precision)
                     if variant in C.CL_VARIANTS else None)
         # one shared length vector (host + device) for all layers
         self.n_tokens = np.zeros(n_slots, dtype=np.int64)
@@ -170,6 +172,8 @@ class Decoder:
                 else:
                     x = torch.randn(n_tokens, d, generator=g, device=self.device).to(torch.bfloat16)
                 cache._prefill(s, x, lw, self.acc)
+            if self.acc is not None:
+                self.acc.release_prefill(s)
         self.n_tokens[:] = n_tokens
         self.lens_dev.fill_(n_tokens)
         torch.cuda.synchronize(self.device)
