@@ -37,6 +37,10 @@ VARIANTS = ("fp16", "kvq", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")  # cach
 CL_VARIANTS = ("xq-cl-mha", "xq-cl-gqa")
 SUPPORTED = ("fp16", "kvq", "xq-mha", "xq-gqa", "xq-cl-mha", "xq-cl-gqa")
 DEFAULT_GROUP_SIZE = 128
+DEFAULT_ACCUMULATOR_BITS = 4  # cache.py:45 (accounting only)
+# arena rows of a backend built by the reference-signature make_cache (which
+# does not name a capacity): a desk-scale session; pass max_len= for more
+DEFAULT_MAX_LEN = 8192
 HEAD_DIM = 128
 ROPE_THETA = 10000.0
 TOKEN, CHANNEL = 0, 1
@@ -216,20 +220,74 @@ class Accumulator:
       reference's whatever precision the remat operand is stored in.
     """
 
-    def __init__(self, n_slots: int, max_len: int, width: int, device="cuda", precision="fp32"):
+    def __init__(self, n_slots: int | None = None, max_len: int | None = None,
+                 width: int | None = None, device="cuda", precision="fp32", *,
+                 accounting_bits: int = DEFAULT_ACCUMULATOR_BITS):
         """precision "fp16": the fp16 copy is the accumulator (``x_hat`` is None),
         which halves the per-layer accumulate traffic twice over (xq-cl-mha
-        only; the reference charges the accumulator 4 bits, cache.py:45)."""
+        only; the reference charges the accumulator 4 bits, cache.py:45).
+
+        ``Accumulator()`` (the reference's call, cache.py:124-133) defers the
+        device arrays to the first backend that uses it, which sizes them."""
         if precision not in ("fp32", "fp16"):
             raise ConfigError(f"accumulator precision {precision!r}")
         self.precision = precision
+        self.accounting_bits = accounting_bits
         self.width = width
-        self.x_hat = (torch.zeros((n_slots, max_len, width), dtype=torch.float32, device=device)
-                      if precision == "fp32" else None)
-        self.x16 = torch.zeros((n_slots, max_len, width), dtype=torch.float16, device=device)
-        self.row64 = torch.zeros((n_slots, width), dtype=torch.float64, device=device)
+        self.x_hat = self.x16 = self.row64 = None
         self._prefill64: dict = {}
         self.seeded = False
+        if n_slots is not None:
+            if max_len is None or width is None:
+                raise ConfigError("Accumulator needs n_slots, max_len and width together")
+            self._allocate(n_slots, max_len, width, torch.device(device))
+
+    def _allocate(self, n_slots, max_len, width, device):
+        self.n_slots, self.L, self.width = n_slots, max_len, width
+        self.x_hat = (torch.zeros((n_slots, max_len, width), dtype=torch.float32, device=device)
+                      if self.precision == "fp32" else None)
+        self.x16 = torch.zeros((n_slots, max_len, width), dtype=torch.float16, device=device)
+        self.row64 = torch.zeros((n_slots, width), dtype=torch.float64, device=device)
+
+    def ensure(self, n_slots: int, max_len: int, width: int, device) -> "Accumulator":
+        """Size a deferred accumulator for a backend (or check an allocated one)."""
+        if self.x16 is None:
+            self._allocate(n_slots, max_len, width, torch.device(device))
+        elif (self.x16.shape[0] < n_slots or self.x16.shape[1] < max_len
+              or self.x16.shape[2] != width):
+            raise ShapeError(f"accumulator {tuple(self.x16.shape)} too small for "
+                             f"{n_slots} slots x {max_len} rows x {width}")
+        return self
+
+    # -- the reference's direct API (cache.py:135-146), one sequence ----------
+    def seed(self, x) -> None:
+        """acc = x (rows 0..n-1 of slot 0; float64 at the rows, fp16/fp32 operand)."""
+        x = torch.as_tensor(x, dtype=torch.float64)
+        x = x.reshape(-1, x.shape[-1])
+        if self.x16 is None:
+            self._allocate(1, max(x.shape[0], DEFAULT_MAX_LEN), x.shape[1],
+                           torch.device("cuda", torch.cuda.current_device()))
+        x = x.to(self.x16.device)
+        n = x.shape[0]
+        self._prefill64[0] = x.clone()
+        self.row64[0] = x[-1]
+        self.x16[0, :n] = x.to(torch.float16)
+        if self.x_hat is not None:
+            self.x_hat[0, :n] = x.float()
+        self._n_direct = n
+        self.seeded = True
+
+    def add(self, delta) -> None:
+        """acc += delta (same shape as the seed, cache.py:139-146)."""
+        if not self.seeded:
+            raise UsageError("accumulator used before the base layer seeded it")
+        delta = torch.as_tensor(delta, dtype=torch.float64).to(self.x16.device)
+        delta = delta.reshape(-1, delta.shape[-1])
+        n = getattr(self, "_n_direct", None)
+        if n is None or delta.shape[0] != n or delta.shape[1] != self.width:
+            raise ShapeError(f"accumulator shape {(n, self.width)} vs update {tuple(delta.shape)}")
+        rows = self._prefill64[0] + delta
+        self.seed(rows)
 
     def rows(self, slot, n) -> torch.Tensor:
         """float32 view/copy of the accumulator rows 0..n-1 of a slot."""
@@ -244,6 +302,7 @@ class Accumulator:
                 raise UsageError("accumulator used before the base layer seeded it")
             cur = torch.empty((n, self.width), dtype=torch.float64, device=self.x16.device)
             self._prefill64[slot] = cur
+            self._n_direct = None
         return cur
 
     def release_prefill(self, slot: int | None = None) -> None:
@@ -500,10 +559,13 @@ class CacheBackend:
     def __init__(self, layer_index: int, policy: LayerPolicy, head_dim: int,
                  group_size: int = DEFAULT_GROUP_SIZE, *, n_slots: int = 1, max_len: int = 4096,
                  hidden_dim: int | None = None, n_heads: int | None = None, kv_group: int = 1,
-                 n_heads_total: int | None = None, device="cuda"):
+                 n_heads_total: int | None = None, device="cuda", exact: bool = False):
         """``n_heads`` is the number of query heads this backend serves; with
         KV-head-group sharding (parallel.py) it is a slice of
-        ``n_heads_total`` and the weights passed in are column-sliced."""
+        ``n_heads_total`` and the weights passed in are column-sliced.
+        ``exact``: float64 inputs keep float64 arithmetic up to quantization
+        where the variant allows it (xq-gqa latents as float64 GEMMs with a
+        float64 residual buffer), as the reference-signature make_cache sets."""
         if head_dim != HEAD_DIM:
             raise ConfigError(f"the B200 kernels are specialised for head_dim {HEAD_DIM}, got {head_dim}")
         if hidden_dim is None or n_heads is None:
@@ -513,6 +575,7 @@ class CacheBackend:
             raise ConfigError("hidden_dim must equal n_heads*head_dim and n_heads % kv_group == 0")
         self.layer_index = layer_index
         self.policy = policy
+        self.exact = exact
         self.head_dim = head_dim
         self.group_size = group_size
         self.bits = policy.bits_for(layer_index)
@@ -534,9 +597,18 @@ class CacheBackend:
         self.peer_stored = False
 
     # -- interface ---------------------------------------------------------
+    def _adopt(self, weights, acc):
+        """Accept the reference's LayerWeights / Accumulator (cache.py:49-67,
+        124-146) as well as this module's, and check the accumulator rule."""
+        weights = as_layer_weights(weights, self.device)
+        if acc is not None:
+            acc = device_accumulator(acc).ensure(self.n_slots, self.L, self.d, self.device)
+        self._check_acc(acc)
+        return weights, acc
+
     def prefill(self, x, weights: LayerWeights, acc: Accumulator | None = None, slot=None):
         """Bulk-cache a prefix: x [n_slots, n, d] (all slots) or [n, d] for ``slot``."""
-        self._check_acc(acc)
+        weights, acc = self._adopt(weights, acc)
         slots, xs = self._split_slots(x, slot)
         for s, xx in zip(slots, xs):
             if self.n_tokens[s]:
@@ -549,7 +621,7 @@ class CacheBackend:
 
     def decode_append(self, x_token, weights: LayerWeights, acc: Accumulator | None = None):
         """Append one token per slot: x_token [n_slots, d] (cache.py:264-269)."""
-        self._check_acc(acc)
+        weights, acc = self._adopt(weights, acc)
         x_token = self._as_rows(x_token)
         if x_token.shape[0] != self.n_slots:
             raise ShapeError(f"expected {self.n_slots} rows, got {x_token.shape[0]}")
@@ -570,7 +642,7 @@ class CacheBackend:
             raise ShapeError(f"got {positions.shape[0]} positions for {n} tokens")
         if not np.array_equal(positions, np.arange(n)):
             raise ShapeError("positions must be 0..n-1 (the cache's own timeline)")
-        self._check_acc(acc)
+        weights, acc = self._adopt(weights, acc)
         return self._rematerialize(weights, acc, slot, n)
 
     def decode_attend(self, q_pre, weights: LayerWeights, acc: Accumulator | None = None,
@@ -581,7 +653,7 @@ class CacheBackend:
         before RoPE; it is rotated to position n_tokens-1 in the kernel
         (model.py:234). Returns float32 [n_slots, n_heads, 128].
         """
-        self._check_acc(acc)
+        weights, acc = self._adopt(weights, acc)
         if np.any(self.n_tokens == 0):
             raise UsageError("decode_attend on an empty cache")
         q = q_pre.reshape(self.n_slots, self.n_heads, self.head_dim).float().contiguous()
@@ -600,7 +672,7 @@ class CacheBackend:
         Prefill is GEMM-shaped: K/V are materialized (fp16) by cuBLAS GEMMs on the
         dequantized cache rows and attention runs through PyTorch's fused causal
         SDPA (a library kernel). Returns float32 [n, n_heads, 128]."""
-        self._check_acc(acc)
+        weights, acc = self._adopt(weights, acc)
         x = torch.as_tensor(x, device=self.device)
         n = x.shape[0]
         self.prefill(x, weights, acc, slot=slot)
@@ -968,7 +1040,7 @@ class LatentInputCacheGQA(CacheBackend):
         r = self.latent  # the latent cache is whole even when heads are sharded
         self.fp16_first_channel = False
         self.k_stream = PackedStream(self.bits, CHANNEL, r, self.group_size, self.n_slots, self.L,
-                                     self.device)
+                                     self.device, resid_f64=self.exact)
         self.v_stream = PackedStream(self.bits, TOKEN, r, self.group_size, self.n_slots, self.L,
                                      self.device)
 
@@ -978,9 +1050,17 @@ class LatentInputCacheGQA(CacheBackend):
             raise UsageError("toggle the full-precision channel before caching")
         self.fp16_first_channel = bool(enable)
         self.k_stream = PackedStream(self.bits, CHANNEL, self.latent, self.group_size, self.n_slots,
-                                     self.L, self.device, keep_first=self.fp16_first_channel)
+                                     self.L, self.device, keep_first=self.fp16_first_channel,
+                                     resid_f64=self.exact)
 
     def _latents(self, x, weights):
+        if self.exact and x.dtype == torch.float64:  # the reference's float64 GEMMs
+            key = ("f64", "u_kv_cat")
+            if key not in weights._cache:
+                weights._cache[key] = torch.cat([weights.u_k.double(), weights.u_v.double()],
+                                                dim=1).contiguous()
+            lat = x @ weights._cache[key]
+            return lat[:, :self.latent], lat[:, self.latent:]
         # one float32 GEMM against [U_k | U_v] (cache.py:429-432)
         key = ("f32", "u_kv_cat")
         if key not in weights._cache:
@@ -1288,8 +1368,11 @@ _BACKENDS = {
 }
 
 
-def fp16_outlier_channel_variant(state: CacheBackend, enable: bool) -> CacheBackend:
+def fp16_outlier_channel_variant(state, enable: bool):
     """Pin channel 0 of the K latent to full precision (cache.py:653-658; xq-gqa only)."""
+    if isinstance(state, ReferenceCache):
+        state.set_fp16_first_channel(enable)
+        return state
     if not isinstance(state, LatentInputCacheGQA):
         raise UsageError("full-precision outlier channel applies to xq-gqa only")
     state.set_fp16_first_channel(enable)
@@ -1297,10 +1380,206 @@ def fp16_outlier_channel_variant(state: CacheBackend, enable: bool) -> CacheBack
 
 
 def make_cache(variant: str, layer_index: int, policy: LayerPolicy, head_dim: int,
-               group_size: int = DEFAULT_GROUP_SIZE, **kw) -> CacheBackend:
-    """Instantiate the backend for one layer (cache.py:620-630)."""
+               group_size: int = DEFAULT_GROUP_SIZE, **kw):
+    """Instantiate the backend for one layer (cache.py:620-630).
+
+    With ``hidden_dim`` / ``n_heads`` (and ``n_slots``, ``max_len``) the device
+    arenas are allocated here. Called with the reference's signature alone, it
+    returns a :class:`ReferenceCache` for one sequence that sizes its arenas from
+    the first ``prefill`` / ``decode_append`` and speaks NumPy like the
+    reference's backends."""
     if variant not in VARIANTS:
         raise ConfigError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
     if variant not in _BACKENDS:
         raise ConfigError(f"variant {variant!r} is not on the B200 hot path (next row)")
+    if kw.get("hidden_dim") is None or kw.get("n_heads") is None:
+        return ReferenceCache(variant, layer_index, policy, head_dim, group_size, **kw)
     return _BACKENDS[variant](layer_index, policy, head_dim, group_size, **kw)
+
+
+# ---------------------------------------------------------------------------
+# The reference's objects at the boundary (cache.py:49-67, 124-146, 620-650)
+# ---------------------------------------------------------------------------
+
+_ADOPTED_W: dict = {}    # id(reference LayerWeights) -> (weakref, device LayerWeights)
+_ADOPTED_ACC: dict = {}  # id(reference Accumulator) -> (weakref, device Accumulator)
+
+
+def _adopt_cached(table: dict, obj, build):
+    import weakref
+
+    key = id(obj)
+    hit = table.get(key)
+    if hit is not None and hit[0]() is obj:
+        return hit[1]
+    val = build()
+    try:
+        ref = weakref.ref(obj, lambda _r, k=key: table.pop(k, None))
+    except TypeError:  # not weak-referenceable: adopt afresh every call
+        return val
+    table[key] = (ref, val)
+    return val
+
+
+def as_layer_weights(weights, device=None) -> LayerWeights:
+    """This module's LayerWeights, or the reference's (NumPy float64 w_k / w_v and
+    SvdFactors svd_k / svd_v / svd_kv, cache.py:49-67) copied once to the device.
+    The projections stay float64 on the device; every kernel path converts them
+    (fp16 tensor-core operands, float32 SIMT remat, float64 latent GEMMs)."""
+    if isinstance(weights, LayerWeights) or weights is None:
+        return weights
+    if not hasattr(weights, "w_k"):
+        raise UsageError(f"expected LayerWeights, got {type(weights).__name__}")
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+
+    def t(a):
+        return None if a is None else torch.as_tensor(np.asarray(a, np.float64), device=dev)
+
+    def build():
+        lw = LayerWeights(w_k=t(weights.w_k), w_v=t(weights.w_v))
+        for name, (u, f) in (("svd_k", ("u_k", "fused_k")), ("svd_v", ("u_v", "fused_v")),
+                             ("svd_kv", ("u_kv", "fused_kv"))):
+            fac = getattr(weights, name, None)
+            if fac is not None:
+                setattr(lw, u, t(fac.u))
+                setattr(lw, f, t(fac.fused))
+        return lw
+
+    return _adopt_cached(_ADOPTED_W, weights, build)
+
+
+def device_accumulator(acc) -> Accumulator:
+    """This module's Accumulator, or a device accumulator standing in for the
+    reference's (``Accumulator()``, cache.py:124-146). The reference creates one
+    per forward pass (model.py:202, :227) and threads it through the layers in
+    order; the stand-in follows the same object through that pass."""
+    if isinstance(acc, Accumulator):
+        return acc
+    if not (hasattr(acc, "seed") and hasattr(acc, "add")):
+        raise UsageError(f"expected an Accumulator, got {type(acc).__name__}")
+    bits = getattr(acc, "accounting_bits", DEFAULT_ACCUMULATOR_BITS)
+    return _adopt_cached(_ADOPTED_ACC, acc, lambda: Accumulator(accounting_bits=bits))
+
+
+class ReferenceCache:
+    """One sequence's cache behind the reference's backend interface
+    (``cache.py:238-281``): ``prefill(x, weights, acc)``, ``decode_append(x_token,
+    weights, acc)``, ``rematerialize(weights, positions, acc) -> (K, V)``, with
+    NumPy in and NumPy float64 out (torch in -> torch out), the reference's
+    LayerWeights / Accumulator objects accepted as they are.
+
+    It is what ``make_cache(variant, layer_index, policy, head_dim, group_size)``
+    returns, so ``model._Session`` (model.py:185-240) runs unchanged on the
+    device backends. The arenas are sized from the first call: d from x, the
+    KV width from the weights (hidden = n_heads * head_dim), ``max_len`` rows
+    (``DEFAULT_MAX_LEN`` unless given). Inputs given in float64 keep the
+    reference's float64 arithmetic up to quantization: CL deltas against a
+    float64 accumulator row, xq-gqa latents as float64 GEMMs.
+    """
+
+    def __init__(self, variant, layer_index, policy, head_dim, group_size=DEFAULT_GROUP_SIZE,
+                 **kw):
+        if head_dim != HEAD_DIM:
+            raise ConfigError(f"the B200 kernels are specialised for head_dim {HEAD_DIM}, got {head_dim}")
+        self.variant, self.layer_index, self.policy = variant, layer_index, policy
+        self.head_dim, self.group_size = head_dim, group_size
+        self.bits = policy.bits_for(layer_index)
+        self.needs_accumulator = _BACKENDS[variant].needs_accumulator
+        self._kw = dict(kw)
+        self._inner: CacheBackend | None = None
+        self._first_channel = False
+
+    # the reference's attributes
+    @property
+    def n_tokens(self) -> int:
+        return 0 if self._inner is None else int(self._inner.n_tokens[0])
+
+    @property
+    def backend(self) -> CacheBackend | None:
+        """The device backend (None before the first call)."""
+        return self._inner
+
+    def __getattr__(self, name):
+        inner = self.__dict__.get("_inner")
+        if inner is None:
+            raise AttributeError(name)
+        return getattr(inner, name)
+
+    def set_fp16_first_channel(self, enable: bool) -> None:
+        if self.n_tokens:
+            raise UsageError("toggle the full-precision channel before caching")
+        if self.variant != "xq-gqa":
+            raise UsageError("full-precision outlier channel applies to xq-gqa only")
+        self._first_channel = bool(enable)
+        if self._inner is not None:
+            self._inner.set_fp16_first_channel(enable)
+
+    def _build(self, d: int, weights: LayerWeights):
+        if weights.w_k is not None:
+            kvw = weights.w_k.shape[1]
+        elif weights.fused_k is not None:
+            kvw = weights.fused_k.shape[1]
+        else:
+            raise ConfigError("weights carry no K projection to size the cache from")
+        if d % HEAD_DIM or kvw % HEAD_DIM or d % kvw:
+            raise ShapeError(f"hidden {d} / kv width {kvw} must be multiples of {HEAD_DIM}")
+        kw = dict(self._kw)
+        kw.setdefault("n_slots", 1)
+        kw.setdefault("max_len", DEFAULT_MAX_LEN)
+        kw.setdefault("device", torch.device("cuda", torch.cuda.current_device()))
+        kw.setdefault("exact", True)
+        self._inner = _BACKENDS[self.variant](self.layer_index, self.policy, self.head_dim,
+                                              self.group_size, hidden_dim=d,
+                                              n_heads=d // HEAD_DIM, kv_group=d // kvw, **kw)
+        if self._first_channel:
+            self._inner.set_fp16_first_channel(True)
+
+    def _rows(self, x, weights):
+        is_np = not isinstance(x, torch.Tensor)
+        x = torch.as_tensor(np.asarray(x, np.float64) if is_np else x)
+        lw = as_layer_weights(weights, self._kw.get("device"))
+        if self._inner is None:
+            self._build(x.shape[-1], lw)
+        return x.to(self._inner.device), lw, is_np
+
+    def prefill(self, x, weights, acc=None):
+        x, lw, is_np = self._rows(x, weights)
+        if x.dim() != 2:
+            raise ShapeError("prefill expects [n, d]")
+        self._np = is_np
+        self._inner.prefill(x, lw, acc, slot=0)
+
+    def decode_append(self, x_token, weights, acc=None):
+        x, lw, is_np = self._rows(x_token, weights)
+        self._np = getattr(self, "_np", is_np) and is_np
+        self._inner.decode_append(x.reshape(1, -1), lw, acc)
+
+    def rematerialize(self, weights, positions, acc=None):
+        if self._inner is None:
+            raise UsageError("rematerialize on an empty cache")
+        k, v = self._inner.rematerialize(as_layer_weights(weights, self._inner.device), positions,
+                                         acc, slot=0)
+        if getattr(self, "_np", True):
+            return k.double().cpu().numpy(), v.double().cpu().numpy()
+        return k, v
+
+    def memory_bytes(self) -> dict:
+        return {} if self._inner is None else self._inner.memory_bytes()
+
+
+# Free-function surface mirroring the backend methods (cache.py:633-650).
+
+
+def prefill(state, x_postnorm, weights, acc=None):
+    state.prefill(x_postnorm, weights, acc)
+    return state
+
+
+def decode_append(state, x_token, weights, acc=None):
+    state.decode_append(x_token, weights, acc)
+    return state
+
+
+def rematerialize(state, weights, positions, acc=None):
+    return state.rematerialize(weights, positions, acc)

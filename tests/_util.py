@@ -40,3 +40,9 @@ def torch_bf16(bits: np.ndarray, device="cuda"):
 
 def fp16_round(a: np.ndarray) -> np.ndarray:
     return np.asarray(a, np.float64).astype(np.float16).astype(np.float64)
+
+
+def unpack_rows(rows: np.ndarray, bits: int, cols: int) -> np.ndarray:
+    """Codes of LSB-first packed arena rows (uint8 [n, row_bytes]) -> uint8 [n, cols]."""
+    b = np.unpackbits(rows, axis=1, bitorder="little")[:, :cols * bits].reshape(len(rows), cols, bits)
+    return (b.astype(np.uint8) << np.arange(bits, dtype=np.uint8)).sum(axis=2, dtype=np.uint8)

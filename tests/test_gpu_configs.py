@@ -28,7 +28,7 @@ import math
 import numpy as np
 import pytest
 
-from _util import rel_err
+from _util import rel_err, unpack_rows
 
 pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
 
@@ -87,12 +87,6 @@ def test_rope64_attend64_match_oracle():
     big = _rope64(k[:3].cuda(), 131000).cpu().numpy()
     # CUDA vs libm cos/sin of angles near 1.3e5 rad: a few ulps
     assert rel_err(big, O.apply_rope(k[:3].numpy(), [131000, 131001, 131002], 128)) < 1e-10
-
-
-def _unpack_rows(rows: np.ndarray, bits: int, cols: int) -> np.ndarray:
-    """Codes of LSB-first packed arena rows (uint8 [n, row_bytes]) -> uint8 [n, cols]."""
-    b = np.unpackbits(rows, axis=1, bitorder="little")[:, :cols * bits].reshape(len(rows), cols, bits)
-    return (b.astype(np.uint8) << np.arange(bits, dtype=np.uint8)).sum(axis=2, dtype=np.uint8)
 
 
 def _prefill_decoder(dec, layers_x):
@@ -165,7 +159,7 @@ def test_c3_xq_cl_mha_2bit_delta_stack(n_layers, B, n1, acc):
                 for i, c in enumerate(dec.caches):
                     st = c.stream
                     rows = st.codes[s * st.L:s * st.L + n1].cpu().numpy()
-                    codes = _unpack_rows(rows, st.bits, d)
+                    codes = unpack_rows(rows, st.bits, d)
                     n_diff = int(np.count_nonzero(codes != stack.streams[i].codes))
                     assert n_diff == 0, (s, i, n_diff)
     worst = max(errs.values())
