@@ -124,6 +124,58 @@ int xq_quantize_rows_cl(const void* x, int32_t x_dtype, int64_t x_row_stride, in
                         uint8_t* codes, int64_t row_bytes, void* params, int32_t* nonfinite_flag,
                         void* stream);
 
+/* xq-gqa decode append (replaces LatentInputCacheGQA._decode, cache.py:429-432,
+ * with _Stream.push, cache.py:210-221): lat = x @ [U_k | U_v] on tcgen05 (bf16
+ * operands, fp32 accumulation) for n_rows tokens (row b = slot b, appended at
+ * position seq_lens[b]-1); the V latent (columns r..2r-1) is quantized per
+ * token into the arena (codes + fp16 (scale, zp), as xq_quantize_rows); the K
+ * latent (columns 0..r-1) goes to row seq_lens[b]-1-k_nflushed[b] of slot b's
+ * float32 residual buffer k_resid [n_rows][128][r]. x: bf16 [n_rows] rows of
+ * x_row_stride elements; u_bf16: [d][2r] row-major. lat_out (optional):
+ * float32 [n_rows][2r]. group_size must be 128, r a multiple of 128, d of 64. */
+int xq_latent_project_append(const void* x_bf16, int64_t x_row_stride, int32_t n_rows, int64_t d,
+                             const void* u_bf16, int32_t r, int32_t bits, int32_t group_size,
+                             const int32_t* seq_lens, const int32_t* k_nflushed, int64_t L_max,
+                             float* k_resid, uint8_t* v_codes, int64_t v_row_bytes, void* v_params,
+                             float* lat_out, int32_t* nonfinite_flag, void* stream);
+
+/* fp16 operand rows of the remat GEMM (quant.dequantize, quant.py:137-153, then
+ * the stream's residual rows, cache.py:223-230): out[i] for i < n_codes is arena
+ * row row0+i dequantized (codes * scale + zp, axis 0 per-token / 1 per-channel),
+ * for n_codes <= i < n_rows the float32 row resid[i - n_codes]; out row stride ldo. */
+int xq_dequant_rows_f16(const uint8_t* codes, int64_t row_bytes, const void* params, int32_t axis,
+                        int32_t bits, int32_t group_size, int64_t cols, int64_t row0,
+                        int64_t n_codes, const float* resid, int64_t n_rows, void* out,
+                        int64_t ldo, void* stream);
+
+/* Remat GEMM on tcgen05 for the bulk paths (prefill K/V rebuild,
+ * cache.py:271-281 over a whole prompt; XQuant-CL latent accumulator update
+ * acc (+)= reconstruct() @ U^T, cache.py:571-589): C[M x N] (+)= A[M x K] .
+ * B[N x K]^T, fp16 row-major operands (lda / ldb / ldc in elements), fp32
+ * accumulation. epilogue 0: C = fp16(acc); 1: C = fp16(RoPE(acc)), row i at
+ * position pos0+i (rope_cs = the [rope_n][64] (cos, sin) table); 2: C += acc.
+ * K must be a multiple of 64. */
+int xq_gemm_f16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                int64_t M, int64_t N, int64_t K, int32_t epilogue, const void* rope_cs,
+                int64_t rope_n, int64_t pos0, void* stream);
+
+/* Causal grouped-query attention of a prefill (model._attention over the
+ * prompt, model.py:150-182, as _Session.prefill calls it, model.py:205-221):
+ * q [n][q_stride] (rotated, head h at columns 128h..), k / v [n][kv_stride]
+ * (k rotated; KV head h / group), fp16 or bf16 (dtype); out float32
+ * [n][out_stride], head h at 128h. Flash-attention (online softmax), K/V read
+ * tile by tile. */
+int xq_prefill_attend(const void* q, const void* k, const void* v, int32_t dtype, int32_t n,
+                      int32_t n_heads, int32_t group, int64_t q_stride, int64_t kv_stride,
+                      float sm_scale, float* out, int64_t out_stride, void* stream);
+
+/* RoPE (linalg.apply_rope, linalg.py:58-95) of n rows of width (whole 128-wide
+ * heads) at positions pos0.. : in float32 / fp16, out fp16 / bf16 (may alias in
+ * when the types match). */
+int xq_rope_rows(const void* in, int32_t in_dtype, int64_t in_stride, int64_t n, int64_t width,
+                 const void* rope_cs, int64_t rope_n, int64_t pos0, void* out, int32_t out_dtype,
+                 int64_t out_stride, void* stream);
+
 /* Per-channel quantization of whole token groups (quant.py:124-134): block b
  * is float32 [group_size, cols] at blocks + b*group_size*cols; its codes go to
  * arena rows dst_row0[b] .. +group_size-1 and its params to param row

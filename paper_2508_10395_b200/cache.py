@@ -148,6 +148,27 @@ class LayerWeights:
         return self._cache[key]
 
 
+_T16: dict = {}
+
+
+def _t16(w: torch.Tensor) -> torch.Tensor:
+    """fp16 W^T (K-major [N, K] rows) of a [K, N] projection, the remat GEMM's B
+    operand; built once per weight tensor (keyed by storage, dropped with it)."""
+    import weakref
+
+    key = (w.data_ptr(), tuple(w.shape), w.dtype)
+    hit = _T16.get(key)
+    if hit is not None and hit[0]() is not None:
+        return hit[1]
+    t = w.t().to(torch.float16).contiguous()
+    try:
+        ref = weakref.ref(w, lambda _r, k=key: _T16.pop(k, None))
+    except TypeError:
+        return t
+    _T16[key] = (ref, t)
+    return t
+
+
 def _dtype_code(t: torch.Tensor) -> int:
     return {torch.float32: N.F32, torch.bfloat16: N.BF16, torch.float16: N.F16,
             torch.float64: N.F64}[t.dtype]
@@ -466,6 +487,11 @@ class PackedStream:
         self.resid[rows, buf_pos] = lat.float()
         if self.resid64 is not None:
             self.resid64[rows, buf_pos] = lat.double()
+        self.flush_full(n_tokens)
+
+    def flush_full(self, n_tokens: np.ndarray):
+        """Quantize the residual buffers that hold a whole group (cache.py:218-221)."""
+        dev = self.resid.device
         full = np.nonzero(n_tokens - self.n_flushed >= self.g)[0]
         if len(full):
             src = self.resid64 if self.resid64 is not None else self.resid
@@ -669,23 +695,26 @@ class CacheBackend:
         (``rematerialize``, cache.py:271-281), rotate q_pre [n, n_heads*128] to
         positions 0..n-1 and attend causally (model.py:150-182).
 
-        Prefill is GEMM-shaped: K/V are materialized (fp16) by cuBLAS GEMMs on the
-        dequantized cache rows and attention runs through PyTorch's fused causal
-        SDPA (a library kernel). Returns float32 [n, n_heads, 128]."""
+        Prefill is GEMM-shaped: K/V of all n positions are materialized in fp16 by
+        the tcgen05 remat GEMM (xq_gemm_f16, RoPE fused into the K epilogue) from
+        fp16 rows of the cache, and a flash-attention kernel (xq_prefill_attend)
+        attends causally. Returns float32 [n, n_heads, 128]."""
         weights, acc = self._adopt(weights, acc)
         x = torch.as_tensor(x, device=self.device)
         n = x.shape[0]
         self.prefill(x, weights, acc, slot=slot)
-        k, v = self._prefill_kv(weights, acc, slot, n)  # fp16, K rotated, [n, kvw]
-        q = q_pre.reshape(n, self.n_heads, self.head_dim).float()
-        q = _rope_rows(q.reshape(n, -1), 0, self.device).view(n, self.n_heads, self.head_dim)
-        qh = q.permute(1, 0, 2)[None].to(torch.float16)
-        kh = k.view(n, self.n_kv, self.head_dim).permute(1, 0, 2)[None]
-        vh = v.view(n, self.n_kv, self.head_dim).permute(1, 0, 2)[None]
-        ctx = torch.nn.functional.scaled_dot_product_attention(
-            qh, kh, vh, is_causal=True, scale=1.0 / math.sqrt(self.head_dim),
-            enable_gqa=self.g > 1)
-        return ctx[0].permute(1, 0, 2).float().contiguous()
+        k, v = self._prefill_kv(weights, acc, slot, n)  # fp16 (bf16 baseline), K rotated, [n, kvw]
+        qf = q_pre.reshape(n, self.n_heads * self.head_dim).float().contiguous()
+        q = torch.empty((n, self.n_heads * self.head_dim), dtype=k.dtype, device=self.device)
+        rope = rope_table(n, self.device)
+        dt = _dtype_code(k)
+        N.call("xq_rope_rows", N.ptr(qf), N.F32, qf.stride(0), n, qf.shape[1], N.ptr(rope),
+               rope.shape[0], 0, N.ptr(q), dt, q.stride(0), N.stream_of(self.device))
+        out = torch.empty((n, self.n_heads, self.head_dim), dtype=torch.float32, device=self.device)
+        N.call("xq_prefill_attend", N.ptr(q), N.ptr(k), N.ptr(v), dt, n, self.n_heads, self.g,
+               q.stride(0), k.stride(0), 1.0 / math.sqrt(self.head_dim), N.ptr(out),
+               self.n_heads * self.head_dim, N.stream_of(self.device))
+        return out
 
     def _prefill_kv(self, weights, acc, slot, n):  # pragma: no cover
         raise NotImplementedError
@@ -698,11 +727,32 @@ class CacheBackend:
                N.stream_of(self.device))
         return out
 
+    def _rows16(self, stream, slot, n):
+        """fp16 [n, width] operand rows of one slot: dequantized codes, then (buffered
+        streams) the residual rows (cache.py:223-230)."""
+        out = torch.empty((n, stream.width), dtype=torch.float16, device=self.device)
+        buffered = getattr(stream, "n_flushed", None) is not None
+        nfl = min(int(stream.n_flushed[slot]), n) if buffered else n
+        resid = stream.resid[slot] if nfl < n else None
+        N.call("xq_dequant_rows_f16", N.ptr(stream.codes), stream.row_bytes, N.ptr(stream.params),
+               stream.axis, stream.bits, stream.g, stream.width, slot * self.L, nfl, N.ptr(resid),
+               n, N.ptr(out), out.stride(0), N.stream_of(self.device))
+        if stream.axis == CHANNEL and stream.first is not None and nfl:
+            out[:nfl, 0] = stream.first[slot * self.L:slot * self.L + nfl].half()
+        return out
+
+    def _gemm(self, a, w_t, epi, n):
+        """fp16 [n, N] = a [n, K] @ w_t[N, K]^T on tcgen05; epi 1 rotates the rows."""
+        out = torch.empty((n, w_t.shape[0]), dtype=torch.float16, device=self.device)
+        rope = rope_table(n, self.device) if epi == 1 else None
+        N.call("xq_gemm_f16", N.ptr(a), a.stride(0), N.ptr(w_t), w_t.stride(0), N.ptr(out),
+               out.stride(0), n, w_t.shape[0], a.shape[1], epi, N.ptr(rope),
+               rope.shape[0] if rope is not None else 0, 0, N.stream_of(self.device))
+        return out
+
     def _kv_from(self, a_k, a_v, wk, wv, n):
-        """K (rotated to 0..n-1) and V in fp16 from A operands and weights (cuBLAS)."""
-        k = a_k.to(torch.float16) @ wk.to(torch.float16)
-        v = a_v.to(torch.float16) @ wv.to(torch.float16)
-        return _rope_rows(k.float(), 0, self.device).to(torch.float16), v
+        """K (rotated to 0..n-1) and V in fp16 from fp16 operand rows and [K, N] weights."""
+        return self._gemm(a_k, _t16(wk), 1, n), self._gemm(a_v, _t16(wv), 0, n)
 
     # -- helpers -------------------------------------------------------------
     def _sync_lens(self):
@@ -872,8 +922,8 @@ class FullPrecisionCache(CacheBackend):
         return self.k[base:base + n].float(), self.v[base:base + n].float()
 
     def _prefill_kv(self, weights, acc, slot, n):
-        base = slot * self.L
-        return self.k[base:base + n].to(torch.float16), self.v[base:base + n].to(torch.float16)
+        base = slot * self.L  # the stored bf16 rows themselves (K already rotated)
+        return self.k[base:base + n], self.v[base:base + n]
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         chunk = tpc * 128 if tpc else kv_chunk_tokens(self.n_slots, max_len, self.n_kv,
@@ -948,8 +998,11 @@ class QuantizedKvCache(CacheBackend):
         return _rope_rows(k, 0, self.device), v
 
     def _prefill_kv(self, weights, acc, slot, n):
-        k, v = self._rematerialize(weights, acc, slot, n)
-        return k.to(torch.float16), v.to(torch.float16)
+        k = self._rows16(self.k_stream, slot, n)  # pre-RoPE K (cache.py:356-360)
+        rope = rope_table(n, self.device)
+        N.call("xq_rope_rows", N.ptr(k), N.F16, k.stride(0), n, k.shape[1], N.ptr(rope),
+               rope.shape[0], 0, N.ptr(k), N.F16, k.stride(0), N.stream_of(self.device))
+        return k, self._rows16(self.v_stream, slot, n)
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         ks, vs = self.k_stream, self.v_stream
@@ -1007,7 +1060,7 @@ class InputCacheMHA(CacheBackend):
 
     def _prefill_kv(self, weights, acc, slot, n):
         a = (self.x16[slot * self.L:slot * self.L + n] if self.passthrough
-             else self._dequant_rows(self.stream, slot, n))
+             else self._rows16(self.stream, slot, n))
         return self._kv_from(a, a, weights.w_k, weights.w_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
@@ -1075,13 +1128,34 @@ class LatentInputCacheGQA(CacheBackend):
         self.k_stream.channel_bulk(slot, lat_k)  # cache.py:203-208
 
     def _decode(self, x, weights, acc, lens):
-        lat_k, lat_v = self._latents(x, weights)
-        self.v_stream.append_token_rows(lat_v.contiguous(), lens)
-        self.k_stream.channel_push(lat_k, self.n_tokens)  # cache.py:218-221
+        if self.exact and x.dtype == torch.float64:  # the reference's float64 latents
+            lat_k, lat_v = self._latents(x, weights)
+            self.v_stream.append_token_rows(lat_v.contiguous(), lens)
+            self.k_stream.channel_push(lat_k, self.n_tokens)  # cache.py:218-221
+            return
+        # one tcgen05 launch: x @ [U_k | U_v] (bf16 operands, fp32 accumulation), the V
+        # latent quantized into its arena, the K latent into the residual buffer
+        xb = x if x.dtype == torch.bfloat16 else x.to(torch.bfloat16)
+        xb = xb.contiguous()
+        ks, vs = self.k_stream, self.v_stream
+        N.call("xq_latent_project_append", N.ptr(xb), xb.stride(0), xb.shape[0], self.d,
+               N.ptr(self._u_cat_bf16(weights)), self.latent, self.bits, self.group_size,
+               N.ptr(lens), N.ptr(ks.nflushed_dev), self.L, N.ptr(ks.resid), N.ptr(vs.codes),
+               vs.row_bytes, N.ptr(vs.params), None, N.ptr(vs.flag), N.stream_of(self.device))
+        ks.flush_full(self.n_tokens)
+
+    @staticmethod
+    def _u_cat_bf16(weights):
+        """[U_k | U_v] in bf16, the tcgen05 operand of the latent projection."""
+        key = ("bf16", "u_kv_cat")
+        if key not in weights._cache:
+            weights._cache[key] = torch.cat([weights.u_k, weights.u_v], dim=1).to(
+                torch.bfloat16).contiguous()
+        return weights._cache[key]
 
     def _prefill_kv(self, weights, acc, slot, n):
-        lat_k = self.k_stream.channel_reconstruct(slot, n)
-        lat_v = self._dequant_rows(self.v_stream, slot, n)
+        lat_k = self._rows16(self.k_stream, slot, n)
+        lat_v = self._rows16(self.v_stream, slot, n)
         return self._kv_from(lat_k, lat_v, weights.fused_k, weights.fused_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
@@ -1175,7 +1249,7 @@ class DeltaInputCacheMHA(CacheBackend):
         self._accumulate(acc, self.is_base, max_len, lens)
 
     def _prefill_kv(self, weights, acc, slot, n):
-        a = self._dequant_rows(self.stream, slot, n) if self.is_base else acc.rows(slot, n)
+        a = self._rows16(self.stream, slot, n) if self.is_base else acc.x16[slot, :n]
         return self._kv_from(a, a, weights.w_k, weights.w_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
@@ -1323,10 +1397,10 @@ class DeltaLatentCacheGQA(CacheBackend):
     def _prefill_kv(self, weights, acc, slot, n):
         _, fused = self._sub(weights)
         if self.is_base:
-            a = self.stream.channel_reconstruct(slot, n)
+            a = self._rows16(self.stream, slot, n)
             return self._kv_from(a, a, fused[:, :self.kv_width], fused[:, self.kv_width:], n)
         wk, wv = self._w_delta(weights)
-        a = acc.x_hat[slot, :n]
+        a = acc.x16[slot, :n]
         return self._kv_from(a, a, wk, wv, n)
 
     def _rematerialize(self, weights, acc, slot, n):

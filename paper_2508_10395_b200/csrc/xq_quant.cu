@@ -287,6 +287,28 @@ __global__ void k_dequant_rows(const uint8_t* __restrict__ codes, int64_t row_by
   }
 }
 
+// fp16 operand rows for the remat GEMM: arena rows row0.. (codes) then, from
+// row n_codes on, the float32 residual rows (per-channel streams, cache.py:223-230)
+__global__ void k_dequant_rows_f16(const uint8_t* __restrict__ codes, int64_t row_bytes,
+                                   const void* __restrict__ params, int axis, int bits, int G,
+                                   int64_t cols, int64_t row0, int64_t n_codes,
+                                   const float* __restrict__ resid, int64_t n_rows,
+                                   __half* __restrict__ out, int64_t ldo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows * cols;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    float v;
+    if (r < n_codes) {
+      const uint32_t code = read_code(codes + (row0 + r) * row_bytes, c, bits);
+      const float2 p = load_params(params, axis, bits, G, cols, row0 + r, c);
+      v = fmaf(static_cast<float>(code), p.x, p.y);
+    } else {
+      v = resid[(r - n_codes) * cols + c];
+    }
+    out[r * ldo + c] = __float2half_rn(v);
+  }
+}
+
 __global__ void k_rope_table(float2* __restrict__ cs, int64_t n_pos, int hd, double theta,
                              int j_major) {
   const int half = hd / 2;
@@ -681,6 +703,22 @@ int xq_dequant_rows(const uint8_t* codes, int64_t row_bytes, const void* params,
   k_dequant_rows<<<grid_for(n_rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
       codes, row_bytes, params, axis, bits, group_size, cols, row0, n_rows, out);
   return check_launch("xq_dequant_rows");
+}
+
+int xq_dequant_rows_f16(const uint8_t* codes, int64_t row_bytes, const void* params, int32_t axis,
+                        int32_t bits, int32_t group_size, int64_t cols, int64_t row0,
+                        int64_t n_codes, const float* resid, int64_t n_rows, void* out,
+                        int64_t ldo, void* stream) {
+  XQ_REQUIRE(bits >= 1 && bits <= 8, XQ_ECONFIG, "bad bits");
+  XQ_REQUIRE(axis == 0 || axis == 1, XQ_ECONFIG, "axis must be 0 or 1");
+  XQ_REQUIRE(n_codes <= n_rows && (n_codes == n_rows || resid != nullptr), XQ_EUSAGE,
+             "rows past n_codes need the residual buffer");
+  XQ_REQUIRE(ldo >= cols, XQ_ESHAPE, "ldo < cols");
+  if (n_rows * cols == 0) return XQ_OK;
+  k_dequant_rows_f16<<<grid_for(n_rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
+      codes, row_bytes, params, axis, bits, group_size, cols, row0, n_codes, resid, n_rows,
+      static_cast<__half*>(out), ldo);
+  return check_launch("xq_dequant_rows_f16");
 }
 
 int xq_rope_table(void* cs_out, int64_t n_pos, int32_t head_dim, double theta, int32_t j_major,

@@ -26,7 +26,8 @@ def _q_rot(q, n):
     return O.apply_rope(q, np.arange(n), 128)
 
 
-@pytest.mark.parametrize("variant,bits", [("xq-mha", 3), ("xq-mha", 4), ("fp16", 16)])
+@pytest.mark.parametrize("variant,bits", [("xq-mha", 3), ("xq-mha", 4), ("fp16", 16), ("kvq", 4),
+                                          ("xq-mha", 16)])
 def test_prefill_mha_against_oracle(variant, bits):
     import torch
 
@@ -45,9 +46,13 @@ def test_prefill_mha_against_oracle(variant, bits):
         q = torch.randn(n, d, generator=g)
         ctx = st.prefill_attend(x.cuda(), q.cuda(), w, slot=slot).cpu().numpy().reshape(n, -1)
         xs = x.double().numpy()
-        if variant == "fp16":
+        if variant == "fp16" or bits == 16:
             ref_st = O.Fp16Cache(128)
             ref_st.append(xs, wk, wv)
+            k, v = ref_st.remat()
+        elif variant == "kvq":
+            ref_st = O.KvqCache(bits, 128, 128)
+            ref_st.prefill(xs @ wk, xs @ wv)
             k, v = ref_st.remat()
         else:
             ref_st = O.XqMhaCache(bits, 128, 128)
