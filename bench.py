@@ -56,6 +56,9 @@ CONFIGS = {
     "c4": dict(workload="xq-gqa 3-bit latent, Llama-3.1-8B shape, batch 32, 16K context",
                shape="llama3.1-8b", variant="xq-gqa", bits=3, batch=32, ctx=16384,
                parallel="heads"),
+    # XQuant-CL on the GQA shape (shared K|V latent subspace)
+    "c6": dict(workload="xq-cl-gqa 3-bit, Llama-3.1-8B shape, batch 8, 16K context",
+               shape="llama3.1-8b", variant="xq-cl-gqa", bits=3, batch=8, ctx=16384),
     "c1": dict(workload="XQuant 4-bit, one Llama-2-7B layer, batch 1, 2K context",
                shape="llama2-7b", variant="xq-mha", bits=4, batch=1, ctx=2048, layers=1),
     # C5 long-context sweep (8K-128K, batch 1-64 over 8 GPUs): one point per run, the
@@ -224,15 +227,18 @@ class CpuReferenceStep:
             kw = {}
             if self.variant == "xq-gqa":
                 kw = self._svd(SvdFactors)
+            if self.variant == "xq-cl-gqa":
+                u, sg, vt = np.linalg.svd(np.hstack([self.w_k, self.w_v]), full_matrices=False)
+                kw = {"svd_kv": SvdFactors(u=u, sigma=sg, b_t=vt)}
             self.lw = LayerWeights(gamma_attn=None, gamma_mlp=None, w_q=z, w_k=self.w_k,
                                    w_v=self.w_v, w_o=z, w_up=z, w_down=z, **kw)
             # a delta layer is the CL steady state; the accumulator is seeded
             # from a synthetic base reconstruction (cache.py:463-467)
             variant = "xq-mha" if self.variant == "xq-mha" else self.variant
             pol = LayerPolicy([self.bits] * 2, base_layers=1, high_precision_prefix=1)
-            self.cache = make_cache(variant, 1 if variant in ("xq-cl-mha",) else 0, pol, 128)
+            self.cache = make_cache(variant, 1 if variant in ("xq-cl-mha", "xq-cl-gqa") else 0, pol, 128)
             self.acc = None
-            if variant == "xq-cl-mha":
+            if variant in ("xq-cl-mha", "xq-cl-gqa"):
                 from xcache.cache import Accumulator
 
                 self.acc = Accumulator()

@@ -139,6 +139,33 @@ int xq_latent_project_append(const void* x_bf16, int64_t x_row_stride, int32_t n
                              float* k_resid, uint8_t* v_codes, int64_t v_row_bytes, void* v_params,
                              float* lat_out, int32_t* nonfinite_flag, void* stream);
 
+/* The same quantizer writing the reference's float64 reconstruction
+ * (codes * scale + zp, fallback.py:134-146) of every block row to recon_out
+ * (may alias blocks). xq-cl-gqa keeps its accumulator at the new token in
+ * float64 through it. */
+int xq_quantize_blocks_per_channel_f64_recon(const double* blocks, int64_t n_blocks, int64_t cols,
+                                             int32_t bits, int32_t group_size,
+                                             const int64_t* dst_row0, uint8_t* codes,
+                                             int64_t row_bytes, void* params, double* recon_out,
+                                             int32_t* nonfinite_flag, void* stream);
+
+/* xq-cl-gqa new-token latent (DeltaLatentCacheGQA._push_base / _push_delta,
+ * cache.py:562-586): lat[b] = (x[b] - acc_row[b]) @ U in float64 (acc_row NULL
+ * for a base layer), U [d][r] float32 or float64; written to row
+ * seq_lens[b]-1-nflushed[b] of slot b's residual buffers resid64 (float64) and
+ * resid32 (its float32 mirror), each [n_rows][group_size][r]. */
+int xq_clgqa_latent64(const void* x, int32_t x_dtype, int64_t x_row_stride, int32_t n_rows,
+                      int64_t d, const double* acc_row, const void* u, int32_t u_dtype, int64_t r,
+                      const int32_t* seq_lens, const int32_t* nflushed, int32_t group_size,
+                      double* resid64, float* resid32, int32_t* nonfinite_flag, void* stream);
+
+/* xq-cl-gqa accumulator at the new token (Accumulator.seed / add of
+ * reconstruct() @ U^T, cache.py:571-572, 588-589): acc_row[b] = (seed) or +=
+ * resid64[b][rec_pos[b]] @ U^T in float64; acc_row [n_rows][d]. */
+int xq_clgqa_row_update(const double* resid64, const int32_t* rec_pos, int32_t n_rows,
+                        int32_t group_size, const void* u, int32_t u_dtype, int64_t d, int64_t r,
+                        int32_t seed, double* acc_row, void* stream);
+
 /* fp16 operand rows of the remat GEMM (quant.dequantize, quant.py:137-153, then
  * the stream's residual rows, cache.py:223-230): out[i] for i < n_codes is arena
  * row row0+i dequantized (codes * scale + zp, axis 0 per-token / 1 per-channel),

@@ -42,6 +42,11 @@ _SIGS = {
     "xq_gemm_f16": [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I32, _P, _I64, _I64, _P],
     "xq_prefill_attend": [_P, _P, _P, _I32, _I32, _I32, _I32, _I64, _I64, _F, _P, _I64, _P],
     "xq_rope_rows": [_P, _I32, _I64, _I64, _I64, _P, _I64, _I64, _P, _I32, _I64, _P],
+    "xq_quantize_blocks_per_channel_f64_recon": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _P,
+                                                 _P, _P, _P],
+    "xq_clgqa_latent64": [_P, _I32, _I64, _I32, _I64, _P, _P, _I32, _I64, _P, _P, _I32, _P, _P,
+                          _P, _P],
+    "xq_clgqa_row_update": [_P, _P, _I32, _I32, _P, _I32, _I64, _I64, _I32, _P, _P],
     "xq_quantize_blocks_per_channel": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P],
     "xq_quantize_blocks_per_channel_f64": [_P, _I64, _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P],
     "xq_dequant_rows": [_P, _I64, _P, _I32, _I32, _I32, _I64, _I64, _I64, _P, _P],

@@ -1301,7 +1301,13 @@ class DeltaLatentCacheGQA(CacheBackend):
     delta kv = (acc @ U) @ fused, run here as acc @ (U @ fused) -- the same
     product reassociated, so the fused kernel reads the fp16 accumulator rows
     like xq-cl-mha with W' = U @ fused_{k|v} (d x kv_width) precomputed once.
-    The accumulator update is a plain [l x r] @ [r x d] GEMM (cuBLAS).
+
+    Decode, per layer: the new token's latent in float64 against the float64
+    accumulator row (``xq_clgqa_latent64``), the per-channel flush of a full
+    group with its float64 reconstruction written back (so the accumulator row
+    follows the reference's reconstruct() exactly), the row update
+    acc_row (+)= rec @ U^T (``xq_clgqa_row_update``), and the fp16 remat operand
+    of every cached row, acc16 (+)= rec16 @ U^T, on the tcgen05 remat GEMM.
     """
 
     variant = "xq-cl-gqa"
@@ -1322,6 +1328,7 @@ class DeltaLatentCacheGQA(CacheBackend):
         # code flip is a full quantization step, large against later deltas)
         self.stream = PackedStream(self.bits, CHANNEL, self.rank, self.group_size, self.n_slots,
                                    self.L, self.device, resid_f64=True)
+        self.rec_pos = torch.zeros(self.n_slots, dtype=torch.int32, device=self.device)
 
     @property
     def is_base(self):
@@ -1332,6 +1339,20 @@ class DeltaLatentCacheGQA(CacheBackend):
         return self.layer_index == self.policy.base_layers - 1
 
     @staticmethod
+    def _sub(weights):
+        if weights.u_kv is None or weights.fused_kv is None:
+            raise ConfigError("xq-cl-gqa needs the shared K/V subspace (u_kv, fused_kv)")
+        return weights.f32("u_kv"), weights.f32("fused_kv")
+
+    @staticmethod
+    def _u(weights):
+        """U as stored (float32 or float64), the float64 GEMVs' operand."""
+        u = weights.u_kv
+        if u.dtype not in (torch.float32, torch.float64):
+            u = weights.f32("u_kv")
+        return u.contiguous(), _dtype_code(u)
+
+    @staticmethod
     def _u64(weights):
         key = ("f64", "u_kv")
         if key not in weights._cache:
@@ -1339,52 +1360,101 @@ class DeltaLatentCacheGQA(CacheBackend):
         return weights._cache[key]
 
     @staticmethod
-    def _sub(weights):
-        if weights.u_kv is None or weights.fused_kv is None:
-            raise ConfigError("xq-cl-gqa needs the shared K/V subspace (u_kv, fused_kv)")
-        return weights.f32("u_kv"), weights.f32("fused_kv")
+    def _u16(weights):
+        """fp16 U [d, r]: the remat GEMM's B operand for acc (+)= rec @ U^T (N=d, K=r)."""
+        key = ("f16", "u_kv")
+        if key not in weights._cache:
+            weights._cache[key] = weights.u_kv.to(torch.float16).contiguous()
+        return weights._cache[key]
 
-    def _update_acc(self, acc, weights, slots, seed):
-        u, _ = self._sub(weights)
+    def _acc16(self, acc, weights, slots, seed):
+        """acc16[s, :n] (+)= rec16 @ U^T for every slot (cache.py:571-572, 588-589)."""
+        u16 = self._u16(weights)
         for s in slots:
-            n = int(self.n_tokens[s]) if self.n_tokens[s] else 0
+            n = int(self.n_tokens[s])
             if n == 0:
                 continue
-            rec = self.stream.channel_reconstruct(s, n)
-            rows = acc.x_hat[s, :n]
-            if seed:
-                torch.matmul(rec, u.t(), out=rows)  # cache.py:571-572
-            else:
-                rows.addmm_(rec, u.t())  # cache.py:588-589
-            acc.x16[s, :n] = rows.to(torch.float16)
+            rec = self._rows16(self.stream, s, n)
+            c = acc.x16[s]
+            N.call("xq_gemm_f16", N.ptr(rec), rec.stride(0), N.ptr(u16), u16.stride(0), N.ptr(c),
+                   c.stride(0), n, self.d, self.rank, 0 if seed else 2, None, 0, 0,
+                   N.stream_of(self.device))
         acc.seeded = True
+
+    def _flush(self, n_tokens):
+        """Flush full residual groups with the float64 reconstruction written back
+        over their rows (the new token's reconstruction stays at its row)."""
+        st = self.stream
+        full = np.nonzero(n_tokens - st.n_flushed >= st.g)[0]
+        if not len(full):
+            return
+        dst = torch.tensor([int(s) * st.L + int(st.n_flushed[s]) for s in full], dtype=torch.int64,
+                           device=self.device)
+        blocks = st.resid64 if len(full) == st.n_slots else st.resid64[torch.as_tensor(full, device=self.device)].contiguous()
+        N.call("xq_quantize_blocks_per_channel_f64_recon", N.ptr(blocks), len(full), st.width,
+               st.bits, st.g, N.ptr(dst), N.ptr(st.codes), st.row_bytes, N.ptr(st.params),
+               N.ptr(blocks), N.ptr(st.flag), N.stream_of(self.device))
+        if blocks is not st.resid64:
+            st.resid64[torch.as_tensor(full, device=self.device)] = blocks
+        st.n_flushed[full] += st.g
+        st.nflushed_dev.copy_(torch.from_numpy(st.n_flushed.astype(np.int32)))
 
     def _prefill(self, slot, x, weights, acc):
         self._sub(weights)
         n = x.shape[0]
+        st = self.stream
         xf = x.double()
         if not self.is_base:
             if not acc.seeded:
                 raise UsageError("accumulator used before the base layer seeded it")
-            xf = xf - acc.x_hat[slot, :n].double()  # cache.py:574-577 (delta = x - acc)
-        self.stream.channel_bulk(slot, xf @ self._u64(weights))
+            xf = xf - acc.prefill_rows(slot, n, seed=False)  # cache.py:574-577 (delta = x - acc)
+        u64 = self._u64(weights)
+        lat = (xf @ u64).contiguous()
+        g = st.g
+        n_full = n // g * g
+        if n_full:  # whole groups: codes + their float64 reconstruction in place of lat
+            dst = torch.tensor([slot * st.L + i for i in range(0, n_full, g)], dtype=torch.int64,
+                               device=self.device)
+            N.call("xq_quantize_blocks_per_channel_f64_recon", N.ptr(lat), n_full // g, st.width,
+                   st.bits, g, N.ptr(dst), N.ptr(st.codes), st.row_bytes, N.ptr(st.params),
+                   N.ptr(lat), N.ptr(st.flag), N.stream_of(self.device))
+        st.resid64[slot, :n - n_full] = lat[n_full:]
+        st.resid[slot, :n - n_full] = lat[n_full:].float()
+        st.n_flushed[slot] = n_full
+        st.nflushed_dev[slot] = n_full
         self.n_tokens[slot] = n  # the accumulator update reads the new length
         if self.is_base and not self.seeds_accumulator:
             return
-        self._update_acc(acc, weights, [slot], seed=self.is_base)
+        rows = acc.prefill_rows(slot, n, seed=self.is_base)
+        upd = lat @ u64.t()  # float64 reconstruction @ U^T (prefill only)
+        if self.is_base:
+            rows.copy_(upd)
+        else:
+            rows += upd
+        self._acc16(acc, weights, [slot], seed=self.is_base)
 
     def _decode(self, x, weights, acc, lens):
         self._sub(weights)
-        xf = x.double()
-        if not self.is_base:
-            if not acc.seeded:
-                raise UsageError("accumulator used before the base layer seeded it")
-            pos = torch.as_tensor(self.n_tokens - 1, device=self.device)
-            xf = xf - acc.x_hat[torch.arange(self.n_slots, device=self.device), pos].double()
-        self.stream.channel_push(xf @ self._u64(weights), self.n_tokens)
+        st = self.stream
+        if not self.is_base and not acc.seeded:
+            raise UsageError("accumulator used before the base layer seeded it")
+        if self.is_base:
+            acc.release_prefill()
+        u, udt = self._u(weights)
+        x = x.contiguous()
+        pos = (self.n_tokens - 1 - st.n_flushed).astype(np.int32)  # before this step's flush
+        N.call("xq_clgqa_latent64", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.d,
+               None if self.is_base else N.ptr(acc.row64), N.ptr(u), udt, self.rank, N.ptr(lens),
+               N.ptr(st.nflushed_dev), st.g, N.ptr(st.resid64), N.ptr(st.resid), N.ptr(st.flag),
+               N.stream_of(self.device))
+        self._flush(self.n_tokens)
         if self.is_base and not self.seeds_accumulator:
             return
-        self._update_acc(acc, weights, range(self.n_slots), seed=self.is_base)
+        self.rec_pos.copy_(torch.from_numpy(pos))
+        N.call("xq_clgqa_row_update", N.ptr(st.resid64), N.ptr(self.rec_pos), self.n_slots, st.g,
+               N.ptr(u), udt, self.d, self.rank, 1 if self.is_base else 0, N.ptr(acc.row64),
+               N.stream_of(self.device))
+        self._acc16(acc, weights, range(self.n_slots), seed=self.is_base)
 
     def _w_delta(self, weights):
         key = ("clgqa_w", id(weights))
@@ -1412,7 +1482,10 @@ class DeltaLatentCacheGQA(CacheBackend):
                                    None, 0, 0, self.rank, fused[:, :self.kv_width].contiguous(),
                                    fused[:, self.kv_width:].contiguous(), slot, n)
         wk, wv = self._w_delta(weights)
-        return DeltaInputCacheMHA._remat_acc(self, acc, wk, wv, slot, n)
+        # parity path from the fp16 remat operand itself (cache.py:595-604)
+        xh = acc.x16[slot, :n].float()
+        k = _rope_rows(xh @ wk, 0, self.device)
+        return k, xh @ wv
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         _, fused = self._sub(weights)

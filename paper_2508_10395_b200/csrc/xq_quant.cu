@@ -192,7 +192,8 @@ __global__ void k_quantize_blocks_per_channel(const T* __restrict__ blocks, int6
                                               int bits, int G, const int64_t* __restrict__ dst0,
                                               uint8_t* __restrict__ codes, int64_t row_bytes,
                                               __half* __restrict__ params,
-                                              int32_t* __restrict__ flag) {
+                                              int32_t* __restrict__ flag,
+                                              double* __restrict__ recon = nullptr) {
   extern __shared__ uint8_t s_codes[];  // [G][32]
   __shared__ double s_mn[4][32], s_mx[4][32];
   __shared__ double s_scale[32], s_zp[32];
@@ -238,6 +239,8 @@ __global__ void k_quantize_blocks_per_channel(const T* __restrict__ blocks, int6
     double q = floor(__dadd_rn(__ddiv_rn(__dsub_rn(v, zp), scale), 0.5));
     q = q < 0.0 ? 0.0 : (q > qmax ? qmax : q);
     s_codes[r * 32 + c] = static_cast<uint8_t>(q);
+    // the reference's float64 reconstruction (fallback.py:134-146), may alias blocks
+    if (recon) recon[(int64_t)b * G * cols + (int64_t)r * cols + ch] = __dadd_rn(__dmul_rn(q, scale), zp);
   }
   __syncthreads();
   // row r of this slice: 32 codes -> `bits` 32-bit words at byte 4*bits*slice
@@ -294,18 +297,49 @@ __global__ void k_dequant_rows_f16(const uint8_t* __restrict__ codes, int64_t ro
                                    int64_t cols, int64_t row0, int64_t n_codes,
                                    const float* __restrict__ resid, int64_t n_rows,
                                    __half* __restrict__ out, int64_t ldo) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows * cols;
+  // one thread = 8 consecutive channels of one row (16-byte store): the 8*bits
+  // code bits are at most 3 bytes apart from a 4-byte aligned window pair
+  const int64_t chunks = cols / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows * chunks;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cols, c = i % cols;
-    float v;
+    const int64_t r = i / chunks, c0 = (i % chunks) * 8;
+    float v[8];
     if (r < n_codes) {
-      const uint32_t code = read_code(codes + (row0 + r) * row_bytes, c, bits);
-      const float2 p = load_params(params, axis, bits, G, cols, row0 + r, c);
-      v = fmaf(static_cast<float>(code), p.x, p.y);
+      const int64_t ar = row0 + r;
+      const uint8_t* row = codes + ar * row_bytes;
+      const int64_t bit0 = c0 * bits;
+      const int64_t w0 = bit0 >> 5;
+      const uint32_t* wrow = reinterpret_cast<const uint32_t*>(row);
+      const int64_t n_words = row_bytes / 4;
+      const uint64_t lo = wrow[w0];
+      const uint64_t hi = (w0 + 1 < n_words) ? wrow[w0 + 1] : 0u;
+      uint64_t win = (lo | (hi << 32)) >> (bit0 & 31);
+      if (axis == 0) {
+        const __half2 p = static_cast<const __half2*>(params)[ar * param_stride(cols, G) + c0 / G];
+        const float sc = __low2float(p), zp = __high2float(p);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = fmaf(static_cast<float>((win >> (j * bits)) & ((1u << bits) - 1)), sc, zp);
+      } else {
+        const int bs = perm_block(XQ_A_CODES_CHANNEL, bits);
+        const __half* prow = static_cast<const __half*>(params) + (ar / G) * 2 * cols;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int64_t c = c0 + j;
+          const int64_t pos = (c / bs) * bs + perm_position(static_cast<int>(c % bs), bs);
+          v[j] = fmaf(static_cast<float>((win >> (j * bits)) & ((1u << bits) - 1)),
+                      __half2float(prow[pos]), __half2float(prow[cols + pos]));
+        }
+      }
     } else {
-      v = resid[(r - n_codes) * cols + c];
+      const float4* rr = reinterpret_cast<const float4*>(resid + (r - n_codes) * cols + c0);
+      const float4 a = rr[0], b = rr[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     }
-    out[r * ldo + c] = __float2half_rn(v);
+    uint4 o;
+    __half2* oh = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) oh[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<uint4*>(out + r * ldo + c0) = o;
   }
 }
 
@@ -571,7 +605,7 @@ template <typename T>
 static int quantize_blocks_per_channel(const T* blocks, int64_t n_blocks, int64_t cols, int32_t bits,
                                        int32_t group_size, const int64_t* dst_row0, uint8_t* codes,
                                        int64_t row_bytes, void* params, int32_t* nonfinite_flag,
-                                       void* stream) {
+                                       void* stream, double* recon = nullptr) {
   XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bits must be one of (2, 3, 4, 8), got %d", bits);
   XQ_REQUIRE(cols % 32 == 0, XQ_ESHAPE, "per-channel width must be a multiple of 32");
   XQ_REQUIRE(group_size >= 1 && group_size <= 1024, XQ_ECONFIG, "bad group_size");
@@ -582,7 +616,7 @@ static int quantize_blocks_per_channel(const T* blocks, int64_t n_blocks, int64_
                                      (cudaStream_t)stream>>>(blocks, cols, bits, group_size,
                                                              dst_row0, codes, row_bytes,
                                                              static_cast<__half*>(params),
-                                                             nonfinite_flag);
+                                                             nonfinite_flag, recon);
   return check_launch("xq_quantize_blocks_per_channel");
 }
 
@@ -705,6 +739,16 @@ int xq_dequant_rows(const uint8_t* codes, int64_t row_bytes, const void* params,
   return check_launch("xq_dequant_rows");
 }
 
+int xq_quantize_blocks_per_channel_f64_recon(const double* blocks, int64_t n_blocks, int64_t cols,
+                                             int32_t bits, int32_t group_size,
+                                             const int64_t* dst_row0, uint8_t* codes,
+                                             int64_t row_bytes, void* params, double* recon_out,
+                                             int32_t* nonfinite_flag, void* stream) {
+  XQ_REQUIRE(recon_out != nullptr, XQ_EUSAGE, "recon_out is required");
+  return quantize_blocks_per_channel(blocks, n_blocks, cols, bits, group_size, dst_row0, codes,
+                                     row_bytes, params, nonfinite_flag, stream, recon_out);
+}
+
 int xq_dequant_rows_f16(const uint8_t* codes, int64_t row_bytes, const void* params, int32_t axis,
                         int32_t bits, int32_t group_size, int64_t cols, int64_t row0,
                         int64_t n_codes, const float* resid, int64_t n_rows, void* out,
@@ -714,8 +758,11 @@ int xq_dequant_rows_f16(const uint8_t* codes, int64_t row_bytes, const void* par
   XQ_REQUIRE(n_codes <= n_rows && (n_codes == n_rows || resid != nullptr), XQ_EUSAGE,
              "rows past n_codes need the residual buffer");
   XQ_REQUIRE(ldo >= cols, XQ_ESHAPE, "ldo < cols");
+  XQ_REQUIRE(cols % 8 == 0 && ldo % 8 == 0 && row_bytes % 4 == 0 &&
+                 reinterpret_cast<uintptr_t>(out) % 16 == 0,
+             XQ_ESHAPE, "cols / ldo must be multiples of 8 and out 16-byte aligned");
   if (n_rows * cols == 0) return XQ_OK;
-  k_dequant_rows_f16<<<grid_for(n_rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(
+  k_dequant_rows_f16<<<grid_for(n_rows * cols / 8, 256), 256, 0, (cudaStream_t)stream>>>(
       codes, row_bytes, params, axis, bits, group_size, cols, row0, n_codes, resid, n_rows,
       static_cast<__half*>(out), ldo);
   return check_launch("xq_dequant_rows_f16");

@@ -134,10 +134,10 @@ class Decoder:
                   device=self.device)
         self.caches = [C.make_cache(variant, i, self.policy, shape.head_dim, **kw)
                        for i in range(len(weights))]
-        # xq-cl-mha: fp16-storage accumulator (the remat operand itself) by default;
-        # xq-cl-gqa keeps float32 (its delta latents are formed in float64)
+        # fp16-storage remat accumulator by default (the deltas themselves are formed
+        # against float64 accumulator rows in either precision)
         if acc_precision is None:
-            acc_precision = "fp16" if variant == "xq-cl-mha" else "fp32"
+            acc_precision = "fp16"
         self.acc = (C.Accumulator(n_slots, max_len, shape.hidden_dim, self.device,
                                   precision=acc_precision)
                     if variant in C.CL_VARIANTS else None)
@@ -235,9 +235,10 @@ class Decoder:
         attend = 3 if absorbed else 2
         if self.variant == "xq-gqa":
             return 1 + attend  # v-latent quantize (+ a K-latent flush every 128 steps)
-        if self.variant == "xq-cl-gqa":  # push (+ flush), fused + merge, acc GEMM per seq
+        if self.variant == "xq-cl-gqa":  # latent64 (+ flush), fused + merge; the seed /
+            # delta layers add the row update and per slot a dequant + remat GEMM
             upd = cache.layer_index >= self.policy.base_layers - 1
-            return 1 + attend + (2 * self.n_slots if upd else 0)
+            return 1 + attend + (1 + 2 * self.n_slots if upd else 0)
         if self.variant == "xq-cl-mha":
             base = cache.layer_index < self.policy.base_layers
             seed = cache.layer_index == self.policy.base_layers - 1

@@ -37,10 +37,11 @@ def absorbed_flops(variant: str, seq_len: int, hidden_dim: int, kv_group: int, n
     (csrc/xq_absorb.cu): K remat 2*l*kdim*d_kv, the V-side GEMM
     sum_t p_t x_t 2*l*kdim*H, q.k 2*l*H*hd; the final per-head projection
     through W_v (2*H*kdim*hd, independent of l) is included. kdim = d for the
-    X / CL caches, r = d_kv for the GQA latents."""
+    X / CL caches, r = d_kv for the GQA latents; xq-cl-gqa counts its delta
+    layers (the d-wide accumulator rows, W' = U @ fused)."""
     d = hidden_dim
     kvw = d / kv_group
-    if variant in ("xq-mha", "xq-cl-mha"):
+    if variant in ("xq-mha", "xq-cl-mha", "xq-cl-gqa"):
         kdim = d
     elif variant == "xq-gqa":
         kdim = kvw
@@ -66,7 +67,7 @@ def cache_bytes(variant: str, seq_len: int, hidden_dim: int, bits: int, kv_group
         return 2.0 * 2.0 * seq_len * kvw
     if variant in ("xq-mha", "xq-cl-mha"):
         return pe * seq_len * d
-    if variant in ("xq-gqa", "kvq"):
+    if variant in ("xq-gqa", "kvq", "xq-cl-gqa"):  # two kvw-wide latents / the shared r = 2 kvw
         return 2.0 * pe * seq_len * kvw
     raise ValueError(variant)
 

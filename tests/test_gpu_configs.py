@@ -168,6 +168,55 @@ def test_c3_xq_cl_mha_2bit_delta_stack(n_layers, B, n1, acc):
     assert worst <= TOL, errs
 
 
+def test_xq_cl_gqa_3bit_llama31_width():
+    """xq-cl-gqa at the Llama-3.1-8B width (d=4096, 32 heads on 8 KV heads, shared
+    K|V latent r=2048): 5 layers (3 base + 2 delta), B=2, l=2049 (16 per-channel
+    flushes in the prefill, the decode token in the residual buffer). Every
+    layer's codes bit-exact with the oracle's float64 chain (cache.py:538-604),
+    attention within 2e-2, the fp16 remat accumulator within 2e-2."""
+    import xq_oracle as O
+
+    from paper_2508_10395_b200 import decode as D
+
+    torch = _torch()
+    dev = torch.device("cuda", 0)
+    d, H, g, n_layers, B, n1 = 4096, 32, 4, 5, 2, 2049
+    shape = D.ModelShape("llama3.1-8b-5L", d, n_layers, H, g)
+    w, wq = D.synthetic_weights(shape, "xq-cl-gqa", dev, seed=21)
+    dec = D.Decoder(shape, "xq-cl-gqa", 3, B, 2176, w, wq, device=dev)
+
+    def layer_x(s, i):
+        gen = torch.Generator(device=dev).manual_seed(500 + s)
+        x = torch.randn(n1, d, generator=gen, device=dev)
+        for _ in range(i):
+            x = x + 0.03 * torch.randn(n1, d, generator=gen, device=dev)
+        return x.to(torch.bfloat16)
+
+    _prefill_decoder(dec, layer_x)
+    x_last = torch.stack([torch.stack([layer_x(s, i)[-1] for s in range(B)]) for i in range(n_layers)])
+    out = torch.empty((n_layers, B, H, 128), dtype=torch.float32, device=dev)
+    dec.step(x_last, attn_out=out)
+    got = out.cpu().numpy()
+    subs = [(lw.u_kv.double().cpu().numpy(), lw.fused_kv.double().cpu().numpy()) for lw in w]
+    for s in range(B):
+        stack = O.XqClGqaStack(dec.policy.bits, 3, 128, 128)
+        xs = [layer_x(s, i).double().cpu().numpy() for i in range(n_layers)]
+        stack.step([x[:-1] for x in xs], subs)
+        o = stack.step([x[-1] for x in xs], subs)
+        for i in range(n_layers):
+            q = torch.matmul(x_last[i, s:s + 1], wq[i]).double().cpu().numpy()  # as the decoder
+            ref = O.attention(O.apply_rope(q, [n1 - 1], 128), o[i][1], o[i][2], H, g)[0]
+            err = rel_err(got[i, s].reshape(-1), ref)
+            print(f"xq-cl-gqa slot {s} layer {i}: rel err {err:.2e}")
+            assert err <= TOL, (s, i, err)
+            st = dec.caches[i].stream
+            nfl = int(st.n_flushed[s])
+            rows = st.codes[s * st.L:s * st.L + nfl].cpu().numpy()
+            assert np.array_equal(unpack_rows(rows, st.bits, st.width), stack.streams[i].codes[:nfl]), (s, i)
+        acc16 = dec.acc.x16[s, :n1].float().cpu().numpy()
+        assert rel_err(acc16, o[-1][3]) <= TOL
+
+
 def test_c4_xq_gqa_3bit_latents():
     """C4 shape: per-channel K latent (128 full groups + 1 residual row after the
     decode push), per-token V latent, 8 KV heads x 4 query heads."""

@@ -108,7 +108,7 @@ def test_decoder_cl_step_matches_oracle():
 def test_decoder_cl_gqa_step_matches_oracle():
     """xq-cl-gqa through the decode engine: 5 layers (base 3), 8 query heads on 2 KV
     heads, the shared K|V subspace from the SVD of [W_k | W_v]; against the oracle
-    with the arena's fp16 scale/zero-point storage on the same inputs."""
+    (the reference's float64 algorithm) on the same inputs."""
     import torch
 
     import xq_oracle as O
@@ -124,7 +124,7 @@ def test_decoder_cl_gqa_step_matches_oracle():
     x = xs.double().numpy()
     subs = [(w[i].u_kv.double().cpu().numpy(), w[i].fused_kv.double().cpu().numpy()) for i in range(L)]
     for b in range(B):
-        stack = O.XqClGqaStack(dec.policy.bits, dec.policy.base_layers, 128, 128, params_f16=True)
+        stack = O.XqClGqaStack(dec.policy.bits, dec.policy.base_layers, 128, 128)
         stack.step([x[i, b, :-1] for i in range(L)], subs)
         o = stack.step([x[i, b, -1] for i in range(L)], subs)
         for i in range(L):

@@ -120,7 +120,7 @@ def test_prefill_cross_layer_against_oracle(variant):
         stack = O.XqClMhaStack(pol.bits, pol.base_layers, 128, 128)
         _, kvs = stack.step(xd, [(w.w_k.double().cpu().numpy(), w.w_v.double().cpu().numpy()) for w in ws])
     else:
-        stack = O.XqClGqaStack(pol.bits, pol.base_layers, 128, 128, params_f16=True)
+        stack = O.XqClGqaStack(pol.bits, pol.base_layers, 128, 128)
         o = stack.step(xd, [(w.u_kv.double().cpu().numpy(), w.fused_kv.double().cpu().numpy()) for w in ws])
         kvs = [(e[1], e[2]) for e in o]
     for i in range(L):
