@@ -394,6 +394,49 @@ class _Null:
         return False
 
 
+def _prefill_leg(cfg, shape, n_layers, weights, w_q, dev, n_max: int = 8192):
+    """One sequence's prompt through every layer's prefill_attend (model.py:205-221):
+    bulk quantize, K/V rebuilt by the tcgen05 remat GEMM (RoPE in its epilogue),
+    causal flash attention. Inputs device-resident; CUDA events around the layers."""
+    import torch
+
+    from paper_2508_10395_b200 import decode as D
+
+    n = min(cfg["ctx"], n_max)
+    try:
+        dec = D.Decoder(shape, cfg["variant"], cfg["bits"], 1, -(-n // 128) * 128, weights, w_q,
+                        device=dev)
+        g = torch.Generator(device=dev).manual_seed(7)
+        xs = [torch.randn(n, shape.hidden_dim, generator=g, device=dev).to(torch.bfloat16)
+              for _ in range(n_layers)]
+        qs = [torch.matmul(x, w) for x, w in zip(xs, w_q)]
+
+        def run():
+            for i, c in enumerate(dec.caches):
+                c.n_tokens[:] = 0
+                c.prefill_attend(xs[i], qs[i], dec.weights[i], dec.acc)
+
+        run()  # warm-up (weight layouts, workspaces)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        d, kvw, H = shape.hidden_dim, shape.kv_width, shape.n_heads
+        kdim = kvw if cfg["variant"] == "xq-gqa" else d
+        flops = n_layers * (2.0 * n * kdim * 2 * kvw + 2.0 * n * n * H * 128)  # remat + causal attn
+        out = {"value": n / t, "unit": "prompt tokens/s", "prompt_tokens": n, "layers": n_layers,
+               "ms": t * 1e3, "tflops_achieved": flops / t / 1e12,
+               "kernels": "xq_quantize_rows (+ CL / latent variants), k_dequant_rows_f16, "
+                          "k_gemm_f16 (tcgen05 remat, RoPE epilogue), k_rope_rows, k_prefill_attend"}
+        del dec, xs, qs
+        return out
+    except torch.OutOfMemoryError as e:
+        return {"value": None, "note": f"prefill leg out of memory: {str(e)[:100]}"}
+
+
 def run_xquant(args, cfg):
     import torch
 
@@ -518,6 +561,11 @@ def run_xquant(args, cfg):
         except torch.OutOfMemoryError as e:
             kvq = {"value": None, "note": f"kvq cache does not fit one B200: {str(e)[:120]}"}
 
+    # ---------------- prefill (the attention block of _Session.prefill) ----------------
+    prefill = None
+    if world == 1 and not args.no_prefill:
+        prefill = _prefill_leg(cfg, shape, n_layers, weights, w_q, dev)
+
     if rank != 0:
         return
     # ---------------- roofline of the dominant kernel ----------------
@@ -565,6 +613,7 @@ def run_xquant(args, cfg):
         "fp16_kv": fp16,
         "speedup_vs_fp16_kv": (value / fp16["value"]) if fp16 and fp16.get("value") else None,
         "kvq": kvq,
+        "prefill": prefill,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": ("k_decode_absorbed (+k_absorb_combine, k_absorb_project)" if absorbed
@@ -603,6 +652,7 @@ def main():
     ap.add_argument("--no-fp16", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kvq", action="store_true", help="also time the kvq baseline at equal bits")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the prefill leg")
     ap.add_argument("--gather", choices=["nccl", "peer"], default="nccl",
                     help="KV-head-group sharding (c4 under torchrun): NCCL all-gather, or the "
                          "fused kernel's peer stores into torch symmetric memory")

@@ -109,3 +109,25 @@ def test_head_sharded_attention_gloo_world2(variant):
         p.join(timeout=240)
         assert p.exitcode == 0
     assert q.get(timeout=5) < 1e-5
+
+
+def test_bench_rank_split():
+    """bench.py's per-rank workload: configs[2] (C3) is one global batch of 16 split
+    by sequence (16/n per GPU), C4 serves the whole batch per KV-head shard, C2 is
+    weak scaling; both arms print the same config dict."""
+    import importlib
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+    bench = importlib.import_module("bench")
+    for world in (1, 2, 4, 8):
+        c3 = [bench._split(bench.CONFIGS["c3"], world, r) for r in range(world)]
+        assert sum(b for b, _, _ in c3) == 16 and all(t == 16 for _, t, _ in c3)
+        assert [s for _, _, s in c3] == [sum(b for b, _, _ in c3[:r]) for r in range(world)]
+        c4 = [bench._split(bench.CONFIGS["c4"], world, r) for r in range(world)]
+        assert all(b == 32 and t == 32 for b, t, _ in c4)
+        c2 = [bench._split(bench.CONFIGS["c2"], world, r) for r in range(world)]
+        assert all(b == 8 and t == 8 * world for b, t, _ in c2)
+        for name in bench.CONFIGS:
+            cfg = bench._config_dict(bench.CONFIGS[name], world)
+            assert cfg["global_batch"] == bench._split(bench.CONFIGS[name], world, 0)[1]
