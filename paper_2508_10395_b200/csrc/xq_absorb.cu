@@ -109,7 +109,7 @@ struct Params {
   const float2* rope;  // frequency-major [64][rope_n]
   int64_t rope_n;
   float q_scale;
-  float* part_o;       // [n_seqs][n_tiles][n_q][kdim]
+  __half* part_o;      // [n_seqs][n_tiles][n_q][kdim] (fp16: half the partial traffic)
   float2* part_ml;     // [n_seqs][n_tiles][n_q] (m, l), m in the log2 domain
   uint64_t w_hint;
   int32_t a_hint;   // fp16-row A: 0 evict-normal, 1 split (see the K-pass TMA loop), 2 evict-last
@@ -787,7 +787,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {
               const int h = c16 * 16 + jj;
-              if (h < p.n_q) sts_f32(stg + 4u * (h * kTileM + row), v[jj]);
+              if (h < p.n_q) {
+                const __half hv = __float2half_rn(v[jj]);
+                asm volatile("st.shared.b16 [%0], %1;" ::"r"(stg + 2u * (h * kTileM + row)),
+                             "h"(*reinterpret_cast<const unsigned short*>(&hv))
+                             : "memory");
+              }
             }
           }
           fence_proxy_async_smem();
@@ -828,7 +833,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // Merge the tile partials: x[b][h][c] = (sum_i 2^(m_i-M) O_i[h][c]) / (sum_i 2^(m_i-M) l_i).
 // Grid (n_seqs*n_q, kdim/512), 128 threads x 4 channels (float4 loads, 8 tiles
 // in flight per thread: the partials are streamed once from HBM/L2).
-__global__ void __launch_bounds__(128) k_absorb_combine(const float* __restrict__ part_o,
+__global__ void __launch_bounds__(128) k_absorb_combine(const __half* __restrict__ part_o,
                                                         const float2* __restrict__ part_ml,
                                                         const int32_t* __restrict__ seq_lens,
                                                         int n_tiles, int n_q, int kdim,
@@ -861,13 +866,19 @@ __global__ void __launch_bounds__(128) k_absorb_combine(const float* __restrict_
   const int c = blockIdx.y * 512 + tid * 4;
   if (c >= kdim) return;
   const int64_t stride = (int64_t)n_q * kdim;  // tile stride of the partials
-  const float* po = part_o + (int64_t)b * n_tiles * stride + (int64_t)h * kdim + c;
+  const __half* po = part_o + (int64_t)b * n_tiles * stride + (int64_t)h * kdim + c;
+  auto ld4 = [&](int64_t off) {  // 4 fp16 partials -> float4 (streaming 8-byte load)
+    const uint2 u = __ldcs(reinterpret_cast<const uint2*>(po + off));
+    const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    return make_float4(lo.x, lo.y, hi.x, hi.y);
+  };
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   int i = 0;
   for (; i + 8 <= nt; i += 8) {
     float4 v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __ldcs(reinterpret_cast<const float4*>(po + (int64_t)(i + k) * stride));
+    for (int k = 0; k < 8; ++k) v[k] = ld4((int64_t)(i + k) * stride);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float w = wts[i + k];
@@ -876,7 +887,7 @@ __global__ void __launch_bounds__(128) k_absorb_combine(const float* __restrict_
     }
   }
   for (; i < nt; ++i) {
-    const float4 v = __ldcs(reinterpret_cast<const float4*>(po + (int64_t)i * stride));
+    const float4 v = ld4((int64_t)i * stride);
     const float w = wts[i];
     acc.x = fmaf(w, v.x, acc.x); acc.y = fmaf(w, v.y, acc.y);
     acc.z = fmaf(w, v.z, acc.z); acc.w = fmaf(w, v.w, acc.w);
@@ -902,43 +913,74 @@ __global__ void __launch_bounds__(256) k_absorb_project(const float* __restrict_
                                                         int n_seqs, int n_q, int group, int kdim,
                                                         const __half* __restrict__ wv,
                                                         const OutPtrs outs) {
-  extern __shared__ float xs[];  // [8][kdim]
-  __shared__ float red[16][8][33];
+  extern __shared__ float xs[];  // [kdim][8]: the 8 sequences' x of one channel contiguous
+  __shared__ float red[8][8][33];
   const int h = blockIdx.x, cb = blockIdx.y, b0 = blockIdx.z * 8, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int nb = n_seqs - b0 < 8 ? n_seqs - b0 : 8;
-  for (int i = tid; i < 8 * kdim; i += 256) {
-    const int s = i / kdim, c = i % kdim;
-    xs[i] = s < nb ? x[((int64_t)(b0 + s) * n_q + h) * kdim + c] : 0.f;
+  const int kd4 = kdim / 4;
+  for (int i = tid; i < 8 * kd4; i += 256) {
+    const int s = i / kd4, c = 4 * (i % kd4);
+    const float4 v = s < nb ? *reinterpret_cast<const float4*>(x + ((int64_t)(b0 + s) * n_q + h) * kdim + c)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    xs[c * 8 + s] = v.x;
+    xs[(c + 1) * 8 + s] = v.y;
+    xs[(c + 2) * 8 + s] = v.z;
+    xs[(c + 3) * 8 + s] = v.w;
   }
   __syncthreads();
-  const int j2 = tid & 15, sl = tid >> 4;  // column pair of the block, channel slice
-  const __half2* w2 =
-      reinterpret_cast<const __half2*>(wv + (int64_t)(h / group) * kdim * 128 + cb * 32) + j2;
-  const int per = kdim / 16, c0 = sl * per;
-  float a0[8], a1[8];
+  // thread = (8-column group q of the 32-column block, channel slice sl of 64):
+  // slice sl takes channels sl, sl+64, ... so a warp's 8 slices read 8 adjacent
+  // W_v rows (16-byte loads) and 8 adjacent x rows
+  const int q = tid & 3, sl = tid >> 2;
+  const uint4* w16 = reinterpret_cast<const uint4*>(wv + (int64_t)(h / group) * kdim * 128 + cb * 32 + q * 8);
+  float a[8][8];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) a0[s] = a1[s] = 0.f;
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[s][j] = 0.f;
 #pragma unroll 4
-  for (int c = c0; c < c0 + per; ++c) {
-    const float2 wf = __half22float2(w2[(int64_t)c * 64]);
+  for (int c = sl; c < kdim; c += 64) {
+    const uint4 wr = __ldg(w16 + (int64_t)c * 16);
+    const __half2* w2 = reinterpret_cast<const __half2*>(&wr);
+    float wf[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const float xv = xs[s * kdim + c];
-      a0[s] = fmaf(xv, wf.x, a0[s]);
-      a1[s] = fmaf(xv, wf.y, a1[s]);
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(w2[j]);
+      wf[2 * j] = f.x;
+      wf[2 * j + 1] = f.y;
     }
-  }
+    const float4 x0 = *reinterpret_cast<const float4*>(xs + c * 8);
+    const float4 x1 = *reinterpret_cast<const float4*>(xs + c * 8 + 4);
+    const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    red[sl][s][2 * j2] = a0[s];
-    red[sl][s][2 * j2 + 1] = a1[s];
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[s][j] = fmaf(xv[s], wf[j], a[s][j]);
+  }
+  // lanes q, q+4, ..., q+28 of a warp hold 8 slices of the same outputs
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = a[s][j];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      a[s][j] = v;
+    }
+  if (lane < 4) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) red[warp][s][lane * 8 + j] = a[s][j];
   }
   __syncthreads();
-  for (int i = tid; i < nb * 32; i += 256) {
-    const int s = i >> 5, j = i & 31;
+  if (tid < nb * 32) {
+    const int s = tid >> 5, j = tid & 31;
     float v = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v += red[k][s][j];
+    for (int k = 0; k < 8; ++k) v += red[k][s][j];
     const int64_t o = ((int64_t)(b0 + s) * n_q + h) * kHeadDim + cb * 32 + j;
     for (int k = 0; k < outs.n; ++k) outs.p[k][o] = v;
   }
@@ -1149,7 +1191,8 @@ int xq_debug_role_profile(uint64_t* out, int32_t reset) {
 
 int64_t xq_absorbed_workspace_bytes(int32_t n_seqs, int32_t max_len, int32_t n_q_heads,
                                     int64_t kdim) {
-  // O partials + (m, l) per tile, then the merged x [n_seqs][n_q][kdim]
+  // O partials (fp16, in a region sized for float32) + (m, l) per tile, then the
+  // merged x [n_seqs][n_q][kdim]
   return (int64_t)n_seqs * n_q_heads *
          ((int64_t)n_tiles_for(max_len) * (kdim + 2) + kdim) * (int64_t)sizeof(float);
 }
@@ -1260,7 +1303,7 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
     return st_;
 
   const int64_t n_tiles = n_tiles_for(max_len);
-  if ((st_ = make_map(&maps.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, workspace, kdim,
+  if ((st_ = make_map(&maps.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, workspace, kdim,
                       (uint64_t)n_seqs * n_tiles * n_q, 128, static_cast<uint32_t>(n_q),
                       CU_TENSOR_MAP_SWIZZLE_NONE, "O partials")) != XQ_OK)
     return st_;
@@ -1285,7 +1328,7 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
   p.rope_n = rope_n;
   p.q_scale = sm_scale * 1.4426950408889634f;
   float* ws = static_cast<float*>(workspace);
-  p.part_o = ws;
+  p.part_o = reinterpret_cast<__half*>(ws);
   p.part_ml = reinterpret_cast<float2*>(ws + (int64_t)n_seqs * p.n_tiles * n_q * kdim);
   // W_k stays L2-resident across the CTA pairs (evict_last). fp16-row A operand
   // (XQuant-CL delta layers): the serpentine sweeps keep the trailing half of each

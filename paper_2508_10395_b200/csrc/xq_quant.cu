@@ -589,6 +589,13 @@ __global__ void __launch_bounds__(256) k_cl_accumulate_w(
   }
 }
 
+// one warp per quantization group of a row (the fp64 group math is a latency
+// chain; a decode step quantizes only a few rows)
+static int rows_threads(int64_t cols, int G) {
+  const int64_t w = 32 * ((cols + G - 1) / G);
+  return static_cast<int>(w < 128 ? 128 : (w > 512 ? 512 : w));  // 72 registers x 512 threads
+}
+
 static int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 148 * 32) g = 148 * 32;
@@ -680,7 +687,7 @@ int xq_quantize_rows(const void* x, int32_t x_dtype, int64_t x_row_stride, int64
              (long long)row_bytes_for(cols, bits));
   XQ_REQUIRE(cols <= 48 * 1024, XQ_ESHAPE, "cols %lld too wide for one CTA", (long long)cols);
   if (n_rows == 0 || cols == 0) return XQ_OK;
-  k_quantize_rows<<<static_cast<unsigned>(n_rows), 128, static_cast<size_t>(cols),
+  k_quantize_rows<<<static_cast<unsigned>(n_rows), rows_threads(cols, group_size), static_cast<size_t>(cols),
                     (cudaStream_t)stream>>>(x, x_dtype, x_row_stride, cols, group_size, bits,
                                             seq_lens, row0, L_max, sub_rows, codes, row_bytes,
                                             static_cast<__half2*>(params), x_eff_out,
@@ -704,7 +711,7 @@ int xq_quantize_rows_cl(const void* x, int32_t x_dtype, int64_t x_row_stride, in
              (long long)row_bytes_for(cols, bits));
   XQ_REQUIRE(cols <= 48 * 1024, XQ_ESHAPE, "cols %lld too wide for one CTA", (long long)cols);
   if (n_rows == 0 || cols == 0) return XQ_OK;
-  k_quantize_rows<<<static_cast<unsigned>(n_rows), 128, static_cast<size_t>(cols),
+  k_quantize_rows<<<static_cast<unsigned>(n_rows), rows_threads(cols, group_size), static_cast<size_t>(cols),
                     (cudaStream_t)stream>>>(x, x_dtype, x_row_stride, cols, group_size, bits,
                                             seq_lens, row0, L_max, nullptr, codes, row_bytes,
                                             static_cast<__half2*>(params), nullptr,
