@@ -54,6 +54,8 @@ extern "C" {
 #define XQ_A_CODES_CHANNEL 1 /* per-channel packed codes + residual fp32 rows    */
 #define XQ_A_F16_ROWS 2      /* plain fp16 rows (XQuant-CL accumulator, 16-bit)  */
 #define XQ_A_SAME 3          /* V side reuses the K-side A operand (MHA)         */
+#define XQ_A_F16_ACC 4       /* fp16 accumulator rows updated in the first K pass */
+                             /* by per-token delta codes (XQuant-CL delta layer)  */
 
 const char* xq_version(void);
 /* Message describing the last non-zero status returned on this host thread. */
@@ -312,6 +314,27 @@ int xq_decode_attend_absorbed(int32_t ak_mode, const void* ak_src, const void* a
                               int32_t group, const float* q_pre, const void* rope_cs,
                               int64_t rope_n, float sm_scale, void* workspace,
                               int64_t workspace_bytes, float* out, void* stream);
+
+/* XQuant-CL delta layer with the accumulate fused in (cache.py:472-481 +
+ * Accumulator.add, cache.py:139-146, then the delta layer's remat from the
+ * accumulator, cache.py:527-535): acc16 is the fp16 accumulator
+ * [n_seqs * L_max, kdim] BEFORE this layer; codes / params are this layer's
+ * per-token delta arena (XQ_A_CODES_TOKEN layout, bits 2/3/4/8). In the first K
+ * pass over each 256-token tile the dequant producers add the dequantized deltas
+ * to the TMA-staged accumulator rows, acc[t] = fp16(float(acc[t]) + code*scale +
+ * zp) for t < seq_lens[b] (the arithmetic of xq_cl_accumulate, bit-identical),
+ * feed the updated rows to the tensor cores and write them back to acc16; the
+ * later K passes and the V side read the updated rows. Replaces xq_cl_accumulate
+ * (seed = 0) followed by xq_decode_attend_absorbed on XQ_A_F16_ROWS. MHA (group
+ * 1) only; other arguments as xq_decode_attend_absorbed. */
+int xq_decode_attend_absorbed_cl(void* acc16, const void* codes, const void* params, int32_t bits,
+                                 int64_t row_bytes, int32_t group_size, int64_t L_max,
+                                 int64_t kdim, const int32_t* seq_lens, int32_t n_seqs,
+                                 int32_t max_len, const void* wk_arranged,
+                                 const void* wv_arranged, int32_t n_kv_heads, const float* q_pre,
+                                 const void* rope_cs, int64_t rope_n, float sm_scale,
+                                 void* workspace, int64_t workspace_bytes, float* out,
+                                 void* stream);
 
 /* xq_decode_attend_absorbed with the projected output [n_seqs][H][128] stored
  * to each of n_outs (1..9) destinations. Under KV-head-group sharding

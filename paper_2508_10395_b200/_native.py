@@ -18,7 +18,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("XQ_LIB") or os.path.join(_PKG, "libxquant.so")
 
 F32, BF16, F16, F64 = 0, 1, 2, 3
-A_CODES_TOKEN, A_CODES_CHANNEL, A_F16_ROWS, A_SAME = 0, 1, 2, 3
+A_CODES_TOKEN, A_CODES_CHANNEL, A_F16_ROWS, A_SAME, A_F16_ACC = 0, 1, 2, 3, 4
 
 _P = C.c_void_p
 _I32 = C.c_int32
@@ -62,6 +62,8 @@ _SIGS = {
     "xq_decode_attend_absorbed_peers": [_I32, _P, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _I32,
                                         _I64, _I32, _I64, _I64, _P, _I32, _I32, _P, _P, _I32,
                                         _I32, _P, _P, _I64, _F, _P, _I64, _P, _I32, _P],
+    "xq_decode_attend_absorbed_cl": [_P, _P, _P, _I32, _I64, _I32, _I64, _I64, _P, _I32, _I32, _P,
+                                     _P, _I32, _P, _P, _I64, _F, _P, _I64, _P, _P],
     "xq_remat_f32": [_I32, _P, _P, _P, _I32, _I32, _I64, _I32, _P, _P, _I32, _I64, _I32, _I64,
                      _I64, _I32, _I32, _P, _P, _I64, _P, _P, _P, _P],
     "xq_cl_accumulate": [_I32, _P, _I64, _P, _I32, _I32, _I64, _P, _I32, _I32, _I64, _P, _P,

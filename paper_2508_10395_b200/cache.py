@@ -258,6 +258,10 @@ class Accumulator:
         self.x_hat = self.x16 = self.row64 = None
         self._prefill64: dict = {}
         self.seeded = False
+        # an xq-cl-mha delta layer's accumulate deferred to its fused decode launch
+        # (xq_decode_attend_absorbed_cl): (backend, lens, max_len); settle() runs it
+        # standalone when anything else needs the remat operand first
+        self.pending = None
         if n_slots is not None:
             if max_len is None or width is None:
                 raise ConfigError("Accumulator needs n_slots, max_len and width together")
@@ -310,8 +314,30 @@ class Accumulator:
         rows = self._prefill64[0] + delta
         self.seed(rows)
 
+    def assign_rows(self, rows16: torch.Tensor, n: int, slot: int | None = None) -> None:
+        """acc = the rows themselves (a 16-bit layer: delta = x - acc is kept exactly,
+        so acc + delta = x): rows16 [n_slots, >= n, d] fp16 (or [>= n, d] for ``slot``)."""
+        self.settle()  # a deferred update of the previous layer would land on top
+        if slot is None:
+            self.x16[:, :n] = rows16[:, :n]
+            if self.x_hat is not None:
+                self.x_hat[:, :n] = rows16[:, :n]
+        else:
+            self.x16[slot, :n] = rows16[:n]
+            if self.x_hat is not None:
+                self.x_hat[slot, :n] = rows16[:n]
+        self.seeded = True
+
+    def settle(self) -> None:
+        """Apply a deferred delta-layer accumulate (the remat operand is then current)."""
+        if self.pending is not None:
+            backend, lens, max_len = self.pending
+            self.pending = None
+            backend._accumulate(self, False, max_len, lens)
+
     def rows(self, slot, n) -> torch.Tensor:
         """float32 view/copy of the accumulator rows 0..n-1 of a slot."""
+        self.settle()
         return self.x_hat[slot, :n] if self.x_hat is not None else self.x16[slot, :n].float()
 
     def prefill_rows(self, slot: int, n: int, seed: bool) -> torch.Tensor:
@@ -569,6 +595,37 @@ class PackedStream:
         if int(self.flag.item()):
             self.flag.zero_()
             raise DataError("input contains NaN or Inf")
+
+
+class RawRows:
+    """16-bit pass-through payload (quant.py:117-118: a bits=16 QuantizedTensor keeps
+    the raw rows; ``_Stream`` never buffers or quantizes them): fp16 rows
+    [n_slots * L_max, width], row ``slot * L_max + t`` = token t. The fused kernels
+    read them as their fp16-row A operand (XQ_A_F16_ROWS)."""
+
+    bits = 16
+
+    def __init__(self, width: int, n_slots: int, max_len: int, device):
+        self.width, self.n_slots, self.L = width, n_slots, max_len
+        self.rows = torch.zeros((n_slots * max_len, width), dtype=torch.float16, device=device)
+
+    def fill(self, x: torch.Tensor, slot: int, pos0: int = 0):
+        r0 = slot * self.L + pos0
+        self.rows[r0:r0 + x.shape[0]] = x.to(torch.float16)
+
+    def append(self, x: torch.Tensor, lens_dev: torch.Tensor):
+        """One row per slot at position lens[b]-1."""
+        idx = torch.arange(self.n_slots, device=x.device) * self.L + lens_dev.long() - 1
+        self.rows[idx] = x.to(torch.float16)
+
+    def slot_rows(self, slot: int, n: int) -> torch.Tensor:
+        return self.rows[slot * self.L:slot * self.L + n]
+
+    def slots_view(self) -> torch.Tensor:
+        return self.rows.view(self.n_slots, self.L, self.width)
+
+    def nbytes(self) -> dict:
+        return {"rows_f16": self.rows.numel() * 2}
 
 
 # ---------------------------------------------------------------------------
@@ -962,7 +1019,7 @@ class QuantizedKvCache(CacheBackend):
     def __init__(self, *a, **kw):
         super().__init__(*a, **kw)
         if self.bits == 16:
-            raise ConfigError("kvq needs a quantized width (2/3/4/8)")
+            raise ConfigError("kvq at 16 bits is QuantizedKvPassthrough (make_cache picks it)")
         self.k_stream = PackedStream(self.bits, CHANNEL, self.kvw, self.group_size, self.n_slots,
                                      self.L, self.device)
         self.v_stream = PackedStream(self.bits, TOKEN, self.kvw, self.group_size, self.n_slots,
@@ -1033,33 +1090,31 @@ class InputCacheMHA(CacheBackend):
         super().__init__(*a, **kw)
         self.passthrough = self.bits == 16
         if self.passthrough:  # bits=16 -> fp16 rows (quant.py:117-118 keeps raw data)
-            self.x16 = torch.zeros((self.n_slots * self.L, self.d), dtype=torch.float16,
-                                   device=self.device)
+            self.raw = RawRows(self.d, self.n_slots, self.L, self.device)
         else:
             self.stream = PackedStream(self.bits, TOKEN, self.d, self.group_size, self.n_slots,
                                        self.L, self.device)
 
     def _prefill(self, slot, x, weights, acc):
         if self.passthrough:
-            self.x16[slot * self.L:slot * self.L + x.shape[0]] = x.to(torch.float16)
+            self.raw.fill(x, slot)
         else:
             self.stream.fill_rows(x.contiguous(), slot, 0)
 
     def _decode(self, x, weights, acc, lens):
         if self.passthrough:
-            idx = torch.arange(self.n_slots, device=self.device) * self.L + lens.long() - 1
-            self.x16[idx] = x.to(torch.float16)
+            self.raw.append(x, lens)
         else:
             self.stream.append_token_rows(x.contiguous(), lens)
 
     def _a_operand(self):
         if self.passthrough:
-            return N.A_F16_ROWS, self.x16, None, 16, 0
+            return N.A_F16_ROWS, self.raw.rows, None, 16, 0
         s = self.stream
         return N.A_CODES_TOKEN, s.codes, s.params, s.bits, s.row_bytes
 
     def _prefill_kv(self, weights, acc, slot, n):
-        a = (self.x16[slot * self.L:slot * self.L + n] if self.passthrough
+        a = (self.raw.slot_rows(slot, n) if self.passthrough
              else self._rows16(self.stream, slot, n))
         return self._kv_from(a, a, weights.w_k, weights.w_v, n)
 
@@ -1076,7 +1131,7 @@ class InputCacheMHA(CacheBackend):
 
     def memory_bytes(self):
         if self.passthrough:
-            return {"x16": self.x16.numel() * 2}
+            return {"x16": self.raw.rows.numel() * 2}
         return self.stream.nbytes()
 
 
@@ -1088,10 +1143,13 @@ class LatentInputCacheGQA(CacheBackend):
 
     def __init__(self, *a, **kw):
         super().__init__(*a, **kw)
-        if self.bits == 16:
-            raise ConfigError("xq-gqa on the B200 path needs a quantized width (2/3/4/8)")
         r = self.latent  # the latent cache is whole even when heads are sharded
         self.fp16_first_channel = False
+        self.passthrough = self.bits == 16
+        if self.passthrough:  # 16-bit latents kept raw (quant.py:117-118), no flush
+            self.k_raw = RawRows(r, self.n_slots, self.L, self.device)
+            self.v_raw = RawRows(r, self.n_slots, self.L, self.device)
+            return
         self.k_stream = PackedStream(self.bits, CHANNEL, r, self.group_size, self.n_slots, self.L,
                                      self.device, resid_f64=self.exact)
         self.v_stream = PackedStream(self.bits, TOKEN, r, self.group_size, self.n_slots, self.L,
@@ -1102,6 +1160,8 @@ class LatentInputCacheGQA(CacheBackend):
         if np.any(self.n_tokens):
             raise UsageError("toggle the full-precision channel before caching")
         self.fp16_first_channel = bool(enable)
+        if self.passthrough:  # every channel is already raw (cache.py:174: bits != 16)
+            return
         self.k_stream = PackedStream(self.bits, CHANNEL, self.latent, self.group_size, self.n_slots,
                                      self.L, self.device, keep_first=self.fp16_first_channel,
                                      resid_f64=self.exact)
@@ -1124,10 +1184,19 @@ class LatentInputCacheGQA(CacheBackend):
 
     def _prefill(self, slot, x, weights, acc):
         lat_k, lat_v = self._latents(x, weights)
+        if self.passthrough:
+            self.k_raw.fill(lat_k, slot)
+            self.v_raw.fill(lat_v, slot)
+            return
         self.v_stream.fill_rows(lat_v.contiguous(), slot, 0)
         self.k_stream.channel_bulk(slot, lat_k)  # cache.py:203-208
 
     def _decode(self, x, weights, acc, lens):
+        if self.passthrough:
+            lat_k, lat_v = self._latents(x, weights)
+            self.k_raw.append(lat_k, lens)
+            self.v_raw.append(lat_v, lens)
+            return
         if self.exact and x.dtype == torch.float64:  # the reference's float64 latents
             lat_k, lat_v = self._latents(x, weights)
             self.v_stream.append_token_rows(lat_v.contiguous(), lens)
@@ -1154,11 +1223,18 @@ class LatentInputCacheGQA(CacheBackend):
         return weights._cache[key]
 
     def _prefill_kv(self, weights, acc, slot, n):
-        lat_k = self._rows16(self.k_stream, slot, n)
-        lat_v = self._rows16(self.v_stream, slot, n)
+        if self.passthrough:
+            lat_k, lat_v = self.k_raw.slot_rows(slot, n), self.v_raw.slot_rows(slot, n)
+        else:
+            lat_k = self._rows16(self.k_stream, slot, n)
+            lat_v = self._rows16(self.v_stream, slot, n)
         return self._kv_from(lat_k, lat_v, weights.fused_k, weights.fused_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
+        if self.passthrough:
+            return self._remat_f32(N.A_F16_ROWS, self.k_raw.rows, None, None, 0, 16, 0,
+                                   N.A_F16_ROWS, self.v_raw.rows, None, 16, 0, self.latent,
+                                   weights.f32("fused_k"), weights.f32("fused_v"), slot, n)
         ks, vs = self.k_stream, self.v_stream
         if ks.first is not None:  # float32 torch path (the SIMT debug kernel has no outlier channel)
             k = ks.channel_reconstruct(slot, n) @ weights.f32("fused_k")
@@ -1170,6 +1246,13 @@ class LatentInputCacheGQA(CacheBackend):
                                weights.f32("fused_k"), weights.f32("fused_v"), slot, n)
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
+        if self.passthrough:  # fp16 latent rows: K side and V side from their own arenas
+            spec = (("gqa", 16), N.A_F16_ROWS, 16, N.A_F16_ROWS, 16, weights.fused_k,
+                    weights.fused_v)
+            self._fused(N.A_F16_ROWS, self.k_raw.rows, None, None, None, 16, 0, N.A_F16_ROWS,
+                        self.v_raw.rows, None, 16, 0, self.latent, spec, weights, self.g, q, lens,
+                        max_len, out, tpc, force_absorbed=True)
+            return
         ks, vs = self.k_stream, self.v_stream
         spec = (("gqa", self.bits), N.A_CODES_CHANNEL, ks.bits, N.A_CODES_TOKEN, vs.bits,
                 weights.fused_k, weights.fused_v)
@@ -1179,8 +1262,9 @@ class LatentInputCacheGQA(CacheBackend):
                     force_absorbed=ks.first is not None, ak_first=ks.first)
 
     def memory_bytes(self):
-        out = {f"k_{k}": v for k, v in self.k_stream.nbytes().items()}
-        out.update({f"v_{k}": v for k, v in self.v_stream.nbytes().items()})
+        ks, vs = (self.k_raw, self.v_raw) if self.passthrough else (self.k_stream, self.v_stream)
+        out = {f"k_{k}": v for k, v in ks.nbytes().items()}
+        out.update({f"v_{k}": v for k, v in vs.nbytes().items()})
         return out
 
 
@@ -1197,10 +1281,16 @@ class DeltaInputCacheMHA(CacheBackend):
         super().__init__(*a, **kw)
         if self.policy.base_layers < 1:
             raise ConfigError("cross-layer variants need at least one base layer")
-        if self.bits == 16:
-            raise ConfigError("xq-cl-mha on the B200 path needs a quantized width (2/3/4/8)")
-        self.stream = PackedStream(self.bits, TOKEN, self.d, self.group_size, self.n_slots,
-                                   self.L, self.device)
+        # 16 bits: the payload (x, or the delta x - acc) is kept exactly, so after the
+        # layer acc = x (cache.py:463-481 with a pass-through QuantizedTensor). The
+        # arena keeps x itself as fp16 rows, which carries the same information as
+        # the delta given acc, and is the layer's remat operand directly.
+        self.passthrough = self.bits == 16
+        if self.passthrough:
+            self.raw = RawRows(self.d, self.n_slots, self.L, self.device)
+        else:
+            self.stream = PackedStream(self.bits, TOKEN, self.d, self.group_size, self.n_slots,
+                                       self.L, self.device)
 
     @property
     def is_base(self):
@@ -1211,6 +1301,8 @@ class DeltaInputCacheMHA(CacheBackend):
         return self.layer_index == self.policy.base_layers - 1
 
     def _accumulate(self, acc, seed, max_len, lens):
+        if acc.pending is not None and acc.pending[0] is not self:
+            acc.settle()  # the previous delta layer's update comes first
         s = self.stream
         x16 = acc.x16 if (acc.x_hat is None or not seed) else None
         N.call("xq_cl_accumulate", 1 if seed else 0, N.ptr(s.codes), s.row_bytes, N.ptr(s.params),
@@ -1220,6 +1312,15 @@ class DeltaInputCacheMHA(CacheBackend):
 
     def _prefill(self, slot, x, weights, acc):
         n = x.shape[0]
+        if self.passthrough:
+            self.raw.fill(x, slot)
+            if self.is_base and not self.seeds_accumulator:
+                return
+            if not self.is_base and not acc.seeded:
+                raise UsageError("accumulator used before the base layer seeded it")
+            acc.prefill_rows(slot, n, seed=self.is_base).copy_(x.double())
+            acc.assign_rows(self.raw.slot_rows(slot, n), n, slot=slot)
+            return
         lens = torch.zeros(self.n_slots, dtype=torch.int32, device=self.device)
         lens[slot] = n
         x = x.contiguous()
@@ -1237,6 +1338,17 @@ class DeltaInputCacheMHA(CacheBackend):
     def _decode(self, x, weights, acc, lens):
         max_len = int(self.n_tokens.max())
         x = x.contiguous()
+        if self.passthrough:
+            self.raw.append(x, lens)
+            if self.is_base and not self.seeds_accumulator:
+                return
+            if not self.is_base and not acc.seeded:
+                raise UsageError("accumulator used before the base layer seeded it")
+            if self.is_base:
+                acc.release_prefill()
+            acc.row64.copy_(x.double())  # acc at the new token = x
+            acc.assign_rows(self.raw.slots_view(), max_len)
+            return
         if self.is_base and not self.seeds_accumulator:
             self.stream.append_token_rows(x, lens)
             return
@@ -1246,14 +1358,27 @@ class DeltaInputCacheMHA(CacheBackend):
             acc.release_prefill()
         # the new token's delta against the float64 accumulator row (cache.py:473-481)
         self.stream.append_token_rows_cl(x, lens, acc.row64, seed=self.is_base)
+        if not self.is_base and acc.x_hat is None:
+            # acc += deq(deltas) waits for this layer's fused decode launch, which
+            # does it in its first K pass (settle() otherwise)
+            acc.settle()
+            acc.pending = (self, lens.clone(), max_len)
+            return
         self._accumulate(acc, self.is_base, max_len, lens)
 
     def _prefill_kv(self, weights, acc, slot, n):
-        a = self._rows16(self.stream, slot, n) if self.is_base else acc.x16[slot, :n]
+        acc.settle()
+        if self.passthrough:
+            a = self.raw.slot_rows(slot, n)
+        else:
+            a = self._rows16(self.stream, slot, n) if self.is_base else acc.x16[slot, :n]
         return self._kv_from(a, a, weights.w_k, weights.w_v, n)
 
     def _rematerialize(self, weights, acc, slot, n):
         wk, wv = weights.f32("w_k"), weights.f32("w_v")
+        if self.passthrough:
+            return self._remat_f32(N.A_F16_ROWS, self.raw.rows, None, None, 0, 16, 0, N.A_SAME,
+                                   None, None, 0, 0, self.d, wk, wv, slot, n)
         if self.is_base:
             s = self.stream
             return self._remat_f32(N.A_CODES_TOKEN, s.codes, s.params, None, 0, s.bits,
@@ -1273,7 +1398,21 @@ class DeltaInputCacheMHA(CacheBackend):
         return torch.stack([e * c - o * s, e * s + o * c], dim=-1).view(n, -1), v
 
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
-        if self.is_base:
+        self.fused_accumulate = False
+        if (acc is not None and acc.pending is not None and acc.pending[0] is self
+                and not self.peer_outs and self._use_absorbed(self.d, max_len)):
+            acc.pending = None
+            self._attend_cl(q, weights, acc, lens, max_len, out)
+            self.fused_accumulate = True
+            return
+        if acc is not None:
+            acc.settle()
+        if self.passthrough:
+            spec = (("mha", N.A_F16_ROWS, 16), N.A_F16_ROWS, 16, N.A_SAME, 16, weights.w_k,
+                    weights.w_v)
+            self._fused(N.A_F16_ROWS, self.raw.rows, None, None, None, 16, 0, N.A_SAME, None, None,
+                        0, 0, self.d, spec, weights, 1, q, lens, max_len, out, tpc)
+        elif self.is_base:
             s = self.stream
             spec = (("mha", N.A_CODES_TOKEN, s.bits), N.A_CODES_TOKEN, s.bits, N.A_SAME, s.bits,
                     weights.w_k, weights.w_v)
@@ -1286,8 +1425,24 @@ class DeltaInputCacheMHA(CacheBackend):
             self._fused(N.A_F16_ROWS, acc.x16, None, None, None, 16, 0, N.A_SAME, None, None, 0,
                         0, self.d, spec, weights, 1, q, lens, max_len, out, tpc)
 
+    def _attend_cl(self, q, weights, acc, lens, max_len, out):
+        """Delta layer: the accumulate (acc += deq(this layer's deltas), cache.py:472-481,
+        139-146) fused into the first K pass of the decode kernel, which then
+        rematerialises from the updated rows (cache.py:527-535)."""
+        s = self.stream
+        spec = (("mha", N.A_F16_ROWS, 16), N.A_F16_ROWS, 16, N.A_SAME, 16, weights.w_k, weights.w_v)
+        key, mk, bk, mv, bv, wk, wv = spec
+        wk_arr, wv_arr = weights.arranged_absorbed(key, mk, bk, mv, bv, wk, wv)
+        rope = rope_table_t(max_len, self.device)
+        nbytes = N.lib.xq_absorbed_workspace_bytes(self.n_slots, max_len, self.n_kv, self.d)
+        ws = _scratch(self.device, nbytes)
+        N.call("xq_decode_attend_absorbed_cl", N.ptr(acc.x16), N.ptr(s.codes), N.ptr(s.params), s.bits,
+               s.row_bytes, self.group_size, self.L, self.d, N.ptr(lens), self.n_slots, max_len,
+               N.ptr(wk_arr), N.ptr(wv_arr), self.n_kv, N.ptr(q), N.ptr(rope), rope.shape[1] // 2,
+               1.0 / math.sqrt(HEAD_DIM), N.ptr(ws), nbytes, N.ptr(out), N.stream_of(self.device))
+
     def memory_bytes(self):
-        return self.stream.nbytes()
+        return (self.raw if self.passthrough else self.stream).nbytes()
 
 
 class DeltaLatentCacheGQA(CacheBackend):
@@ -1317,18 +1472,29 @@ class DeltaLatentCacheGQA(CacheBackend):
         super().__init__(*a, **kw)
         if self.policy.base_layers < 1:
             raise ConfigError("cross-layer variants need at least one base layer")
-        if self.bits == 16:
-            raise ConfigError("xq-cl-gqa on the B200 path needs a quantized width (2/3/4/8)")
         kv_width = self.d // self.g
         if 2 * kv_width > self.d:  # model.py:135-142: the shared subspace only when 2*kvw <= d
             raise ConfigError("xq-cl-gqa needs a shared K/V subspace (2*kv_width <= hidden_dim)")
         self.rank = 2 * kv_width
         self.kv_width = kv_width
+        self.rec_pos = torch.zeros(self.n_slots, dtype=torch.int32, device=self.device)
+        self.passthrough = self.bits == 16
+        if self.passthrough:
+            # 16 bits: the latent rows are kept raw (quant.py:117-118) as fp16, the
+            # remat operand; the new token's float64 latent lives in a one-row
+            # buffer per slot (row 0), which the accumulator row update reads
+            self.raw = RawRows(self.rank, self.n_slots, self.L, self.device)
+            self.lat64 = torch.zeros((self.n_slots, 1, self.rank), dtype=torch.float64,
+                                     device=self.device)
+            self.lat32 = torch.zeros((self.n_slots, 1, self.rank), dtype=torch.float32,
+                                     device=self.device)
+            self.pos_m1 = torch.zeros(self.n_slots, dtype=torch.int32, device=self.device)
+            self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+            return
         # latents formed and quantized in float64 like the reference's (a base-layer
         # code flip is a full quantization step, large against later deltas)
         self.stream = PackedStream(self.bits, CHANNEL, self.rank, self.group_size, self.n_slots,
                                    self.L, self.device, resid_f64=True)
-        self.rec_pos = torch.zeros(self.n_slots, dtype=torch.int32, device=self.device)
 
     @property
     def is_base(self):
@@ -1374,7 +1540,7 @@ class DeltaLatentCacheGQA(CacheBackend):
             n = int(self.n_tokens[s])
             if n == 0:
                 continue
-            rec = self._rows16(self.stream, s, n)
+            rec = self.raw.slot_rows(s, n) if self.passthrough else self._rows16(self.stream, s, n)
             c = acc.x16[s]
             N.call("xq_gemm_f16", N.ptr(rec), rec.stride(0), N.ptr(u16), u16.stride(0), N.ptr(c),
                    c.stride(0), n, self.d, self.rank, 0 if seed else 2, None, 0, 0,
@@ -1402,7 +1568,6 @@ class DeltaLatentCacheGQA(CacheBackend):
     def _prefill(self, slot, x, weights, acc):
         self._sub(weights)
         n = x.shape[0]
-        st = self.stream
         xf = x.double()
         if not self.is_base:
             if not acc.seeded:
@@ -1410,6 +1575,20 @@ class DeltaLatentCacheGQA(CacheBackend):
             xf = xf - acc.prefill_rows(slot, n, seed=False)  # cache.py:574-577 (delta = x - acc)
         u64 = self._u64(weights)
         lat = (xf @ u64).contiguous()
+        if self.passthrough:
+            self.raw.fill(lat, slot)
+            self.n_tokens[slot] = n
+            if self.is_base and not self.seeds_accumulator:
+                return
+            rows = acc.prefill_rows(slot, n, seed=self.is_base)
+            upd = lat @ u64.t()
+            if self.is_base:
+                rows.copy_(upd)
+            else:
+                rows += upd
+            self._acc16(acc, weights, [slot], seed=self.is_base)
+            return
+        st = self.stream
         g = st.g
         n_full = n // g * g
         if n_full:  # whole groups: codes + their float64 reconstruction in place of lat
@@ -1435,13 +1614,16 @@ class DeltaLatentCacheGQA(CacheBackend):
 
     def _decode(self, x, weights, acc, lens):
         self._sub(weights)
-        st = self.stream
         if not self.is_base and not acc.seeded:
             raise UsageError("accumulator used before the base layer seeded it")
         if self.is_base:
             acc.release_prefill()
         u, udt = self._u(weights)
         x = x.contiguous()
+        if self.passthrough:
+            self._decode16(x, u, udt, acc, lens, weights)
+            return
+        st = self.stream
         pos = (self.n_tokens - 1 - st.n_flushed).astype(np.int32)  # before this step's flush
         N.call("xq_clgqa_latent64", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.d,
                None if self.is_base else N.ptr(acc.row64), N.ptr(u), udt, self.rank, N.ptr(lens),
@@ -1452,6 +1634,24 @@ class DeltaLatentCacheGQA(CacheBackend):
             return
         self.rec_pos.copy_(torch.from_numpy(pos))
         N.call("xq_clgqa_row_update", N.ptr(st.resid64), N.ptr(self.rec_pos), self.n_slots, st.g,
+               N.ptr(u), udt, self.d, self.rank, 1 if self.is_base else 0, N.ptr(acc.row64),
+               N.stream_of(self.device))
+        self._acc16(acc, weights, range(self.n_slots), seed=self.is_base)
+
+    def _decode16(self, x, u, udt, acc, lens, weights):
+        """16-bit decode: the float64 latent (x - acc_row) @ U of the new token into
+        row 0 of the one-row buffers (nflushed = len-1 puts it there), stored raw as
+        fp16; the accumulator row and the fp16 remat operand as for coded layers."""
+        torch.sub(lens, 1, out=self.pos_m1)
+        N.call("xq_clgqa_latent64", N.ptr(x), _dtype_code(x), x.stride(0), x.shape[0], self.d,
+               None if self.is_base else N.ptr(acc.row64), N.ptr(u), udt, self.rank, N.ptr(lens),
+               N.ptr(self.pos_m1), 1, N.ptr(self.lat64), N.ptr(self.lat32), N.ptr(self.flag),
+               N.stream_of(self.device))
+        self.raw.append(self.lat32[:, 0], lens)
+        if self.is_base and not self.seeds_accumulator:
+            return
+        self.rec_pos.zero_()
+        N.call("xq_clgqa_row_update", N.ptr(self.lat64), N.ptr(self.rec_pos), self.n_slots, 1,
                N.ptr(u), udt, self.d, self.rank, 1 if self.is_base else 0, N.ptr(acc.row64),
                N.stream_of(self.device))
         self._acc16(acc, weights, range(self.n_slots), seed=self.is_base)
@@ -1467,7 +1667,7 @@ class DeltaLatentCacheGQA(CacheBackend):
     def _prefill_kv(self, weights, acc, slot, n):
         _, fused = self._sub(weights)
         if self.is_base:
-            a = self._rows16(self.stream, slot, n)
+            a = self.raw.slot_rows(slot, n) if self.passthrough else self._rows16(self.stream, slot, n)
             return self._kv_from(a, a, fused[:, :self.kv_width], fused[:, self.kv_width:], n)
         wk, wv = self._w_delta(weights)
         a = acc.x16[slot, :n]
@@ -1475,6 +1675,10 @@ class DeltaLatentCacheGQA(CacheBackend):
 
     def _rematerialize(self, weights, acc, slot, n):
         _, fused = self._sub(weights)
+        if self.is_base and self.passthrough:
+            return self._remat_f32(N.A_F16_ROWS, self.raw.rows, None, None, 0, 16, 0, N.A_SAME, None,
+                                   None, 0, 0, self.rank, fused[:, :self.kv_width].contiguous(),
+                                   fused[:, self.kv_width:].contiguous(), slot, n)
         if self.is_base:
             s = self.stream
             return self._remat_f32(N.A_CODES_CHANNEL, s.codes, s.params, s.resid,
@@ -1490,9 +1694,15 @@ class DeltaLatentCacheGQA(CacheBackend):
     def _attend(self, q, weights, acc, lens, max_len, out, tpc):
         _, fused = self._sub(weights)
         if self.is_base:
-            s = self.stream
             fk = weights._cache.setdefault(("clgqa_fk", id(weights)), fused[:, :self.kv_width].contiguous())
             fv = weights._cache.setdefault(("clgqa_fv", id(weights)), fused[:, self.kv_width:].contiguous())
+            if self.passthrough:
+                spec = (("clgqa-base", 16), N.A_F16_ROWS, 16, N.A_SAME, 16, fk, fv)
+                self._fused(N.A_F16_ROWS, self.raw.rows, None, None, None, 16, 0, N.A_SAME, None, None,
+                            0, 0, self.rank, spec, weights, self.g, q, lens, max_len, out, tpc,
+                            force_absorbed=True)
+                return
+            s = self.stream
             spec = (("clgqa-base", s.bits), N.A_CODES_CHANNEL, s.bits, N.A_SAME, s.bits, fk, fv)
             self._fused(N.A_CODES_CHANNEL, s.codes, s.params, s.resid, s.nflushed_dev, s.bits,
                         s.row_bytes, N.A_SAME, None, None, 0, 0, self.rank, spec, weights, self.g,
@@ -1505,7 +1715,14 @@ class DeltaLatentCacheGQA(CacheBackend):
                         force_absorbed=True)
 
     def memory_bytes(self):
-        return self.stream.nbytes()
+        return (self.raw if self.passthrough else self.stream).nbytes()
+
+
+class QuantizedKvPassthrough(FullPrecisionCache):
+    """``kvq`` at 16 bits: K and V are kept raw (quant.py:117-118), which is the
+    fp16 baseline's cache (cache.py:326-360 with pass-through tensors)."""
+
+    variant = "kvq"
 
 
 _BACKENDS = {
@@ -1541,7 +1758,15 @@ def make_cache(variant: str, layer_index: int, policy: LayerPolicy, head_dim: in
         raise ConfigError(f"variant {variant!r} is not on the B200 hot path (next row)")
     if kw.get("hidden_dim") is None or kw.get("n_heads") is None:
         return ReferenceCache(variant, layer_index, policy, head_dim, group_size, **kw)
-    return _BACKENDS[variant](layer_index, policy, head_dim, group_size, **kw)
+    return backend_class(variant, policy.bits_for(layer_index))(layer_index, policy, head_dim,
+                                                                group_size, **kw)
+
+
+def backend_class(variant: str, bits: int):
+    """The backend of a variant at a layer's bit width (kvq at 16 bits keeps K/V raw)."""
+    if variant == "kvq" and bits == 16:
+        return QuantizedKvPassthrough
+    return _BACKENDS[variant]
 
 
 # ---------------------------------------------------------------------------
@@ -1676,7 +1901,7 @@ class ReferenceCache:
         kw.setdefault("max_len", DEFAULT_MAX_LEN)
         kw.setdefault("device", torch.device("cuda", torch.cuda.current_device()))
         kw.setdefault("exact", True)
-        self._inner = _BACKENDS[self.variant](self.layer_index, self.policy, self.head_dim,
+        self._inner = backend_class(self.variant, self.bits)(self.layer_index, self.policy, self.head_dim,
                                               self.group_size, hidden_dim=d,
                                               n_heads=d // HEAD_DIM, kv_group=d // kvw, **kw)
         if self._first_channel:

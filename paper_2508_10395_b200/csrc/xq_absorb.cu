@@ -114,6 +114,7 @@ struct Params {
   uint64_t w_hint;
   int32_t a_hint;   // fp16-row A: 0 evict-normal, 1 split (see the K-pass TMA loop), 2 evict-last
   int32_t a_split;  // split: chunks at the start of each sweep loaded evict-first
+  __half* acc_out;  // XQ_A_F16_ACC: the accumulator rows updated in the first K pass
   uint32_t off_p, off_codes, off_q, off_sc, off_rope, off_stg, off_bar;
 };
 
@@ -160,6 +161,49 @@ XQ_DEVINL void walk(const Params& p, int cluster, int n_clusters, KF&& kfn, VF&&
   }
 }
 
+// code m (natural channel order) of a row's 64-code chunk
+template <int BITS>
+XQ_DEVINL uint32_t code_at(const uint32_t (&w)[2 * BITS], int m) {
+  const int bit = m * BITS, wi = bit >> 5, sh = bit & 31;
+  uint32_t v = w[wi] >> sh;
+  if (sh + BITS > 32) v |= w[wi + 1] << (32 - sh);
+  return v & ((1u << BITS) - 1u);
+}
+
+// One producer thread's row of a 64-channel chunk of the XQuant-CL accumulator:
+// acc = fp16(float(acc) + code * scale + zp) (the arithmetic of k_cl_accumulate_w,
+// xq_quant.cu), in place in the TMA-staged SWIZZLE_128B A stage and written back
+// to the accumulator row in global memory (gdst: 64 fp16, 16-byte aligned).
+template <int BITS>
+XQ_DEVINL void acc_update_chunk(uint32_t tile, const RowSwizzle& sw, uint32_t crow, __half2 sz,
+                                __half* gdst) {
+  uint32_t raw[2 * BITS];
+  lds_raw<BITS>(crow, raw);
+  const float2 f = __half22float2(sz);
+  const float2 s2 = make_float2(f.x, f.x), z2 = make_float2(f.y, f.y);
+  const float2 m2 = make_float2(-8388608.f, -8388608.f);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {  // 16-byte chunk c: channels 8c .. 8c+7
+    const uint4 old = lds128(tile + sw.off[c]);
+    uint32_t hw[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // float(code) exactly as 2^23 + code - 2^23; then the scalar form's roundings,
+      // two lanes at a time: fmaf(code, s, z), old + v, fp16
+      const float2 cf = __fadd2_rn(
+          make_float2(__uint_as_float(0x4B000000u | code_at<BITS>(raw, 8 * c + 2 * j)),
+                      __uint_as_float(0x4B000000u | code_at<BITS>(raw, 8 * c + 2 * j + 1))),
+          m2);
+      const float2 v = __ffma2_rn(cf, s2, z2);
+      hw[j] = as_u32(__float22half2_rn(__fadd2_rn(__half22float2(from_u32<__half2>(hw[j])), v)));
+    }
+    sts128(tile + sw.off[c], hw[0], hw[1], hw[2], hw[3]);
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(gdst + 8 * c), "r"(hw[0]),
+                 "r"(hw[1]), "r"(hw[2]), "r"(hw[3])
+                 : "memory");
+  }
+}
+
 template <int AK, int AV, int BITS, int GROUP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_decode_absorbed(const __grid_constant__ CUtensorMap tmap_w,
@@ -168,8 +212,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmap_va,
                       const __grid_constant__ CUtensorMap tmap_vp,
                       const __grid_constant__ CUtensorMap tmap_o, const Params p) {
+  // PROD: the dequant producers arrive on every A stage (they fill it, or, with ACC,
+  // update it in the first K pass and only arrive afterwards); TMA_A: the fp16 A
+  // rows come by TMA (all passes without producers, the later passes with ACC)
+  constexpr bool ACC = AK == XQ_A_F16_ACC;
   constexpr bool PROD = AK != XQ_A_F16_ROWS;
+  constexpr bool TMA_A = !PROD || ACC;
   static_assert((AK == XQ_A_F16_ROWS) == (AV == XQ_A_F16_ROWS), "fp16 rows feed both sides or neither");
+  static_assert((AK == XQ_A_F16_ACC) == (AV == XQ_A_F16_ACC) && (!ACC || GROUP == 1),
+                "the fused CL accumulate feeds both sides of an MHA layer");
   static_assert(AV != XQ_A_CODES_CHANNEL || AK == XQ_A_CODES_CHANNEL,
                 "a per-channel V side shares the K side's stream (xq-cl-gqa base layers)");
 
@@ -196,7 +247,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* pready = tempty + 2;
   uint64_t* xfull = pready + 1;
   uint64_t* xread = xfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xread + 1);
+  uint64_t* afull = xread + 1;          // ACC: old accumulator rows landed (per A stage)
+  uint64_t* accw = afull + kMaxStages;  // ACC: both CTAs' updated rows are in global memory
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accw + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -207,6 +260,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const long long prof_t0 = clock64();
 #endif
   using CF = Cfg<GROUP>;
+  // grouped-query scores as mma.sync products (4 query heads per KV head fill half
+  // of an n8 tile); MHA keeps per-row FFMA2 dot products
+  constexpr bool kMmaScores = GROUP == 4;
   constexpr int STAGES = CF::kStages;
   constexpr int KH = CF::KH;
   constexpr uint32_t kABStage = CF::kABStage;
@@ -234,6 +290,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbar_init(pready, 8);   // leader's: 4 epilogue warps per CTA
     mbar_init(xfull, 128);  // the peer's 128 epilogue threads (their scores landed here)
     mbar_init(xread, 128);  // the peer's 128 epilogue threads (they read out their landing rows)
+    for (int s = 0; s < kMaxStages; ++s) mbar_init(&afull[s], 1);
+    mbar_init(accw, 2 * 256);  // every producer thread (8 warps) of both CTAs, once per tile
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -264,31 +322,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr bool PIPE = Cfg<GROUP>::NBUF == 2;  // see walk(): overlap tile k+1's first K pass with tile k's softmax
   if (warp == 0) {
     // ------------------------------------------------ TMA: W_k halves (+ fp16 A rows)
-    uint32_t it = 0;
+    uint32_t it = 0, tk = 0;  // tk: tiles whose updated accumulator rows were awaited (ACC)
     walk<PIPE>(p, cluster, n_clusters,
       [&](const Tile& tl, int ps) {
         const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
+        // ACC: the first K pass gets its A stages from the producers; later passes
+        // read the rows they wrote back, once both CTAs' producers are done
+        const bool a_tma = TMA_A && !(ACC && ps == 0);
+        if (ACC && ps == 1) mbar_wait_cluster(accw, (tk++) & 1u);
         // fp16 A rows: odd passes walk the channel chunks backwards, so a pass
         // starts on the chunks the previous one read last (still in L2). The
         // 74 clusters' 2 MB tiles exceed L2, and a forward-only walk re-reads
         // every pass from HBM. The MMA accumulates in issue order, so only the
         // fp32 summation order changes. Code-fed passes keep the forward order
         // (the producers' chunk mapping; their codes tiles fit L2).
-        const bool rev = !PROD && kSerpentine && (ps & 1);
+        const bool rev = TMA_A && kSerpentine && (ps & 1);
         for (int kc = 0; kc < nkc; ++kc, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           const int kcc = rev ? nkc - 1 - kc : kc;
           XQ_PROF(0, mbar_wait(&empty[s], ph ^ 1));
           if (elect_one()) {
             uint8_t* st = sAB + s * kABStage;
-            constexpr uint32_t kTx = 2 * (kBBytes + (PROD ? 0u : kABytes));
+            const uint32_t kTx = 2 * (kBBytes + (a_tma ? kABytes : 0u));
             if (leader) mbar_arrive_expect_tx(&full[s], kTx);
             else mbar_arrive_remote(full_leader0 + 8 * s);
 #pragma unroll
             for (int sub = 0; sub < KH / 2; ++sub)  // KV head KH*ps + 2*sub + rank
               tma_load_2d_pair(st + kABytes + sub * kBSub, &tmap_w, &full[s], kcc * kChunk,
                                (KH * ps + 2 * sub + static_cast<int>(rank)) * 128, p.w_hint);
-            if constexpr (!PROD)
+            if (a_tma)
               // split: the first half of a sweep is the part the previous
               // sweep left in L2 (demote it), the second half is what the next
               // sweep reads first (keep it)
@@ -301,13 +363,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       },
       [&](const Tile& tl) {
         const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
+        if (ACC && p.n_pass == 1) mbar_wait_cluster(accw, (tk++) & 1u);
       for (int bb = 0; bb < nblk; ++bb) {
         for (int j = 0; j < 4; ++j, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           XQ_PROF(0, mbar_wait(&empty[s], ph ^ 1));
           if (elect_one()) {
             uint8_t* st = sAB + s * kABStage;
-            if constexpr (PROD) {
+            if constexpr (!TMA_A) {
               if (leader) mbar_arrive(&full[s]);
               else mbar_arrive_remote(full_leader0 + 8 * s);
             } else {
@@ -397,7 +460,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 2) {
     // ------------------------------------------------ TMA: codes ring
-    if constexpr (PROD) {
+    if constexpr (ACC) {
+      // first K pass of each tile: per 128-channel group the delta codes + (scale, zp)
+      // quads (codes ring) and, into the two A stages of the group, this CTA's old
+      // accumulator rows (signalled locally: the producers update them in place)
+      uint32_t ci = 0, cphase = 0, it = 0;
+      // the stage uses of the later passes and the V side are waited on too, in
+      // order: a parity wait only tells phases apart one apart, so skipping ahead to
+      // the next tile's first pass could match a phase two behind (and load into a
+      // stage still in use)
+      auto follow = [&](int n_uses) {
+        for (int u = 0; u < n_uses; ++u, ++it) mbar_wait(&empty[it % STAGES], ((it / STAGES) & 1) ^ 1);
+      };
+      walk<PIPE>(p, cluster, n_clusters,
+        [&](const Tile& tl, int ps) {
+          if (ps != 0) {
+            follow(nkc);
+            return;
+          }
+          const int32_t arow = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM) +
+                               static_cast<int32_t>(rank) * kTileM;
+          // the old rows and the codes come from HBM and the A ring is only STAGES
+          // deep: L2 prefetches kAccPf groups ahead keep the stage loads L2 hits
+          constexpr int kAccPf = 4;
+          auto prefetch = [&](int g) {
+            if (g < ngrp && elect_one()) {
+              tma_prefetch_l2_2d(&tmap_ka, (2 * g) * kChunk, arow);
+              tma_prefetch_l2_2d(&tmap_ka, (2 * g + 1) * kChunk, arow);
+              tma_prefetch_l2_2d(&tmap_kp, g * 16 * BITS, arow);
+            }
+            __syncwarp();
+          };
+          for (int g = 0; g < kAccPf; ++g) prefetch(g);
+          for (int g = 0; g < ngrp; ++g) {
+            prefetch(g + kAccPf);
+            const uint32_t cs = ci, cph = cphase;
+            if (++ci == static_cast<uint32_t>(CSTAGES)) {
+              ci = 0;
+              cphase ^= 1u;
+            }
+            XQ_PROF(5, mbar_wait(&cempty[cs], cph ^ 1));
+            if (elect_one()) {
+              uint8_t* st = sC + cs * p.cstage_bytes;
+              mbar_arrive_expect_tx(&cfull[cs], p.k_tx);
+              tma_load_2d(st, &tmap_kp, &cfull[cs], g * 16 * BITS, arow, kEvictFirst);
+              tma_load_2d(st + p.k_code_bytes, &tmap_vp, &cfull[cs], 4 * (g & ~3), arow, kEvictFirst);
+            }
+            __syncwarp();
+            for (int h = 0; h < 2; ++h, ++it) {
+              const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+              mbar_wait(&empty[s], ph ^ 1);
+              if (elect_one()) {
+                mbar_arrive_expect_tx(&afull[s], kABytes);
+                tma_load_2d(sAB + s * kABStage, &tmap_ka, &afull[s], (2 * g + h) * kChunk, arow,
+                            kEvictFirst);
+              }
+              __syncwarp();
+            }
+          }
+        },
+        [&](const Tile&) { follow(nkc); });
+    } else if constexpr (PROD) {
       uint32_t ci = 0, cphase = 0;  // ring slot / phase of the next codes stage
       auto next_slot = [&](uint32_t& cs, uint32_t& cph) {
         cs = ci;
@@ -453,7 +576,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
     // ------------------------------------------------ dequant producers
-    if constexpr (PROD) {
+    if constexpr (ACC) {
+      // XQuant-CL accumulate in the first K pass: each thread owns token row r of
+      // this CTA's 128; group gp handles the 128-channel groups g == gp (mod 2),
+      // i.e. A-stage uses u with (u / 2) % 2 == gp in every pass and on the V side
+      const int gp = (warp - kProdWarp0) >> 2;
+      const int r = ((warp - kProdWarp0) & 3) * 32 + lane;
+      const RowSwizzle sw(r);
+      const uint32_t sAB_a = smem_u32(sAB), sC_a = smem_u32(sC);
+      const uint32_t accw_l = mapa_shared(smem_u32(accw), rank);
+      const uint32_t accw_p = mapa_shared(smem_u32(accw), rank ^ 1u);
+      uint32_t ci = 0, cphase = 0;  // codes ring (stages alternate between the groups)
+      uint32_t it = 0;              // A-stage uses, both groups
+      uint32_t apar = 0;            // bit s: parity of stage s's next afull phase
+      auto arrive_full = [&](uint32_t s) {
+        if (leader) mbar_arrive_if(&full[s], lane == 0);
+        else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
+      };
+      auto pass_through = [&](int n_uses) {  // TMA-fed stages: arrive once each is free
+        for (int u = 0; u < n_uses; ++u, ++it) {
+          if (((u >> 1) & 1) != gp) continue;
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
+          arrive_full(s);
+        }
+      };
+      walk<PIPE>(p, cluster, n_clusters,
+        [&](const Tile& tl, int ps) {
+          if (ps != 0) {
+            pass_through(nkc);
+            return;
+          }
+          const int tok = tl.t * kPairM + static_cast<int>(rank) * kTileM + r;
+          const bool valid = tok < tl.len;
+          __half* grow = p.acc_out + ((int64_t)tl.b * p.L_max + tok) * p.kdim;
+          for (int g = 0; g < ngrp; ++g) {
+            const uint32_t cs = ci, cph = cphase;
+            if (++ci == static_cast<uint32_t>(CSTAGES)) {
+              ci = 0;
+              cphase ^= 1u;
+            }
+            const bool mine = (g & 1) == gp;
+            const uint32_t cst = sC_a + cs * p.cstage_bytes;
+            if (mine) XQ_PROF(6, mbar_wait(&cfull[cs], cph));
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h, ++it) {
+              const uint32_t s = it % STAGES;
+              const uint32_t aph = (apar >> s) & 1u;
+              apar ^= 1u << s;
+              if (!mine) continue;
+              XQ_PROF(7, mbar_wait(&afull[s], aph));
+              if (valid) {
+                const int kc = 2 * g + h;
+                const __half2 sz = from_u32<__half2>(lds32(cst + p.k_code_bytes + r * 16 + 4 * (g & 3)));
+                acc_update_chunk<BITS>(sAB_a + s * kABStage, sw, cst + r * (16 * BITS) + h * 8 * BITS,
+                                       sz, grow + kc * kChunk);
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
+              arrive_full(s);
+            }
+            if (mine) mbar_arrive_if(&cempty[cs], lane == 0);
+          }
+          // the updated rows, visible to the TMA loads of the later passes and of the
+          // peer's V side (async proxy) before the arrivals both CTAs' warp 0 wait on
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          mbar_arrive_remote_release(accw_l);
+          mbar_arrive_remote_release(accw_p);
+        },
+        [&](const Tile&) { pass_through(nkc); });
+    } else if constexpr (PROD) {
       const int gp = (warp - kProdWarp0) >> 2;
       const int r = ((warp - kProdWarp0) & 3) * 32 + lane;
       const RowSwizzle sw_k(r);       // K side: row = token r of this CTA's 128
@@ -546,9 +738,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t q_a = smem_u32(q_s), sc_a = smem_u32(sc_s);
     const uint32_t land_a = sc_a + 4u * (peer * nbh) * kTileM;  // rows of the peer's heads
     const uint32_t ro_a = smem_u32(rope_off), rb_a = smem_u32(rope_base);
-    // offsets table: cos/sin(r0*theta_j), r0 < 16 (table positions 0..15)
+    // offsets table: cos/sin(r0*theta_j), r0 < 16 (table positions 0..15); [64 j][16 r0]
+    // for the per-row FFMA scores, [16 r0][64 j] for the mma fragments (pairs of j)
     for (int i = et; i < 64 * 16; i += 128)
-      rope_off[i] = p.rope[(int64_t)(i >> 4) * p.rope_n + (i & 15)];
+      rope_off[i] = kMmaScores ? p.rope[(int64_t)(i & 63) * p.rope_n + (i >> 6)]
+                               : p.rope[(int64_t)(i >> 4) * p.rope_n + (i & 15)];
     const int r0 = row & 15, r1 = row >> 4;
     const uint32_t stg_a = smem_u32(smem + p.off_stg);
     uint32_t tc = 0, ti = 0;
@@ -563,7 +757,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int64_t tp = (int64_t)t * kPairM + rank * kTileM + 16 * (i >> 6);
         rope_base[i] = p.rope[(int64_t)(i & 63) * p.rope_n + (tp < p.rope_n ? tp : 0)];
       }
-      {
+      if constexpr (kMmaScores) {
+        // q as the B fragments of mma m16n8k16 (n = the KV head's query heads, 4 of
+        // 8 used; k = split RoPE dims), fp16: entry (kvh, kk, lane) = {b0b1, b2b3}
+        // of k16 block kk, rotated to len-1 and scaled here
+        const int n_ent = p.n_kv * 8 * 32;
+        for (int i = et; i < n_ent; i += 128) {
+          const int ln = i & 31, kk = (i >> 5) & 7, kvh = i >> 8;
+          const int g = ln >> 2, tig = ln & 3;
+          uint32_t b01 = 0u, b23 = 0u;
+          if (g < GROUP) {
+            const float* qp = p.q_pre + ((int64_t)b * p.n_q + kvh * GROUP + g) * kHeadDim;
+            const int j0 = (kk & 3) * 16 + 2 * tig;  // frequency of split dim kk*16 + 2*tig
+            const bool odd = kk >= 4;                // dims 64.. hold the second of each pair
+            auto rot2 = [&](int j) {                 // split dims (j, j+1) of this half
+              const float4 e = *reinterpret_cast<const float4*>(qp + 2 * j);
+              const float2 c0 = p.rope[(int64_t)j * p.rope_n + pos];
+              const float2 c1 = p.rope[(int64_t)(j + 1) * p.rope_n + pos];
+              const float r0 = odd ? (e.x * c0.y + e.y * c0.x) : (e.x * c0.x - e.y * c0.y);
+              const float r1 = odd ? (e.z * c1.y + e.w * c1.x) : (e.z * c1.x - e.w * c1.y);
+              return as_u32(__floats2half2_rn(r0 * p.q_scale, r1 * p.q_scale));
+            };
+            b01 = rot2(j0);
+            b23 = rot2(j0 + 8);
+          }
+          sts64(q_a + 8u * i, b01, b23);
+        }
+      } else {
         const float2 cs = p.rope[(int64_t)(et >> 1) * p.rope_n + pos];
         for (int h = 0; h < p.n_q; ++h) {
           const float* qp = p.q_pre + ((int64_t)b * p.n_q + h) * kHeadDim;
@@ -595,6 +815,97 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const long long pt_k = clock64();
 #endif
         tc_fence_after();
+        if constexpr (kMmaScores) {
+          // Grouped-query scores on the tensor cores: per m16 tile of this warp's 32
+          // token rows, K is read from TMEM in the mma fragment order (16x256b),
+          // rotated in registers (FFMA2, cos/sin by angle addition), rounded to fp16
+          // as the A fragments, and multiplied with the q fragments (n = the 4 query
+          // heads of the KV head): 16 mma.sync per KV head and warp replace the
+          // 4 x 128 FFMA2 and the q loads of the per-row form.
+          const int g = lane >> 2, tig = lane & 3;
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const uint32_t lane_addr = static_cast<uint32_t>(ew * 32 + 16 * mt) << 16;
+            const int r1m = 2 * ew + mt;
+            float acc[KH][4];
+#pragma unroll
+            for (int kh = 0; kh < KH; ++kh)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[kh][i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              // cos/sin of rows (g, g+8) x frequencies 16c + 2*tig + {0, 1, 8, 9}, in the
+              // fragment register order: i -> row (i & 2 ? g+8 : g), j + (i & 1) + (i & 4 ? 8 : 0)
+              float2 cs8[8];
+              {
+                const int j0 = 16 * c + 2 * tig;
+                const float4 b0 = lds_f4(rb_a + 8u * (r1m * 64 + j0));
+                const float4 b1 = lds_f4(rb_a + 8u * (r1m * 64 + j0 + 8));
+                const float4 o00 = lds_f4(ro_a + 8u * (g * 64 + j0));
+                const float4 o01 = lds_f4(ro_a + 8u * (g * 64 + j0 + 8));
+                const float4 o10 = lds_f4(ro_a + 8u * ((g + 8) * 64 + j0));
+                const float4 o11 = lds_f4(ro_a + 8u * ((g + 8) * 64 + j0 + 8));
+                auto cmul = [](float bx, float by, float ox, float oy) {
+                  return make_float2(bx * ox - by * oy, by * ox + bx * oy);
+                };
+                cs8[0] = cmul(b0.x, b0.y, o00.x, o00.y);
+                cs8[1] = cmul(b0.z, b0.w, o00.z, o00.w);
+                cs8[2] = cmul(b0.x, b0.y, o10.x, o10.y);
+                cs8[3] = cmul(b0.z, b0.w, o10.z, o10.w);
+                cs8[4] = cmul(b1.x, b1.y, o01.x, o01.y);
+                cs8[5] = cmul(b1.z, b1.w, o01.z, o01.w);
+                cs8[6] = cmul(b1.x, b1.y, o11.x, o11.y);
+                cs8[7] = cmul(b1.z, b1.w, o11.z, o11.w);
+              }
+#pragma unroll
+              for (int kh = 0; kh < KH; ++kh) {
+                const int kvh = KH * ps + kh;
+                if (kvh < p.n_kv) {
+                  uint32_t ek[8], ok[8];
+                  tmem_ld16x256b_x2(tmem + lane_addr + a * 256 + kh * 128 + c * 16, ek);
+                  tmem_ld16x256b_x2(tmem + lane_addr + a * 256 + kh * 128 + 64 + c * 16, ok);
+                  tmem_wait_ld();
+                  uint32_t are[4], aro[4];
+#pragma unroll
+                  for (int q2 = 0; q2 < 4; ++q2) {  // RoPE (linalg.py:92-93) of two values
+                    const float2 e = make_float2(__uint_as_float(ek[2 * q2]),
+                                                 __uint_as_float(ek[2 * q2 + 1]));
+                    const float2 o = make_float2(__uint_as_float(ok[2 * q2]),
+                                                 __uint_as_float(ok[2 * q2 + 1]));
+                    const float2 cv = make_float2(cs8[2 * q2].x, cs8[2 * q2 + 1].x);
+                    const float2 sv = make_float2(cs8[2 * q2].y, cs8[2 * q2 + 1].y);
+                    const float2 nsv = make_float2(-sv.x, -sv.y);
+                    const float2 re = __ffma2_rn(e, cv, __fmul2_rn(o, nsv));
+                    const float2 ro = __ffma2_rn(e, sv, __fmul2_rn(o, cv));
+                    are[q2] = as_u32(__float22half2_rn(re));
+                    aro[q2] = as_u32(__float22half2_rn(ro));
+                  }
+                  const uint2 qe = lds64(q_a + 8u * ((kvh * 8 + c) * 32 + lane));
+                  const uint2 qo = lds64(q_a + 8u * ((kvh * 8 + 4 + c) * 32 + lane));
+                  mma_16816_f16(acc[kh], are, qe.x, qe.y);
+                  mma_16816_f16(acc[kh], aro, qo.x, qo.y);
+                }
+              }
+            }
+            // D fragment: (row g, heads 2tig, 2tig+1), (row g+8, the same heads)
+            const int rowa = ew * 32 + 16 * mt + g;
+            const int toka = t * kPairM + static_cast<int>(rank) * kTileM + rowa;
+            const bool va = toka < len, vb = toka + 8 < len;
+            if (2 * tig < GROUP) {
+#pragma unroll
+              for (int kh = 0; kh < KH; ++kh) {
+                const int kvh = KH * ps + kh;
+                if (kvh < p.n_kv) {
+                  const uint32_t s0 = sc_a + 4u * ((kvh * GROUP + 2 * tig) * kTileM + rowa);
+                  sts_f32(s0, va ? acc[kh][0] : -INFINITY);
+                  sts_f32(s0 + 4u * kTileM, va ? acc[kh][1] : -INFINITY);
+                  sts_f32(s0 + 32u, vb ? acc[kh][2] : -INFINITY);
+                  sts_f32(s0 + 4u * kTileM + 32u, vb ? acc[kh][3] : -INFINITY);
+                }
+              }
+            }
+          }
+        } else {
         // K columns of a head come split (W_k rows arranged so): cols 0-63 hold
         // the first element of each RoPE pair, cols 64-127 the second, so
         // pairs of frequencies map to register pairs and the rotation + dot
@@ -660,6 +971,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                       valid ? sc[kh][gi].x + sc[kh][gi].y : -INFINITY);
           }
         }
+        }  // per-row FFMA scores
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -1099,7 +1411,9 @@ template <int AK, int AV, int BITS, int GROUP>
 int plan_smem(Params& p, size_t& total) {
   constexpr bool PROD = AK != XQ_A_F16_ROWS;
   const uint32_t k_code = PROD ? 128u * 16u * BITS : 0u;
-  const uint32_t k_par = AK == XQ_A_CODES_TOKEN ? 128u * 16u : (AK == XQ_A_CODES_CHANNEL ? 512u : 0u);
+  const uint32_t k_par = (AK == XQ_A_CODES_TOKEN || AK == XQ_A_F16_ACC)
+                             ? 128u * 16u
+                             : (AK == XQ_A_CODES_CHANNEL ? 512u : 0u);
   const uint32_t v_par = AV == XQ_A_CODES_TOKEN ? 128u * 16u : (AV == XQ_A_CODES_CHANNEL ? 512u : 0u);
   p.k_code_bytes = k_code;
   p.k_tx = k_code + k_par;
@@ -1115,11 +1429,11 @@ int plan_smem(Params& p, size_t& total) {
   const uint32_t qp = PIPE ? (512u * p.n_q + 1023u) / 1024u * 1024u
                            : ((512u * (p.n_q > p.nbh ? p.n_q : p.nbh)) + 1023u) / 1024u * 1024u;
   const uint32_t pbytes = PIPE ? (512u * p.nbh + 1023u) / 1024u * 1024u : 0u;
-  const uint32_t stg = PIPE ? 512u * p.n_q : 0u;
+  const uint32_t stg = PIPE ? 256u * p.n_q : 0u;  // one fp16 [n_q x 128] O block
   const uint32_t fixed = qp + pbytes + stg                  // q / P (+ P, staging)
                          + 512u * p.nb                      // scores (+ the peer's, exchanged)
                          + (64 * 16 + 8 * 64) * 8           // RoPE offset + base tables
-                         + (4 * kMaxStages + 7) * 8 + 16;   // barriers + tmem slot
+                         + (5 * kMaxStages + 8) * 8 + 16;   // barriers + tmem slot
   const uint32_t budget = 227u * 1024u - 1024u;
   using CF = Cfg<GROUP>;
   const int stages = CF::kStages;
@@ -1165,6 +1479,27 @@ int dispatch_bits(int bits, const Maps& m, const Params& p, cudaStream_t st) {
     case 8: return launch<AK, AV, 8, GROUP>(m, p, st);
     default: return fail(XQ_ECONFIG, "unsupported bits %d", bits);
   }
+}
+
+// k_absorb_combine + k_absorb_project after a k_decode_absorbed launch
+int merge_and_project(const Params& p, const int32_t* seq_lens, int group,
+                      const void* wv_arranged, const OutPtrs& op, cudaStream_t st) {
+  int status;
+  const int n_seqs = p.n_seqs, n_q = p.n_q;
+  const int64_t kdim = p.kdim;
+  float* x_attn = reinterpret_cast<float*>(p.part_ml + (int64_t)n_seqs * p.n_tiles * n_q);
+  k_absorb_combine<<<dim3(n_seqs * n_q, static_cast<unsigned>((kdim + 511) / 512)), 128,
+                     p.n_tiles * sizeof(float), st>>>(p.part_o, p.part_ml, seq_lens, p.n_tiles,
+                                                      n_q, p.kdim, x_attn);
+  if ((status = check_launch("k_absorb_combine")) != XQ_OK) return status;
+  const size_t psmem = 8 * (size_t)kdim * sizeof(float);
+  // (dynamic; the kernel's 17 KB static reduction buffer comes on top)
+  if ((status = ensure_smem(reinterpret_cast<const void*>(k_absorb_project), psmem,
+                            "cudaFuncSetAttribute(project)")) != XQ_OK)
+    return status;
+  k_absorb_project<<<dim3(n_q, 4, (n_seqs + 7) / 8), 256, psmem, st>>>(
+      x_attn, n_seqs, n_q, group, p.kdim, static_cast<const __half*>(wv_arranged), op);
+  return check_launch("k_absorb_project");
 }
 
 }  // namespace
@@ -1281,9 +1616,12 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
                XQ_ECONFIG, "shared A operand must be CODES_TOKEN, CODES_CHANNEL or F16_ROWS");
     XQ_REQUIRE(ak_mode != XQ_A_CODES_CHANNEL || L_max % group_size == 0, XQ_ECONFIG,
                "per-channel A operand needs L_max % 128 == 0");
+  } else if (ak_mode == XQ_A_F16_ROWS) {  // 16-bit xq-gqa: raw K / V latent rows
+    XQ_REQUIRE(av_mode == XQ_A_F16_ROWS, XQ_ECONFIG,
+               "split fp16-row K latent needs an fp16-row V latent");
   } else {
     XQ_REQUIRE(ak_mode == XQ_A_CODES_CHANNEL && av_mode == XQ_A_CODES_TOKEN, XQ_ECONFIG,
-               "split K/V A operands support (CODES_CHANNEL, CODES_TOKEN) only");
+               "split K/V A operands support (CODES_CHANNEL, CODES_TOKEN) or (F16_ROWS, F16_ROWS)");
     XQ_REQUIRE(ak_bits == av_bits, XQ_ECONFIG, "K and V latent bits must match");
     XQ_REQUIRE(L_max % group_size == 0, XQ_ECONFIG, "per-channel K latent needs L_max % 128 == 0");
   }
@@ -1307,7 +1645,7 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
                       (uint64_t)n_seqs * n_tiles * n_q, 128, static_cast<uint32_t>(n_q),
                       CU_TENSOR_MAP_SWIZZLE_NONE, "O partials")) != XQ_OK)
     return st_;
-  Params p;
+  Params p{};
   p.k_resid = ak_resid;
   XQ_REQUIRE(ak_first == nullptr || (ak_mode == XQ_A_CODES_CHANNEL && !mha), XQ_ECONFIG,
              "the full-precision first channel applies to the per-channel K latent (xq-gqa)");
@@ -1360,6 +1698,13 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
         default: return fail(XQ_ECONFIG, "unsupported query group %d (1, 2, 4)", group);
       }
     }
+  } else if (ak_mode == XQ_A_F16_ROWS) {  // K passes read tmap_ka, the V side tmap_va
+    switch (group) {
+      case 1: status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 1>(maps, p, st); break;
+      case 2: status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 2>(maps, p, st); break;
+      case 4: status = launch<XQ_A_F16_ROWS, XQ_A_F16_ROWS, 4, 4>(maps, p, st); break;
+      default: return fail(XQ_ECONFIG, "unsupported GQA group %d (1, 2, 4)", group);
+    }
   } else {
     switch (group) {
       case 1: status = dispatch_bits<XQ_A_CODES_CHANNEL, XQ_A_CODES_TOKEN, 1>(ak_bits, maps, p, st); break;
@@ -1369,19 +1714,89 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
     }
   }
   if (status != XQ_OK) return status;
-  float* x_attn = reinterpret_cast<float*>(p.part_ml + (int64_t)n_seqs * p.n_tiles * n_q);
-  k_absorb_combine<<<dim3(n_seqs * n_q, static_cast<unsigned>((kdim + 511) / 512)), 128,
-                     p.n_tiles * sizeof(float), st>>>(p.part_o, p.part_ml, seq_lens, p.n_tiles,
-                                                      n_q, p.kdim, x_attn);
-  if ((status = check_launch("k_absorb_combine")) != XQ_OK) return status;
-  const size_t psmem = 8 * (size_t)kdim * sizeof(float);
-  // (dynamic; the kernel's 17 KB static reduction buffer comes on top)
-  if ((status = ensure_smem(reinterpret_cast<const void*>(k_absorb_project), psmem,
-                            "cudaFuncSetAttribute(project)")) != XQ_OK)
-    return status;
-  k_absorb_project<<<dim3(n_q, 4, (n_seqs + 7) / 8), 256, psmem, st>>>(
-      x_attn, n_seqs, n_q, group, p.kdim, static_cast<const __half*>(wv_arranged), op);
-  return check_launch("k_absorb_project");
+  return merge_and_project(p, seq_lens, group, wv_arranged, op, st);
+}
+
+int xq_decode_attend_absorbed_cl(void* acc16, const void* codes, const void* params, int32_t bits,
+                                 int64_t row_bytes, int32_t group_size, int64_t L_max,
+                                 int64_t kdim, const int32_t* seq_lens, int32_t n_seqs,
+                                 int32_t max_len, const void* wk_arranged,
+                                 const void* wv_arranged, int32_t n_kv_heads, const float* q_pre,
+                                 const void* rope_cs, int64_t rope_n, float sm_scale,
+                                 void* workspace, int64_t workspace_bytes, float* out,
+                                 void* stream) {
+  XQ_REQUIRE(acc16 && codes && params && out, XQ_EUSAGE, "null argument");
+  XQ_REQUIRE(rope_n >= max_len, XQ_ESHAPE, "rope table shorter than max_len");
+  XQ_REQUIRE(kdim % 256 == 0 && kdim >= 256, XQ_ESHAPE,
+             "kdim must be a positive multiple of 256, got %lld", (long long)kdim);
+  XQ_REQUIRE(group_size == kG, XQ_ECONFIG,
+             "the fused kernel is specialised for group_size 128 (the reference default), got %d",
+             group_size);
+  XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bad bits %d", bits);
+  XQ_REQUIRE(n_seqs >= 1 && n_kv_heads >= 1, XQ_ESHAPE, "empty batch");
+  XQ_REQUIRE(max_len <= L_max && max_len >= 1, XQ_ESHAPE, "max_len out of range");
+  const int n_q = n_kv_heads;
+  XQ_REQUIRE(n_q <= kMaxHeads, XQ_ECONFIG, "at most %d query heads per launch, got %d", kMaxHeads, n_q);
+  XQ_REQUIRE(workspace_bytes >= xq_absorbed_workspace_bytes(n_seqs, max_len, n_q, kdim), XQ_ESHAPE,
+             "workspace too small");
+  const int64_t w_rows = (int64_t)(n_kv_heads + 3) / 4 * 512;
+  const int64_t arena_rows = (int64_t)n_seqs * L_max;
+  Maps maps;
+  int st_;
+  // ka / va: the accumulator rows (K-pass and V-side boxes); kp / vp: the delta
+  // codes and their (scale, zp) quads (per-token stream maps)
+  if ((st_ = make_map(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wk_arranged, kdim,
+                      (uint64_t)w_rows, kChunk, 128, CU_TENSOR_MAP_SWIZZLE_128B, "W_k")) != XQ_OK)
+    return st_;
+  if ((st_ = stream_maps(XQ_A_F16_ROWS, 16, acc16, nullptr, 0, kdim, group_size, arena_rows, 128,
+                         &maps.ka, &maps.kp)) != XQ_OK)
+    return st_;
+  if ((st_ = stream_maps(XQ_A_F16_ROWS, 16, acc16, nullptr, 0, kdim, group_size, arena_rows, 64,
+                         &maps.va, &maps.vp)) != XQ_OK)
+    return st_;
+  if ((st_ = stream_maps(XQ_A_CODES_TOKEN, bits, codes, params, row_bytes, kdim, group_size,
+                         arena_rows, 128, &maps.kp, &maps.vp)) != XQ_OK)
+    return st_;
+  const int64_t n_tiles = n_tiles_for(max_len);
+  if ((st_ = make_map(&maps.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, workspace, kdim,
+                      (uint64_t)n_seqs * n_tiles * n_q, 128, static_cast<uint32_t>(n_q),
+                      CU_TENSOR_MAP_SWIZZLE_NONE, "O partials")) != XQ_OK)
+    return st_;
+  Params p{};
+  p.kdim = static_cast<int32_t>(kdim);
+  p.L_max = L_max;
+  p.seq_lens = seq_lens;
+  p.n_seqs = n_seqs;
+  p.n_tiles = static_cast<int32_t>(n_tiles);
+  p.n_units = n_seqs * p.n_tiles;
+  p.n_kv = n_kv_heads;
+  p.n_q = n_q;
+  p.nb = nb_for(n_q);
+  p.nbh = p.nb / 2;
+  p.q_pre = q_pre;
+  p.rope = static_cast<const float2*>(rope_cs);
+  p.rope_n = rope_n;
+  p.q_scale = sm_scale * 1.4426950408889634f;
+  float* ws = static_cast<float*>(workspace);
+  p.part_o = reinterpret_cast<__half*>(ws);
+  p.part_ml = reinterpret_cast<float2*>(ws + (int64_t)n_seqs * p.n_tiles * n_q * kdim);
+  p.w_hint = kEvictLast;
+  p.a_hint = 1;  // the later passes' fp16 rows: the split L2 policy of the F16 path
+  p.a_split = (p.kdim / kChunk) / 2;
+  p.acc_out = static_cast<__half*>(acc16);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int status;
+  switch (bits) {
+    case 2: status = launch<XQ_A_F16_ACC, XQ_A_F16_ACC, 2, 1>(maps, p, st); break;
+    case 3: status = launch<XQ_A_F16_ACC, XQ_A_F16_ACC, 3, 1>(maps, p, st); break;
+    case 4: status = launch<XQ_A_F16_ACC, XQ_A_F16_ACC, 4, 1>(maps, p, st); break;
+    default: status = launch<XQ_A_F16_ACC, XQ_A_F16_ACC, 8, 1>(maps, p, st); break;
+  }
+  if (status != XQ_OK) return status;
+  OutPtrs op{};
+  op.n = 1;
+  op.p[0] = out;
+  return merge_and_project(p, seq_lens, 1, wv_arranged, op, st);
 }
 
 }  // extern "C"

@@ -54,7 +54,8 @@ XQ_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins == (1u << 26)) {
-      printf("xq: mbarrier wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      printf("xq: mbarrier wait timeout block %d thread %d bar 0x%x parity %u\n", blockIdx.x,
+             threadIdx.x, smem_u32(bar), parity);
       __trap();
     }
   }
@@ -108,7 +109,8 @@ XQ_DEVINL void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait_cluster(bar, parity)) {
     if (++spins == (1u << 26)) {
-      printf("xq: cluster mbarrier wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      printf("xq: cluster mbarrier wait timeout block %d thread %d bar 0x%x parity %u\n",
+             blockIdx.x, threadIdx.x, smem_u32(bar), parity);
       __trap();
     }
   }
@@ -195,6 +197,13 @@ XQ_DEVINL void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
       : "memory");
+}
+// L2 prefetch of one TMA box (no shared-memory destination, no completion)
+XQ_DEVINL void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 // Bulk tensor store shared -> global (bulk-group completion)
 XQ_DEVINL void tma_store_2d(const CUtensorMap* map, uint32_t smem_src, int32_t c0, int32_t c1) {
@@ -328,6 +337,30 @@ XQ_DEVINL void tmem_ld16(uint32_t taddr, float (&v)[16]) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr)
       : "memory");
+}
+
+// 16 lanes x 16 columns in the mma.sync m16n8 fragment order (two 16x256b
+// blocks): thread t gets r0,r1 = lane t/4, cols 2(t%4), +1; r2,r3 = lane 8+t/4,
+// the same cols; r4..r7 = the same for cols 8.. (tools/tmem_layout_probe.cu).
+XQ_DEVINL void tmem_ld16x256b_x2(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+
+// D(16x8 fp32) += A(16x16 fp16, row) * B(16x8 fp16, col)
+XQ_DEVINL void mma_16816_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+XQ_DEVINL void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
 
 // Store to the same-offset shared variable of another CTA of the cluster

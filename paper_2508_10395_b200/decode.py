@@ -242,6 +242,8 @@ class Decoder:
         if self.variant == "xq-cl-mha":
             base = cache.layer_index < self.policy.base_layers
             seed = cache.layer_index == self.policy.base_layers - 1
+            if getattr(cache, "fused_accumulate", False):
+                return 1 + attend  # the delta accumulate ran inside the fused launch
             return 1 + attend + (0 if base and not seed else 1)
         return 1 + attend  # quantize
 

@@ -77,8 +77,9 @@ def device_backends(monkeypatch):
 
 
 @pytest.mark.parametrize("variant,bits", [
-    ("xq-mha", 4), ("xq-mha", 3), ("xq-mha", 16), ("fp16", 16), ("kvq", 4),
-    ("xq-cl-mha", 4), ("xq-cl-mha", 2), ("xq-gqa", 4), ("xq-gqa", 3), ("xq-cl-gqa", 4)])
+    ("xq-mha", 4), ("xq-mha", 3), ("xq-mha", 16), ("fp16", 16), ("kvq", 4), ("kvq", 16),
+    ("xq-cl-mha", 4), ("xq-cl-mha", 2), ("xq-cl-mha", 16), ("xq-gqa", 4), ("xq-gqa", 3),
+    ("xq-gqa", 16), ("xq-cl-gqa", 4), ("xq-cl-gqa", 16)])
 def test_reference_session_on_device_backends(variant, bits, request):
     model = _model(gqa=variant in ("xq-gqa", "xq-cl-gqa"))
     ref, _ = _session_logits(model, variant, bits)

@@ -16,6 +16,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# where the summaries go (on the GPU box: a directory under gpurun_out/ that travels back)
+OUT = os.environ.get("PROFILE_OUT", os.path.join(ROOT, "profiles"))
 
 
 def launches(src, tag, cfg):
@@ -40,9 +42,9 @@ def launches(src, tag, cfg):
              f"{'total_ms':>10} {'share':>6} {'count':>6}  kernel"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"{v[1] / 1e3:10.3f} {100 * v[1] / tot:5.1f}% {v[0]:6d}  {k}")
-    out = os.path.join(ROOT, "profiles", f"{tag}_launch_shares.txt")
+    out = os.path.join(OUT, f"{tag}_launch_shares.txt")
     open(out, "w").write("\n".join(lines) + "\n")
-    shutil.copy(src, os.path.join(ROOT, "profiles", f"{tag}_launches.csv"))
+    shutil.copy(src, os.path.join(OUT, f"{tag}_launches.csv"))
     print("\n".join(lines[:12]))
 
 
@@ -99,7 +101,7 @@ def kernel(rep, tag, key, cfg):
                          capture_output=True, text=True).stdout
     lines.append("# hottest source lines (share of all warp-stall samples, top two stall reasons)")
     lines.extend(hot.rstrip().splitlines())
-    out = os.path.join(ROOT, "profiles", f"{tag}_decode_kernel.txt")
+    out = os.path.join(OUT, f"{tag}_decode_kernel.txt")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
@@ -109,7 +111,9 @@ def kernel(rep, tag, key, cfg):
 
     bscale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}
-    js_path = os.path.join(ROOT, "profiles", "decode_kernel_ncu.json")
+    js_path = os.path.join(OUT, "decode_kernel_ncu.json")
+    if not os.path.exists(js_path) and os.path.exists(os.path.join(ROOT, "profiles", "decode_kernel_ncu.json")):
+        shutil.copy(os.path.join(ROOT, "profiles", "decode_kernel_ncu.json"), js_path)
     js = json.load(open(js_path)) if os.path.exists(js_path) else {}
     js[key] = {
         "dram_bytes_per_launch": num("dram__bytes_read.sum", bscale) + num("dram__bytes_write.sum", bscale),
@@ -126,6 +130,6 @@ if __name__ == "__main__":
     # python tools/summarize_profiles.py gpurun_out r01 c2   (files of tools/profile_round.sh)
     src, tag = sys.argv[1], sys.argv[2]
     cfg = sys.argv[3] if len(sys.argv) > 3 else "c2"
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    os.makedirs(OUT, exist_ok=True)
     launches(os.path.join(src, f"launches_bench_{cfg}.csv"), f"{tag}_{cfg}", cfg)
     kernel(os.path.join(src, f"decode_full_{cfg}.ncu-rep"), f"{tag}_{cfg}", KEYS[cfg], cfg)
