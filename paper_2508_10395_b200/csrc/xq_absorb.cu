@@ -114,7 +114,12 @@ struct Params {
   uint64_t w_hint;
   int32_t a_hint;   // fp16-row A: 0 evict-normal, 1 split (see the K-pass TMA loop), 2 evict-last
   int32_t a_split;  // split: chunks at the start of each sweep loaded evict-first
-  __half* acc_out;  // XQ_A_F16_ACC: the accumulator rows updated in the first K pass
+  // XQ_A_F16_ACC: the accumulator rows (updated in place, one tile ahead of the
+  // passes that read them) and this layer's per-token delta codes
+  __half* acc_out;
+  const uint8_t* d_codes;
+  const __half2* d_params;
+  int64_t d_row_bytes, d_pstride;
   uint32_t off_p, off_codes, off_q, off_sc, off_rope, off_stg, off_bar;
 };
 
@@ -161,46 +166,60 @@ XQ_DEVINL void walk(const Params& p, int cluster, int n_clusters, KF&& kfn, VF&&
   }
 }
 
-// code m (natural channel order) of a row's 64-code chunk
+// One warp's accumulator row update: acc = fp16(float(acc) + code * scale + zp) for
+// every channel (the arithmetic of k_cl_accumulate_w in xq_quant.cu, bit-identical),
+// lane l taking channels 256k + 8l .. +7 (512 contiguous bytes per warp access).
 template <int BITS>
-XQ_DEVINL uint32_t code_at(const uint32_t (&w)[2 * BITS], int m) {
-  const int bit = m * BITS, wi = bit >> 5, sh = bit & 31;
-  uint32_t v = w[wi] >> sh;
-  if (sh + BITS > 32) v |= w[wi + 1] << (32 - sh);
-  return v & ((1u << BITS) - 1u);
-}
-
-// One producer thread's row of a 64-channel chunk of the XQuant-CL accumulator:
-// acc = fp16(float(acc) + code * scale + zp) (the arithmetic of k_cl_accumulate_w,
-// xq_quant.cu), in place in the TMA-staged SWIZZLE_128B A stage and written back
-// to the accumulator row in global memory (gdst: 64 fp16, 16-byte aligned).
-template <int BITS>
-XQ_DEVINL void acc_update_chunk(uint32_t tile, const RowSwizzle& sw, uint32_t crow, __half2 sz,
-                                __half* gdst) {
-  uint32_t raw[2 * BITS];
-  lds_raw<BITS>(crow, raw);
-  const float2 f = __half22float2(sz);
-  const float2 s2 = make_float2(f.x, f.x), z2 = make_float2(f.y, f.y);
-  const float2 m2 = make_float2(-8388608.f, -8388608.f);
+XQ_DEVINL void acc_update_row(__half* acc, const uint8_t* codes, const __half2* params, int kdim,
+                              int lane) {
+  constexpr uint32_t kMask = (1u << BITS) - 1u;
+  constexpr int kU = 4;  // 256-channel blocks in flight
+  for (int k0 = 0; k0 < kdim; k0 += 256 * kU) {
+    uint4 old[kU];
+    uint2 cw[kU];
+    __half2 sz[kU];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {  // 16-byte chunk c: channels 8c .. 8c+7
-    const uint4 old = lds128(tile + sw.off[c]);
-    uint32_t hw[4] = {old.x, old.y, old.z, old.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      // float(code) exactly as 2^23 + code - 2^23; then the scalar form's roundings,
-      // two lanes at a time: fmaf(code, s, z), old + v, fp16
-      const float2 cf = __fadd2_rn(
-          make_float2(__uint_as_float(0x4B000000u | code_at<BITS>(raw, 8 * c + 2 * j)),
-                      __uint_as_float(0x4B000000u | code_at<BITS>(raw, 8 * c + 2 * j + 1))),
-          m2);
-      const float2 v = __ffma2_rn(cf, s2, z2);
-      hw[j] = as_u32(__float22half2_rn(__fadd2_rn(__half22float2(from_u32<__half2>(hw[j])), v)));
+    for (int k = 0; k < kU; ++k) {
+      const int c0 = k0 + 256 * k + 8 * lane;
+      if (c0 >= kdim) continue;
+      old[k] = *reinterpret_cast<const uint4*>(acc + c0);
+      const uint8_t* cp = codes + c0 * BITS / 8;
+      if constexpr (BITS == 3) {  // 3 bytes at any alignment: one or two aligned words
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(cp) & ~uintptr_t(3));
+        const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(cp) & 3u);
+        const uint32_t lo = __ldg(wp), hi = sh >= 2u ? __ldg(wp + 1) : 0u;
+        cw[k] = make_uint2(__funnelshift_r(lo, hi, 8u * sh), 0u);
+      } else if constexpr (BITS == 2) {
+        cw[k] = make_uint2(__ldg(reinterpret_cast<const unsigned short*>(cp)), 0u);
+      } else if constexpr (BITS == 4) {
+        cw[k] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(cp)), 0u);
+      } else {
+        cw[k] = __ldg(reinterpret_cast<const uint2*>(cp));
+      }
+      sz[k] = __ldg(params + c0 / kG);
     }
-    sts128(tile + sw.off[c], hw[0], hw[1], hw[2], hw[3]);
-    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(gdst + 8 * c), "r"(hw[0]),
-                 "r"(hw[1]), "r"(hw[2]), "r"(hw[3])
-                 : "memory");
+#pragma unroll
+    for (int k = 0; k < kU; ++k) {
+      const int c0 = k0 + 256 * k + 8 * lane;
+      if (c0 >= kdim) continue;
+      const float2 f = __half22float2(sz[k]);
+      uint32_t hw[4] = {old[k].x, old[k].y, old[k].z, old[k].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = 2 * j + e;
+          const uint32_t word = (BITS == 8 && m >= 4) ? cw[k].y : cw[k].x;
+          v[e] = fmaf(static_cast<float>((word >> ((m * BITS) % 32)) & kMask), f.x, f.y);
+        }
+        const float2 o = __half22float2(from_u32<__half2>(hw[j]));
+        hw[j] = as_u32(__floats2half2_rn(o.x + v[0], o.y + v[1]));
+      }
+      asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(acc + c0), "r"(hw[0]),
+                   "r"(hw[1]), "r"(hw[2]), "r"(hw[3])
+                   : "memory");
+    }
   }
 }
 
@@ -212,12 +231,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmap_va,
                       const __grid_constant__ CUtensorMap tmap_vp,
                       const __grid_constant__ CUtensorMap tmap_o, const Params p) {
-  // PROD: the dequant producers arrive on every A stage (they fill it, or, with ACC,
-  // update it in the first K pass and only arrive afterwards); TMA_A: the fp16 A
-  // rows come by TMA (all passes without producers, the later passes with ACC)
+  // PROD: dequant producers fill every A stage from packed codes; otherwise the fp16
+  // A rows come by TMA. ACC: the producer warps instead update the accumulator rows
+  // of the cluster's next tile in global memory while the current tile's passes run
   constexpr bool ACC = AK == XQ_A_F16_ACC;
-  constexpr bool PROD = AK != XQ_A_F16_ROWS;
-  constexpr bool TMA_A = !PROD || ACC;
+  constexpr bool PROD = AK != XQ_A_F16_ROWS && !ACC;
+  constexpr bool TMA_A = !PROD;
   static_assert((AK == XQ_A_F16_ROWS) == (AV == XQ_A_F16_ROWS), "fp16 rows feed both sides or neither");
   static_assert((AK == XQ_A_F16_ACC) == (AV == XQ_A_F16_ACC) && (!ACC || GROUP == 1),
                 "the fused CL accumulate feeds both sides of an MHA layer");
@@ -247,9 +266,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* pready = tempty + 2;
   uint64_t* xfull = pready + 1;
   uint64_t* xread = xfull + 1;
-  uint64_t* afull = xread + 1;          // ACC: old accumulator rows landed (per A stage)
-  uint64_t* accw = afull + kMaxStages;  // ACC: both CTAs' updated rows are in global memory
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accw + 1);
+  uint64_t* accw = xread + 1;   // ACC: both CTAs' rows of the next tile are updated
+  uint64_t* tstart = accw + 1;  // ACC: warp 0 started a tile (the producers may go on)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tstart + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -290,8 +309,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mbar_init(pready, 8);   // leader's: 4 epilogue warps per CTA
     mbar_init(xfull, 128);  // the peer's 128 epilogue threads (their scores landed here)
     mbar_init(xread, 128);  // the peer's 128 epilogue threads (they read out their landing rows)
-    for (int s = 0; s < kMaxStages; ++s) mbar_init(&afull[s], 1);
     mbar_init(accw, 2 * 256);  // every producer thread (8 warps) of both CTAs, once per tile
+    mbar_init(tstart, 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -326,10 +345,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     walk<PIPE>(p, cluster, n_clusters,
       [&](const Tile& tl, int ps) {
         const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
-        // ACC: the first K pass gets its A stages from the producers; later passes
-        // read the rows they wrote back, once both CTAs' producers are done
-        const bool a_tma = TMA_A && !(ACC && ps == 0);
-        if (ACC && ps == 1) mbar_wait_cluster(accw, (tk++) & 1u);
+        // ACC: the tile's rows are read once both CTAs' producers have updated them
+        const bool a_tma = TMA_A;
+        if (ACC && ps == 0) {
+          mbar_wait_cluster(accw, (tk++) & 1u);
+          if (elect_one()) mbar_arrive(tstart);
+          __syncwarp();
+        }
         // fp16 A rows: odd passes walk the channel chunks backwards, so a pass
         // starts on the chunks the previous one read last (still in L2). The
         // 74 clusters' 2 MB tiles exceed L2, and a forward-only walk re-reads
@@ -363,7 +385,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       },
       [&](const Tile& tl) {
         const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
-        if (ACC && p.n_pass == 1) mbar_wait_cluster(accw, (tk++) & 1u);
       for (int bb = 0; bb < nblk; ++bb) {
         for (int j = 0; j < 4; ++j, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
@@ -460,67 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 2) {
     // ------------------------------------------------ TMA: codes ring
-    if constexpr (ACC) {
-      // first K pass of each tile: per 128-channel group the delta codes + (scale, zp)
-      // quads (codes ring) and, into the two A stages of the group, this CTA's old
-      // accumulator rows (signalled locally: the producers update them in place)
-      uint32_t ci = 0, cphase = 0, it = 0;
-      // the stage uses of the later passes and the V side are waited on too, in
-      // order: a parity wait only tells phases apart one apart, so skipping ahead to
-      // the next tile's first pass could match a phase two behind (and load into a
-      // stage still in use)
-      auto follow = [&](int n_uses) {
-        for (int u = 0; u < n_uses; ++u, ++it) mbar_wait(&empty[it % STAGES], ((it / STAGES) & 1) ^ 1);
-      };
-      walk<PIPE>(p, cluster, n_clusters,
-        [&](const Tile& tl, int ps) {
-          if (ps != 0) {
-            follow(nkc);
-            return;
-          }
-          const int32_t arow = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM) +
-                               static_cast<int32_t>(rank) * kTileM;
-          // the old rows and the codes come from HBM and the A ring is only STAGES
-          // deep: L2 prefetches kAccPf groups ahead keep the stage loads L2 hits
-          constexpr int kAccPf = 4;
-          auto prefetch = [&](int g) {
-            if (g < ngrp && elect_one()) {
-              tma_prefetch_l2_2d(&tmap_ka, (2 * g) * kChunk, arow);
-              tma_prefetch_l2_2d(&tmap_ka, (2 * g + 1) * kChunk, arow);
-              tma_prefetch_l2_2d(&tmap_kp, g * 16 * BITS, arow);
-            }
-            __syncwarp();
-          };
-          for (int g = 0; g < kAccPf; ++g) prefetch(g);
-          for (int g = 0; g < ngrp; ++g) {
-            prefetch(g + kAccPf);
-            const uint32_t cs = ci, cph = cphase;
-            if (++ci == static_cast<uint32_t>(CSTAGES)) {
-              ci = 0;
-              cphase ^= 1u;
-            }
-            XQ_PROF(5, mbar_wait(&cempty[cs], cph ^ 1));
-            if (elect_one()) {
-              uint8_t* st = sC + cs * p.cstage_bytes;
-              mbar_arrive_expect_tx(&cfull[cs], p.k_tx);
-              tma_load_2d(st, &tmap_kp, &cfull[cs], g * 16 * BITS, arow, kEvictFirst);
-              tma_load_2d(st + p.k_code_bytes, &tmap_vp, &cfull[cs], 4 * (g & ~3), arow, kEvictFirst);
-            }
-            __syncwarp();
-            for (int h = 0; h < 2; ++h, ++it) {
-              const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-              mbar_wait(&empty[s], ph ^ 1);
-              if (elect_one()) {
-                mbar_arrive_expect_tx(&afull[s], kABytes);
-                tma_load_2d(sAB + s * kABStage, &tmap_ka, &afull[s], (2 * g + h) * kChunk, arow,
-                            kEvictFirst);
-              }
-              __syncwarp();
-            }
-          }
-        },
-        [&](const Tile&) { follow(nkc); });
-    } else if constexpr (PROD) {
+    if constexpr (PROD) {
       uint32_t ci = 0, cphase = 0;  // ring slot / phase of the next codes stage
       auto next_slot = [&](uint32_t& cs, uint32_t& cph) {
         cs = ci;
@@ -577,74 +538,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
     // ------------------------------------------------ dequant producers
     if constexpr (ACC) {
-      // XQuant-CL accumulate in the first K pass: each thread owns token row r of
-      // this CTA's 128; group gp handles the 128-channel groups g == gp (mod 2),
-      // i.e. A-stage uses u with (u / 2) % 2 == gp in every pass and on the V side
-      const int gp = (warp - kProdWarp0) >> 2;
-      const int r = ((warp - kProdWarp0) & 3) * 32 + lane;
-      const RowSwizzle sw(r);
-      const uint32_t sAB_a = smem_u32(sAB), sC_a = smem_u32(sC);
+      // XQuant-CL accumulate (cache.py:472-481, Accumulator.add cache.py:139-146),
+      // one tile ahead: the cluster's first tile is updated before anything reads
+      // it; tile i+1 while warp 0 and the tensor cores work on tile i (its rows are
+      // disjoint). Warp w takes rows w, w+8, .. of this CTA's 128 and walks each
+      // row 256 channels at a time (lane: 8 channels, 16-byte coalesced accesses).
+      const int pw = warp - kProdWarp0;
       const uint32_t accw_l = mapa_shared(smem_u32(accw), rank);
       const uint32_t accw_p = mapa_shared(smem_u32(accw), rank ^ 1u);
-      uint32_t ci = 0, cphase = 0;  // codes ring (stages alternate between the groups)
-      uint32_t it = 0;              // A-stage uses, both groups
-      uint32_t apar = 0;            // bit s: parity of stage s's next afull phase
-      auto arrive_full = [&](uint32_t s) {
-        if (leader) mbar_arrive_if(&full[s], lane == 0);
-        else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
-      };
-      auto pass_through = [&](int n_uses) {  // TMA-fed stages: arrive once each is free
-        for (int u = 0; u < n_uses; ++u, ++it) {
-          if (((u >> 1) & 1) != gp) continue;
-          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
-          XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
-          arrive_full(s);
-        }
-      };
-      walk<PIPE>(p, cluster, n_clusters,
-        [&](const Tile& tl, int ps) {
-          if (ps != 0) {
-            pass_through(nkc);
-            return;
-          }
+      uint32_t ti = 0;
+      for (int u = cluster; u < p.n_units; u += n_clusters) {
+        Tile tl;
+        if (!get_unit(p, u, tl.b, tl.t, tl.len)) continue;
+        if (ti > 0) mbar_wait(tstart, (ti - 1) & 1u);  // tile ti-1 is under way
+        for (int r = pw; r < kTileM; r += 8) {
           const int tok = tl.t * kPairM + static_cast<int>(rank) * kTileM + r;
-          const bool valid = tok < tl.len;
-          __half* grow = p.acc_out + ((int64_t)tl.b * p.L_max + tok) * p.kdim;
-          for (int g = 0; g < ngrp; ++g) {
-            const uint32_t cs = ci, cph = cphase;
-            if (++ci == static_cast<uint32_t>(CSTAGES)) {
-              ci = 0;
-              cphase ^= 1u;
-            }
-            const bool mine = (g & 1) == gp;
-            const uint32_t cst = sC_a + cs * p.cstage_bytes;
-            if (mine) XQ_PROF(6, mbar_wait(&cfull[cs], cph));
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h, ++it) {
-              const uint32_t s = it % STAGES;
-              const uint32_t aph = (apar >> s) & 1u;
-              apar ^= 1u << s;
-              if (!mine) continue;
-              XQ_PROF(7, mbar_wait(&afull[s], aph));
-              if (valid) {
-                const int kc = 2 * g + h;
-                const __half2 sz = from_u32<__half2>(lds32(cst + p.k_code_bytes + r * 16 + 4 * (g & 3)));
-                acc_update_chunk<BITS>(sAB_a + s * kABStage, sw, cst + r * (16 * BITS) + h * 8 * BITS,
-                                       sz, grow + kc * kChunk);
-              }
-              fence_proxy_async_smem();
-              __syncwarp();
-              arrive_full(s);
-            }
-            if (mine) mbar_arrive_if(&cempty[cs], lane == 0);
-          }
-          // the updated rows, visible to the TMA loads of the later passes and of the
-          // peer's V side (async proxy) before the arrivals both CTAs' warp 0 wait on
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          mbar_arrive_remote_release(accw_l);
-          mbar_arrive_remote_release(accw_p);
-        },
-        [&](const Tile&) { pass_through(nkc); });
+          if (tok >= tl.len) break;
+          const int64_t row = (int64_t)tl.b * p.L_max + tok;
+          acc_update_row<BITS>(p.acc_out + row * p.kdim, p.d_codes + row * p.d_row_bytes,
+                               p.d_params + row * p.d_pstride, p.kdim, lane);
+        }
+        // the updated rows, visible to the TMA loads of both CTAs (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        mbar_arrive_remote_release(accw_l);
+        mbar_arrive_remote_release(accw_p);
+        ++ti;
+      }
     } else if constexpr (PROD) {
       const int gp = (warp - kProdWarp0) >> 2;
       const int r = ((warp - kProdWarp0) & 3) * 32 + lane;
@@ -1409,11 +1328,9 @@ int64_t n_tiles_for(int32_t max_len) {
 // Shared-memory plan: [AB ring][P][codes ring][q][scores][peer scores][barriers]
 template <int AK, int AV, int BITS, int GROUP>
 int plan_smem(Params& p, size_t& total) {
-  constexpr bool PROD = AK != XQ_A_F16_ROWS;
+  constexpr bool PROD = AK != XQ_A_F16_ROWS && AK != XQ_A_F16_ACC;  // codes-ring modes
   const uint32_t k_code = PROD ? 128u * 16u * BITS : 0u;
-  const uint32_t k_par = (AK == XQ_A_CODES_TOKEN || AK == XQ_A_F16_ACC)
-                             ? 128u * 16u
-                             : (AK == XQ_A_CODES_CHANNEL ? 512u : 0u);
+  const uint32_t k_par = AK == XQ_A_CODES_TOKEN ? 128u * 16u : (AK == XQ_A_CODES_CHANNEL ? 512u : 0u);
   const uint32_t v_par = AV == XQ_A_CODES_TOKEN ? 128u * 16u : (AV == XQ_A_CODES_CHANNEL ? 512u : 0u);
   p.k_code_bytes = k_code;
   p.k_tx = k_code + k_par;
@@ -1743,8 +1660,8 @@ int xq_decode_attend_absorbed_cl(void* acc16, const void* codes, const void* par
   const int64_t arena_rows = (int64_t)n_seqs * L_max;
   Maps maps;
   int st_;
-  // ka / va: the accumulator rows (K-pass and V-side boxes); kp / vp: the delta
-  // codes and their (scale, zp) quads (per-token stream maps)
+  // ka / va: the accumulator rows (K-pass and V-side boxes); the producer warps read
+  // the delta codes and their (scale, zp) directly
   if ((st_ = make_map(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, wk_arranged, kdim,
                       (uint64_t)w_rows, kChunk, 128, CU_TENSOR_MAP_SWIZZLE_128B, "W_k")) != XQ_OK)
     return st_;
@@ -1754,9 +1671,7 @@ int xq_decode_attend_absorbed_cl(void* acc16, const void* codes, const void* par
   if ((st_ = stream_maps(XQ_A_F16_ROWS, 16, acc16, nullptr, 0, kdim, group_size, arena_rows, 64,
                          &maps.va, &maps.vp)) != XQ_OK)
     return st_;
-  if ((st_ = stream_maps(XQ_A_CODES_TOKEN, bits, codes, params, row_bytes, kdim, group_size,
-                         arena_rows, 128, &maps.kp, &maps.vp)) != XQ_OK)
-    return st_;
+  XQ_REQUIRE(row_bytes == row_bytes_for(kdim, bits), XQ_ESHAPE, "row_bytes mismatch");
   const int64_t n_tiles = n_tiles_for(max_len);
   if ((st_ = make_map(&maps.o, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, workspace, kdim,
                       (uint64_t)n_seqs * n_tiles * n_q, 128, static_cast<uint32_t>(n_q),
@@ -1784,6 +1699,10 @@ int xq_decode_attend_absorbed_cl(void* acc16, const void* codes, const void* par
   p.a_hint = 1;  // the later passes' fp16 rows: the split L2 policy of the F16 path
   p.a_split = (p.kdim / kChunk) / 2;
   p.acc_out = static_cast<__half*>(acc16);
+  p.d_codes = static_cast<const uint8_t*>(codes);
+  p.d_params = static_cast<const __half2*>(params);
+  p.d_row_bytes = row_bytes;
+  p.d_pstride = param_stride(kdim, group_size);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int status;
   switch (bits) {
