@@ -590,7 +590,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       };
       // two A stages per codes stage; fill(tile address, h) writes stage h
-      auto stages2 = [&](auto&& fill) {
+      // two A stages per codes stage: once stage h is free, conv(st, h, v) converts
+      // it into registers and store(tile, h, v) writes it (measured: converting
+      // before the wait and releasing the codes stage early did not change C2/C4)
+      auto stages2 = [&](auto&& conv, auto&& store) {
         const uint32_t st = sC_a + cs * p.cstage_bytes;
         XQ_PROF(6, mbar_wait(&cfull[cs], cph));
 #pragma unroll 1
@@ -601,7 +604,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ph ^= 1u;
           }
           XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
-          fill(sAB_a + s * kABStage, st, h);
+          uint32_t v[32];
+          conv(st, h, v);
+          store(sAB_a + s * kABStage, h, v);
           fence_proxy_async_smem();
           __syncwarp();
           if (leader) mbar_arrive_if(&full[s], lane == 0);
@@ -615,29 +620,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
           const int tok_k = tl.t * kPairM + static_cast<int>(rank) * kTileM + r;
           for (int g = gp; g < ngrp; g += 2)
-            stages2([&](uint32_t tile, uint32_t st, int h) {
-              produce_chunk<AK, BITS>(tile, st, st + p.k_code_bytes, sw_k, r, tok_k < tl.len,
-                                      tok_k, tl.b, nfl, 2 * g + h,
-                                      p.k_first ? p.k_first + (int64_t)tl.b * p.L_max + tok_k : nullptr,
-                                      p.k_resid, p.kdim);
-            });
+            stages2(
+                [&](uint32_t st, int h, uint32_t(&v)[32]) {
+                  convert_chunk<AK, BITS>(st, st + p.k_code_bytes, r, tok_k < tl.len, tok_k, tl.b, nfl,
+                                          2 * g + h,
+                                          p.k_first ? p.k_first + (int64_t)tl.b * p.L_max + tok_k : nullptr,
+                                          p.k_resid, p.kdim, v);
+                },
+                [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_k.store(tile, v); });
         },
         [&](const Tile& tl) {
           const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
           for (int g = gp; g < ngrp; g += 2)
-            stages2([&](uint32_t tile, uint32_t st, int h) {
-              const int gv = (g & ~1) + static_cast<int>(rank);
-              const int crow = h * 64 + (r & 63);
-              const int tok = tl.t * kPairM + (g & 1) * kTileM + crow;
-              if constexpr (AV == XQ_A_CODES_TOKEN)
-                produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
-                                        tok < tl.len, tok, tl.b, 1 << 30, 2 * gv + hh, nullptr,
-                                        nullptr, p.kdim);
-              else if constexpr (AV == XQ_A_CODES_CHANNEL)  // same stream as the K side
-                produce_chunk<AV, BITS>(tile + hh * kMNHalf, st, st + 128 * 16 * BITS, sw_v, crow,
-                                        tok < tl.len, tok, tl.b, nfl, 2 * gv + hh, nullptr,
-                                        p.k_resid, p.kdim);
-            });
+            stages2(
+                [&](uint32_t st, int h, uint32_t(&v)[32]) {
+                  const int gv = (g & ~1) + static_cast<int>(rank);
+                  const int crow = h * 64 + (r & 63);
+                  const int tok = tl.t * kPairM + (g & 1) * kTileM + crow;
+                  if constexpr (AV == XQ_A_CODES_TOKEN)
+                    convert_chunk<AV, BITS>(st, st + 128 * 16 * BITS, crow, tok < tl.len, tok, tl.b,
+                                            1 << 30, 2 * gv + hh, nullptr, nullptr, p.kdim, v);
+                  else if constexpr (AV == XQ_A_CODES_CHANNEL)  // same stream as the K side
+                    convert_chunk<AV, BITS>(st, st + 128 * 16 * BITS, crow, tok < tl.len, tok, tl.b,
+                                            nfl, 2 * gv + hh, nullptr, p.k_resid, p.kdim, v);
+                },
+                [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_v.store(tile + hh * kMNHalf, v); });
         });
     }
   } else if (warp >= kEpiWarp0) {
@@ -781,9 +788,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int kvh = KH * ps + kh;
                 if (kvh < p.n_kv) {
                   uint32_t ek[8], ok[8];
+#ifdef XQ_EXP_NOSCORE  // timing experiment only: the epilogue without the K reads
+                  for (int i = 0; i < 8; ++i) ek[i] = ok[i] = 0u;
+#else
                   tmem_ld16x256b_x2(tmem + lane_addr + a * 256 + kh * 128 + c * 16, ek);
                   tmem_ld16x256b_x2(tmem + lane_addr + a * 256 + kh * 128 + 64 + c * 16, ok);
                   tmem_wait_ld();
+#endif
                   uint32_t are[4], aro[4];
 #pragma unroll
                   for (int q2 = 0; q2 < 4; ++q2) {  // RoPE (linalg.py:92-93) of two values

@@ -112,17 +112,20 @@ struct RowSwizzle {
   }
 };
 
-// One producer thread: convert its row's 64-channel chunk of one A stream.
-// tile / cstage / pstage are 32-bit shared addresses.
+// One producer thread: convert its row's 64-channel chunk of one A stream into 32
+// fp16 pairs in producer order (registers; the caller stores them once the A stage is
+// free, so the conversion overlaps the wait). cstage / pstage are 32-bit shared
+// addresses of the staged codes and parameters.
 template <int MODE, int BITS>
-XQ_DEVINL void produce_chunk(uint32_t tile, uint32_t cstage, uint32_t pstage, const RowSwizzle& sw,
-                             int row, bool valid, int tok, int b, int nflushed, int kc,
-                             const float* first_row, const float* resid, int kdim) {
-  uint32_t v[32];
+XQ_DEVINL void convert_chunk(uint32_t cstage, uint32_t pstage, int row, bool valid, int tok, int b,
+                             int nflushed, int kc, const float* first_row, const float* resid,
+                             int kdim, uint32_t (&v)[32]) {
+#ifdef XQ_EXP_NOCONV  // timing experiment only (tools/build_variant.sh): producers without the conversion
+  valid = false;
+#endif
   if (!valid) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = 0u;
-    sw.store(tile, v);
     return;
   }
   const uint32_t crow = cstage + row * (16 * BITS) + (kc & 1) * 8 * BITS;
@@ -166,6 +169,15 @@ XQ_DEVINL void produce_chunk(uint32_t tile, uint32_t cstage, uint32_t pstage, co
       }
     }
   }
+}
+
+// convert_chunk + the SWIZZLE_128B row store (tile: the A stage's 32-bit shared address)
+template <int MODE, int BITS>
+XQ_DEVINL void produce_chunk(uint32_t tile, uint32_t cstage, uint32_t pstage, const RowSwizzle& sw,
+                             int row, bool valid, int tok, int b, int nflushed, int kc,
+                             const float* first_row, const float* resid, int kdim) {
+  uint32_t v[32];
+  convert_chunk<MODE, BITS>(cstage, pstage, row, valid, tok, b, nflushed, kc, first_row, resid, kdim, v);
   sw.store(tile, v);
 }
 
