@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(kL64Warps * 32)
 }
 
 // acc_row[b][k] (+)= sum_j rec[b][j] * U[k][j]; rec[b] = row pos_b of slot b's
-// float64 residual buffer (the new token's reconstruction). Warp per row k of U.
+// float64 residual buffer (the new token's reconstruction). Warp per row k of U; up
+// to kL64Rows slots per pass share each U element (independent FMA chains), fixed
+// summation order per (b, k).
 template <typename UT>
 __global__ void __launch_bounds__(256)
     k_row64_update(const double* __restrict__ resid64, const int32_t* __restrict__ rec_pos,
@@ -102,15 +104,31 @@ __global__ void __launch_bounds__(256)
   const int64_t k = static_cast<int64_t>(blockIdx.x) * 8 + warp;
   if (k >= d) return;
   const UT* urow = u + k * r;
-  for (int b = 0; b < n_rows; ++b) {
-    const double* rec = resid64 + (static_cast<int64_t>(b) * G + rec_pos[b]) * r;
-    double s = 0.0;
-    for (int64_t j = lane; j < r; j += 32) s = __fma_rn(rec[j], static_cast<double>(urow[j]), s);
+  for (int b0 = 0; b0 < n_rows; b0 += kL64Rows) {
+    const int nb = min(kL64Rows, n_rows - b0);
+    const double* rec[kL64Rows];
+    double s[kL64Rows];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-    if (lane == 0) {
-      double* a = acc_row + static_cast<int64_t>(b) * d + k;
-      *a = seed ? s : __dadd_rn(*a, s);
+    for (int i = 0; i < kL64Rows; ++i) {
+      rec[i] = resid64 + (static_cast<int64_t>(b0 + (i < nb ? i : 0)) * G + rec_pos[b0 + (i < nb ? i : 0)]) * r;
+      s[i] = 0.0;
+    }
+    for (int64_t j = lane; j < r; j += 32) {
+      const double uv = static_cast<double>(urow[j]);
+#pragma unroll
+      for (int i = 0; i < kL64Rows; ++i)
+        if (i < nb) s[i] = __fma_rn(rec[i][j], uv, s[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kL64Rows; ++i) {
+      if (i >= nb) break;
+      double v = s[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane == 0) {
+        double* a = acc_row + static_cast<int64_t>(b0 + i) * d + k;
+        *a = seed ? v : __dadd_rn(*a, v);
+      }
     }
   }
 }

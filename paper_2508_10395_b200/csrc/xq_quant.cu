@@ -343,6 +343,71 @@ __global__ void k_dequant_rows_f16(const uint8_t* __restrict__ codes, int64_t ro
   }
 }
 
+// The same for 2/3/4/8-bit codes, specialised: a thread owns 8 channels of kRowsPerBlk
+// consecutive rows (one 16-byte store per row, coalesced across the warp); per-channel
+// (scale, zp) are loaded once per thread, the rows of a block lie in one 128-token group.
+constexpr int kRowsPerBlk = 32;
+template <int BITS, int AXIS>
+__global__ void __launch_bounds__(128) k_dequant_rows_f16_t(
+    const uint8_t* __restrict__ codes, int64_t row_bytes, const void* __restrict__ params, int G,
+    int cols, int64_t row0, int n_codes, const float* __restrict__ resid, int n_rows,
+    __half* __restrict__ out, int64_t ldo) {
+  constexpr uint32_t kMask = (1u << BITS) - 1u;
+  const int c0 = 8 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (c0 >= cols) return;
+  const int r_lo = blockIdx.y * kRowsPerBlk;
+  const int r_hi = min(n_rows, r_lo + kRowsPerBlk);
+  float2 pc[8];
+  if (AXIS == 1 && r_lo < n_codes) {  // per-channel (scale, zp) of the block's token group
+    constexpr int BS = BITS == 2 ? 16 : BITS == 3 ? 32 : BITS == 4 ? 8 : 4;
+    const __half* prow = static_cast<const __half*>(params) + ((row0 + r_lo) / G) * 2 * cols;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = c0 + j;
+      const int pos = (c / BS) * BS + perm_position(c % BS, BS);
+      pc[j] = make_float2(__half2float(prow[pos]), __half2float(prow[cols + pos]));
+    }
+  }
+  const int64_t pstride = param_stride(cols, G);
+  for (int r = r_lo; r < r_hi; ++r) {
+    float v[8];
+    if (r < n_codes) {
+      const int64_t ar = row0 + r;
+      const uint8_t* cp = codes + ar * row_bytes + (c0 / 8) * BITS;  // 8 codes = BITS bytes
+      uint2 cw;
+      if constexpr (BITS == 3) {
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(cp) & ~uintptr_t(3));
+        const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(cp) & 3u);
+        const uint32_t lo = __ldg(wp), hi = sh >= 2u ? __ldg(wp + 1) : 0u;
+        cw = make_uint2(__funnelshift_r(lo, hi, 8u * sh), 0u);
+      } else if constexpr (BITS == 2) {
+        cw = make_uint2(__ldg(reinterpret_cast<const unsigned short*>(cp)), 0u);
+      } else if constexpr (BITS == 4) {
+        cw = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(cp)), 0u);
+      } else {
+        cw = __ldg(reinterpret_cast<const uint2*>(cp));
+      }
+      float2 pt = make_float2(0.f, 0.f);
+      if (AXIS == 0) pt = __half22float2(static_cast<const __half2*>(params)[ar * pstride + c0 / G]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t word = (BITS == 8 && j >= 4) ? cw.y : cw.x;
+        const float code = static_cast<float>((word >> ((j * BITS) % 32)) & kMask);
+        v[j] = AXIS == 0 ? fmaf(code, pt.x, pt.y) : fmaf(code, pc[j].x, pc[j].y);
+      }
+    } else {
+      const float4* rr = reinterpret_cast<const float4*>(resid + (int64_t)(r - n_codes) * cols + c0);
+      const float4 a = rr[0], b = rr[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+    uint4 o;
+    __half2* oh = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) oh[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<uint4*>(out + (int64_t)r * ldo + c0) = o;
+  }
+}
+
 __global__ void k_rope_table(float2* __restrict__ cs, int64_t n_pos, int hd, double theta,
                              int j_major) {
   const int half = hd / 2;
@@ -769,6 +834,30 @@ int xq_dequant_rows_f16(const uint8_t* codes, int64_t row_bytes, const void* par
                  reinterpret_cast<uintptr_t>(out) % 16 == 0,
              XQ_ESHAPE, "cols / ldo must be multiples of 8 and out 16-byte aligned");
   if (n_rows * cols == 0) return XQ_OK;
+  // specialised kernel: whole 128-token groups per block row (per-channel), 32-bit indices
+  if (valid_bits(bits) && cols < (int64_t(1) << 30) && n_rows < (int64_t(1) << 30) &&
+      (axis == 0 || (group_size % kRowsPerBlk == 0 && row0 % group_size == 0))) {
+    const dim3 grid(static_cast<unsigned>((cols / 8 + 127) / 128),
+                    static_cast<unsigned>((n_rows + kRowsPerBlk - 1) / kRowsPerBlk));
+    auto go = [&](auto kern) {
+      kern<<<grid, 128, 0, (cudaStream_t)stream>>>(codes, row_bytes, params, group_size,
+                                                    static_cast<int>(cols), row0,
+                                                    static_cast<int>(n_codes), resid,
+                                                    static_cast<int>(n_rows),
+                                                    static_cast<__half*>(out), ldo);
+    };
+    switch (bits * 2 + axis) {
+      case 4: go(k_dequant_rows_f16_t<2, 0>); break;
+      case 5: go(k_dequant_rows_f16_t<2, 1>); break;
+      case 6: go(k_dequant_rows_f16_t<3, 0>); break;
+      case 7: go(k_dequant_rows_f16_t<3, 1>); break;
+      case 8: go(k_dequant_rows_f16_t<4, 0>); break;
+      case 9: go(k_dequant_rows_f16_t<4, 1>); break;
+      case 16: go(k_dequant_rows_f16_t<8, 0>); break;
+      default: go(k_dequant_rows_f16_t<8, 1>); break;
+    }
+    return check_launch("xq_dequant_rows_f16");
+  }
   k_dequant_rows_f16<<<grid_for(n_rows * cols / 8, 256), 256, 0, (cudaStream_t)stream>>>(
       codes, row_bytes, params, axis, bits, group_size, cols, row0, n_codes, resid, n_rows,
       static_cast<__half*>(out), ldo);
