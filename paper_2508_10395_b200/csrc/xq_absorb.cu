@@ -182,7 +182,11 @@ XQ_DEVINL void acc_update_row(__half* acc, const uint8_t* codes, const __half2* 
     for (int k = 0; k < kU; ++k) {
       const int c0 = k0 + 256 * k + 8 * lane;
       if (c0 >= kdim) continue;
-      old[k] = *reinterpret_cast<const uint4*>(acc + c0);
+      // evict-first: the next tile's rows must not push the current tile's A rows out
+      // of L2 (2% fewer cycles per C3 delta launch, profiles/r02_c3_acc_hint_ab.txt)
+      asm volatile("ld.global.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
+                   : "=r"(old[k].x), "=r"(old[k].y), "=r"(old[k].z), "=r"(old[k].w)
+                   : "l"(acc + c0), "l"(kEvictFirst));
       const uint8_t* cp = codes + c0 * BITS / 8;
       if constexpr (BITS == 3) {  // 3 bytes at any alignment: one or two aligned words
         const uint32_t* wp = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(cp) & ~uintptr_t(3));
@@ -216,8 +220,8 @@ XQ_DEVINL void acc_update_row(__half* acc, const uint8_t* codes, const __half2* 
         const float2 o = __half22float2(from_u32<__half2>(hw[j]));
         hw[j] = as_u32(__floats2half2_rn(o.x + v[0], o.y + v[1]));
       }
-      asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(acc + c0), "r"(hw[0]),
-                   "r"(hw[1]), "r"(hw[2]), "r"(hw[3])
+      asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(acc + c0),
+                   "r"(hw[0]), "r"(hw[1]), "r"(hw[2]), "r"(hw[3]), "l"(kEvictFirst)
                    : "memory");
     }
   }
