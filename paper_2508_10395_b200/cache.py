@@ -879,6 +879,8 @@ class CacheBackend:
                N.stream_of(self.device))
 
     def _use_absorbed(self, kdim: int, max_len: int) -> bool:
+        if self.group_size != DEFAULT_GROUP_SIZE:
+            return kdim % 256 == 0  # the unabsorbed kernel takes 128-channel groups only
         if kdim % 256 or self.absorb is False:
             return False
         return self.absorb is True or self._absorb_pays(max_len)
@@ -1020,6 +1022,8 @@ class QuantizedKvCache(CacheBackend):
         super().__init__(*a, **kw)
         if self.bits == 16:
             raise ConfigError("kvq at 16 bits is QuantizedKvPassthrough (make_cache picks it)")
+        if self.group_size != DEFAULT_GROUP_SIZE:
+            raise ConfigError(f"the kvq decode kernel takes 128-wide groups, got {self.group_size}")
         self.k_stream = PackedStream(self.bits, CHANNEL, self.kvw, self.group_size, self.n_slots,
                                      self.L, self.device)
         self.v_stream = PackedStream(self.bits, TOKEN, self.kvw, self.group_size, self.n_slots,
@@ -1144,6 +1148,9 @@ class LatentInputCacheGQA(CacheBackend):
     def __init__(self, *a, **kw):
         super().__init__(*a, **kw)
         r = self.latent  # the latent cache is whole even when heads are sharded
+        if self.group_size != DEFAULT_GROUP_SIZE and self.bits != 16:
+            raise ConfigError("the per-channel K latent needs 128-token groups (one per CTA tile) "
+                              f"on the B200 path, got group_size {self.group_size}")
         self.fp16_first_channel = False
         self.passthrough = self.bits == 16
         if self.passthrough:  # 16-bit latents kept raw (quant.py:117-118), no flush
@@ -1472,6 +1479,9 @@ class DeltaLatentCacheGQA(CacheBackend):
         super().__init__(*a, **kw)
         if self.policy.base_layers < 1:
             raise ConfigError("cross-layer variants need at least one base layer")
+        if self.group_size != DEFAULT_GROUP_SIZE and self.bits != 16:
+            raise ConfigError("the per-channel latent needs 128-token groups (one per CTA tile) "
+                              f"on the B200 path, got group_size {self.group_size}")
         kv_width = self.d // self.g
         if 2 * kv_width > self.d:  # model.py:135-142: the shared subspace only when 2*kvw <= d
             raise ConfigError("xq-cl-gqa needs a shared K/V subspace (2*kv_width <= hidden_dim)")

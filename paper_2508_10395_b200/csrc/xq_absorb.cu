@@ -116,6 +116,7 @@ struct Params {
   int32_t a_split;  // split: chunks at the start of each sweep loaded evict-first
   // XQ_A_F16_ACC: the accumulator rows (updated in place, one tile ahead of the
   // passes that read them) and this layer's per-token delta codes
+  int32_t G;  // per-token quantization group (32 / 64 / 128; per-channel token groups: 128)
   __half* acc_out;
   const uint8_t* d_codes;
   const __half2* d_params;
@@ -171,7 +172,7 @@ XQ_DEVINL void walk(const Params& p, int cluster, int n_clusters, KF&& kfn, VF&&
 // lane l taking channels 256k + 8l .. +7 (512 contiguous bytes per warp access).
 template <int BITS>
 XQ_DEVINL void acc_update_row(__half* acc, const uint8_t* codes, const __half2* params, int kdim,
-                              int lane) {
+                              int G, int lane) {
   constexpr uint32_t kMask = (1u << BITS) - 1u;
   constexpr int kU = 4;  // 256-channel blocks in flight
   for (int k0 = 0; k0 < kdim; k0 += 256 * kU) {
@@ -200,7 +201,7 @@ XQ_DEVINL void acc_update_row(__half* acc, const uint8_t* codes, const __half2* 
       } else {
         cw[k] = __ldg(reinterpret_cast<const uint2*>(cp));
       }
-      sz[k] = __ldg(params + c0 / kG);
+      sz[k] = __ldg(params + c0 / G);
     }
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
@@ -508,7 +509,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               mbar_arrive_expect_tx(&cfull[cs], p.k_tx);
               tma_load_2d(st, &tmap_ka, &cfull[cs], g * 16 * BITS, arow, kEvictNormal);
               if constexpr (AK == XQ_A_CODES_TOKEN)
-                tma_load_2d(st + p.k_code_bytes, &tmap_kp, &cfull[cs], 4 * (g & ~3), arow, kEvictNormal);
+                tma_load_2d(st + p.k_code_bytes, &tmap_kp, &cfull[cs], 4 * (((g * kG) / p.G) & ~3), arow,
+                            kEvictNormal);
               else
                 tma_load_2d(st + p.k_code_bytes, &tmap_kp, &cfull[cs], g * 128, 2 * (arow / kG),
                             kEvictNormal);
@@ -532,7 +534,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], gv * 128, 2 * (arow / kG),
                             kEvictNormal);
               else
-                tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (gv & ~3), arow,
+                tma_load_2d(st + 128 * 16 * BITS, &tmap_vp, &cfull[cs], 4 * (((gv * kG) / p.G) & ~3), arow,
                             kEvictNormal);
             }
             __syncwarp();
@@ -560,7 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (tok >= tl.len) break;
           const int64_t row = (int64_t)tl.b * p.L_max + tok;
           acc_update_row<BITS>(p.acc_out + row * p.kdim, p.d_codes + row * p.d_row_bytes,
-                               p.d_params + row * p.d_pstride, p.kdim, lane);
+                               p.d_params + row * p.d_pstride, p.kdim, p.G, lane);
         }
         // the updated rows, visible to the TMA loads of both CTAs (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -629,7 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                   convert_chunk<AK, BITS>(st, st + p.k_code_bytes, r, tok_k < tl.len, tok_k, tl.b, nfl,
                                           2 * g + h,
                                           p.k_first ? p.k_first + (int64_t)tl.b * p.L_max + tok_k : nullptr,
-                                          p.k_resid, p.kdim, v);
+                                          p.k_resid, p.kdim, v, p.G);
                 },
                 [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_k.store(tile, v); });
         },
@@ -643,7 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                   const int tok = tl.t * kPairM + (g & 1) * kTileM + crow;
                   if constexpr (AV == XQ_A_CODES_TOKEN)
                     convert_chunk<AV, BITS>(st, st + 128 * 16 * BITS, crow, tok < tl.len, tok, tl.b,
-                                            1 << 30, 2 * gv + hh, nullptr, nullptr, p.kdim, v);
+                                            1 << 30, 2 * gv + hh, nullptr, nullptr, p.kdim, v, p.G);
                   else if constexpr (AV == XQ_A_CODES_CHANNEL)  // same stream as the K side
                     convert_chunk<AV, BITS>(st, st + 128 * 16 * BITS, crow, tok < tl.len, tok, tl.b,
                                             nfl, 2 * gv + hh, nullptr, p.k_resid, p.kdim, v);
@@ -1527,8 +1529,11 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
   XQ_REQUIRE(rope_n >= max_len, XQ_ESHAPE, "rope table shorter than max_len");
   XQ_REQUIRE(kdim % 256 == 0 && kdim >= 256, XQ_ESHAPE,
              "kdim must be a positive multiple of 256, got %lld", (long long)kdim);
-  XQ_REQUIRE(group_size == kG, XQ_ECONFIG,
-             "the fused kernel is specialised for group_size 128 (the reference default), got %d",
+  XQ_REQUIRE(group_size == 32 || group_size == 64 || group_size == kG, XQ_ECONFIG,
+             "the fused kernel takes quantization groups of 32, 64 or 128 channels, got %d",
+             group_size);
+  XQ_REQUIRE(group_size == kG || (ak_mode != XQ_A_CODES_CHANNEL && av_mode != XQ_A_CODES_CHANNEL),
+             XQ_ECONFIG, "per-channel streams need 128-token groups (one per CTA tile), got %d",
              group_size);
   XQ_REQUIRE(n_seqs >= 1 && n_kv_heads >= 1, XQ_ESHAPE, "empty batch");
   XQ_REQUIRE(max_len <= L_max && max_len >= 1, XQ_ESHAPE, "max_len out of range");
@@ -1607,6 +1612,7 @@ int xq_decode_attend_absorbed_peers(int32_t ak_mode, const void* ak_src, const v
   p.w_hint = kEvictLast;
   p.a_hint = 1;
   p.a_split = (p.kdim / kChunk) / 2;
+  p.G = group_size;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int status;
   if (mha) {
@@ -1661,8 +1667,8 @@ int xq_decode_attend_absorbed_cl(void* acc16, const void* codes, const void* par
   XQ_REQUIRE(rope_n >= max_len, XQ_ESHAPE, "rope table shorter than max_len");
   XQ_REQUIRE(kdim % 256 == 0 && kdim >= 256, XQ_ESHAPE,
              "kdim must be a positive multiple of 256, got %lld", (long long)kdim);
-  XQ_REQUIRE(group_size == kG, XQ_ECONFIG,
-             "the fused kernel is specialised for group_size 128 (the reference default), got %d",
+  XQ_REQUIRE(group_size == 32 || group_size == 64 || group_size == kG, XQ_ECONFIG,
+             "the fused kernel takes quantization groups of 32, 64 or 128 channels, got %d",
              group_size);
   XQ_REQUIRE(valid_bits(bits), XQ_ECONFIG, "bad bits %d", bits);
   XQ_REQUIRE(n_seqs >= 1 && n_kv_heads >= 1, XQ_ESHAPE, "empty batch");
@@ -1713,6 +1719,7 @@ int xq_decode_attend_absorbed_cl(void* acc16, const void* codes, const void* par
   p.w_hint = kEvictLast;
   p.a_hint = 1;  // the later passes' fp16 rows: the split L2 policy of the F16 path
   p.a_split = (p.kdim / kChunk) / 2;
+  p.G = group_size;
   p.acc_out = static_cast<__half*>(acc16);
   p.d_codes = static_cast<const uint8_t*>(codes);
   p.d_params = static_cast<const __half2*>(params);

@@ -119,7 +119,7 @@ struct RowSwizzle {
 template <int MODE, int BITS>
 XQ_DEVINL void convert_chunk(uint32_t cstage, uint32_t pstage, int row, bool valid, int tok, int b,
                              int nflushed, int kc, const float* first_row, const float* resid,
-                             int kdim, uint32_t (&v)[32]) {
+                             int kdim, uint32_t (&v)[32], int G = kDqG) {
 #ifdef XQ_EXP_NOCONV  // timing experiment only (tools/build_variant.sh): producers without the conversion
   valid = false;
 #endif
@@ -132,10 +132,23 @@ XQ_DEVINL void convert_chunk(uint32_t cstage, uint32_t pstage, int row, bool val
   if constexpr (MODE == XQ_A_CODES_TOKEN) {
     uint32_t raw[2 * BITS];
     lds_raw<BITS>(crow, raw);
-    // G = 128: this chunk's group is kc/2; the staged quad starts at group (kc/2) & ~3
-    const __half2 sz = from_u32<__half2>(lds32(pstage + row * 16 + 4 * ((kc >> 1) & 3)));
-    const __half2 s2 = __low2half2(sz), z2 = __high2half2(sz);
-    convert_raw<BITS, false>(raw, &s2, &z2, v);
+    // the chunk's first group is kc*64/G; the staged quad of (scale, zp) starts at a
+    // multiple of 4 groups (G = 128: kc/2, G = 64: kc, G = 32: 2kc and 2kc+1)
+    const int gi = ((kc * kDqChunk) / G) & 3;
+    const __half2 sz = from_u32<__half2>(lds32(pstage + row * 16 + 4 * gi));
+    if (G >= kDqChunk) {
+      const __half2 s2 = __low2half2(sz), z2 = __high2half2(sz);
+      convert_raw<BITS, false>(raw, &s2, &z2, v);
+    } else {  // G = 32: pairs 0-15 (channel blocks of the first 32) and 16-31 (producer order)
+      const __half2 sz1 = from_u32<__half2>(lds32(pstage + row * 16 + 4 * (gi + 1)));
+      __half2 s2[32], z2[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        s2[j] = j < 16 ? __low2half2(sz) : __low2half2(sz1);
+        z2[j] = j < 16 ? __high2half2(sz) : __high2half2(sz1);
+      }
+      convert_raw<BITS, true>(raw, s2, z2, v);
+    }
   } else {  // XQ_A_CODES_CHANNEL
     constexpr int BS = BITS == 2 ? 16 : BITS == 3 ? 32 : BITS == 4 ? 8 : 4;
     if (tok < nflushed) {
