@@ -26,10 +26,11 @@ namespace xq {
 namespace {
 
 constexpr int kGemmThreads = 256;
-constexpr int kGM = 128, kGN = 256, kGK = 64;
+constexpr int kGM = 128, kGN = 256, kGK = 64;  // per CTA: 128 rows of A, 128 of the pair's 256 B rows
+constexpr int kGPairM = 2 * kGM;               // a CTA pair computes 256 x 256
 constexpr int kGStages = 4;
-constexpr uint32_t kGABytes = kGM * 128;   // [128 rows][64 K] fp16
-constexpr uint32_t kGBBytes = kGN * 128;   // [256 rows][64 K] fp16
+constexpr uint32_t kGABytes = kGM * 128;       // [128 rows][64 K] fp16
+constexpr uint32_t kGBBytes = (kGN / 2) * 128;  // this CTA's half of the pair's B tile
 constexpr uint32_t kGStage = kGABytes + kGBBytes;
 
 struct GemmParams {
@@ -42,103 +43,135 @@ struct GemmParams {
   int64_t pos0;
 };
 
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// One 256 x 256 output tile per CTA pair (cta_group::2): each CTA stages its 128 rows
+// of A and its half of B's 256 rows, the leader issues M=256 N=256 MMAs, and each
+// CTA's epilogue drains its 128 rows. Per CTA and 64-deep stage the pair moves 32 KB
+// of operands from L2 for 1024 MMA cycles (the 1-SM 128 x 256 form needed 48 KB per
+// 512): half the L2 traffic per FLOP, which was the limit of the 1-SM kernel.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_gemm_f16(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGStages * kGStage);
   uint64_t* empty = full + kGStages;
-  uint64_t* tfull = empty + kGStages;   // [2] accumulator ready
-  uint64_t* tempty = tfull + 2;         // [2] accumulator drained (4 epilogue warps)
+  uint64_t* tfull = empty + kGStages;   // [2] accumulator ready (both CTAs, multicast commit)
+  uint64_t* tempty = tfull + 2;         // [2] accumulator drained (leader's: 4 warps x 2 CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int n_tiles_total = p.m_tiles * p.n_tiles;
   const int nkc = static_cast<int>(p.K / kGK);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 2);  // the two CTAs' TMA warps (bytes of both land here)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 8);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_slot, 512);
-    tmem_relinquish();
+    tmem_alloc2(tmem_slot, 512);
+    tmem_relinquish2();
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t full_leader0 = mapa_shared(smem_u32(&full[0]), 0);
+  const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
 
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch_desc(&amap);
       tma_prefetch_desc(&bmap);
       uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x) {
+      for (int tile = cluster; tile < n_tiles_total; tile += n_clusters) {
         const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
         for (int kc = 0; kc < nkc; ++kc, ++it) {
           const uint32_t s = it % kGStages, ph = (it / kGStages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * kGStage;
-          mbar_arrive_expect_tx(&full[s], kGStage);
-          tma_load_2d(st, &amap, &full[s], kc * kGK, mt * kGM, kEvictNormal);
-          tma_load_2d(st + kGABytes, &bmap, &full[s], kc * kGK, nt * kGN, kEvictLast);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * kGStage);
+          else mbar_arrive_remote(full_leader0 + 8 * s);
+          tma_load_2d_pair(st, &amap, &full[s], kc * kGK, mt * kGPairM + static_cast<int>(rank) * kGM,
+                           kEvictNormal);
+          tma_load_2d_pair(st + kGABytes, &bmap, &full[s], kc * kGK,
+                           nt * kGN + static_cast<int>(rank) * (kGN / 2), kEvictLast);
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    constexpr uint32_t kIdesc = idesc_f16_f32(kGM, kGN);
-    const uint64_t a0 = sdesc_sw128(smem_u32(smem));
-    const uint64_t b0 = sdesc_sw128(smem_u32(smem + kGABytes));
-    uint32_t it = 0, tc = 0;
-    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++tc) {
-      const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-      mbar_wait(&tempty[a], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + a * kGN;
-      for (int kc = 0; kc < nkc; ++kc, ++it) {
-        const uint32_t s = it % kGStages, ph = (it / kGStages) & 1;
-        mbar_wait(&full[s], ph);
+    if (leader) {
+      constexpr uint32_t kIdesc = idesc_f16_f32(kGPairM, kGN);
+      const uint64_t a0 = sdesc_sw128(smem_u32(smem));
+      const uint64_t b0 = sdesc_sw128(smem_u32(smem + kGABytes));
+      uint32_t it = 0, tc = 0;
+      for (int tile = cluster; tile < n_tiles_total; tile += n_clusters, ++tc) {
+        const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
+        mbar_wait_cluster(&tempty[a], aph ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint64_t ad = a0 + ((s * kGStage) >> 4), bd = b0 + ((s * kGStage) >> 4);
+        const uint32_t d = tmem + a * kGN;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const uint32_t s = it % kGStages, ph = (it / kGStages) & 1;
+          mbar_wait_cluster(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = a0 + ((s * kGStage) >> 4), bd = b0 + ((s * kGStage) >> 4);
 #pragma unroll
-          for (int k = 0; k < kGK / 16; ++k)
-            mma_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc, (kc | k) != 0);
-          mma_commit(&empty[s]);
+            for (int k = 0; k < kGK / 16; ++k)
+              mma2_f16_ss(d, ad + 2 * k, bd + 2 * k, kIdesc, (kc | k) != 0);
+            mma2_commit_both(&empty[s]);
+          }
+          __syncwarp();
         }
+        if (elect_one()) mma2_commit_both(&tfull[a]);
         __syncwarp();
       }
-      if (elect_one()) mma_commit(&tfull[a]);
-      __syncwarp();
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const int row_in = ew * 32 + lane;
     const uint32_t tlane = static_cast<uint32_t>(ew * 32) << 16;
     uint32_t tc = 0;
-    for (int tile = blockIdx.x; tile < n_tiles_total; tile += gridDim.x, ++tc) {
+    for (int tile = cluster; tile < n_tiles_total; tile += n_clusters, ++tc) {
       const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
       const uint32_t a = tc & 1, aph = (tc >> 1) & 1;
-      mbar_wait(&tfull[a], aph);
-      tc_fence_after();
-      const int64_t row = static_cast<int64_t>(mt) * kGM + row_in;
+      const int64_t row = static_cast<int64_t>(mt) * kGPairM + static_cast<int64_t>(rank) * kGM + row_in;
       const bool row_ok = row < p.M;
       __half* crow = p.C + row * p.ldc;
+      const bool add = p.epi == 2;
+      // the add epilogue's old C rows do not depend on the MMA: the first 32 columns are
+      // loaded before the accumulator is ready, each next chunk before the current one's math
+      uint4 oldc[4];
+      auto load_old = [&](int g) {
+        const int64_t n0 = static_cast<int64_t>(nt) * kGN + g * 32;
+        if (add && row_ok && n0 + 32 <= p.N) {
+          const uint4* src = reinterpret_cast<const uint4*>(crow + n0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) oldc[q] = src[q];
+        }
+      };
+      load_old(0);
+      mbar_wait(&tfull[a], aph);
+      tc_fence_after();
       const float2* rope = p.rope ? p.rope + (p.pos0 + row) * 64 : nullptr;
 #pragma unroll 1
       for (int g = 0; g < kGN / 32; ++g) {
         float v[32];
         tmem_ld32(tmem + tlane + a * kGN + g * 32, v);
+        uint4 cur[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cur[q] = oldc[q];
+        if (g + 1 < kGN / 32) load_old(g + 1);
         tmem_wait_ld();
         const int64_t n0 = static_cast<int64_t>(nt) * kGN + g * 32;
         if (row_ok && n0 < p.N) {
@@ -160,9 +193,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             float f[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) f[i] = v[8 * q + i];
-            if (p.epi == 2) {
-              const uint4 old = dst[q];
-              const __half2* h = reinterpret_cast<const __half2*>(&old);
+            if (add) {
+              const __half2* h = reinterpret_cast<const __half2*>(&cur[q]);
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const float2 o = __half22float2(h[i]);
@@ -179,7 +211,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         } else {
           for (int i = 0; i < ncols; ++i) {
             float f = v[i];
-            if (p.epi == 2) f += __half2float(crow[n0 + i]);
+            if (add) f += __half2float(crow[n0 + i]);
             crow[n0 + i] = __float2half_rn(f);
           }
         }
@@ -187,13 +219,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[a]);
+      if (lane == 0) {
+        if (leader) mbar_arrive(&tempty[a]);
+        else mbar_arrive_remote(tempty_leader0 + 8 * a);
+      }
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc2(tmem, 512);
   }
 }
 
@@ -228,13 +264,13 @@ extern "C" int xq_gemm_f16(const void* A, int64_t lda, const void* B, int64_t ld
                        (uint64_t)lda * 2, kGK, kGM, CU_TENSOR_MAP_SWIZZLE_128B, "A")) != XQ_OK)
     return st;
   if ((st = tma_map_2d(&bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, B, (uint64_t)K, (uint64_t)N,
-                       (uint64_t)ldb * 2, kGK, kGN, CU_TENSOR_MAP_SWIZZLE_128B, "B")) != XQ_OK)
+                       (uint64_t)ldb * 2, kGK, kGN / 2, CU_TENSOR_MAP_SWIZZLE_128B, "B")) != XQ_OK)
     return st;
   GemmParams p;
   p.M = M;
   p.N = N;
   p.K = K;
-  p.m_tiles = static_cast<int32_t>((M + kGM - 1) / kGM);
+  p.m_tiles = static_cast<int32_t>((M + kGPairM - 1) / kGPairM);
   p.n_tiles = static_cast<int32_t>((N + kGN - 1) / kGN);
   p.C = static_cast<__half*>(C);
   p.ldc = ldc;
@@ -246,7 +282,7 @@ extern "C" int xq_gemm_f16(const void* A, int64_t lda, const void* B, int64_t ld
                         "cudaFuncSetAttribute(gemm_f16)")) != XQ_OK)
     return st;
   const int tiles = p.m_tiles * p.n_tiles;
-  const int grid = tiles < num_sms_dev() ? tiles : num_sms_dev();
-  k_gemm_f16<<<grid, kGemmThreads, smem, static_cast<cudaStream_t>(stream)>>>(amap, bmap, p);
+  const int pairs = tiles < num_sms_dev() / 2 ? tiles : num_sms_dev() / 2;
+  k_gemm_f16<<<2 * pairs, kGemmThreads, smem, static_cast<cudaStream_t>(stream)>>>(amap, bmap, p);
   return check_launch("k_gemm_f16");
 }

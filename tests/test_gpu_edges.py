@@ -3,7 +3,7 @@
 * ragged batches (different lengths per slot), l = 1, lengths that are not
   multiples of the 256-token pair tile;
 * every code width (2/3/4/8) and the 16-bit pass-through of xq-mha;
-* NaN/Inf input -> DataError (quant.py:114-115), group_size != 128 ->
+* NaN/Inf input -> DataError (quant.py:114-115), unsupported group sizes ->
   ConfigError, empty cache -> UsageError;
 * xq-gqa before its first per-channel flush (all rows in the residual buffer);
 * full C2 shape (d=4096, 32 heads, l=32769, 3-bit): the fused output against
@@ -90,18 +90,24 @@ def test_nonfinite_input_raises_data_error():
         st.stream.check_finite()
 
 
-def test_group_size_other_than_128_rejected_by_fused_kernel():
+def test_unsupported_group_sizes_rejected():
+    """The fused kernel takes 32/64/128-channel groups for per-token streams
+    (tests/test_gpu_groups.py); other sizes, and per-channel streams with other token
+    groups, raise the reference's ConfigError instead of computing garbage."""
     import torch
 
     from paper_2508_10395_b200 import cache as M
     from paper_2508_10395_b200.errors import ConfigError
 
-    st = M.make_cache("xq-mha", 0, M.LayerPolicy.uniform(4, 1), 128, 64, n_slots=1,
+    st = M.make_cache("xq-mha", 0, M.LayerPolicy.uniform(4, 1), 128, 16, n_slots=1,
                       max_len=256, hidden_dim=256, n_heads=2)
     w = _weights(256, 256)
     st.prefill(torch.randn(5, 256).to(torch.bfloat16).cuda(), w)
     with pytest.raises(ConfigError):
         st.decode_attend(torch.randn(1, 2, 128).cuda(), w)
+    with pytest.raises(ConfigError):
+        M.make_cache("xq-gqa", 0, M.LayerPolicy.uniform(4, 1), 128, 64, n_slots=1, max_len=256,
+                     hidden_dim=512, n_heads=4, kv_group=2)
 
 
 def test_empty_cache_usage_errors():
