@@ -176,6 +176,18 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 _ROPE: dict = {}
 _SCRATCH: dict = {}
+_REC: dict = {}
+
+
+def _rec_rows(device, rows: int, width: int) -> torch.Tensor:
+    """Per-device fp16 staging rows [rows, width] of the xq-cl-gqa accumulator GEMM
+    (zero-initialised, so rows never written hold finite values; shared by the layers)."""
+    device = torch.device(device)
+    key = (device.index if device.index is not None else torch.cuda.current_device(), width)
+    cur = _REC.get(key)
+    if cur is None or cur.shape[0] < rows:
+        _REC[key] = cur = torch.zeros((rows, width), dtype=torch.float16, device=device)
+    return cur[:rows]
 
 
 def _scratch(device, nbytes: int) -> torch.Tensor:
@@ -784,10 +796,11 @@ class CacheBackend:
                N.stream_of(self.device))
         return out
 
-    def _rows16(self, stream, slot, n):
+    def _rows16(self, stream, slot, n, out=None):
         """fp16 [n, width] operand rows of one slot: dequantized codes, then (buffered
-        streams) the residual rows (cache.py:223-230)."""
-        out = torch.empty((n, stream.width), dtype=torch.float16, device=self.device)
+        streams) the residual rows (cache.py:223-230); into ``out`` when given."""
+        if out is None:
+            out = torch.empty((n, stream.width), dtype=torch.float16, device=self.device)
         buffered = getattr(stream, "n_flushed", None) is not None
         nfl = min(int(stream.n_flushed[slot]), n) if buffered else n
         resid = stream.resid[slot] if nfl < n else None
@@ -1544,8 +1557,29 @@ class DeltaLatentCacheGQA(CacheBackend):
         return weights._cache[key]
 
     def _acc16(self, acc, weights, slots, seed):
-        """acc16[s, :n] (+)= rec16 @ U^T for every slot (cache.py:571-572, 588-589)."""
+        """acc16[s, :n] (+)= rec16 @ U^T for every slot (cache.py:571-572, 588-589).
+
+        When every slot is in use and filled to at least 3/4 of the accumulator rows, the
+        slots' reconstructions are staged in one shared buffer and multiplied in one GEMM
+        over all rows (rows past a slot's length hold finite stale values and are never
+        attended to; the seeding layer rewrites them every step)."""
         u16 = self._u16(weights)
+        slots = [s for s in slots if self.n_tokens[s] > 0]
+        la = acc.x16.shape[1]
+        if (len(slots) == self.n_slots > 1 and not self.passthrough
+                and 4 * int(self.n_tokens.max()) >= 3 * la):
+            buf = _rec_rows(self.device, self.n_slots * la, self.rank)
+            for s in slots:
+                n = int(self.n_tokens[s])
+                self._rows16(self.stream, s, n, out=buf[s * la:s * la + n])
+            c = acc.x16
+            N.call("xq_gemm_f16", N.ptr(buf), buf.stride(0), N.ptr(u16), u16.stride(0), N.ptr(c),
+                   c.stride(1), self.n_slots * la, self.d, self.rank, 0 if seed else 2, None, 0, 0,
+                   N.stream_of(self.device))
+            acc.seeded = True
+            self.acc16_launches = len(slots) + 1
+            return
+        self.acc16_launches = 2 * len(slots)
         for s in slots:
             n = int(self.n_tokens[s])
             if n == 0:

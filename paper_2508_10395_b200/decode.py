@@ -236,9 +236,9 @@ class Decoder:
         if self.variant == "xq-gqa":
             return 1 + attend  # v-latent quantize (+ a K-latent flush every 128 steps)
         if self.variant == "xq-cl-gqa":  # latent64 (+ flush), fused + merge; the seed /
-            # delta layers add the row update and per slot a dequant + remat GEMM
+            # delta layers add the row update, per slot a dequant and the remat GEMM(s)
             upd = cache.layer_index >= self.policy.base_layers - 1
-            return 1 + attend + (1 + 2 * self.n_slots if upd else 0)
+            return 1 + attend + (1 + getattr(cache, "acc16_launches", 2 * self.n_slots) if upd else 0)
         if self.variant == "xq-cl-mha":
             base = cache.layer_index < self.policy.base_layers
             seed = cache.layer_index == self.policy.base_layers - 1
