@@ -99,6 +99,65 @@ XQ_DEVINL void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Codes to floats without a conversion instruction: code j of the lane's 8 is ORed
+// in place into the mantissa of 2^23 (one LOP3), 2^23 subtracted, giving the exact
+// value code * 2^code_sh(j). Codes whose field would reach the exponent (bit 23) are
+// taken from the word shifted right by pre_shift first. The 2^-code_sh factors fold
+// into the K scales and into a final rescale of the V accumulators (powers of two:
+// the products and sums are the same floats as with the plain codes).
+template <int BITS>
+constexpr int code_off(int j) { return BITS == 8 ? 8 * (j & 3) : BITS * j; }  // bit in its word
+template <int BITS>
+constexpr int pre_shift(int j) {
+  return code_off<BITS>(j) + BITS - 1 <= 22 ? 0 : BITS * ((23 - BITS) / BITS + 1);
+}
+template <int BITS>
+constexpr int code_sh(int j) { return code_off<BITS>(j) - pre_shift<BITS>(j); }
+
+XQ_DEVINL uint32_t or_magic(uint32_t w) {
+  uint32_t r;  // opaque to the optimizer, which would refold the AND / OR pair
+  asm("or.b32 %0, %1, 0x4B000000;" : "=r"(r) : "r"(w));
+  return r;
+}
+template <int BITS>
+XQ_DEVINL float2 code_pair(uint2 raw, int j) {
+  float f[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int c = 2 * j + e;
+    const uint32_t w = ((BITS == 8 && c >= 4) ? raw.y : raw.x) >> pre_shift<BITS>(c);
+    const uint32_t mask = ((1u << BITS) - 1u) << code_sh<BITS>(c);
+    // (w | C) & (mask | C) == (w & mask) | C: one AND per code once the word carries C
+    f[e] = __uint_as_float(or_magic(w) & (mask | 0x4B000000u));
+  }
+  return __fadd2_rn(make_float2(f[0], f[1]), make_float2(-8388608.f, -8388608.f));
+}
+template <int BITS>
+XQ_DEVINL float code_unit(int c) { return __int_as_float((127 - code_sh<BITS>(c)) << 23); }  // 2^-sh
+
+// Sums of N values per lane over the 16 lanes of a half-warp, transposed: each
+// exchange step halves the values a lane carries, so N = 8 or 16 sums take N - 1
+// (+1) shuffles instead of 4N. Lane hl ends with the sum of value hl >> (4 - log2 N).
+template <int N>
+XQ_DEVINL float xreduce16(float (&v)[N], int hl) {
+#pragma unroll
+  for (int st = 0; st < 4; ++st) {
+    const int m = 8 >> st, n = N >> (st + 1);
+    if (n >= 1) {
+      const bool up = (hl & m) != 0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const float send = up ? v[i] : v[i + n];
+        const float keep = up ? v[i + n] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
+    }
+  }
+  return v[0];
+}
+
 XQ_DEVINL __half2 from_u32h2(uint32_t u) { return *reinterpret_cast<const __half2*>(&u); }
 
 // raw8 from a staged row (shared address of the head's 16*BITS code bytes)
@@ -130,39 +189,49 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
   const int n_q = p.n_kv * GROUP;
   const int nfl = p.k_nflushed[b], vnfl = p.v_nflushed[b];
 
-  __shared__ float2 s_off[16][64];  // cos/sin(r theta_j), r < 16
-  for (int i = threadIdx.x; i < 16 * 64; i += kThreads) s_off[i >> 6][i & 63] = p.rope[i];
-  float q[GROUP][8];
-  {
-    const int pos = len - 1;
-#pragma unroll
-    for (int gi = 0; gi < GROUP; ++gi) {
-      const float* qp = p.q_pre + ((int64_t)b * n_q + h * GROUP + gi) * kHeadDim + 8 * hl;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 cs = p.rope[(int64_t)pos * 64 + 4 * hl + j];
-        const float e0 = qp[2 * j], e1 = qp[2 * j + 1];
-        q[gi][2 * j] = (e0 * cs.x - e1 * cs.y) * p.q_scale;
-        q[gi][2 * j + 1] = (e0 * cs.y + e1 * cs.x) * p.q_scale;
-      }
-    }
+  constexpr int kN = GROUP * kUnroll;  // (head, token) scores per half-warp and block
+  constexpr int kLogN = kN == 16 ? 4 : 3;
+  static_assert(kN == 8 || kN == 16, "kvq: 8 or 16 scores per half-warp block");
+  // lane-major tables ([.][j][hl] holds channel pair 4hl + j): conflict-free reads
+  __shared__ float2 s_off[16][64];  // cos/sin(r theta_c), r < 16
+  for (int i = threadIdx.x; i < 16 * 64; i += kThreads) {
+    const int c = i & 63;
+    s_off[i >> 6][(c & 3) * 16 + (c >> 2)] = p.rope[i];
+  }
+  // the query heads rotated to their position and scaled (log2 domain); each warp
+  // re-rotates its lanes' channel pairs to every block base below
+  __shared__ float2 s_q[GROUP][64];
+  for (int i = threadIdx.x; i < GROUP * 64; i += kThreads) {
+    const int gi = i >> 6, c = i & 63;
+    const float2 cs = p.rope[(int64_t)(len - 1) * 64 + c];
+    const float2 e = reinterpret_cast<const float2*>(
+        p.q_pre + ((int64_t)b * n_q + h * GROUP + gi) * kHeadDim)[c];
+    s_q[gi][(c & 3) * 16 + (c >> 2)] = make_float2((e.x * cs.x - e.y * cs.y) * p.q_scale,
+                                                   (e.x * cs.y + e.y * cs.x) * p.q_scale);
   }
   __syncthreads();
-  float m[GROUP], l[GROUP], o[GROUP][8];
+  // o = sum_t p_t * (code_t * s_t + z_t) is accumulated as sum_t (p_t s_t) code_t in
+  // float2 pairs plus a per-head sum_t p_t z_t (pz), added to every channel at the end
+  float m[GROUP], l[GROUP], pz[GROUP];
+  float2 o[GROUP][4];
 #pragma unroll
   for (int gi = 0; gi < GROUP; ++gi) {
     m[gi] = -INFINITY;
     l[gi] = 0.f;
+    pz[gi] = 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[gi][j] = 0.f;
+    for (int j = 0; j < 4; ++j) o[gi][j] = make_float2(0.f, 0.f);
   }
+  // this lane's (head, token) after the transposed reduction
+  const int my = hl >> (4 - kLogN), my_g = my / kUnroll, my_u = my % kUnroll;
   const int64_t row0 = (int64_t)b * p.L_max;
   const int bs = perm_block(XQ_A_CODES_CHANNEL, BITS);
   int cur_grp = -1;
-  float2 kp[8];  // (scale, zp) of this lane's 8 K channels for the current token group
-  // warp w takes blocks of kBlk = 2*kUnroll tokens (16-aligned: one RoPE base,
-  // one K group); half-warp `half` the tokens 2u + half. Codes arrive through a
-  // per-warp cp.async ring (rows past t1 clamp to t1 - 1 and are masked).
+  // (scale * 2^-code_sh, zp) of this lane's 8 K channels for the current token group
+  float2 kps[4], kpz[4];
+  // per-warp cp.async ring of token blocks: warp w takes blocks of kBlk = 2*kUnroll
+  // tokens (16-aligned: one RoPE base, one K group); half-warp `half` the tokens
+  // 2u + half (rows past t1 clamp to t1 - 1 and are masked).
   extern __shared__ __align__(16) uint8_t kvq_smem[];
   const uint32_t ring = smem_u32(kvq_smem) + warp * kStages * kStageB;
   auto issue = [&](int wb, int stg) {
@@ -186,24 +255,49 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
   // w, w + nw, ...: the per-channel K params load once per group
   constexpr int kBpg = 128 / kBlk;
   auto wb_of = [&](int k) { return t0 + ((k / kBpg) * kNw + warp) * 128 + (k % kBpg) * kBlk; };
+  // cos/sin(wbase theta) of the lane's 4 frequencies, loaded one block ahead
+  auto base_of = [&](int wb, float2 (&cs)[4]) {
+    const int64_t row = (int64_t)min(wb, len - 1) * 64 + 4 * hl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cs[j] = __ldg(p.rope + row + j);
+  };
 #pragma unroll
   for (int k = 0; k < kStages - 1; ++k) issue(wb_of(k), k);
+  float2 nbase[4];
+  base_of(wb_of(0), nbase);
   int stage = 0;
   for (int kb = 0, wbase = wb_of(0); wbase < t1; wbase = wb_of(++kb)) {
     const int grp = wbase / p.G;
     if (grp != cur_grp && wbase < nfl) {
       const __half* prow = p.k_params + (row0 / p.G + grp) * 2 * p.kvw;
+      float ks[8], kz[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int c = h * kHeadDim + 8 * hl + j;
         const int ppos = (c / bs) * bs + perm_position(c % bs, bs);
-        kp[j] = make_float2(__half2float(prow[ppos]), __half2float(prow[p.kvw + ppos]));
+        ks[j] = __half2float(prow[ppos]) * code_unit<BITS>(j);
+        kz[j] = __half2float(prow[p.kvw + ppos]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        kps[j] = make_float2(ks[2 * j], ks[2 * j + 1]);
+        kpz[j] = make_float2(kz[2 * j], kz[2 * j + 1]);
       }
       cur_grp = grp;
     }
-    float2 base[4];  // cos/sin(wbase theta_j) of this lane's 4 frequencies
+    // q rotated back to the block base, qb = R(wbase)^T q, so that
+    // q . R(wbase + r) k = qb . R(r) k with R(r) from the shared offset table
+    float2 qb[GROUP][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) base[j] = __ldg(p.rope + (int64_t)wbase * 64 + 4 * hl + j);
+    for (int j = 0; j < 4; ++j) {
+      const float2 cs = nbase[j];
+#pragma unroll
+      for (int gi = 0; gi < GROUP; ++gi) {
+        const float2 qq = s_q[gi][j * 16 + hl];
+        qb[gi][j] = make_float2(fmaf(qq.x, cs.x, qq.y * cs.y), fmaf(qq.y, cs.x, -qq.x * cs.y));
+      }
+    }
+    base_of(wb_of(kb + 1), nbase);
     cp_async_wait<kStages - 2>();
     __syncwarp();
     const uint32_t sa = ring + stage * kStageB;
@@ -216,78 +310,91 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
       vraw[u] = raw8_s<BITS>(sa + kBlk * kRowB + r * kRowB, hl);
       vsz[u] = from_u32h2(lds32(sa + 2 * kBlk * kRowB + 4u * r));
     }
-    // K phase: dequant + RoPE in registers, scores of the group's query heads
-    float sc[GROUP][kUnroll];
+    // K phase: dequant + RoPE in registers, partial dot products of the group's heads
+    float part[kN];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int r = 2 * u + half;
       const int t = min(wbase + r, t1 - 1);
-      float kv[8];
+      float2 kv[4];
       if (t < nfl) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          kv[j] = fmaf(static_cast<float>(code_j<BITS>(kraw[u], j)), kp[j].x, kp[j].y);
+        for (int j = 0; j < 4; ++j)
+          kv[j] = __ffma2_rn(code_pair<BITS>(kraw[u], j), kps[j], kpz[j]);
       } else {
         const float4* rr = reinterpret_cast<const float4*>(
             p.k_resid + ((int64_t)b * p.G + (t - nfl)) * p.kvw + h * kHeadDim + 8 * hl);
         const float4 a0 = rr[0], a1 = rr[1];
-        kv[0] = a0.x; kv[1] = a0.y; kv[2] = a0.z; kv[3] = a0.w;
-        kv[4] = a1.x; kv[5] = a1.y; kv[6] = a1.z; kv[7] = a1.w;
+        kv[0] = make_float2(a0.x, a0.y); kv[1] = make_float2(a0.z, a0.w);
+        kv[2] = make_float2(a1.x, a1.y); kv[3] = make_float2(a1.z, a1.w);
       }
-      float kf[8];
+      float2 acc[GROUP];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {  // RoPE at position wbase + r (linalg.py:92-93)
-        const float2 of = s_off[r][4 * hl + j];
-        const float cs = base[j].x * of.x - base[j].y * of.y;
-        const float sn = base[j].y * of.x + base[j].x * of.y;
-        kf[2 * j] = kv[2 * j] * cs - kv[2 * j + 1] * sn;
-        kf[2 * j + 1] = kv[2 * j] * sn + kv[2 * j + 1] * cs;
+      for (int gi = 0; gi < GROUP; ++gi) acc[gi] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // RoPE at offset r from the block base (linalg.py:92-93)
+        const float2 of = s_off[r][j * 16 + hl];
+        const float2 kf = make_float2(fmaf(kv[j].x, of.x, -kv[j].y * of.y),
+                                      fmaf(kv[j].x, of.y, kv[j].y * of.x));
+#pragma unroll
+        for (int gi = 0; gi < GROUP; ++gi) acc[gi] = __ffma2_rn(qb[gi][j], kf, acc[gi]);
       }
 #pragma unroll
-      for (int gi = 0; gi < GROUP; ++gi) {
-        float d = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) d = fmaf(q[gi][j], kf[j], d);
-#pragma unroll
-        for (int off = 8; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-        sc[gi][u] = (wbase + r < t1) ? d : -INFINITY;
-      }
+      for (int gi = 0; gi < GROUP; ++gi) part[gi * kUnroll + u] = acc[gi].x + acc[gi].y;
     }
-    float mn[GROUP];
+    // this lane's score, the block max of each head, its probability, then every
+    // (head, token) probability broadcast to the half-warp for the V phase
+    float sc = xreduce16<kN>(part, hl);
+    if (wbase + 2 * my_u + half >= t1) sc = -INFINITY;
+    float mt = sc;
+#pragma unroll
+    for (int bit = 4 - kLogN; bit < 4 - kLogN + (kLogN - (GROUP == 4 ? 2 : GROUP == 2 ? 1 : 0)); ++bit)
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1 << bit));
+    float mn_my = 0.f;
 #pragma unroll
     for (int gi = 0; gi < GROUP; ++gi) {
-      float mt = -INFINITY;
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) mt = fmaxf(mt, sc[gi][u]);
-      mn[gi] = fmaxf(m[gi], mt);
-      const float alpha = (m[gi] == -INFINITY) ? 0.f : exp2f(m[gi] - mn[gi]);
+      const float mg = GROUP == 1 ? mt
+                                  : __shfl_sync(0xffffffffu, mt, (lane & 16) | ((gi * kUnroll) << (4 - kLogN)));
+      const float mn = fmaxf(m[gi], mg);
+      const float alpha = (m[gi] == -INFINITY) ? 0.f : exp2f(m[gi] - mn);
       l[gi] *= alpha;
+      pz[gi] *= alpha;
+      const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[gi][j] *= alpha;
-      m[gi] = mn[gi];
+      for (int j = 0; j < 4; ++j) o[gi][j] = __fmul2_rn(o[gi][j], a2);
+      m[gi] = mn;
+      if (gi == my_g) mn_my = mn;
     }
-    // V phase: dequant once per token, p.V for every query head of the group
+    const float p_my = (sc == -INFINITY) ? 0.f : exp2f(sc - mn_my);
+    // V phase: p * scale times the codes, p * zp into pz; residual rows as floats
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int t = min(wbase + 2 * u + half, t1 - 1);
-      float vf[8];
+      float2 vf[4];
+      float2 sz;
       if (t < vnfl) {
-        const float2 sz = __half22float2(vsz[u]);
+        sz = __half22float2(vsz[u]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) vf[j] = fmaf(static_cast<float>(code_j<BITS>(vraw[u], j)), sz.x, sz.y);
-      } else {
+        for (int j = 0; j < 4; ++j) vf[j] = code_pair<BITS>(vraw[u], j);
+      } else {  // scaled like the codes (2^code_sh), undone with them at the end
+        sz = make_float2(1.f, 0.f);
         const float4* rr = reinterpret_cast<const float4*>(
             p.v_resid + ((int64_t)b * p.G + (t - vnfl)) * p.kvw + h * kHeadDim + 8 * hl);
         const float4 a0 = rr[0], a1 = rr[1];
-        vf[0] = a0.x; vf[1] = a0.y; vf[2] = a0.z; vf[3] = a0.w;
-        vf[4] = a1.x; vf[5] = a1.y; vf[6] = a1.z; vf[7] = a1.w;
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          vf[j] = make_float2(a[2 * j] / code_unit<BITS>(2 * j), a[2 * j + 1] / code_unit<BITS>(2 * j + 1));
       }
 #pragma unroll
       for (int gi = 0; gi < GROUP; ++gi) {
-        const float pr = (sc[gi][u] == -INFINITY) ? 0.f : exp2f(sc[gi][u] - mn[gi]);
+        const float pr = __shfl_sync(0xffffffffu, p_my, (lane & 16) | ((gi * kUnroll + u) << (4 - kLogN)));
         l[gi] += pr;
+        pz[gi] = fmaf(pr, sz.y, pz[gi]);
+        const float ps = pr * sz.x;
+        const float2 ps2 = make_float2(ps, ps);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[gi][j] = fmaf(pr, vf[j], o[gi][j]);
+        for (int j = 0; j < 4; ++j) o[gi][j] = __ffma2_rn(ps2, vf[j], o[gi][j]);
       }
     }
     __syncwarp();  // every lane has read this stage before it is refilled
@@ -304,7 +411,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
       s_l[stream][gi] = l[gi];
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s_o[stream][gi][8 * hl + j] = o[gi][j];
+    for (int j = 0; j < 4; ++j) {
+      s_o[stream][gi][8 * hl + 2 * j] = fmaf(o[gi][j].x, code_unit<BITS>(2 * j), pz[gi]);
+      s_o[stream][gi][8 * hl + 2 * j + 1] = fmaf(o[gi][j].y, code_unit<BITS>(2 * j + 1), pz[gi]);
+    }
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < GROUP * kHeadDim; idx += kThreads) {
