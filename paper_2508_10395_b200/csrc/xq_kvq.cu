@@ -193,10 +193,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
   constexpr int kLogN = kN == 16 ? 4 : 3;
   static_assert(kN == 8 || kN == 16, "kvq: 8 or 16 scores per half-warp block");
   // lane-major tables ([.][j][hl] holds channel pair 4hl + j): conflict-free reads
-  __shared__ float2 s_off[16][64];  // cos/sin(r theta_c), r < 16
+  // cos/sin(r theta_c), r < 16, lane-major: [r][jp][hl] holds the lane's channel pairs
+  // 4hl + 2jp and 4hl + 2jp + 1 (one conflict-free 16-byte read per two pairs)
+  __shared__ __align__(16) float2 s_off[16][2][16][2];
   for (int i = threadIdx.x; i < 16 * 64; i += kThreads) {
     const int c = i & 63;
-    s_off[i >> 6][(c & 3) * 16 + (c >> 2)] = p.rope[i];
+    s_off[i >> 6][(c & 3) >> 1][c >> 2][c & 1] = p.rope[i];
   }
   // the query heads rotated to their position and scaled (log2 domain); each warp
   // re-rotates its lanes' channel pairs to every block base below
@@ -234,19 +236,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
   // 2u + half (rows past t1 clamp to t1 - 1 and are masked).
   extern __shared__ __align__(16) uint8_t kvq_smem[];
   const uint32_t ring = smem_u32(kvq_smem) + warp * kStages * kStageB;
+  // this lane's 16-byte chunks of a block (BITS per row): row and byte offsets, fixed
+  constexpr int kChunks = kBlk * BITS, kIters = (kChunks + 31) / 32;
+  int c_row[kIters], c_q16[kIters];
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    const int i = lane + 32 * it;
+    c_row[it] = i / BITS;
+    c_q16[it] = 16 * (i % BITS);
+  }
+  const uint8_t* kc = p.k_codes + row0 * p.row_bytes;
+  const uint8_t* vc = p.v_codes + row0 * p.row_bytes;
+  const __half2* vpar = p.v_params + row0 * p.vp_stride + h;
   auto issue = [&](int wb, int stg) {
     if (wb < t1) {
       const uint32_t sa = ring + stg * kStageB;
-      for (int i = lane; i < kBlk * BITS; i += 32) {  // BITS 16-byte chunks per row
-        const int r = i / BITS, qq = i % BITS;
-        const int64_t t = min(wb + r, t1 - 1);
-        const int64_t src = (row0 + t) * p.row_bytes + (int64_t)h * kRowB + 16 * qq;
-        cp_async16(sa + r * kRowB + 16u * qq, p.k_codes + src);
-        cp_async16(sa + kBlk * kRowB + r * kRowB + 16u * qq, p.v_codes + src);
+      const bool full = wb + kBlk <= t1;
+#pragma unroll
+      for (int it = 0; it < kIters; ++it) {
+        if (lane + 32 * it < kChunks) {
+          const int t = full ? wb + c_row[it] : min(wb + c_row[it], t1 - 1);
+          const int64_t src = (int64_t)t * p.row_bytes + (h * kRowB + c_q16[it]);
+          const uint32_t dst = sa + c_row[it] * kRowB + c_q16[it];
+          cp_async16(dst, kc + src);
+          cp_async16(dst + kBlk * kRowB, vc + src);
+        }
       }
       if (lane < kBlk) {
         const int64_t t = min(wb + lane, t1 - 1);
-        cp_async4(sa + 2 * kBlk * kRowB + 4u * lane, p.v_params + (row0 + t) * p.vp_stride + h);
+        cp_async4(sa + 2 * kBlk * kRowB + 4u * lane, vpar + t * p.vp_stride);
       }
     }
     cp_async_commit();
@@ -267,9 +285,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
   base_of(wb_of(0), nbase);
   int stage = 0;
   for (int kb = 0, wbase = wb_of(0); wbase < t1; wbase = wb_of(++kb)) {
-    const int grp = wbase / p.G;
+    const int grp = wbase / kT;  // group_size is 128 (checked on the host)
     if (grp != cur_grp && wbase < nfl) {
-      const __half* prow = p.k_params + (row0 / p.G + grp) * 2 * p.kvw;
+      const __half* prow = p.k_params + (row0 / kT + grp) * 2 * p.kvw;
       float ks[8], kz[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -310,37 +328,50 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
       vraw[u] = raw8_s<BITS>(sa + kBlk * kRowB + r * kRowB, hl);
       vsz[u] = from_u32h2(lds32(sa + 2 * kBlk * kRowB + 4u * r));
     }
-    // K phase: dequant + RoPE in registers, partial dot products of the group's heads
+    // K phase: dequant + RoPE in registers, partial dot products of the group's heads.
+    // K groups flush whole (nfl % 128 == 0), so a block is all codes or all residual.
     float part[kN];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    auto k_scores = [&](int u, const float2 (&kv)[4]) {
       const int r = 2 * u + half;
-      const int t = min(wbase + r, t1 - 1);
-      float2 kv[4];
-      if (t < nfl) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          kv[j] = __ffma2_rn(code_pair<BITS>(kraw[u], j), kps[j], kpz[j]);
-      } else {
-        const float4* rr = reinterpret_cast<const float4*>(
-            p.k_resid + ((int64_t)b * p.G + (t - nfl)) * p.kvw + h * kHeadDim + 8 * hl);
-        const float4 a0 = rr[0], a1 = rr[1];
-        kv[0] = make_float2(a0.x, a0.y); kv[1] = make_float2(a0.z, a0.w);
-        kv[2] = make_float2(a1.x, a1.y); kv[3] = make_float2(a1.z, a1.w);
-      }
       float2 acc[GROUP];
 #pragma unroll
       for (int gi = 0; gi < GROUP; ++gi) acc[gi] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {  // RoPE at offset r from the block base (linalg.py:92-93)
-        const float2 of = s_off[r][j * 16 + hl];
-        const float2 kf = make_float2(fmaf(kv[j].x, of.x, -kv[j].y * of.y),
-                                      fmaf(kv[j].x, of.y, kv[j].y * of.x));
+      for (int jp = 0; jp < 2; ++jp) {  // RoPE at offset r from the block base (linalg.py:92-93)
+        const float4 o4 = *reinterpret_cast<const float4*>(&s_off[r][jp][hl][0]);
 #pragma unroll
-        for (int gi = 0; gi < GROUP; ++gi) acc[gi] = __ffma2_rn(qb[gi][j], kf, acc[gi]);
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * jp + e;
+          const float2 of = e ? make_float2(o4.z, o4.w) : make_float2(o4.x, o4.y);  // (cos, sin)
+          // (x c - y s, x s + y c): two packed ops with broadcast / swapped / negated halves
+          const float2 t = __fmul2_rn(make_float2(kv[j].y, kv[j].y), make_float2(of.y, of.x));
+          const float2 kf = __ffma2_rn(make_float2(kv[j].x, kv[j].x), of, make_float2(-t.x, t.y));
+#pragma unroll
+          for (int gi = 0; gi < GROUP; ++gi) acc[gi] = __ffma2_rn(qb[gi][j], kf, acc[gi]);
+        }
       }
 #pragma unroll
       for (int gi = 0; gi < GROUP; ++gi) part[gi * kUnroll + u] = acc[gi].x + acc[gi].y;
+    };
+    if (wbase < nfl) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        float2 kv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) kv[j] = __ffma2_rn(code_pair<BITS>(kraw[u], j), kps[j], kpz[j]);
+        k_scores(u, kv);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int t = min(wbase + 2 * u + half, t1 - 1);
+        const float4* rr = reinterpret_cast<const float4*>(
+            p.k_resid + ((int64_t)b * p.G + (t - nfl)) * p.kvw + h * kHeadDim + 8 * hl);
+        const float4 a0 = rr[0], a1 = rr[1];
+        const float2 kv[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w),
+                              make_float2(a1.x, a1.y), make_float2(a1.z, a1.w)};
+        k_scores(u, kv);
+      }
     }
     // this lane's score, the block max of each head, its probability, then every
     // (head, token) probability broadcast to the half-warp for the V phase
@@ -367,34 +398,46 @@ __global__ void __launch_bounds__(kThreads, 2) k_kvq_decode(const Params p) {
     }
     const float p_my = (sc == -INFINITY) ? 0.f : exp2f(sc - mn_my);
     // V phase: p * scale times the codes, p * zp into pz; residual rows as floats
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int t = min(wbase + 2 * u + half, t1 - 1);
-      float2 vf[4];
-      float2 sz;
-      if (t < vnfl) {
-        sz = __half22float2(vsz[u]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) vf[j] = code_pair<BITS>(vraw[u], j);
-      } else {  // scaled like the codes (2^code_sh), undone with them at the end
-        sz = make_float2(1.f, 0.f);
-        const float4* rr = reinterpret_cast<const float4*>(
-            p.v_resid + ((int64_t)b * p.G + (t - vnfl)) * p.kvw + h * kHeadDim + 8 * hl);
-        const float4 a0 = rr[0], a1 = rr[1];
-        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          vf[j] = make_float2(a[2 * j] / code_unit<BITS>(2 * j), a[2 * j + 1] / code_unit<BITS>(2 * j + 1));
-      }
+    auto v_accum = [&](int u, const float2 (&vf)[4], float2 sz) {
 #pragma unroll
       for (int gi = 0; gi < GROUP; ++gi) {
         const float pr = __shfl_sync(0xffffffffu, p_my, (lane & 16) | ((gi * kUnroll + u) << (4 - kLogN)));
         l[gi] += pr;
         pz[gi] = fmaf(pr, sz.y, pz[gi]);
         const float ps = pr * sz.x;
-        const float2 ps2 = make_float2(ps, ps);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o[gi][j] = __ffma2_rn(ps2, vf[j], o[gi][j]);
+        for (int j = 0; j < 4; ++j) o[gi][j] = __ffma2_rn(make_float2(ps, ps), vf[j], o[gi][j]);
+      }
+    };
+    if (wbase + kBlk <= vnfl) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        float2 vf[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) vf[j] = code_pair<BITS>(vraw[u], j);
+        v_accum(u, vf, __half22float2(vsz[u]));
+      }
+    } else {  // the block reaches the V residual rows (V flushes are not group-aligned)
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int t = min(wbase + 2 * u + half, t1 - 1);
+        float2 vf[4];
+        float2 sz;
+        if (t < vnfl) {
+          sz = __half22float2(vsz[u]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) vf[j] = code_pair<BITS>(vraw[u], j);
+        } else {  // scaled like the codes (2^code_sh), undone with them at the end
+          sz = make_float2(1.f, 0.f);
+          const float4* rr = reinterpret_cast<const float4*>(
+              p.v_resid + ((int64_t)b * p.G + (t - vnfl)) * p.kvw + h * kHeadDim + 8 * hl);
+          const float4 a0 = rr[0], a1 = rr[1];
+          const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            vf[j] = make_float2(a[2 * j] / code_unit<BITS>(2 * j), a[2 * j + 1] / code_unit<BITS>(2 * j + 1));
+        }
+        v_accum(u, vf, sz);
       }
     }
     __syncwarp();  // every lane has read this stage before it is refilled
