@@ -78,13 +78,18 @@ constexpr int kMaxHeads = 64;
 constexpr bool kSerpentine = XQ_SERPENTINE != 0;  // fp16-row K passes alternate chunk direction
 constexpr uint32_t kABytes = kTileM * 128;  // [128 x 64] fp16 = 16 KB
 constexpr uint32_t kBSub = 128 * 128;       // 128 W rows x 64 channels (one KV head)
-// KV heads per K pass: 4 for MHA (two N=256 MMAs share each A stage: half the
-// dequant work per FLOP, one 512-column accumulator), 2 for GQA (one N=256
-// MMA, double-buffered accumulators: the GQA epilogue has 4x the score work
-// per MMA and must overlap the next pass).
+// KV heads per K pass: 4 (two N=256 MMAs share each A stage: half the dequant work
+// per FLOP, one 512-column accumulator). GQA ran 2 heads per pass with
+// double-buffered accumulators so its heavier score epilogue overlapped the next
+// pass; 4 heads per pass halve the producers' per-channel conversions instead,
+// which is the larger cost: C4 took 7.5% fewer cycles per launch
+// (profiles/r02_gqa_kh4_ab.txt). XQ_GQA_KH=2 restores the pipelined variant.
+#ifndef XQ_GQA_KH
+#define XQ_GQA_KH 4
+#endif
 template <int GROUP>
 struct Cfg {
-  static constexpr int KH = GROUP == 1 ? 4 : 2;
+  static constexpr int KH = GROUP == 1 ? 4 : XQ_GQA_KH;
   static constexpr int NBUF = KH == 2 ? 2 : 1;         // accumulator buffers
   static constexpr uint32_t kBBytes = (KH / 2) * kBSub;  // this CTA's W rows per stage
   static constexpr uint32_t kABStage = kABytes + kBBytes;
