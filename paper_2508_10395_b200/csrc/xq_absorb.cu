@@ -121,6 +121,9 @@ struct Params {
   int32_t a_split;  // split: chunks at the start of each sweep loaded evict-first
   // XQ_A_F16_ACC: the accumulator rows (updated in place, one tile ahead of the
   // passes that read them) and this layer's per-token delta codes
+  // GROUP 4: q as the B fragments of the score mma, per sequence (k_q_frags, once per
+  // launch, in the spare half of the fp16 partials region): [n_seqs][n_kv][8][32]
+  const uint2* q_frag;
   int32_t G;  // per-token quantization group (32 / 64 / 128; per-channel token groups: 128)
   __half* acc_out;
   const uint8_t* d_codes;
@@ -231,6 +234,44 @@ XQ_DEVINL void acc_update_row(__half* acc, const uint8_t* codes, const __half2* 
                    : "memory");
     }
   }
+}
+
+// One entry (kvh, kk, lane) of the GQA score mma's B fragments: q heads kvh*4 + g
+// (n = g, 4 of 8 used), k16 block kk of the split RoPE dims, rotated to pos and
+// scaled, fp16 pairs {b0b1, b2b3}.
+XQ_DEVINL uint2 q_frag_entry(const float* qb, const float2* rope, int64_t rope_n, int pos,
+                             float q_scale, int i, int group) {
+  const int ln = i & 31, kk = (i >> 5) & 7, kvh = i >> 8;
+  const int g = ln >> 2, tig = ln & 3;
+  if (g >= group) return make_uint2(0u, 0u);
+  const float* qp = qb + (int64_t)(kvh * group + g) * kHeadDim;
+  const int j0 = (kk & 3) * 16 + 2 * tig;  // frequency of split dim kk*16 + 2*tig
+  const bool odd = kk >= 4;                // dims 64.. hold the second of each pair
+  auto rot2 = [&](int j) {                 // split dims (j, j+1) of this half
+    const float4 e = *reinterpret_cast<const float4*>(qp + 2 * j);
+    const float2 c0 = rope[(int64_t)j * rope_n + pos];
+    const float2 c1 = rope[(int64_t)(j + 1) * rope_n + pos];
+    const float r0 = odd ? (e.x * c0.y + e.y * c0.x) : (e.x * c0.x - e.y * c0.y);
+    const float r1 = odd ? (e.z * c1.y + e.w * c1.x) : (e.z * c1.x - e.w * c1.y);
+    const __half2 h = __floats2half2_rn(r0 * q_scale, r1 * q_scale);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  };
+  return make_uint2(rot2(j0), rot2(j0 + 8));
+}
+
+// The B fragments of every sequence, once per launch (grid n_seqs): the fused
+// kernel copies its sequence's 2 KB per KV head at each tile start instead of
+// recomputing them from q and the RoPE table.
+__global__ void __launch_bounds__(256) k_q_frags(const float* __restrict__ q_pre,
+                                                 const float2* __restrict__ rope, int64_t rope_n,
+                                                 const int32_t* __restrict__ seq_lens, int n_q,
+                                                 int n_kv, int group, float q_scale,
+                                                 uint2* __restrict__ out) {
+  const int b = blockIdx.x, n_ent = n_kv * 256;
+  const int pos = seq_lens[b] - 1;
+  const float* qb = q_pre + (int64_t)b * n_q * kHeadDim;
+  for (int i = threadIdx.x; i < n_ent; i += 256)
+    out[(int64_t)b * n_ent + i] = q_frag_entry(qb, rope, rope_n, pos < 0 ? 0 : pos, q_scale, i, group);
 }
 
 template <int AK, int AV, int BITS, int GROUP>
@@ -687,6 +728,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       [&](const Tile& tl, int ps) {
       const int b = tl.b, t = tl.t, len = tl.len;
       if (ps == 0) {  // tile setup: q rotated to len-1, the RoPE base rows
+#ifdef XQ_ROLE_PROFILE
+      const long long pt_s = clock64();
+#endif
       const int pos = len - 1;
       if (!PIPE && et == 0) tma_store_wait_read<0>();  // previous tile's O stores have read q_s / sc_s
       named_bar_sync(1, 128);  // previous tile's readers of q_s / sc_s / rope_base are done
@@ -695,30 +739,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         rope_base[i] = p.rope[(int64_t)(i & 63) * p.rope_n + (tp < p.rope_n ? tp : 0)];
       }
       if constexpr (kMmaScores) {
-        // q as the B fragments of mma m16n8k16 (n = the KV head's query heads, 4 of
-        // 8 used; k = split RoPE dims), fp16: entry (kvh, kk, lane) = {b0b1, b2b3}
-        // of k16 block kk, rotated to len-1 and scaled here
-        const int n_ent = p.n_kv * 8 * 32;
-        for (int i = et; i < n_ent; i += 128) {
-          const int ln = i & 31, kk = (i >> 5) & 7, kvh = i >> 8;
-          const int g = ln >> 2, tig = ln & 3;
-          uint32_t b01 = 0u, b23 = 0u;
-          if (g < GROUP) {
-            const float* qp = p.q_pre + ((int64_t)b * p.n_q + kvh * GROUP + g) * kHeadDim;
-            const int j0 = (kk & 3) * 16 + 2 * tig;  // frequency of split dim kk*16 + 2*tig
-            const bool odd = kk >= 4;                // dims 64.. hold the second of each pair
-            auto rot2 = [&](int j) {                 // split dims (j, j+1) of this half
-              const float4 e = *reinterpret_cast<const float4*>(qp + 2 * j);
-              const float2 c0 = p.rope[(int64_t)j * p.rope_n + pos];
-              const float2 c1 = p.rope[(int64_t)(j + 1) * p.rope_n + pos];
-              const float r0 = odd ? (e.x * c0.y + e.y * c0.x) : (e.x * c0.x - e.y * c0.y);
-              const float r1 = odd ? (e.z * c1.y + e.w * c1.x) : (e.z * c1.x - e.w * c1.y);
-              return as_u32(__floats2half2_rn(r0 * p.q_scale, r1 * p.q_scale));
-            };
-            b01 = rot2(j0);
-            b23 = rot2(j0 + 8);
-          }
-          sts64(q_a + 8u * i, b01, b23);
+        // q as the B fragments of mma m16n8k16 (k_q_frags: entry (kvh, kk, lane) =
+        // {b0b1, b2b3} of k16 block kk), copied for this tile's sequence
+        const int n_ent4 = p.n_kv * 128;  // 16-byte pairs of entries
+        const uint4* src = reinterpret_cast<const uint4*>(p.q_frag + (int64_t)b * p.n_kv * 256);
+#pragma unroll 8
+        for (int i = et; i < n_ent4; i += 128) {
+          const uint4 v = __ldg(src + i);
+          sts128(q_a + 16u * i, v.x, v.y, v.z, v.w);
         }
       } else {
         const float2 cs = p.rope[(int64_t)(et >> 1) * p.rope_n + pos];
@@ -731,6 +759,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       named_bar_sync(1, 128);
+#ifdef XQ_ROLE_PROFILE
+      prof_acc[15] += clock64() - pt_s;
+#endif
       }
       const int tok = t * kPairM + rank * kTileM + row;
       const bool valid = tok < len;
@@ -1404,6 +1435,13 @@ int launch(const Maps& m, Params p, cudaStream_t st) {
   if ((status = ensure_smem(reinterpret_cast<const void*>(kern), 227 * 1024,
                             "cudaFuncSetAttribute(decode_absorbed)")) != XQ_OK)
     return status;
+  if constexpr (GROUP == 4) {  // the score mma's q fragments (spare half of the fp16 partials)
+    uint2* qf = reinterpret_cast<uint2*>(p.part_o + (int64_t)p.n_seqs * p.n_tiles * p.n_q * p.kdim);
+    k_q_frags<<<p.n_seqs, 256, 0, st>>>(p.q_pre, p.rope, p.rope_n, p.seq_lens, p.n_q, p.n_kv, GROUP,
+                                        p.q_scale, qf);
+    if ((status = check_launch("k_q_frags")) != XQ_OK) return status;
+    p.q_frag = qf;
+  }
   const int pairs = p.n_units < num_sms() / 2 ? p.n_units : num_sms() / 2;
   kern<<<2 * pairs, kThreads, smem, st>>>(m.w, m.ka, m.kp, m.va, m.vp, m.o, p);
   return check_launch("k_decode_absorbed");

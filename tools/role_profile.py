@@ -51,7 +51,7 @@ names = [("W-TMA", "empty", 0, n_cta), ("MMA", "tempty", 1, n_cta // 2), ("MMA",
          ("producer", "empty", 7, 8 * n_cta), ("epilogue", "tfull(K)", 8, 4 * n_cta),
          ("epilogue", "xfull", 9, 4 * n_cta), ("epilogue", "tfull(V)", 10, 4 * n_cta),
          ("epilogue", "[busy K]", 12, 4 * n_cta), ("epilogue", "[busy X]", 13, 4 * n_cta),
-         ("epilogue", "[busy V]", 14, 4 * n_cta)]
+         ("epilogue", "[busy V]", 14, 4 * n_cta), ("epilogue", "[setup]", 15, 4 * n_cta)]
 print(f"{args.config}: {args.layers} layers, cycles per CTA (sum over launches) {total:.3e}")
 for role, bar, c, nw in names:
     print(f"  {role:10s} waits on {bar:9s}: {100 * v[c] / nw / total:5.1f}% of its time")
