@@ -280,7 +280,7 @@ int xq_decode_attend(int32_t ak_mode, const void* ak_src, const void* ak_params,
  * Same result as xq_decode_attend, computed with the exact reassociation
  *   sum_t p_t (A_V[t] @ W_v[:, kv]) = (sum_t p_t A_V[t]) @ W_v[:, kv]
  * (cache.py:385-387 + model.py:178-181): the K side is rematerialised on
- * tcgen05 as before (two KV heads per pass); the V side is one
+ * tcgen05 as before (four KV heads per pass); the V side is one
  * [kdim x n_q] tcgen05 GEMM over each 256-token tile's probabilities plus a
  * per-head projection through W_v at the end. kdim % 256 == 0. */
 

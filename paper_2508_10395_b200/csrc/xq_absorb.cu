@@ -274,6 +274,112 @@ __global__ void __launch_bounds__(256) k_q_frags(const float* __restrict__ q_pre
     out[(int64_t)b * n_ent + i] = q_frag_entry(qb, rope, rope_n, pos < 0 ? 0 : pos, q_scale, i, group);
 }
 
+// Grouped-query scores of KV heads KB .. KB+NK-1 of K pass ps for the 32 token rows
+// of TMEM lane quadrant q4 (the epilogue warps, and with HELP the second producer
+// group, which takes the upper half of a 4-head pass). Per m16 tile, K is read from
+// TMEM in the mma fragment order (16x256b), rotated in registers (FFMA2, cos/sin by
+// angle addition), rounded to fp16 as the A fragments and multiplied with the q
+// fragments (n = the 4 query heads of the KV head): 16 mma.sync per KV head and warp
+// replace the 4 x 128 FFMA2 and the q loads of the per-row form. The TMEM loads run
+// one (mt, c, kh) item ahead: the next item's two loads are issued right after the
+// wait for the current one (tcgen05.wait::ld waits for every outstanding load).
+// Scores land in sc [q head][128 rows] (-inf past the sequence end).
+template <int KH, int KB, int NK, int GROUP>
+XQ_DEVINL void gqa_scores(uint32_t tmem_acc, int q4, int lane, int ps, int n_kv, int tok0, int len,
+                          uint32_t q_a, uint32_t ro_a, uint32_t rb_a, uint32_t sc_a) {
+  const int g = lane >> 2, tig = lane & 3;
+  constexpr int NI = 2 * 4 * NK;  // (mt, c, kh) items
+  uint32_t kbe[2][8], kbo[2][8];  // ping-pong K fragments (even / odd halves)
+  auto issue = [&](int it, uint32_t(&ek)[8], uint32_t(&ok)[8]) {
+    const int mt = it / (4 * NK), c = (it / NK) & 3, kh = KB + it % NK;
+    const uint32_t base =
+        tmem_acc + (static_cast<uint32_t>(q4 * 32 + 16 * mt) << 16) + kh * 128 + c * 16;
+    tmem_ld16x256b_x2(base, ek);
+    tmem_ld16x256b_x2(base + 64, ok);
+  };
+  issue(0, kbe[0], kbo[0]);
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int r1m = 2 * q4 + mt;
+    float acc[NK][4];
+#pragma unroll
+    for (int j = 0; j < NK; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[j][i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      // cos/sin of rows (g, g+8) x frequencies 16c + 2*tig + {0, 1, 8, 9}, in the
+      // fragment register order: i -> row (i & 2 ? g+8 : g), j + (i & 1) + (i & 4 ? 8 : 0)
+      float2 cs8[8];
+      {
+        const int j0 = 16 * c + 2 * tig;
+        const float4 b0 = lds_f4(rb_a + 8u * (r1m * 64 + j0));
+        const float4 b1 = lds_f4(rb_a + 8u * (r1m * 64 + j0 + 8));
+        const float4 o00 = lds_f4(ro_a + 8u * (g * 64 + j0));
+        const float4 o01 = lds_f4(ro_a + 8u * (g * 64 + j0 + 8));
+        const float4 o10 = lds_f4(ro_a + 8u * ((g + 8) * 64 + j0));
+        const float4 o11 = lds_f4(ro_a + 8u * ((g + 8) * 64 + j0 + 8));
+        auto cmul = [](float bx, float by, float ox, float oy) {
+          return make_float2(bx * ox - by * oy, by * ox + bx * oy);
+        };
+        cs8[0] = cmul(b0.x, b0.y, o00.x, o00.y);
+        cs8[1] = cmul(b0.z, b0.w, o00.z, o00.w);
+        cs8[2] = cmul(b0.x, b0.y, o10.x, o10.y);
+        cs8[3] = cmul(b0.z, b0.w, o10.z, o10.w);
+        cs8[4] = cmul(b1.x, b1.y, o01.x, o01.y);
+        cs8[5] = cmul(b1.z, b1.w, o01.z, o01.w);
+        cs8[6] = cmul(b1.x, b1.y, o11.x, o11.y);
+        cs8[7] = cmul(b1.z, b1.w, o11.z, o11.w);
+      }
+#pragma unroll
+      for (int j = 0; j < NK; ++j) {
+        const int kvh = KH * ps + KB + j;
+        const int itm = (mt * 4 + c) * NK + j;  // compile time after unrolling
+        tmem_wait_ld();
+        if (itm + 1 < NI) issue(itm + 1, kbe[(itm + 1) & 1], kbo[(itm + 1) & 1]);
+        if (kvh < n_kv) {
+          const uint32_t(&ek)[8] = kbe[itm & 1];
+          const uint32_t(&ok)[8] = kbo[itm & 1];
+          uint32_t are[4], aro[4];
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) {  // RoPE (linalg.py:92-93) of two values
+            const float2 e = make_float2(__uint_as_float(ek[2 * q2]), __uint_as_float(ek[2 * q2 + 1]));
+            const float2 o = make_float2(__uint_as_float(ok[2 * q2]), __uint_as_float(ok[2 * q2 + 1]));
+            const float2 cv = make_float2(cs8[2 * q2].x, cs8[2 * q2 + 1].x);
+            const float2 sv = make_float2(cs8[2 * q2].y, cs8[2 * q2 + 1].y);
+            const float2 nsv = make_float2(-sv.x, -sv.y);
+            const float2 re = __ffma2_rn(e, cv, __fmul2_rn(o, nsv));
+            const float2 ro = __ffma2_rn(e, sv, __fmul2_rn(o, cv));
+            are[q2] = as_u32(__float22half2_rn(re));
+            aro[q2] = as_u32(__float22half2_rn(ro));
+          }
+          const uint2 qe = lds64(q_a + 8u * ((kvh * 8 + c) * 32 + lane));
+          const uint2 qo = lds64(q_a + 8u * ((kvh * 8 + 4 + c) * 32 + lane));
+          mma_16816_f16(acc[j], are, qe.x, qe.y);
+          mma_16816_f16(acc[j], aro, qo.x, qo.y);
+        }
+      }
+    }
+    // D fragment: (row g, heads 2tig, 2tig+1), (row g+8, the same heads)
+    const int rowa = q4 * 32 + 16 * mt + g;
+    const int toka = tok0 + rowa;
+    const bool va = toka < len, vb = toka + 8 < len;
+    if (2 * tig < GROUP) {
+#pragma unroll
+      for (int j = 0; j < NK; ++j) {
+        const int kvh = KH * ps + KB + j;
+        if (kvh < n_kv) {
+          const uint32_t s0 = sc_a + 4u * ((kvh * GROUP + 2 * tig) * kTileM + rowa);
+          sts_f32(s0, va ? acc[j][0] : -INFINITY);
+          sts_f32(s0 + 4u * kTileM, va ? acc[j][1] : -INFINITY);
+          sts_f32(s0 + 32u, vb ? acc[j][2] : -INFINITY);
+          sts_f32(s0 + 4u * kTileM + 32u, vb ? acc[j][3] : -INFINITY);
+        }
+      }
+    }
+  }
+}
+
 template <int AK, int AV, int BITS, int GROUP>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_decode_absorbed(const __grid_constant__ CUtensorMap tmap_w,
@@ -335,6 +441,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr bool kMmaScores = GROUP == 4;
   constexpr int STAGES = CF::kStages;
   constexpr int KH = CF::KH;
+  // HELP: the second producer group (warps 8-11, TMEM lane quadrants 0-3) drains the
+  // upper two KV heads of each 4-head GQA pass while the epilogue drains the lower
+  // two. The drain is latency-bound (one warp per SM sub-partition); with one
+  // 512-column accumulator the MMA waits for it before every pass.
+  constexpr bool kHelp = kMmaScores && KH == 4 && !ACC;
   constexpr uint32_t kABStage = CF::kABStage;
   constexpr uint32_t kBBytes = CF::kBBytes;
   const int CSTAGES = p.cstages;
@@ -355,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], kHelp ? 16 : 8);  // epilogue (+ helper) warps of both CTAs
     }
     mbar_init(pready, 8);   // leader's: 4 epilogue warps per CTA
     mbar_init(xfull, 128);  // the peer's 128 epilogue threads (their scores landed here)
@@ -589,6 +700,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kProdWarp0 && warp < kEpiWarp0) {
     // ------------------------------------------------ dequant producers
+    // HELP (warps 8-11): after producing its stages of a K pass, drain the pass's
+    // upper two KV heads (scores -> sc_s), then go on with the next item's stages
+    uint32_t tch = 0;  // accumulator uses seen (K passes and V-side uses)
+    auto help = [&](const Tile& tl, int ps) {
+      if constexpr (kHelp) {
+        if (ps == 0) named_bar_sync(2, 256);  // the epilogue set up this tile's q / RoPE base
+        mbar_wait(&tfull[0], tch & 1u);
+        tc_fence_after();
+        gqa_scores<KH, KH / 2, KH / 2, GROUP>(tmem, warp & 3, lane, ps, p.n_kv,
+                                             tl.t * kPairM + static_cast<int>(rank) * kTileM, tl.len,
+                                             smem_u32(q_s), smem_u32(rope_off), smem_u32(rope_base),
+                                             smem_u32(sc_s));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[0]);
+          else mbar_arrive_remote(tempty_leader0);
+        }
+        ++tch;
+        if (ps == p.n_pass - 1) named_bar_arrive(3, 256);  // scores of the tile's last pass
+      }
+    };
     if constexpr (ACC) {
       // XQuant-CL accumulate (cache.py:472-481, Accumulator.add cache.py:139-146),
       // one tile ahead: the cluster's first tile is updated before anything reads
@@ -668,7 +801,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         advance();
       };
       walk<PIPE>(p, cluster, n_clusters,
-        [&](const Tile& tl, int) {
+        [&](const Tile& tl, int ps) {
           const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
           const int tok_k = tl.t * kPairM + static_cast<int>(rank) * kTileM + r;
           for (int g = gp; g < ngrp; g += 2)
@@ -680,8 +813,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                           p.k_resid, p.kdim, v, p.G);
                 },
                 [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_k.store(tile, v); });
+          if (kHelp && gp == 1) help(tl, ps);
         },
         [&](const Tile& tl) {
+          if (kHelp && gp == 1) tch += nuse;
           const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
           for (int g = gp; g < ngrp; g += 2)
             stages2(
@@ -698,6 +833,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 },
                 [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_v.store(tile + hh * kMNHalf, v); });
         });
+    } else if constexpr (kHelp) {  // fp16-row A by TMA: the producer warps only help
+      if (warp >= kProdWarp0 + 4)
+        walk<PIPE>(p, cluster, n_clusters, [&](const Tile& tl, int ps) { help(tl, ps); },
+                   [&](const Tile&) { tch += nuse; });
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------ epilogue (this CTA's 128 rows)
@@ -759,6 +898,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       named_bar_sync(1, 128);
+      if constexpr (kHelp) named_bar_arrive(2, 256);  // q / RoPE base ready for the helpers
 #ifdef XQ_ROLE_PROFILE
       prof_acc[15] += clock64() - pt_s;
 #endif
@@ -784,99 +924,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
         tc_fence_after();
         if constexpr (kMmaScores) {
-          // Grouped-query scores on the tensor cores: per m16 tile of this warp's 32
-          // token rows, K is read from TMEM in the mma fragment order (16x256b),
-          // rotated in registers (FFMA2, cos/sin by angle addition), rounded to fp16
-          // as the A fragments, and multiplied with the q fragments (n = the 4 query
-          // heads of the KV head): 16 mma.sync per KV head and warp replace the
-          // 4 x 128 FFMA2 and the q loads of the per-row form.
-          const int g = lane >> 2, tig = lane & 3;
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            const uint32_t lane_addr = static_cast<uint32_t>(ew * 32 + 16 * mt) << 16;
-            const int r1m = 2 * ew + mt;
-            float acc[KH][4];
-#pragma unroll
-            for (int kh = 0; kh < KH; ++kh)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) acc[kh][i] = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              // cos/sin of rows (g, g+8) x frequencies 16c + 2*tig + {0, 1, 8, 9}, in the
-              // fragment register order: i -> row (i & 2 ? g+8 : g), j + (i & 1) + (i & 4 ? 8 : 0)
-              float2 cs8[8];
-              {
-                const int j0 = 16 * c + 2 * tig;
-                const float4 b0 = lds_f4(rb_a + 8u * (r1m * 64 + j0));
-                const float4 b1 = lds_f4(rb_a + 8u * (r1m * 64 + j0 + 8));
-                const float4 o00 = lds_f4(ro_a + 8u * (g * 64 + j0));
-                const float4 o01 = lds_f4(ro_a + 8u * (g * 64 + j0 + 8));
-                const float4 o10 = lds_f4(ro_a + 8u * ((g + 8) * 64 + j0));
-                const float4 o11 = lds_f4(ro_a + 8u * ((g + 8) * 64 + j0 + 8));
-                auto cmul = [](float bx, float by, float ox, float oy) {
-                  return make_float2(bx * ox - by * oy, by * ox + bx * oy);
-                };
-                cs8[0] = cmul(b0.x, b0.y, o00.x, o00.y);
-                cs8[1] = cmul(b0.z, b0.w, o00.z, o00.w);
-                cs8[2] = cmul(b0.x, b0.y, o10.x, o10.y);
-                cs8[3] = cmul(b0.z, b0.w, o10.z, o10.w);
-                cs8[4] = cmul(b1.x, b1.y, o01.x, o01.y);
-                cs8[5] = cmul(b1.z, b1.w, o01.z, o01.w);
-                cs8[6] = cmul(b1.x, b1.y, o11.x, o11.y);
-                cs8[7] = cmul(b1.z, b1.w, o11.z, o11.w);
-              }
-#pragma unroll
-              for (int kh = 0; kh < KH; ++kh) {
-                const int kvh = KH * ps + kh;
-                if (kvh < p.n_kv) {
-                  uint32_t ek[8], ok[8];
-#ifdef XQ_EXP_NOSCORE  // timing experiment only: the epilogue without the K reads
-                  for (int i = 0; i < 8; ++i) ek[i] = ok[i] = 0u;
-#else
-                  tmem_ld16x256b_x2(tmem + lane_addr + a * 256 + kh * 128 + c * 16, ek);
-                  tmem_ld16x256b_x2(tmem + lane_addr + a * 256 + kh * 128 + 64 + c * 16, ok);
-                  tmem_wait_ld();
-#endif
-                  uint32_t are[4], aro[4];
-#pragma unroll
-                  for (int q2 = 0; q2 < 4; ++q2) {  // RoPE (linalg.py:92-93) of two values
-                    const float2 e = make_float2(__uint_as_float(ek[2 * q2]),
-                                                 __uint_as_float(ek[2 * q2 + 1]));
-                    const float2 o = make_float2(__uint_as_float(ok[2 * q2]),
-                                                 __uint_as_float(ok[2 * q2 + 1]));
-                    const float2 cv = make_float2(cs8[2 * q2].x, cs8[2 * q2 + 1].x);
-                    const float2 sv = make_float2(cs8[2 * q2].y, cs8[2 * q2 + 1].y);
-                    const float2 nsv = make_float2(-sv.x, -sv.y);
-                    const float2 re = __ffma2_rn(e, cv, __fmul2_rn(o, nsv));
-                    const float2 ro = __ffma2_rn(e, sv, __fmul2_rn(o, cv));
-                    are[q2] = as_u32(__float22half2_rn(re));
-                    aro[q2] = as_u32(__float22half2_rn(ro));
-                  }
-                  const uint2 qe = lds64(q_a + 8u * ((kvh * 8 + c) * 32 + lane));
-                  const uint2 qo = lds64(q_a + 8u * ((kvh * 8 + 4 + c) * 32 + lane));
-                  mma_16816_f16(acc[kh], are, qe.x, qe.y);
-                  mma_16816_f16(acc[kh], aro, qo.x, qo.y);
-                }
-              }
-            }
-            // D fragment: (row g, heads 2tig, 2tig+1), (row g+8, the same heads)
-            const int rowa = ew * 32 + 16 * mt + g;
-            const int toka = t * kPairM + static_cast<int>(rank) * kTileM + rowa;
-            const bool va = toka < len, vb = toka + 8 < len;
-            if (2 * tig < GROUP) {
-#pragma unroll
-              for (int kh = 0; kh < KH; ++kh) {
-                const int kvh = KH * ps + kh;
-                if (kvh < p.n_kv) {
-                  const uint32_t s0 = sc_a + 4u * ((kvh * GROUP + 2 * tig) * kTileM + rowa);
-                  sts_f32(s0, va ? acc[kh][0] : -INFINITY);
-                  sts_f32(s0 + 4u * kTileM, va ? acc[kh][1] : -INFINITY);
-                  sts_f32(s0 + 32u, vb ? acc[kh][2] : -INFINITY);
-                  sts_f32(s0 + 4u * kTileM + 32u, vb ? acc[kh][3] : -INFINITY);
-                }
-              }
-            }
-          }
+          // scores on the tensor cores (gqa_scores); with HELP the second producer
+          // group takes the pass's KV heads KH/2 .. KH-1 in parallel
+          const int tok0 = t * kPairM + static_cast<int>(rank) * kTileM;
+          if constexpr (kHelp)
+            gqa_scores<KH, 0, KH / 2, GROUP>(tmem + a * 256, ew, lane, ps, p.n_kv, tok0, len, q_a,
+                                            ro_a, rb_a, sc_a);
+          else
+            gqa_scores<KH, 0, KH, GROUP>(tmem + a * 256, ew, lane, ps, p.n_kv, tok0, len, q_a, ro_a,
+                                        rb_a, sc_a);
         } else {
         // K columns of a head come split (W_k rows arranged so): cols 0-63 hold
         // the first element of each RoPE pair, cols 64-127 the second, so
@@ -955,6 +1011,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         ++tc;
       if (ps == p.n_pass - 1) {
+      if constexpr (kHelp) named_bar_sync(3, 256);  // the helpers' scores are in sc_s
       // ---- exchange: the peer owns query heads [peer*nbh, peer*nbh + nbh)
 #ifdef XQ_ROLE_PROFILE
       const long long pt_x = clock64();
@@ -1093,8 +1150,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #ifdef XQ_ROLE_PROFILE
         prof_acc[14] += clock64() - pt_v;
 #endif
-          if (leader) mbar_arrive(&tempty[a]);
-          else mbar_arrive_remote(tempty_leader0 + 8 * a);
+#pragma unroll
+          for (int k = 0; k < (kHelp ? 2 : 1); ++k) {  // HELP: also the helper's share
+            if (leader) mbar_arrive(&tempty[a]);
+            else mbar_arrive_remote(tempty_leader0 + 8 * a);
+          }
         }
       }
       });

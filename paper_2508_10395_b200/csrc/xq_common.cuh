@@ -185,6 +185,9 @@ XQ_DEVINL void fence_proxy_async_smem() {
 XQ_DEVINL void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+XQ_DEVINL void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // ---------------------------------------------------------------- TMA
 XQ_DEVINL void tma_prefetch_desc(const CUtensorMap* map) {
