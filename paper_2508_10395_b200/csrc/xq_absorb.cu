@@ -37,6 +37,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "xq_common.cuh"
 #include "xq_dequant.cuh"
 #include "xq_host.h"
@@ -446,6 +448,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // two. The drain is latency-bound (one warp per SM sub-partition); with one
   // 512-column accumulator the MMA waits for it before every pass.
   constexpr bool kHelp = kMmaScores && KH == 4 && !ACC;
+  // PACKV: a V-side A stage is 16 KB of the 48 KB ring slot, so with dequant
+  // producers both A stages of a V codes stage share one slot (one empty wait and
+  // one full arrival): the ring holds twice the V stages the producers can fill
+  // while the epilogue runs the softmax, and the V side (producer-bound: its MMAs
+  // are N = heads) starts from a deeper buffer
+  constexpr bool kPackV = PROD && CF::kABStage >= 2 * kABytes;
+  constexpr int kVSub = kPackV ? 2 : 1;  // V A stages per ring slot
   constexpr uint32_t kABStage = CF::kABStage;
   constexpr uint32_t kBBytes = CF::kBBytes;
   const int CSTAGES = p.cstages;
@@ -548,7 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       [&](const Tile& tl) {
         const int32_t row_tile = static_cast<int32_t>((int64_t)tl.b * p.L_max + tl.t * kPairM);
       for (int bb = 0; bb < nblk; ++bb) {
-        for (int j = 0; j < 4; ++j, ++it) {
+        for (int j = 0; j < 4; j += kVSub, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           XQ_PROF(0, mbar_wait(&empty[s], ph ^ 1));
           if (elect_one()) {
@@ -620,16 +629,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
             const uint32_t d = tmem + a * 256 + bi * p.nb;
-            for (int j = 0; j < 4; ++j, ++it) {
+            for (int j0 = 0; j0 < 4; j0 += kVSub, ++it) {
               const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
               XQ_PROF(4, mbar_wait_cluster(&full[s], ph));
               tc_fence_after();
-              const uint64_t ad = descv0 + ((s * kABStage) >> 4);
-              const uint64_t bd = descp0 + ((j * pstage) >> 4);
               if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)  // 16 tokens = two 8-row K groups = 2048 B of A
-                  mma2_f16_ss(d, ad + k * (2048 >> 4), bd + 2 * k, kIdescV, (j | k) != 0);
+                for (int js = 0; js < kVSub; ++js) {  // the slot's A stages (token quarters)
+                  const int j = j0 + js;
+                  const uint64_t ad = descv0 + ((s * kABStage + js * kABytes) >> 4);
+                  const uint64_t bd = descp0 + ((j * pstage) >> 4);
+#pragma unroll
+                  for (int k = 0; k < 4; ++k)  // 16 tokens = two 8-row K groups = 2048 B of A
+                    mma2_f16_ss(d, ad + k * (2048 >> 4), bd + 2 * k, kIdescV, (j | k) != 0);
+                }
                 mma2_commit_both(&empty[s]);
               }
               __syncwarp();
@@ -761,45 +774,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // by 2 per stage, A stages by 4
       uint32_t cs = static_cast<uint32_t>(gp), cph = 0;
       if (cs >= static_cast<uint32_t>(CSTAGES)) cs -= CSTAGES;  // (CSTAGES >= 2)
-      uint32_t as = static_cast<uint32_t>(2 * gp) % STAGES, aph = (2 * gp) / STAGES;
-      auto advance = [&]() {
+      // ai: running ring-slot index of this group's next A stage. K items use two
+      // slots per codes stage (this group's at 2*gp + 4k + h of the item); packed V
+      // items one (gp + 2k), entered with ai -= gp and left with ai += gp
+      uint32_t ai = static_cast<uint32_t>(2 * gp);
+      auto advance = [&](uint32_t slots) {
         cs += 2;
         if (cs >= static_cast<uint32_t>(CSTAGES)) {
           cs -= CSTAGES;
           cph ^= 1u;
         }
-        as += 4;
-        while (as >= STAGES) {
-          as -= STAGES;
-          aph ^= 1u;
-        }
+        ai += 2 * slots;
       };
       // two A stages per codes stage; fill(tile address, h) writes stage h
       // two A stages per codes stage: once stage h is free, conv(st, h, v) converts
       // it into registers and store(tile, h, v) writes it (measured: converting
       // before the wait and releasing the codes stage early did not change C2/C4)
-      auto stages2 = [&](auto&& conv, auto&& store) {
+      // packed (V side with PACKV): both A stages into one slot, at +h * 16 KB
+      auto stages2 = [&](auto&& conv, auto&& store, auto packed_c) {
+        constexpr bool packed = decltype(packed_c)::value;
         const uint32_t st = sC_a + cs * p.cstage_bytes;
         XQ_PROF(6, mbar_wait(&cfull[cs], cph));
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
-          uint32_t s = as + h, ph = aph;
-          if (s >= STAGES) {
-            s -= STAGES;
-            ph ^= 1u;
-          }
-          XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
+          const uint32_t idx = packed ? ai : ai + h;
+          const uint32_t s = idx % STAGES, ph = (idx / STAGES) & 1u;
+          if (!packed || h == 0) XQ_PROF(7, mbar_wait(&empty[s], ph ^ 1));
           uint32_t v[32];
           conv(st, h, v);
-          store(sAB_a + s * kABStage, h, v);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (leader) mbar_arrive_if(&full[s], lane == 0);
-          else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
+          store(sAB_a + s * kABStage + (packed ? h * kABytes : 0u), h, v);
+          if (!packed || h == 1) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (leader) mbar_arrive_if(&full[s], lane == 0);
+            else mbar_arrive_remote_if(full_leader0 + 8 * s, lane == 0);
+          }
         }
         mbar_arrive_if(&cempty[cs], lane == 0);
-        advance();
+        advance(packed ? 1u : 2u);
       };
+      using Unpacked = std::integral_constant<bool, false>;
+      using PackedV = std::integral_constant<bool, kPackV>;
       walk<PIPE>(p, cluster, n_clusters,
         [&](const Tile& tl, int ps) {
           const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
@@ -812,11 +827,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                           p.k_first ? p.k_first + (int64_t)tl.b * p.L_max + tok_k : nullptr,
                                           p.k_resid, p.kdim, v, p.G);
                 },
-                [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_k.store(tile, v); });
+                [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_k.store(tile, v); }, Unpacked());
           if (kHelp && gp == 1) help(tl, ps);
         },
         [&](const Tile& tl) {
           if (kHelp && gp == 1) tch += nuse;
+          if (kPackV) ai -= static_cast<uint32_t>(gp);
           const int nfl = (AK == XQ_A_CODES_CHANNEL) ? __ldg(p.k_nflushed + tl.b) : 0;
           for (int g = gp; g < ngrp; g += 2)
             stages2(
@@ -831,7 +847,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     convert_chunk<AV, BITS>(st, st + 128 * 16 * BITS, crow, tok < tl.len, tok, tl.b,
                                             nfl, 2 * gv + hh, nullptr, p.k_resid, p.kdim, v);
                 },
-                [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_v.store(tile + hh * kMNHalf, v); });
+                [&](uint32_t tile, int, const uint32_t(&v)[32]) { sw_v.store(tile + hh * kMNHalf, v); },
+                PackedV());
+          if (kPackV) ai += static_cast<uint32_t>(gp);
         });
     } else if constexpr (kHelp) {  // fp16-row A by TMA: the producer warps only help
       if (warp >= kProdWarp0 + 4)
