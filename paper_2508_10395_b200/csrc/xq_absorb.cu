@@ -286,9 +286,16 @@ __global__ void __launch_bounds__(256) k_q_frags(const float* __restrict__ q_pre
 // one (mt, c, kh) item ahead: the next item's two loads are issued right after the
 // wait for the current one (tcgen05.wait::ld waits for every outstanding load).
 // Scores land in sc [q head][128 rows] (-inf past the sequence end).
+// kv_of(ps, kh): the KV head in accumulator slot kh of pass ps (see SPLIT in the
+// kernel); the q fragments are stored in pass order (slot KH*ps + kh).
+template <int KH>
+XQ_DEVINL int kv_of(bool split, int ps, int kh) {
+  return split ? (kh & 1) + 2 * ps + 4 * (kh >> 1) : KH * ps + kh;
+}
+
 template <int KH, int KB, int NK, int GROUP>
-XQ_DEVINL void gqa_scores(uint32_t tmem_acc, int q4, int lane, int ps, int n_kv, int tok0, int len,
-                          uint32_t q_a, uint32_t ro_a, uint32_t rb_a, uint32_t sc_a) {
+XQ_DEVINL void gqa_scores(uint32_t tmem_acc, int q4, int lane, int ps, bool split, int n_kv, int tok0,
+                          int len, uint32_t q_a, uint32_t ro_a, uint32_t rb_a, uint32_t sc_a) {
   const int g = lane >> 2, tig = lane & 3;
   constexpr int NI = 2 * 4 * NK;  // (mt, c, kh) items
   uint32_t kbe[2][8], kbo[2][8];  // ping-pong K fragments (even / odd halves)
@@ -335,7 +342,8 @@ XQ_DEVINL void gqa_scores(uint32_t tmem_acc, int q4, int lane, int ps, int n_kv,
       }
 #pragma unroll
       for (int j = 0; j < NK; ++j) {
-        const int kvh = KH * ps + KB + j;
+        const int slot = KH * ps + KB + j;  // q fragments in pass order
+        const int kvh = kv_of<KH>(split, ps, KB + j);
         const int itm = (mt * 4 + c) * NK + j;  // compile time after unrolling
         tmem_wait_ld();
         if (itm + 1 < NI) issue(itm + 1, kbe[(itm + 1) & 1], kbo[(itm + 1) & 1]);
@@ -355,8 +363,8 @@ XQ_DEVINL void gqa_scores(uint32_t tmem_acc, int q4, int lane, int ps, int n_kv,
             are[q2] = as_u32(__float22half2_rn(re));
             aro[q2] = as_u32(__float22half2_rn(ro));
           }
-          const uint2 qe = lds64(q_a + 8u * ((kvh * 8 + c) * 32 + lane));
-          const uint2 qo = lds64(q_a + 8u * ((kvh * 8 + 4 + c) * 32 + lane));
+          const uint2 qe = lds64(q_a + 8u * ((slot * 8 + c) * 32 + lane));
+          const uint2 qo = lds64(q_a + 8u * ((slot * 8 + 4 + c) * 32 + lane));
           mma_16816_f16(acc[j], are, qe.x, qe.y);
           mma_16816_f16(acc[j], aro, qo.x, qo.y);
         }
@@ -369,7 +377,7 @@ XQ_DEVINL void gqa_scores(uint32_t tmem_acc, int q4, int lane, int ps, int n_kv,
     if (2 * tig < GROUP) {
 #pragma unroll
       for (int j = 0; j < NK; ++j) {
-        const int kvh = KH * ps + KB + j;
+        const int kvh = kv_of<KH>(split, ps, KB + j);
         if (kvh < n_kv) {
           const uint32_t s0 = sc_a + 4u * ((kvh * GROUP + 2 * tig) * kTileM + rowa);
           sts_f32(s0, va ? acc[j][0] : -INFINITY);
@@ -448,6 +456,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // two. The drain is latency-bound (one warp per SM sub-partition); with one
   // 512-column accumulator the MMA waits for it before every pass.
   constexpr bool kHelp = kMmaScores && KH == 4 && !ACC;
+  // SPLIT (8 KV heads, 4 query heads each, two passes): pass ps takes KV heads
+  // {2ps, 2ps+1, 2ps+4, 2ps+5}, so each CTA gets half of the query heads it owns
+  // (rank r owns KV heads 4r..4r+3) from each pass, and the score exchange and
+  // softmax of those heads run after pass 0 under pass 1's MMAs instead of all
+  // after pass 1. The pass-0 q fragments (pass order) are dead by then, so P
+  // (8 KB, aliasing them) can be written early.
+  const bool split = kMmaScores && KH == 4 && p.n_kv == 2 * KH;
   // PACKV: a V-side A stage is 16 KB of the 48 KB ring slot, so with dequant
   // producers both A stages of a V codes stage share one slot (one empty wait and
   // one full arrival): the ring holds twice the V stages the producers can fill
@@ -540,9 +555,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (leader) mbar_arrive_expect_tx(&full[s], kTx);
             else mbar_arrive_remote(full_leader0 + 8 * s);
 #pragma unroll
-            for (int sub = 0; sub < KH / 2; ++sub)  // KV head KH*ps + 2*sub + rank
+            for (int sub = 0; sub < KH / 2; ++sub)  // KV head kv_of(ps, 2*sub + rank)
               tma_load_2d_pair(st + kABytes + sub * kBSub, &tmap_w, &full[s], kcc * kChunk,
-                               (KH * ps + 2 * sub + static_cast<int>(rank)) * 128, p.w_hint);
+                               kv_of<KH>(split, ps, 2 * sub + static_cast<int>(rank)) * 128, p.w_hint);
             if (a_tma)
               // split: the first half of a sweep is the part the previous
               // sweep left in L2 (demote it), the second half is what the next
@@ -721,7 +736,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (ps == 0) named_bar_sync(2, 256);  // the epilogue set up this tile's q / RoPE base
         mbar_wait(&tfull[0], tch & 1u);
         tc_fence_after();
-        gqa_scores<KH, KH / 2, KH / 2, GROUP>(tmem, warp & 3, lane, ps, p.n_kv,
+        gqa_scores<KH, KH / 2, KH / 2, GROUP>(tmem, warp & 3, lane, ps, split, p.n_kv,
                                              tl.t * kPairM + static_cast<int>(rank) * kTileM, tl.len,
                                              smem_u32(q_s), smem_u32(rope_off), smem_u32(rope_base),
                                              smem_u32(sc_s));
@@ -732,7 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           else mbar_arrive_remote(tempty_leader0);
         }
         ++tch;
-        if (ps == p.n_pass - 1) named_bar_arrive(3, 256);  // scores of the tile's last pass
+        if (split || ps == p.n_pass - 1) named_bar_arrive(3, 256);  // scores the exchange reads
       }
     };
     if constexpr (ACC) {
@@ -880,7 +895,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                : p.rope[(int64_t)(i >> 4) * p.rope_n + (i & 15)];
     const int r0 = row & 15, r1 = row >> 4;
     const uint32_t stg_a = smem_u32(smem + p.off_stg);
-    uint32_t tc = 0, ti = 0;
+    uint32_t tc = 0, ti = 0, xc = 0;  // xc: score exchanges (xread / xfull phase)
     walk<PIPE>(p, cluster, n_clusters,
       [&](const Tile& tl, int ps) {
       const int b = tl.b, t = tl.t, len = tl.len;
@@ -903,7 +918,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll 8
         for (int i = et; i < n_ent4; i += 128) {
           const uint4 v = __ldg(src + i);
-          sts128(q_a + 16u * i, v.x, v.y, v.z, v.w);
+          const int kvh = i >> 7;  // stored in pass order: slot KH*ps + kh of kv_of(ps, kh)
+          const int slot = split ? ((kvh >> 1) & 1) * KH + (kvh & 1) + 2 * (kvh >> 2) : kvh;
+          sts128(q_a + 16u * (slot * 128 + (i & 127)), v.x, v.y, v.z, v.w);
         }
       } else {
         const float2 cs = p.rope[(int64_t)(et >> 1) * p.rope_n + pos];
@@ -946,11 +963,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // group takes the pass's KV heads KH/2 .. KH-1 in parallel
           const int tok0 = t * kPairM + static_cast<int>(rank) * kTileM;
           if constexpr (kHelp)
-            gqa_scores<KH, 0, KH / 2, GROUP>(tmem + a * 256, ew, lane, ps, p.n_kv, tok0, len, q_a,
-                                            ro_a, rb_a, sc_a);
+            gqa_scores<KH, 0, KH / 2, GROUP>(tmem + a * 256, ew, lane, ps, split, p.n_kv, tok0, len,
+                                            q_a, ro_a, rb_a, sc_a);
           else
-            gqa_scores<KH, 0, KH, GROUP>(tmem + a * 256, ew, lane, ps, p.n_kv, tok0, len, q_a, ro_a,
-                                        rb_a, sc_a);
+            gqa_scores<KH, 0, KH, GROUP>(tmem + a * 256, ew, lane, ps, split, p.n_kv, tok0, len, q_a,
+                                        ro_a, rb_a, sc_a);
         } else {
         // K columns of a head come split (W_k rows arranged so): cols 0-63 hold
         // the first element of each RoPE pair, cols 64-127 the second, so
@@ -1018,8 +1035,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         }  // per-row FFMA scores
+        // exchange + softmax after this pass: every pass with SPLIT, else the last
+        const bool xpass = split || ps == p.n_pass - 1;
         tc_fence_before();
         __syncwarp();
+        // HELP: the helpers' scores of this pass are in sc_s (synced before the
+        // accumulator is released, so the helpers cannot arrive for the next pass
+        // before this wait)
+        if (kHelp && xpass) named_bar_sync(3, 256);
         if (lane == 0) {
 #ifdef XQ_ROLE_PROFILE
         prof_acc[12] += clock64() - pt_k;
@@ -1028,8 +1051,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           else mbar_arrive_remote(tempty_leader0 + 8 * a);
         }
         ++tc;
-      if (ps == p.n_pass - 1) {
-      if constexpr (kHelp) named_bar_sync(3, 256);  // the helpers' scores are in sc_s
+      if (xpass) {
+      // this exchange's local heads [h0, h1) (and the peer's same-numbered heads)
+      const int h0 = split ? ps * (nbh / 2) : 0;
+      const int h1 = split ? h0 + nbh / 2 : nbh;
       // ---- exchange: the peer owns query heads [peer*nbh, peer*nbh + nbh)
 #ifdef XQ_ROLE_PROFILE
       const long long pt_x = clock64();
@@ -1041,45 +1066,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int hl = 0; hl < kMaxHeads / 2; ++hl) {
           const int h = static_cast<int>(peer) * nbh + hl;
-          outv[hl] = (hl < nbh && h < p.n_q) ? lds_f32(sc_a + 4u * (h * kTileM + row)) : -INFINITY;
+          outv[hl] = (hl >= h0 && hl < h1 && h < p.n_q) ? lds_f32(sc_a + 4u * (h * kTileM + row))
+                                                        : -INFINITY;
         }
         mbar_arrive_remote_release(xread_peer);        // my landing rows may be overwritten
-        XQ_PROF(9, mbar_wait_cluster(xread, ti & 1));  // the peer's landing rows are free
+        XQ_PROF(9, mbar_wait_cluster(xread, xc & 1));  // the peer's landing rows are free
 #pragma unroll
         for (int hl = 0; hl < kMaxHeads / 2; ++hl)
-          if (hl < nbh)  // into the peer's landing row of my head hl
+          if (hl >= h0 && hl < h1)  // into the peer's landing row of my head hl
             st_cluster_f32(sc_peer + 4u * ((static_cast<int>(rank) * nbh + hl) * kTileM + row),
                            outv[hl]);
         mbar_arrive_remote_release(xfull_peer);
-        XQ_PROF(9, mbar_wait_cluster(xfull, ti & 1));
+        XQ_PROF(9, mbar_wait_cluster(xfull, xc & 1));
+        ++xc;
       }
-      // ---- softmax over the 256 tokens of the tile for this CTA's heads -> P
+      // ---- softmax over the 256 tokens of the tile for heads [h0, h1) -> P
       named_bar_sync(1, 128);  // every epilogue warp is done with q_s (P overwrites it)
-      {
-        const int seg = et & 7;  // tokens seg*32 .. +31 of the pair tile
-        const int half = seg >> 2;
-        for (int hl = et >> 3; hl < nbh; hl += 16) {
+      // ST tokens per thread: 32 (8 threads per head) or, for the 8 heads of a SPLIT
+      // exchange, 16 (16 threads per head)
+      auto softmax = [&](auto st_c) {
+        constexpr int ST = decltype(st_c)::value;
+        constexpr int NSEG = 256 / ST;
+        constexpr int HPI = 128 / NSEG;  // heads per iteration
+        const int seg = et % NSEG;       // tokens seg*ST .. +ST-1 of the pair tile
+        const int tk0 = seg * ST;
+        const int half = tk0 / kTileM;
+        for (int hl = h0 + et / NSEG; hl < h1; hl += HPI) {
           const int h = static_cast<int>(rank) * nbh + hl;
           const uint32_t src = ((half == static_cast<int>(rank)) ? (sc_a + 4u * h * kTileM)
                                                                  : (land_a + 4u * hl * kTileM)) +
-                               4u * (seg & 3) * 32;
-          float s[32];
+                               4u * (tk0 % kTileM);
+          float s[ST];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < ST / 4; ++i) {
             const float4 v = (h < p.n_q) ? lds_f4(src + 16u * i)
                                          : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
             s[4 * i] = v.x; s[4 * i + 1] = v.y; s[4 * i + 2] = v.z; s[4 * i + 3] = v.w;
           }
           float m = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) m = fmaxf(m, s[i]);
-          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
-          float l = 0.f;
-          uint32_t pk[16];
+          for (int i = 0; i < ST; ++i) m = fmaxf(m, s[i]);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int o = 1; o < NSEG; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          float l = 0.f;
+          uint32_t pk[ST / 2];
+#pragma unroll
+          for (int i = 0; i < ST / 2; ++i) {
             const float p0 = (m == -INFINITY) ? 0.f : exp2f(s[2 * i] - m);
             const float p1 = (m == -INFINITY) ? 0.f : exp2f(s[2 * i + 1] - m);
             const __half2 hp = __floats2half2_rn(p0, p1);
@@ -1088,18 +1120,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             l += pr.x + pr.y;
             pk[i] = as_u32(hp);
           }
-          l += __shfl_xor_sync(0xffffffffu, l, 1);
-          l += __shfl_xor_sync(0xffffffffu, l, 2);
-          l += __shfl_xor_sync(0xffffffffu, l, 4);
-          // P stage j = seg/2 holds tokens 64j..64j+63 as one 128-byte row per head
-          const uint32_t pst = sP_a + (seg >> 1) * (nbh * 128);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            sts128(pst + sw128_offset(hl, (seg & 1) * 4 + c), pk[4 * c], pk[4 * c + 1],
+          for (int o = 1; o < NSEG; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+          // P stage j = tk0/64 holds tokens 64j..64j+63 as one 128-byte row per head
+          const uint32_t pst = sP_a + (tk0 / 64) * (nbh * 128);
+#pragma unroll
+          for (int c = 0; c < ST / 8; ++c)
+            sts128(pst + sw128_offset(hl, (tk0 % 64) / 8 + c), pk[4 * c], pk[4 * c + 1],
                    pk[4 * c + 2], pk[4 * c + 3]);
           if (seg == 0 && h < p.n_q)
             p.part_ml[((int64_t)b * p.n_tiles + t) * p.n_q + h] = make_float2(m, l);
         }
+      };
+      if (split) softmax(std::integral_constant<int, 16>());
+      else softmax(std::integral_constant<int, 32>());
+      if (ps == p.n_pass - 1) {  // P complete: the V side may start
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -1109,8 +1144,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (leader) mbar_arrive(pready);
           else mbar_arrive_remote(pready_leader);
         }
+        ++ti;
       }
-      ++ti;
       }
       },
       [&](const Tile& tl) {
