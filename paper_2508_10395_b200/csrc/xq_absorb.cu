@@ -1151,7 +1151,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       [&](const Tile& tl) {
       const int b = tl.b, t = tl.t;
       // ---- V side: drain O^T[channels x heads] of this tile
-      int blk = 0;
+      int blk = 0, vbatch = 0;
       for (int us = 0; us < nuse; ++us, ++tc) {
         const uint32_t a = CF::NBUF == 2 ? (tc & 1) : 0u;
         const uint32_t aph = CF::NBUF == 2 ? ((tc >> 1) & 1) : (tc & 1);
@@ -1161,19 +1161,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
         tc_fence_after();
         // each [n_q x 128-channel] block is staged in shared memory and written
-        // by one TMA bulk store. Staging buffers: the score region, plus the
-        // q/P region when this is the tile's only V-side accumulator use (with
-        // more uses, later uses' MMAs still read P while this one drains).
-        // (pipelined: the next tile's scores and q already live there -> a
+        // by one TMA bulk store. Staging buffers (8 KB at n_q = 32): both halves of
+        // the score region, plus both halves of the q/P region when this is the
+        // tile's only V-side accumulator use (with more uses, later uses' MMAs
+        // still read P while this one drains). Blocks go out in batches of that
+        // many buffers: one barrier and one store wait per batch, not per block.
+        // (pipelined: the next tile's scores and q already live there -> one
         // dedicated staging buffer)
-        const bool two_bufs = !PIPE && nuse == 1;
+        const int nbuf = PIPE ? 1 : (nuse == 1 ? 4 : 2);
+        const uint32_t blkb = 256u * p.n_q;  // bytes of one staged block
+        auto stg_of = [&](int k) -> uint32_t {
+          return PIPE ? stg_a : (k < 2 ? sc_a + k * blkb : q_a + (k - 2) * blkb);
+        };
+        int k = 0;  // position in the current batch
         for (int bi = 0; bi < bpu && blk < nblk; ++bi, ++blk) {
-          const uint32_t stg = PIPE ? stg_a : ((two_bufs && (blk & 1)) ? q_a : sc_a);
-          if (et == 0) {  // the store that last read `stg` is done
-            if (two_bufs) tma_store_wait_read<1>();
-            else tma_store_wait_read<0>();
+          const uint32_t stg = stg_of(k);
+          if (k == 0 && vbatch > 0) {  // the previous batch's stores have read the buffers
+            if (et == 0) tma_store_wait_read<0>();
+            named_bar_sync(1, 128);
           }
-          named_bar_sync(1, 128);
           for (int c16 = 0; c16 < p.nb / 16; ++c16) {
             float v[16];
             tmem_ld16(tmem + tlane + a * 256 + bi * p.nb + c16 * 16, v);
@@ -1189,12 +1195,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               }
             }
           }
-          fence_proxy_async_smem();
-          named_bar_sync(1, 128);
-          if (et == 0) {
-            tma_store_2d(&tmap_o, stg, blk * 256 + static_cast<int>(rank) * 128,
-                         static_cast<int32_t>(((int64_t)b * p.n_tiles + t) * p.n_q));
-            tma_store_commit();
+          ++k;
+          if (k == nbuf || bi + 1 == bpu || blk + 1 == nblk) {  // batch complete: store it
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (et == 0) {
+              for (int j = 0; j < k; ++j)
+                tma_store_2d(&tmap_o, stg_of(j), (blk - k + 1 + j) * 256 + static_cast<int>(rank) * 128,
+                             static_cast<int32_t>(((int64_t)b * p.n_tiles + t) * p.n_q));
+              tma_store_commit();
+            }
+            k = 0;
+            ++vbatch;
           }
         }
         tc_fence_before();
