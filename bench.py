@@ -616,7 +616,7 @@ def run_xquant(args, cfg):
         "prefill": prefill,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("k_decode_absorbed (+k_absorb_combine, k_absorb_project)" if absorbed
+                     "kernel": ("k_decode_absorbed (+k_absorb_finish: tile merge + W_v projection)" if absorbed
                                 else "k_decode_attend (+k_combine)"),
                      "flops_per_launch": flops_launch, "launch_us": per_launch * 1e6,
                      "flops_note": ("algorithmic FLOPs of the V-absorbed path (sysmodel.absorbed_flops); "

@@ -1583,12 +1583,189 @@ int dispatch_bits(int bits, const Maps& m, const Params& p, cudaStream_t st) {
   }
 }
 
+// k_absorb_combine + k_absorb_project in one launch. A cluster of 4 CTAs takes one
+// query head h and S sequences; CTA r merges the tile partials of channels
+// [r*kdim/4, (r+1)*kdim/4) into x (shared memory, fp32; 16-byte loads, 8 tiles in
+// flight) and projects them through its rows of W_v[:, kv(h)]; CTA 0 sums the four
+// [S x 128] partial projections over DSMEM and writes the outputs. Same arithmetic as
+// the two kernels up to the fp32 summation order of the projection.
+constexpr int kFinishCta = 4;
+template <int S>
+__global__ void __cluster_dims__(kFinishCta, 1, 1) __launch_bounds__(256)
+    k_absorb_finish(const __half* __restrict__ part_o, const float2* __restrict__ part_ml,
+                    const int32_t* __restrict__ seq_lens, int n_seqs, int n_tiles, int n_q,
+                    int group, int kdim, const __half* __restrict__ wv, const OutPtrs outs) {
+  extern __shared__ float fsm[];  // x [S][kq], then weights [S][n_tiles]
+  __shared__ float red[8][S][128];
+  __shared__ float inv_s[S];
+  __shared__ int nt_s[S];
+  const uint32_t r = cluster_ctarank();
+  const int h = blockIdx.x / kFinishCta, b0 = blockIdx.y * S, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int kq = kdim / kFinishCta, c0 = static_cast<int>(r) * kq;
+  float* xs = fsm;
+  float* wts = fsm + S * kq;
+  // weights of the tiles of sequence s (warp s): 2^(m_i - M), and 1 / L
+  for (int s = warp; s < S; s += 8) {
+    const int b = b0 + s;
+    int nt = 0;
+    float inv = 0.f;
+    if (b < n_seqs) {
+      nt = (seq_lens[b] + kPairM - 1) / kPairM;
+      const float2* ml = part_ml + (int64_t)b * n_tiles * n_q + h;
+      float M = -INFINITY;
+      for (int i = lane; i < nt; i += 32) M = fmaxf(M, ml[(int64_t)i * n_q].x);
+      M = warp_max(M);
+      float L = 0.f;
+      for (int i = lane; i < nt; i += 32) {
+        const float2 v = ml[(int64_t)i * n_q];
+        const float wgt = (v.x == -INFINITY) ? 0.f : exp2f(v.x - M);
+        wts[s * n_tiles + i] = wgt;
+        L = fmaf(wgt, v.y, L);
+      }
+      L = warp_sum(L);
+      inv = L > 0.f ? 1.f / L : 0.f;
+    }
+    if (lane == 0) {
+      nt_s[s] = nt;
+      inv_s[s] = inv;
+    }
+  }
+  __syncthreads();
+  // merge: item = (sequence, 8 channels of this CTA's quarter)
+  const int64_t stride = (int64_t)n_q * kdim;  // tile stride of the partials
+  for (int it = tid; it < S * (kq / 8); it += 256) {
+    const int s = it / (kq / 8), cl = 8 * (it % (kq / 8));
+    const int nt = nt_s[s];
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (nt > 0) {
+      const __half* po = part_o + (int64_t)(b0 + s) * n_tiles * stride + (int64_t)h * kdim + c0 + cl;
+      const float* w = wts + s * n_tiles;
+      int i = 0;
+      for (; i + 8 <= nt; i += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldcs(reinterpret_cast<const uint4*>(po + (int64_t)(i + k) * stride));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float wk = w[i + k];
+          const __half2* h2 = reinterpret_cast<const __half2*>(&v[k]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(h2[e]);
+            acc[2 * e] = fmaf(wk, f.x, acc[2 * e]);
+            acc[2 * e + 1] = fmaf(wk, f.y, acc[2 * e + 1]);
+          }
+        }
+      }
+      for (; i < nt; ++i) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(po + (int64_t)i * stride));
+        const float wk = w[i];
+        const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __half22float2(h2[e]);
+          acc[2 * e] = fmaf(wk, f.x, acc[2 * e]);
+          acc[2 * e + 1] = fmaf(wk, f.y, acc[2 * e + 1]);
+        }
+      }
+    }
+    const float inv = inv_s[s];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) xs[s * kq + cl + e] = acc[e] * inv;
+  }
+  __syncthreads();
+  // project this quarter: thread = (8-column group cg of 128, channel slice sl of 16)
+  const int cg = tid & 15, sl = tid >> 4;
+  const uint4* w16 = reinterpret_cast<const uint4*>(wv + ((int64_t)(h / group) * kdim + c0) * 128 + cg * 8);
+  float a[S][8];
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[s][j] = 0.f;
+#pragma unroll 4
+  for (int c = sl; c < kq; c += 16) {
+    const uint4 wr = __ldg(w16 + (int64_t)c * 16);
+    const __half2* w2 = reinterpret_cast<const __half2*>(&wr);
+    float wf[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __half22float2(w2[j]);
+      wf[2 * j] = f.x;
+      wf[2 * j + 1] = f.y;
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const float xv = xs[s * kq + c];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[s][j] = fmaf(xv, wf[j], a[s][j]);
+    }
+  }
+  // lanes l and l^16 hold slices 2w and 2w+1 of the same columns
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[s][j] += __shfl_xor_sync(0xffffffffu, a[s][j], 16);
+  if (lane < 16) {
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) red[warp][s][cg * 8 + j] = a[s][j];
+  }
+  __syncthreads();
+  // this CTA's partial projection [S][128] -> red[0]
+  for (int i = tid; i < S * 128; i += 256) {
+    const int s = i >> 7, j = i & 127;
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v += red[k][s][j];
+    red[0][s][j] = v;
+  }
+  cluster_sync();  // every CTA's partial is in its red[0]
+  if (r == 0) {
+    const uint32_t base = smem_u32(&red[0][0][0]);
+    for (int i = tid; i < S * 128; i += 256) {
+      const int s = i >> 7, j = i & 127;
+      if (b0 + s >= n_seqs) continue;
+      float v = red[0][s][j];
+#pragma unroll
+      for (int q = 1; q < kFinishCta; ++q) v += ld_cluster_f32(mapa_shared(base + 4u * i, q));
+      const int64_t o = ((int64_t)(b0 + s) * n_q + h) * kHeadDim + j;
+      for (int k = 0; k < outs.n; ++k) outs.p[k][o] = v;
+    }
+  }
+  cluster_sync();  // the peers' red[0] stays alive until CTA 0 has read it
+}
+
 // k_absorb_combine + k_absorb_project after a k_decode_absorbed launch
 int merge_and_project(const Params& p, const int32_t* seq_lens, int group,
                       const void* wv_arranged, const OutPtrs& op, cudaStream_t st) {
   int status;
   const int n_seqs = p.n_seqs, n_q = p.n_q;
   const int64_t kdim = p.kdim;
+#ifndef XQ_SPLIT_FINISH
+  if (kdim % (8 * kFinishCta) == 0) {
+    // sequences per cluster: the most (<= 8) that still gives >= 128 clusters
+    int S = 8;
+    while (S > 1 && (int64_t)n_q * ((n_seqs + S - 1) / S) < 128) S >>= 1;
+    const dim3 grid(kFinishCta * n_q, (n_seqs + S - 1) / S);
+    const size_t fsmem = (size_t)S * (kdim / kFinishCta + p.n_tiles) * sizeof(float);
+    const __half* wvh = static_cast<const __half*>(wv_arranged);
+    auto go = [&](auto kern) -> int {
+      int st2 = ensure_smem(reinterpret_cast<const void*>(kern), fsmem, "cudaFuncSetAttribute(finish)");
+      if (st2 != XQ_OK) return st2;
+      kern<<<grid, 256, fsmem, st>>>(p.part_o, p.part_ml, seq_lens, n_seqs, p.n_tiles, n_q, group,
+                                     static_cast<int>(kdim), wvh, op);
+      return check_launch("k_absorb_finish");
+    };
+    switch (S) {
+      case 8: return go(k_absorb_finish<8>);
+      case 4: return go(k_absorb_finish<4>);
+      case 2: return go(k_absorb_finish<2>);
+      default: return go(k_absorb_finish<1>);
+    }
+  }
+#endif
   float* x_attn = reinterpret_cast<float*>(p.part_ml + (int64_t)n_seqs * p.n_tiles * n_q);
   k_absorb_combine<<<dim3(n_seqs * n_q, static_cast<unsigned>((kdim + 511) / 512)), 128,
                      p.n_tiles * sizeof(float), st>>>(p.part_o, p.part_ml, seq_lens, p.n_tiles,

@@ -368,6 +368,11 @@ XQ_DEVINL void sts64(uint32_t addr, uint32_t a, uint32_t b) {
 
 // Store to the same-offset shared variable of another CTA of the cluster
 // (address from mapa_shared).
+XQ_DEVINL float ld_cluster_f32(uint32_t cluster_addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
 XQ_DEVINL void st_cluster_f32(uint32_t cluster_addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
 }

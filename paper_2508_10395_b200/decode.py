@@ -230,10 +230,13 @@ class Decoder:
             return 3  # kv_append, kv_decode, combine
         if self.variant == "kvq":
             return 2  # kvq decode, combine (+ quantizer launches on flushes)
-        # fused decode + merge: absorbed = fused, combine, project (+ the q fragments of
+        # fused decode + merge: absorbed = fused, then k_absorb_finish (combine + project
+        # in one launch when kdim % 32 == 0, else the two kernels) (+ the q fragments of
         # the grouped-query score mma); unabsorbed = fused, combine
-        absorbed = cache._use_absorbed(cache_kdim(cache), int(cache.n_tokens.max()))
-        attend = (4 if self.shape.kv_group == 4 else 3) if absorbed else 2
+        kdim = cache_kdim(cache)
+        absorbed = cache._use_absorbed(kdim, int(cache.n_tokens.max()))
+        merge = 1 if kdim % 32 == 0 else 2
+        attend = (1 + merge + (1 if self.shape.kv_group == 4 else 0)) if absorbed else 2
         if self.variant == "xq-gqa":
             return 1 + attend  # v-latent quantize (+ a K-latent flush every 128 steps)
         if self.variant == "xq-cl-gqa":  # latent64 (+ flush), fused + merge; the seed /
