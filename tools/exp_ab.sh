@@ -10,6 +10,6 @@ for v in "$@"; do
     XQ_LIB=$lib timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-fp16 \
       --no-prefill 2>/dev/null | python -c "import json,sys
 d=json.loads([l for l in sys.stdin if l.startswith('{')][-1])
-r=d['roofline']; print('${v:-base}', '$c', round(d['value'],2), 'launch_us', round(r['launch_us']), 'frac', round(r['frac'],3), 'MHz', d['clocks']['sm_mhz'], 'cyc_M', round(r['launch_us']*d['clocks']['sm_mhz']/1e6, 3))"
+r=d['roofline']; print('${v:-default}', '$c', round(d['value'],2), 'launch_us', round(r['launch_us']), 'frac', round(r['frac'],3), 'MHz', d['clocks']['sm_mhz'], 'cyc_M', round(r['launch_us']*d['clocks']['sm_mhz']/1e6, 3))"
   done
 done
