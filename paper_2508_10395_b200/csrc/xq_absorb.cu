@@ -269,11 +269,13 @@ __global__ void __launch_bounds__(256) k_q_frags(const float* __restrict__ q_pre
                                                  const int32_t* __restrict__ seq_lens, int n_q,
                                                  int n_kv, int group, float q_scale,
                                                  uint2* __restrict__ out) {
+  // block (sequence b, KV head blockIdx.y): one entry per thread (the RoPE table reads
+  // are scattered, so the launch is latency-bound; one entry deep keeps it short)
   const int b = blockIdx.x, n_ent = n_kv * 256;
   const int pos = seq_lens[b] - 1;
   const float* qb = q_pre + (int64_t)b * n_q * kHeadDim;
-  for (int i = threadIdx.x; i < n_ent; i += 256)
-    out[(int64_t)b * n_ent + i] = q_frag_entry(qb, rope, rope_n, pos < 0 ? 0 : pos, q_scale, i, group);
+  const int i = blockIdx.y * 256 + threadIdx.x;
+  out[(int64_t)b * n_ent + i] = q_frag_entry(qb, rope, rope_n, pos < 0 ? 0 : pos, q_scale, i, group);
 }
 
 // Grouped-query scores of KV heads KB .. KB+NK-1 of K pass ps for the 32 token rows
@@ -1562,7 +1564,7 @@ int launch(const Maps& m, Params p, cudaStream_t st) {
     return status;
   if constexpr (GROUP == 4) {  // the score mma's q fragments (spare half of the fp16 partials)
     uint2* qf = reinterpret_cast<uint2*>(p.part_o + (int64_t)p.n_seqs * p.n_tiles * p.n_q * p.kdim);
-    k_q_frags<<<p.n_seqs, 256, 0, st>>>(p.q_pre, p.rope, p.rope_n, p.seq_lens, p.n_q, p.n_kv, GROUP,
+    k_q_frags<<<dim3(p.n_seqs, p.n_kv), 256, 0, st>>>(p.q_pre, p.rope, p.rope_n, p.seq_lens, p.n_q, p.n_kv, GROUP,
                                         p.q_scale, qf);
     if ((status = check_launch("k_q_frags")) != XQ_OK) return status;
     p.q_frag = qf;
