@@ -470,7 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // one full arrival): the ring holds twice the V stages the producers can fill
   // while the epilogue runs the softmax, and the V side (producer-bound: its MMAs
   // are N = heads) starts from a deeper buffer
-  constexpr bool kPackV = PROD && CF::kABStage >= 2 * kABytes;
+  constexpr bool kPackV = CF::kABStage >= 2 * kABytes;  // (fp16-row A: two TMA boxes per slot)
   constexpr int kVSub = kPackV ? 2 : 1;  // V A stages per ring slot
   constexpr uint32_t kABStage = CF::kABStage;
   constexpr uint32_t kBBytes = CF::kBBytes;
@@ -583,13 +583,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (leader) mbar_arrive(&full[s]);
               else mbar_arrive_remote(full_leader0 + 8 * s);
             } else {
-              if (leader) mbar_arrive_expect_tx(&full[s], 2 * kABytes);
+              if (leader) mbar_arrive_expect_tx(&full[s], 2 * kABytes * kVSub);
               else mbar_arrive_remote(full_leader0 + 8 * s);
 #pragma unroll
-              for (int hh = 0; hh < 2; ++hh)
-                tma_load_2d_pair(st + hh * kMNHalf, &tmap_va, &full[s],
-                                 bb * 256 + rank * 128 + hh * 64, row_tile + 64 * j,
-                                 p.a_hint != 0 ? kEvictFirst : kEvictNormal);  // last use
+              for (int js = 0; js < kVSub; ++js)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+                  tma_load_2d_pair(st + js * kABytes + hh * kMNHalf, &tmap_va, &full[s],
+                                   bb * 256 + rank * 128 + hh * 64, row_tile + 64 * (j + js),
+                                   p.a_hint != 0 ? kEvictFirst : kEvictNormal);  // last use
             }
           }
           __syncwarp();
